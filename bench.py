@@ -1,0 +1,379 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 live-autoscaling data plane (one JSON line on rank 0).
+
+Workloads (BASELINE.json configs):
+  N = 1  : O(1) host-cache load of a Llama-2 7B bf16 shard (13.48 GB) into one
+           B200 -- plan ``mem0 -> gpu0`` (pcie) from the reference planner,
+           copy-engine staging on a side stream + per-layer readiness tracking.
+  N >= 2 : live scale-up 1 -> N: the source instance on gpu0 multicasts its
+           shard to N-1 new GPUs; plan from ``generate_plan`` (group=True:
+           gpu0 -> rep gpu1 over NVLink, rep -> NVLS multicast to the rest).
+One step = one complete scale-up (every target holds the bit-exact shard and
+its tracker has published every layer).  value = delivered bytes / time
+(delivered = shard x number of receiving GPUs), max over ranks.
+e2e = the same metric through the public API (planning included) with the
+shard starting in the pinned O(1) host cache: ``mem0 -> gpu0`` + NVLS fan-out
+to every other GPU, host->device bytes inside the timed region, per-layer
+stamps read back to the host.
+
+``--impl reference`` times the reference's CPU path: the oracle's torch CPU
+copies of every layer unit along the same plan (all host threads), rank 0 only.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+NVLINK_PEAK_GBPS = 770.0     # B200_PROFILING.md: measured peer copy per direction (900 nominal)
+NVLINK_NOMINAL_GBPS = 900.0
+PCIE_PEAK_GBPS = 63.0        # PCIe Gen5 x16 per direction, nominal
+METRIC = "scale-up delivered GB/s (Llama-2 7B bf16 shard into every new B200)"
+
+
+def parse_args():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=5)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", default="blitz", choices=["blitz", "reference"])
+    p.add_argument("--arch", default="llama2-7b")
+    p.add_argument("--tile-kib", type=int, default=1024)
+    p.add_argument("--nctas", type=int, default=32)
+    p.add_argument("--engine", default="vector", choices=["vector", "tma"])
+    p.add_argument("--fanout", default="auto", choices=["auto", "nvls", "chain", "star"])
+    p.add_argument("--no-group", action="store_true", help="plan chains instead of NVLink fan-out")
+    p.add_argument("--stage-engine", default="ce", choices=["ce", "sm"])
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--cpu-sample-units", type=int, default=4)
+    return p.parse_args()
+
+
+# ---- clocks ------------------------------------------------------------------------------
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 200 ms during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.rows: list[list[str]] = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.device}", f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            threading.Thread(target=self._read, daemon=True).start()
+        except FileNotFoundError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def stop(self) -> dict:
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+        sm = [float(r[1]) for r in self.rows if len(r) > 8 and r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if len(r) > 8 and r[2].replace(".", "").isdigit()]
+        reasons = set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in self.rows:
+            if len(r) > 8:
+                for name, v in zip(names, r[5:9]):
+                    if v.lower() == "active":
+                        reasons.add(name)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ---- distributed helpers ---------------------------------------------------------------------
+
+
+def dist_max(values: list[float], world: int) -> list[float]:
+    if world == 1:
+        return values
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor(values, dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return t.cpu().tolist()
+
+
+def dist_sum(value: float, world: int) -> float:
+    if world == 1:
+        return value
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([value], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t)
+    return float(t.item())
+
+
+# ---- CPU baseline (the oracle restatement; bounded sample) ----------------------------------------
+
+
+def cpu_copy_baseline(plan, layout, units: int, steps: int = 1) -> dict:
+    """Torch CPU copies of the first ``units`` layer units along ``plan`` (all threads)."""
+    import torch
+    from oracle import dataplane_ref as ref
+
+    threads = os.cpu_count() or 1
+    torch.set_num_threads(threads)
+    units = max(1, min(units, layout.num_layers))
+    nbytes = layout.unit_off[units - 1] + layout.unit_bytes[units - 1]
+    nodes = {e.src for e in plan.edges} | set(plan.targets())
+    src_nodes = {e.src for e in plan.edges} - set(plan.targets())
+    bufs = {}
+    seed_buf = torch.from_numpy(ref.random_words((nbytes + 15) // 16 * 16, 5)[:nbytes].copy())
+    for n in nodes:
+        bufs[n] = seed_buf.clone() if n in src_nodes else torch.empty(nbytes, dtype=torch.uint8)
+    bounds = [(layout.unit_off[k], layout.unit_off[k] + layout.unit_bytes[k]) for k in range(units)]
+    ref.execute_plan_cpu(plan, bufs, bounds)  # warm (page faults)
+    times = []
+    for _ in range(steps):
+        t0 = time.perf_counter()
+        ref.execute_plan_cpu(plan, bufs, bounds)
+        times.append(time.perf_counter() - t0)
+    for n in plan.targets():
+        assert torch.equal(bufs[n], seed_buf), "CPU baseline copy mismatch"
+    delivered = sum(layout.unit_bytes[:units]) * len(plan.targets())
+    secs = min(times)
+    return {"value": delivered / secs / 1e9, "unit": "GB/s", "cores": threads, "kind": "port",
+            "sample": f"layer units 1..{units} of the shard ({delivered / 1e9:.2f} GB delivered "
+                      f"to {len(plan.targets())} destination buffer(s)), torch CPU copy_ along "
+                      f"the plan edges, best of {steps}",
+            "seconds": secs}
+
+
+# ---- reference arm ------------------------------------------------------------------------------
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", str(args.gpus)))
+    if rank != 0:
+        return
+    from paper_2412_17246_b200 import slab as S
+    from paper_2412_17246_b200.scaleup import plan_for
+
+    arch = S.ARCHS[args.arch]
+    layout = S.SlabLayout.for_arch(arch, tile_bytes=args.tile_kib * 1024)
+    gpus = [f"gpu{i}" for i in range(world)]
+    if world == 1:
+        plan, _, _ = plan_for(arch, ["mem0"], ["gpu0"])
+        workload = f"{arch.name} O(1) host-cache load mem0->gpu0 (CPU restatement)"
+    else:
+        plan, _, _ = plan_for(arch, ["gpu0"], gpus[1:], group=not args.no_group)
+        workload = f"{arch.name} live scale-up 1->{world} (CPU restatement of the plan's copies)"
+    for _ in range(args.warmup):
+        cpu_copy_baseline(plan, layout, args.cpu_sample_units, steps=1)
+    t0 = time.perf_counter()
+    res = cpu_copy_baseline(plan, layout, args.cpu_sample_units, steps=args.steps)
+    wall = time.perf_counter() - t0
+    line = {
+        "impl": "reference", "metric": METRIC, "value": res["value"], "unit": "GB/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": res["seconds"] * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "u8", "data": "synthetic",
+        "config": {"workload": workload, "sample_units": args.cpu_sample_units},
+        "cpu_baseline": {k: res[k] for k in ("value", "unit", "cores", "kind", "sample")},
+        "e2e": {"value": res["value"], "unit": "GB/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+        "wall_s": wall,
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---- our arm ----------------------------------------------------------------------------------------
+
+
+def run_blitz(args):
+    import torch
+    from paper_2412_17246_b200 import slab as S
+    from paper_2412_17246_b200.dataplane import (ENGINE_TMA, ENGINE_VECTOR, DeviceSlab, Fabric,
+                                                 HostCache, plan_roles)
+    from paper_2412_17246_b200.scaleup import ScaleUpSession, plan_for
+
+    fabric = Fabric.from_env()
+    N, rank = fabric.world, fabric.rank
+    arch = S.ARCHS[args.arch]
+    layout = S.SlabLayout.for_arch(arch, tile_bytes=args.tile_kib * 1024)
+    payload = layout.payload_bytes()
+    gpus = [f"gpu{i}" for i in range(N)]
+    node_rank = {g: i for i, g in enumerate(gpus)}
+    engine = ENGINE_TMA if args.engine == "tma" else ENGINE_VECTOR
+    seed = 241217
+    my = gpus[rank]
+
+    def host_cache_for(plan, tag):
+        """Pinned O(1) host copy, only in the process whose GPU stages from it."""
+        role = plan_roles(plan).get(my)
+        if role is None or role.parent is None or not role.parent.startswith("mem"):
+            return None
+        hc = HostCache(layout)
+        tmp = DeviceSlab(layout, fabric.device)
+        tmp.fill_random(seed)
+        hc.tensor.copy_(tmp.data.cpu())
+        tmp.close()
+        return hc
+
+    if N == 1:
+        plan, model, est = plan_for(arch, ["mem0"], ["gpu0"])
+        workload = f"{arch.name} bf16 O(1) pinned host-cache load mem0->gpu0 (copy engines), per-layer readiness"
+        bound, peak, peak_src = "pcie", PCIE_PEAK_GBPS, "PCIe Gen5 x16 nominal per direction"
+    else:
+        plan, model, est = plan_for(arch, ["gpu0"], gpus[1:], group=not args.no_group)
+        workload = (f"{arch.name} bf16 live scale-up 1->{N}: plan "
+                    f"{[(e.src, e.dst) for e in plan.edges]} fan-out {plan.nvlink_fanout}")
+        bound, peak, peak_src = "nvlink", NVLINK_PEAK_GBPS, "B200_PROFILING.md measured peer copy per direction (900 nominal)"
+    receivers = len(plan.targets())
+    delivered = payload * receivers
+    hc = host_cache_for(plan, "value")
+    sess = ScaleUpSession(fabric, layout, plan, node_rank, host_cache=hc, engine=engine,
+                          nctas=args.nctas, fanout_mode=args.fanout, seed=seed,
+                          stage_engine=args.stage_engine)
+
+    # warm-up (first one verified bit-exact on every receiver)
+    ok = True
+    for w in range(max(args.warmup, 1)):
+        r = sess.run(verify=(w == 0))
+        if w == 0:
+            ok = bool(r.verified)
+    ok_all = dist_sum(0.0 if ok else 1.0, N) == 0.0
+
+    clocks = ClockSampler(fabric.device)
+    fabric.barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    steps, kern, first_layer, last_layer = [], [], [], []
+    wall0 = time.perf_counter()
+    for _ in range(args.steps):
+        r = sess.run(time_kernel=True)
+        steps.append(r.elapsed_ms)
+        kern.append(r.kernel_ms if r.kernel_ms is not None else 0.0)
+        if r.layer_ms:
+            first_layer.append(r.layer_ms[0])
+            last_layer.append(r.layer_ms[-1])
+    fabric.barrier()
+    torch.cuda.synchronize()
+    wall = time.perf_counter() - wall0
+    clk = clocks.stop()
+    step_ms = dist_max(steps, N)
+    kern_ms = dist_max(kern, N)
+    fl = dist_max([statistics.mean(first_layer) if first_layer else 0.0], N)[0]
+    launches = dist_sum(float(sess.executor.kernels_per_launch() * args.steps), N)
+    ms = statistics.mean(step_ms)
+    value = delivered / (ms / 1e3) / 1e9
+    dom_kernel_ms = statistics.mean(kern_ms)
+    # dominant mover: bytes that cross the bound link per launch = one shard
+    achieved = payload / (dom_kernel_ms / 1e3) / 1e9 if dom_kernel_ms > 0 else None
+    final_ok = sess.verify(sess.executor.epoch)
+    final_all = dist_sum(0.0 if final_ok else 1.0, N) == 0.0
+    sess.close()
+    if hc is not None:
+        hc.close()
+
+    # ---- e2e: public API, shard starts in pinned host memory ---------------------------------
+    e2e = None
+    if not args.no_e2e:
+        e2e_plan, _, _ = plan_for(arch, ["mem0"], gpus)
+        hc2 = host_cache_for(e2e_plan, "e2e")
+        sess2 = ScaleUpSession(fabric, layout, e2e_plan, node_rank, host_cache=hc2, engine=engine,
+                               nctas=args.nctas, fanout_mode=args.fanout, seed=seed,
+                               stage_engine=args.stage_engine)
+        for w in range(max(1, min(args.warmup, 2))):
+            sess2.run(verify=(w == 0))
+        e2e_t = []
+        for _ in range(args.steps):
+            fabric.barrier()
+            t0 = time.perf_counter()
+            # the user's call: plan (reference API) + execute + read readiness back
+            p, _, _ = plan_for(arch, ["mem0"], gpus)
+            assert p.edges == e2e_plan.edges and p.nvlink_fanout == e2e_plan.nvlink_fanout
+            r = sess2.run()
+            stamps = sess2.slab.stamps.cpu()  # d2h: per-layer arrival stamps
+            e2e_t.append(time.perf_counter() - t0)
+        e2e_s = dist_max(e2e_t, N)
+        e2e_ok = dist_sum(0.0 if sess2.verify(sess2.executor.epoch) else 1.0, N) == 0.0
+        h2d = payload  # one shard crosses PCIe per step
+        d2h = int(stamps.numel() * 8) * N
+        e2e = {"value": payload * len(e2e_plan.targets()) / statistics.mean(e2e_s) / 1e9,
+               "unit": "GB/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+               "workload": f"public API: plan_for(mem0 -> {gpus}) + ScaleUpSession.run() + "
+                           f"stamp readback; plan {[(e.src, e.dst, e.kind) for e in e2e_plan.edges]}"
+                           f" fan-out {e2e_plan.nvlink_fanout}",
+               "bit_exact": e2e_ok}
+        sess2.close()
+        if hc2 is not None:
+            hc2.close()
+
+    cpu = None
+    if rank == 0:
+        cpu = cpu_copy_baseline(plan, layout, args.cpu_sample_units, steps=1)
+        cpu.pop("seconds", None)
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": N, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "u8", "data": "synthetic",
+            "config": {"workload": workload, "model": arch.name, "shard_bytes": payload,
+                       "receivers": receivers, "tile_bytes": layout.tile_off[1] - layout.tile_off[0]
+                       if layout.ntiles else 0, "ntiles": layout.ntiles, "nctas": args.nctas,
+                       "engine": args.engine, "fanout": sess.executor.fanout_mode,
+                       "stage_engine": args.stage_engine,
+                       "l2": "inputs (13.48 GB shard) exceed the 126 MB L2; no flush needed",
+                       "parallelism": f"1 process per GPU, {N} GPU(s)"},
+            "scale_up_ms": ms, "per_dest_GBps": payload / (ms / 1e3) / 1e9,
+            "first_layer_ms": fl,
+            "modeled_ms_eta1": {k: v * 1e3 for k, v in est.per_target_completion.items()},
+            "bit_exact": bool(ok_all and final_all),
+            "roofline": {"bound": bound, "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": (achieved / peak) if achieved else None, "traffic": None,
+                         "peak_source": peak_src, "kernel_ms": dom_kernel_ms,
+                         "frac_of_nominal": (achieved / (NVLINK_NOMINAL_GBPS if bound == "nvlink"
+                                                         else PCIE_PEAK_GBPS)) if achieved else None},
+            "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
+            "clocks": clk, "wall_s": wall,
+        }
+        print(json.dumps(line), flush=True)
+    fabric.barrier()
+
+
+def main():
+    args = parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_blitz(args)
+    if int(os.environ.get("WORLD_SIZE", "1")) > 1:
+        import torch.distributed as dist
+        if dist.is_initialized():
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

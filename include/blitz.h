@@ -1,0 +1,156 @@
+/* blitz.h -- C ABI of libblitz.so, the sm_100a live-autoscaling data plane.
+ *
+ * Plain pointers, sizes and stream handles; no torch types.  Every entry point
+ * returns 0 on success or a negative BZ_E* code, with a message available from
+ * bz_last_error() (thread-local).  Nothing here falls back to the CPU: a CUDA
+ * failure is returned to the caller, which raises.
+ *
+ * The reference (/root/reference/pkg/src/scalesim) has NO native layer -- it
+ * models these mechanisms as arithmetic.  Each entry point names the modeled
+ * item it realises:
+ *   weight slabs + peer mesh     <- the pre-established NVLink/RDMA connection pool
+ *                                   (SURVEY.md §5 "communication backend")
+ *   bz_push_tiles                <- a chain edge's store-and-forward transfer
+ *                                   (planner.py:240-244 PlanEdge hop; simcore.py:690-703)
+ *   bz_multicast_tiles           <- ScalePlan.nvlink_fanout intra-host broadcast
+ *                                   (planner.py:86-87, 245-253)
+ *   bz_stage_tiles_ce / _sm      <- mem<h> -> gpu pcie source edge; autoscaler.baseline_load_time
+ *                                   (topology.py:174-176; autoscaler.py:102-117)
+ *   bz_track_layers              <- per-layer LayerLoaded(k) events
+ *                                   (simcore.py:727-733, 752-763; livescale.py:458-468)
+ *   bz_wait_layer                <- gating execution of layer k on its arrival
+ *   bz_gemm_bf16                 <- the per-layer prefill cost model ModelSpec.prefill_ms
+ *                                   (parampool.py:58-62): the real layer GEMMs
+ *
+ * Memory model.  A slab is one VMM allocation (cuMemCreate, POSIX-FD
+ * shareable) holding a model shard laid out layer by layer, followed by a
+ * u32 tile-flag array.  Tiles never straddle layers.  flag[t] >= epoch means
+ * tile t of this slab holds the bytes of transfer `epoch`.
+ */
+#ifndef BLITZ_H
+#define BLITZ_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+  BZ_OK = 0,
+  BZ_ECUDA = -1,    /* CUDA runtime/driver error */
+  BZ_EINVAL = -2,   /* bad arguments */
+  BZ_ESYS = -3,     /* OS error (pidfd, fd passing) */
+  BZ_EUNSUP = -4    /* device lacks the feature (e.g. NVLS multicast) */
+};
+
+#define BZ_MAX_DST 8
+
+const char* bz_last_error(void);
+int bz_version(void);
+
+/* ---- devices ------------------------------------------------------------ */
+int bz_device_count(int* n);
+int bz_device_caps(int dev, int* multicast, int* posix_fd, int* fabric, int* sm_count);
+/* Enable peer access from `dev` to every other visible device (the "connection pool"). */
+int bz_enable_peer_mesh(int dev);
+
+/* ---- weight slabs (VMM) ------------------------------------------------------- */
+typedef struct {
+  uint64_t ptr;        /* device VA of the mapping in this process */
+  uint64_t bytes;      /* mapped size (rounded to granularity) */
+  uint64_t handle;     /* CUmemGenericAllocationHandle */
+  int dev;             /* device the memory lives on */
+  int fd;              /* exported POSIX fd (owner) or imported fd, -1 if none */
+} bz_slab;
+
+/* Physical allocation on `dev`, mapped RW for `dev`.  Rounded up to the
+ * multicast granularity so it can be bound into a multicast object. */
+int bz_slab_create(int dev, uint64_t bytes, bz_slab* out);
+/* Export as a POSIX fd (stored in out->fd). */
+int bz_slab_export(bz_slab* slab);
+/* Import a peer process's slab: (owner_pid, owner_fd) come from bz_slab_export
+ * in that process; mapped RW for `local_dev`, giving a peer VA over NVLink. */
+int bz_slab_import(int local_dev, int owner_pid, int owner_fd, uint64_t bytes, bz_slab* out);
+int bz_slab_free(bz_slab* slab);
+
+/* ---- NVLS multicast ----------------------------------------------------------- */
+typedef struct {
+  uint64_t handle;     /* CUmemGenericAllocationHandle of the multicast object */
+  uint64_t mc_ptr;     /* VA of the multicast mapping in this process (0 until mapped) */
+  uint64_t bytes;
+  int fd;
+} bz_mc;
+
+int bz_mc_granularity(int dev, int ndev, uint64_t* min_gran, uint64_t* rec_gran);
+int bz_mc_create(int ndev, uint64_t bytes, bz_mc* out);         /* root; exports fd */
+int bz_mc_import(int owner_pid, int owner_fd, uint64_t bytes, bz_mc* out);
+int bz_mc_add_device(bz_mc* mc, int dev);
+int bz_mc_bind(bz_mc* mc, int dev, const bz_slab* slab, uint64_t slab_offset,
+               uint64_t mc_offset, uint64_t bytes);
+int bz_mc_map(bz_mc* mc, int dev);
+int bz_mc_free(bz_mc* mc, int dev, uint64_t bound_bytes);
+
+/* ---- tile transfer kernels ---------------------------------------------------- */
+/* Tile table: tile t covers bytes [tile_off[t], tile_off[t+1]) of a slab
+ * (device array of ntiles+1 int64, 16-byte aligned offsets).
+ *
+ * bz_push_tiles: copy tiles [t0, t1) from `src` to each of the ndst
+ * destination bases (peer VAs or local), then publish dst_flags[d][t] = epoch
+ * with a system-scope release.  If wait_flags != NULL the tile is forwarded
+ * only after wait_flags[t] >= epoch (store-and-forward relay of a chain hop).
+ * engine: 0 = 16-byte vector LD/ST, 1 = TMA bulk copy (cp.async.bulk). */
+int bz_push_tiles(const void* src, void* const* dst, uint32_t* const* dst_flags, int ndst,
+                  const uint32_t* wait_flags, const int64_t* tile_off, int t0, int t1,
+                  uint32_t epoch, int nctas, int engine, void* stream);
+
+/* bz_multicast_tiles: one multimem.st stream into the multicast VA `mc_dst`
+ * (bound to every receiver's slab); flags go through `mc_flags` (the
+ * multicast VA of the receivers' flag arrays). */
+int bz_multicast_tiles(const void* src, void* mc_dst, uint32_t* mc_flags,
+                       const uint32_t* wait_flags, const int64_t* tile_off, int t0, int t1,
+                       uint32_t epoch, int nctas, void* stream);
+
+/* Host staging from pinned memory. _ce: copy engine, one cudaMemcpyAsync per
+ * group of `tiles_per_copy` tiles followed by a flag update; _sm: a kernel that
+ * reads the mapped host buffer (zero-copy) with 16-byte loads. */
+int bz_stage_tiles_ce(const void* host_src, void* dst, uint32_t* dst_flags,
+                      const int64_t* tile_off_host, int t0, int t1, int tiles_per_copy,
+                      uint32_t epoch, void* stream);
+int bz_stage_tiles_sm(const void* host_src, void* dst, uint32_t* dst_flags,
+                      const int64_t* tile_off, int t0, int t1, uint32_t epoch, int nctas,
+                      void* stream);
+
+/* ---- layer readiness ---------------------------------------------------------------- */
+/* One-warp tracker: for k = 0..nlayers-1 in order, waits until every tile of
+ * layer k (tiles [layer_tile[k], layer_tile[k+1])) has flag >= epoch, then
+ * publishes loaded[0] = k+1 (release, monotone) and stamps[k] = %globaltimer ns. */
+int bz_track_layers(const uint32_t* flags, const int32_t* layer_tile, int nlayers,
+                    uint32_t epoch, uint32_t* loaded, uint64_t* stamps, void* stream);
+/* In-stream publish (producer on this GPU, e.g. copy-engine staging): after the
+ * preceding work in `stream`, stamp[0] = %globaltimer, then *loaded = value. */
+int bz_publish_layer(uint32_t* loaded, uint32_t value, uint64_t* stamp, void* stream);
+/* Stream gate: blocks `stream` until *loaded >= k (cuStreamWaitValue32 GEQ). */
+int bz_wait_layer(const uint32_t* loaded, uint32_t k, void* stream);
+/* Device gate kernel variant of the same (spins with ld.acquire.sys). */
+int bz_wait_flag_kernel(const uint32_t* flag, uint32_t value, void* stream);
+
+/* ---- payload + verification ---------------------------------------------------------- */
+/* Deterministic random bits: 64-bit word i = splitmix64(seed + i). */
+int bz_fill_random(void* dst, uint64_t bytes, uint64_t seed, void* stream);
+/* Per-tile 64-bit fingerprints of [tile_off[t], tile_off[t+1]) into out[t - t0]. */
+int bz_tile_fingerprints(const void* base, const int64_t* tile_off, int t0, int t1,
+                         uint64_t* out, void* stream);
+/* Plain copy of a small buffer into a peer/local buffer followed by a release
+ * flag store (activation handoff of cooperative execution). */
+int bz_handoff(const void* src, void* dst, uint64_t bytes, uint32_t* flag, uint32_t value,
+               int nctas, void* stream);
+
+/* ---- kernels timed by the caller ----------------------------------------------------- */
+int bz_sm_count(int dev, int* n);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* BLITZ_H */

@@ -70,3 +70,109 @@ def host_lib() -> _HostLib:
     if _host is None:
         _host = _HostLib()
     return _host
+
+
+# ---- libblitz.so (include/blitz.h) ----------------------------------------------------
+
+class BlitzError(RuntimeError):
+    """A libblitz call failed; carries bz_last_error()."""
+
+
+class BzSlab(ctypes.Structure):
+    _fields_ = [("ptr", ctypes.c_uint64), ("bytes", ctypes.c_uint64), ("handle", ctypes.c_uint64),
+                ("dev", ctypes.c_int), ("fd", ctypes.c_int)]
+
+
+class BzMc(ctypes.Structure):
+    _fields_ = [("handle", ctypes.c_uint64), ("mc_ptr", ctypes.c_uint64), ("bytes", ctypes.c_uint64),
+                ("fd", ctypes.c_int)]
+
+
+_P = ctypes.c_void_p
+_I = ctypes.c_int
+_U32 = ctypes.c_uint32
+_U64 = ctypes.c_uint64
+_PP = ctypes.POINTER(ctypes.c_void_p)
+_PI = ctypes.POINTER(ctypes.c_int)
+_PU64 = ctypes.POINTER(ctypes.c_uint64)
+
+# name -> argtypes; every function returns int status
+_SIGNATURES = {
+    "bz_version": [],
+    "bz_device_count": [_PI],
+    "bz_device_caps": [_I, _PI, _PI, _PI, _PI],
+    "bz_enable_peer_mesh": [_I],
+    "bz_slab_create": [_I, _U64, ctypes.POINTER(BzSlab)],
+    "bz_slab_export": [ctypes.POINTER(BzSlab)],
+    "bz_slab_import": [_I, _I, _I, _U64, ctypes.POINTER(BzSlab)],
+    "bz_slab_free": [ctypes.POINTER(BzSlab)],
+    "bz_mc_granularity": [_I, _I, _PU64, _PU64],
+    "bz_mc_create": [_I, _U64, ctypes.POINTER(BzMc)],
+    "bz_mc_import": [_I, _I, _U64, ctypes.POINTER(BzMc)],
+    "bz_mc_add_device": [ctypes.POINTER(BzMc), _I],
+    "bz_mc_bind": [ctypes.POINTER(BzMc), _I, ctypes.POINTER(BzSlab), _U64, _U64, _U64],
+    "bz_mc_map": [ctypes.POINTER(BzMc), _I],
+    "bz_mc_free": [ctypes.POINTER(BzMc), _I, _U64],
+    "bz_push_tiles": [_P, _PP, _PP, _I, _P, _P, _I, _I, _U32, _I, _I, _P],
+    "bz_multicast_tiles": [_P, _P, _P, _P, _P, _I, _I, _U32, _I, _P],
+    "bz_stage_tiles_ce": [_P, _P, _P, _P, _I, _I, _I, _U32, _P],
+    "bz_stage_tiles_sm": [_P, _P, _P, _P, _I, _I, _U32, _I, _P],
+    "bz_track_layers": [_P, _P, _I, _U32, _P, _P, _P],
+    "bz_publish_layer": [_P, _U32, _P, _P],
+    "bz_wait_layer": [_P, _U32, _P],
+    "bz_wait_flag_kernel": [_P, _U32, _P],
+    "bz_fill_random": [_P, _U64, _U64, _P],
+    "bz_tile_fingerprints": [_P, _P, _I, _I, _P, _P],
+    "bz_handoff": [_P, _P, _U64, _P, _U32, _I, _P],
+    "bz_sm_count": [_I, _PI],
+}
+
+
+def exported_symbols() -> list[str]:
+    return sorted(_SIGNATURES) + ["bz_last_error"]
+
+
+class _CudaLib:
+    """Checked wrapper over libblitz.so: every non-zero status raises BlitzError."""
+
+    def __init__(self):
+        self.lib = _load(CUDA_LIB)
+        self.lib.bz_last_error.restype = ctypes.c_char_p
+        self.lib.bz_last_error.argtypes = []
+        for name, args in _SIGNATURES.items():
+            fn = getattr(self.lib, name)
+            fn.restype = ctypes.c_int
+            fn.argtypes = args
+
+    def __getattr__(self, name):
+        if not name.startswith("bz_"):
+            raise AttributeError(name)
+        fn = getattr(self.lib, name)
+
+        def call(*args):
+            rc = fn(*args)
+            if rc != 0:
+                msg = self.lib.bz_last_error().decode(errors="replace")
+                raise BlitzError(f"{name} failed (rc={rc}): {msg}")
+            return rc
+
+        call.__name__ = name
+        return call
+
+
+_cuda: Optional[_CudaLib] = None
+
+
+def cuda_lib() -> _CudaLib:
+    """libblitz.so; raises NativeLibraryMissing if it was not built (no fallback)."""
+    global _cuda
+    if _cuda is None:
+        _cuda = _CudaLib()
+    return _cuda
+
+
+def ptr_array(values: Sequence[int]):
+    arr = (ctypes.c_void_p * max(1, len(values)))()
+    for i, v in enumerate(values):
+        arr[i] = int(v)
+    return arr

@@ -1,0 +1,577 @@
+"""B200 parameter data plane: executes a ``ScalePlan`` with real bytes.
+
+Reference mapping (``/root/reference/pkg/src/scalesim``):
+
+* ``ScalePlan.edges`` (planner.py:72-109) -> a chain hop: the edge's sender
+  pushes every tile of its slab into the receiver's slab through a peer
+  mapping (``bz_push_tiles``); a sender that is itself a receiver forwards
+  tile ``t`` as soon as its own flag ``t`` is raised (store-and-forward of
+  planner.py:240-244 at tile granularity, so a hop costs one tile of fill,
+  not one layer).
+* ``ScalePlan.nvlink_fanout`` (planner.py:86-87, 245-253) -> the
+  representative relays each tile into an NVLS multicast object bound to the
+  slabs of the whole fan-out group (``bz_multicast_tiles``): one stream out of
+  the representative, replicated by the NVSwitch.  Without NVLS the group is
+  served as a pipelined sibling chain.
+* ``mem<h>`` sources (topology.py:174-176) -> the O(1) pinned host cache is
+  staged by the copy engines on a side stream (``bz_stage_tiles_ce``).
+* ``simcore`` per-layer ``layer`` events (simcore.py:727-733) -> every receiver
+  runs a one-warp tracker (``bz_track_layers``) that raises a monotone
+  ``loaded_layers`` counter in device memory and stamps each layer's arrival
+  with ``%globaltimer``; compute streams gate on it (``bz_wait_layer``).
+
+Process model: one process per GPU (``torchrun``); a slab is exported once
+as a POSIX fd, peers import it with ``pidfd_getfd`` -- the pre-established
+connection pool of PAPER.md:997-1006, no communicator creation on the scale
+path.  ``torch.distributed`` is only used to exchange (pid, fd) pairs and for
+barriers.  A single process can also drive several slabs on one GPU
+("loopback"), which is how the single-GPU tests exercise the same kernels.
+"""
+
+from __future__ import annotations
+
+import os
+from dataclasses import dataclass, field
+from typing import Optional, Sequence
+
+import numpy as np
+import torch
+
+from ._native import BzMc, BzSlab, cuda_lib, ptr_array
+from .planner import ScalePlan
+from .slab import SlabLayout
+
+ENGINE_VECTOR = 0
+ENGINE_TMA = 1
+
+
+class _CudaView:
+    """Expose raw device memory to torch without copying."""
+
+    def __init__(self, ptr: int, nbytes: int, typestr: str, itemsize: int):
+        self.__cuda_array_interface__ = {
+            "shape": (nbytes // itemsize,), "typestr": typestr, "data": (int(ptr), False),
+            "version": 3, "strides": None,
+        }
+
+
+def device_view(ptr: int, nbytes: int, dtype: torch.dtype, device) -> torch.Tensor:
+    typestr = {torch.uint8: "|u1", torch.int32: "<i4", torch.int64: "<i8",
+               torch.int16: "<i2"}[dtype]
+    item = torch.empty((), dtype=dtype).element_size()
+    return torch.as_tensor(_CudaView(ptr, nbytes, typestr, item), device=device)
+
+
+# ---- control plane (pid/fd exchange) ---------------------------------------------------
+
+
+class Fabric:
+    """This process's GPU plus the control channel to the other ranks."""
+
+    def __init__(self, device: int, rank: int = 0, world: int = 1, group=None):
+        self.device = device
+        self.rank = rank
+        self.world = world
+        self.group = group
+        self.lib = cuda_lib()
+        import ctypes
+        vals = [ctypes.c_int() for _ in range(4)]
+        self.lib.bz_device_caps(device, *[ctypes.byref(v) for v in vals])
+        self.multicast_supported = bool(vals[0].value)
+        self.posix_fd_supported = bool(vals[1].value)
+        self.sm_count = vals[3].value
+
+    @classmethod
+    def from_env(cls) -> "Fabric":
+        """torchrun-style environment; initialises a gloo control group if needed."""
+        rank = int(os.environ.get("RANK", "0"))
+        world = int(os.environ.get("WORLD_SIZE", "1"))
+        local = int(os.environ.get("LOCAL_RANK", str(rank)))
+        torch.cuda.set_device(local)
+        group = None
+        if world > 1:
+            import torch.distributed as dist
+            if not dist.is_initialized():
+                dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+            group = dist.new_group(backend="gloo")
+        return cls(local, rank, world, group)
+
+    def allgather(self, obj):
+        if self.world == 1:
+            return [obj]
+        import torch.distributed as dist
+        out = [None] * self.world
+        dist.all_gather_object(out, obj, group=self.group)
+        return out
+
+    def barrier(self):
+        if self.world > 1:
+            import torch.distributed as dist
+            dist.barrier(group=self.group)
+
+
+# ---- slabs -----------------------------------------------------------------------------
+
+
+class DeviceSlab:
+    """One VMM allocation holding a shard (layer units, tiles) + its tile flags."""
+
+    def __init__(self, layout: SlabLayout, device: int):
+        self.layout = layout
+        self.device = device
+        self.lib = cuda_lib()
+        self.raw = BzSlab()
+        self.lib.bz_slab_create(device, layout.total_bytes, self.raw)
+        dev = torch.device("cuda", device)
+        self.data = device_view(self.raw.ptr, layout.data_bytes, torch.uint8, dev)
+        self.flags = device_view(self.raw.ptr + layout.flag_offset, layout.ntiles * 4,
+                                 torch.int32, dev)
+        self.flags.zero_()
+        self.tile_off = torch.from_numpy(layout.tile_off).to(dev)
+        self.layer_tile = torch.from_numpy(layout.layer_tile).to(dev)
+        self.loaded = torch.zeros(1, dtype=torch.int32, device=dev)
+        self.stamps = torch.zeros(layout.num_layers + 1, dtype=torch.int64, device=dev)
+        self._exported = False
+
+    @property
+    def ptr(self) -> int:
+        return int(self.raw.ptr)
+
+    @property
+    def flags_ptr(self) -> int:
+        return int(self.raw.ptr + self.layout.flag_offset)
+
+    def export(self) -> tuple[int, int, int]:
+        """(pid, fd, bytes) a peer needs to map this slab."""
+        if not self._exported:
+            self.lib.bz_slab_export(self.raw)
+            self._exported = True
+        return (os.getpid(), int(self.raw.fd), int(self.raw.bytes))
+
+    def fill_random(self, seed: int, stream=None):
+        s = _stream_handle(stream)
+        self.lib.bz_fill_random(self.ptr, self.layout.data_bytes, seed, s)
+
+    def fingerprints(self, stream=None) -> torch.Tensor:
+        out = torch.empty(self.layout.ntiles, dtype=torch.int64, device=self.data.device)
+        self.lib.bz_tile_fingerprints(self.ptr, self.tile_off.data_ptr(), 0, self.layout.ntiles,
+                                      out.data_ptr(), _stream_handle(stream))
+        return out
+
+    def close(self):
+        if self.raw.ptr:
+            torch.cuda.synchronize(self.device)
+            self.lib.bz_slab_free(self.raw)
+
+
+class PeerSlab:
+    """A peer process's slab mapped into this process (NVLink peer VA)."""
+
+    def __init__(self, local_device: int, pid: int, fd: int, nbytes: int, layout: SlabLayout):
+        self.lib = cuda_lib()
+        self.raw = BzSlab()
+        self.lib.bz_slab_import(local_device, pid, fd, nbytes, self.raw)
+        self.layout = layout
+
+    @property
+    def ptr(self) -> int:
+        return int(self.raw.ptr)
+
+    @property
+    def flags_ptr(self) -> int:
+        return int(self.raw.ptr + self.layout.flag_offset)
+
+    def close(self):
+        if self.raw.ptr:
+            self.lib.bz_slab_free(self.raw)
+
+
+class MulticastGroup:
+    """NVLS multicast object bound to the slabs of a fan-out group."""
+
+    def __init__(self, fabric: Fabric, slab: DeviceSlab, members: Sequence[int]):
+        self.fabric = fabric
+        self.members = sorted(members)
+        self.lib = cuda_lib()
+        self.raw = BzMc()
+        self.bound = 0
+        me = fabric.rank
+        root = self.members[0]
+        nbytes = int(slab.raw.bytes)
+        info = None
+        if me == root:
+            self.lib.bz_mc_create(len(self.members), nbytes, self.raw)
+            info = (os.getpid(), int(self.raw.fd), nbytes)
+        infos = fabric.allgather(info)
+        root_info = infos[root]
+        if me in self.members and me != root:
+            self.lib.bz_mc_import(root_info[0], root_info[1], root_info[2], self.raw)
+        fabric.barrier()  # root's fd stays open until every member imported
+        if me in self.members:
+            self.lib.bz_mc_add_device(self.raw, fabric.device)
+        fabric.barrier()
+        if me in self.members:
+            self.lib.bz_mc_bind(self.raw, fabric.device, slab.raw, 0, 0, nbytes)
+            self.bound = nbytes
+        fabric.barrier()
+        if me in self.members:
+            self.lib.bz_mc_map(self.raw, fabric.device)
+        self.layout = slab.layout
+
+    @property
+    def ptr(self) -> int:
+        return int(self.raw.mc_ptr)
+
+    @property
+    def flags_ptr(self) -> int:
+        return int(self.raw.mc_ptr + self.layout.flag_offset)
+
+    def close(self):
+        if self.raw.handle:
+            self.lib.bz_mc_free(self.raw, self.fabric.device, self.bound)
+
+
+def _stream_handle(stream) -> int:
+    if stream is None:
+        return int(torch.cuda.current_stream().cuda_stream)
+    return int(stream.cuda_stream)
+
+
+# ---- host cache -------------------------------------------------------------------------
+
+
+class HostCache:
+    """The O(1) host copy of a shard: page-locked memory the copy engines read.
+
+    ``shm_name`` backs it with /dev/shm so every GPU process of the host maps
+    the same single copy (one copy per host, parampool.py one-copy policy).
+    """
+
+    def __init__(self, layout: SlabLayout, shm_name: Optional[str] = None, create: bool = True):
+        self.layout = layout
+        nbytes = layout.data_bytes
+        if shm_name:
+            path = f"/dev/shm/{shm_name}"
+            if create:
+                with open(path, "wb") as f:
+                    f.truncate(nbytes)
+            self.array = np.memmap(path, dtype=np.uint8, mode="r+", shape=(nbytes,))
+            self.tensor = torch.from_numpy(self.array)
+        else:
+            self.tensor = torch.empty(nbytes, dtype=torch.uint8)
+        self.path = f"/dev/shm/{shm_name}" if shm_name else None
+        cudart = torch.cuda.cudart()
+        rc = cudart.cudaHostRegister(self.tensor.data_ptr(), nbytes, 1 | 2)  # portable | mapped
+        if int(rc) != 0:
+            raise RuntimeError(f"cudaHostRegister failed ({rc})")
+        self.registered = True
+        self.tile_off_host = np.ascontiguousarray(layout.tile_off)
+
+    @property
+    def ptr(self) -> int:
+        return int(self.tensor.data_ptr())
+
+    def close(self, unlink: bool = False):
+        if self.registered:
+            torch.cuda.cudart().cudaHostUnregister(self.tensor.data_ptr())
+            self.registered = False
+        if unlink and self.path and os.path.exists(self.path):
+            os.unlink(self.path)
+
+
+# ---- plan roles ---------------------------------------------------------------------------
+
+
+@dataclass
+class Role:
+    """What one node does in a plan (derived identically on every rank)."""
+
+    node: str
+    parent: Optional[str] = None          # edge sender (gpu or mem) that feeds this node
+    children: list[str] = field(default_factory=list)   # chain edges out of this node
+    fanout: list[str] = field(default_factory=list)     # NVLink siblings this rep serves
+    rep: Optional[str] = None             # if this node is a fan-out sibling: its rep
+
+    @property
+    def receives(self) -> bool:
+        return self.parent is not None or self.rep is not None
+
+
+def plan_roles(plan: ScalePlan) -> dict[str, Role]:
+    roles: dict[str, Role] = {}
+
+    def role(n: str) -> Role:
+        return roles.setdefault(n, Role(n))
+
+    for e in plan.edges:
+        role(e.src).children.append(e.dst)
+        role(e.dst).parent = e.src
+    for rep, sibs in plan.nvlink_fanout.items():
+        role(rep).fanout = list(sibs)
+        for s in sibs:
+            role(s).rep = rep
+    return roles
+
+
+def expand_tp(plan: ScalePlan, tp: int) -> list[ScalePlan]:
+    """Per-TP-rank plans: rank r of every anchor gpu<g> is gpu<g+r> (simcore.py:321-323)."""
+    if tp == 1:
+        return [plan]
+    from .planner import PlanEdge
+
+    def shift(n: str, r: int) -> str:
+        return f"gpu{int(n[3:]) + r}" if n.startswith("gpu") else n
+
+    out = []
+    for r in range(tp):
+        edges = [PlanEdge(shift(e.src, r), shift(e.dst, r), e.gbps, e.kind) for e in plan.edges]
+        fan = {shift(k, r): [shift(s, r) for s in v] for k, v in plan.nvlink_fanout.items()}
+        chains = [[shift(n, r) for n in c] for c in plan.chains]
+        out.append(ScalePlan(edges=edges, chains=chains, nvlink_fanout=fan))
+    return out
+
+
+# ---- executor -------------------------------------------------------------------------------
+
+
+@dataclass
+class TransferTiming:
+    elapsed_ms: float                    # this rank: start -> last tile landed + tracked
+    layer_ms: list[float]                # per-layer arrival after start (receivers)
+    bytes_received: int
+
+
+class ScaleExecutor:
+    """Runs one node's share of a plan on its GPU, every epoch a fresh transfer.
+
+    ``node_rank`` maps plan nodes (``gpu<i>``) to process ranks.  Every rank
+    constructs the executor with the same plan; collective setup (fd exchange,
+    multicast binding) happens in ``__init__``.
+    """
+
+    def __init__(self, fabric: Fabric, plan: ScalePlan, slab: DeviceSlab,
+                 node_rank: dict[str, int], host_cache: Optional[HostCache] = None,
+                 engine: int = ENGINE_VECTOR, nctas: int = 32, fanout_mode: str = "auto",
+                 stage_engine: str = "ce", tiles_per_copy: int = 8):
+        self.fabric = fabric
+        self.plan = plan
+        self.slab = slab
+        self.layout = slab.layout
+        self.node_rank = dict(node_rank)
+        self.rank_node = {r: n for n, r in node_rank.items()}
+        self.node = self.rank_node.get(fabric.rank)
+        self.roles = plan_roles(plan)
+        self.role = self.roles.get(self.node, Role(self.node)) if self.node else Role("")
+        self.host_cache = host_cache
+        self.engine = engine
+        self.nctas = nctas
+        self.stage_engine = stage_engine
+        self.tiles_per_copy = tiles_per_copy
+        self.lib = cuda_lib()
+        if fanout_mode == "auto":
+            fanout_mode = "nvls" if fabric.multicast_supported and fabric.world > 1 else "chain"
+        self.fanout_mode = fanout_mode
+        dev = torch.device("cuda", fabric.device)
+        self.streams = {k: torch.cuda.Stream(device=dev) for k in ("copy", "fan", "track", "stage")}
+        self.epoch = 0
+
+        # every rank exports its slab; peers it sends to are imported
+        exports = fabric.allgather((self.node, slab.export()))
+        self.peers: dict[str, PeerSlab] = {}
+        for n in self._unicast_targets():
+            r = self.node_rank[n]
+            pid, fd, nbytes = exports[r][1]
+            self.peers[n] = PeerSlab(fabric.device, pid, fd, nbytes, self.layout)
+        fabric.barrier()
+        self.mc: Optional[MulticastGroup] = None
+        if self.fanout_mode == "nvls":
+            # one multicast object per fan-out group, built collectively in plan order
+            for rep, sibs in plan.nvlink_fanout.items():
+                members = [self.node_rank[rep]] + [self.node_rank[s] for s in sibs]
+                grp = MulticastGroup(fabric, slab, members)
+                if self.node == rep:
+                    self.mc = grp
+                elif fabric.rank in members:
+                    self._member_group = grp
+
+    # chain children, plus siblings when the fan-out is served by unicast
+    def _unicast_targets(self) -> list[str]:
+        out = list(self.role.children)
+        if self.fanout_mode == "chain" and self.role.fanout:
+            out.append(self.role.fanout[0])
+        if self.fanout_mode == "chain" and self.role.rep is not None:
+            sibs = self.plan.nvlink_fanout[self.role.rep]
+            i = sibs.index(self.node)
+            if i + 1 < len(sibs):
+                out.append(sibs[i + 1])
+        if self.fanout_mode == "star" and self.role.fanout:
+            out.extend(self.role.fanout)
+        return out
+
+    def _feeds(self) -> tuple[list[str], bool]:
+        """(unicast destinations, relay?) for this node's push kernel."""
+        return self._unicast_targets(), self.role.receives
+
+    def dominant_stream(self) -> Optional[str]:
+        """Stream of this rank's bulk mover (for per-kernel timing), if any."""
+        if self.role.parent is not None and self.role.parent.startswith("mem"):
+            return "stage"
+        if self.fanout_mode == "nvls" and self.role.fanout:
+            return "fan"
+        if self._unicast_targets():
+            return "copy"
+        return None
+
+    def launch(self, epoch: Optional[int] = None, track: bool = True, kernel_events=None):
+        """Enqueue this rank's work for a new transfer; returns the epoch.
+
+        ``kernel_events=(start, end)`` brackets the bulk mover on its own stream.
+        """
+        self.epoch = epoch if epoch is not None else self.epoch + 1
+        e = self.epoch
+        lay, slab = self.layout, self.slab
+        st = self.streams
+        dom = self.dominant_stream()
+        if kernel_events is not None and dom is not None:
+            kernel_events[0].record(st[dom])
+        if self.role.receives and track:
+            # reset loaded_layers and stamp this rank's launch time, then track in order
+            self.lib.bz_publish_layer(slab.loaded.data_ptr(), 0, slab.stamps.data_ptr()
+                                      + 8 * lay.num_layers, st["track"].cuda_stream)
+            self.lib.bz_track_layers(slab.flags_ptr, slab.layer_tile.data_ptr(), lay.num_layers, e,
+                                     slab.loaded.data_ptr(), slab.stamps.data_ptr(),
+                                     st["track"].cuda_stream)
+        if self.role.parent is not None and self.role.parent.startswith("mem"):
+            self._stage(e)
+        dsts, relay = self._feeds()
+        if dsts:
+            ptrs = ptr_array([self.peers[n].ptr for n in dsts])
+            flags = ptr_array([self.peers[n].flags_ptr for n in dsts])
+            self.lib.bz_push_tiles(slab.ptr, ptrs, flags, len(dsts),
+                                   slab.flags_ptr if relay else None, slab.tile_off.data_ptr(),
+                                   0, lay.ntiles, e, self.nctas, self.engine, st["copy"].cuda_stream)
+        if self.fanout_mode == "nvls" and self.role.fanout:
+            self.lib.bz_multicast_tiles(slab.ptr, self.mc.ptr, self.mc.flags_ptr,
+                                        slab.flags_ptr if relay else None, slab.tile_off.data_ptr(),
+                                        0, lay.ntiles, e, self.nctas, st["fan"].cuda_stream)
+        if kernel_events is not None and dom is not None:
+            kernel_events[1].record(st[dom])
+        return e
+
+    def kernels_per_launch(self) -> int:
+        """Our kernels one ``launch`` enqueues on this rank (CE memcpys excluded)."""
+        n = 0
+        if self.role.receives:
+            n += 2  # publish + tracker
+        if self.role.parent is not None and self.role.parent.startswith("mem"):
+            n += (self.layout.ntiles + self.tiles_per_copy - 1) // self.tiles_per_copy \
+                if self.stage_engine == "ce" else 1
+        if self._unicast_targets():
+            n += 1
+        if self.fanout_mode == "nvls" and self.role.fanout:
+            n += 1
+        return n
+
+    def _stage(self, e: int):
+        hc, slab, lay = self.host_cache, self.slab, self.layout
+        if hc is None:
+            raise RuntimeError(f"{self.node} is fed by {self.role.parent} but no host cache was given")
+        s = self.streams["stage"].cuda_stream
+        if self.stage_engine == "ce":
+            self.lib.bz_stage_tiles_ce(hc.ptr, slab.ptr, slab.flags_ptr,
+                                       hc.tile_off_host.ctypes.data, 0, lay.ntiles,
+                                       self.tiles_per_copy, e, s)
+        else:
+            self.lib.bz_stage_tiles_sm(hc.ptr, slab.ptr, slab.flags_ptr, slab.tile_off.data_ptr(),
+                                       0, lay.ntiles, e, self.nctas, s)
+
+    def synchronize(self):
+        for s in self.streams.values():
+            s.synchronize()
+
+    def layer_arrivals_ms(self) -> list[float]:
+        """Per-layer arrival on this GPU, ms after this rank's launch (receivers only)."""
+        st = self.slab.stamps.cpu().tolist()
+        t0 = st[self.layout.num_layers]
+        return [(x - t0) / 1e6 for x in st[: self.layout.num_layers]]
+
+    def close(self):
+        self.synchronize()
+        for p in self.peers.values():
+            p.close()
+        for grp in (self.mc, getattr(self, "_member_group", None)):
+            if grp is not None:
+                grp.close()
+
+
+# ---- loopback (several slabs driven by one process on one GPU) -------------------------------
+
+
+def execute_plan_loopback(plan: ScalePlan, slabs: dict[str, DeviceSlab], epoch: int,
+                          host_cache: Optional[HostCache] = None, engine: int = ENGINE_VECTOR,
+                          nctas: int = 32, stage_engine: str = "ce", stream=None) -> None:
+    """Execute ``plan`` with every node's slab on this GPU, hop by hop on one stream.
+
+    The same kernels as the multi-GPU path; hops are stream-ordered, so a relay
+    finds its upstream flags already raised (no cross-kernel spinning on one GPU).
+    Fan-out groups are served as a sibling chain.
+    """
+    lib = cuda_lib()
+    s = _stream_handle(stream)
+    roles = plan_roles(plan)
+    order = _topological(plan)
+    for node in order:
+        role = roles[node]
+        if node.startswith("mem"):
+            continue
+        slab = slabs[node]
+        lay = slab.layout
+        if role.parent is not None and role.parent.startswith("mem"):
+            if host_cache is None:
+                raise RuntimeError("host cache required")
+            if stage_engine == "ce":
+                lib.bz_stage_tiles_ce(host_cache.ptr, slab.ptr, slab.flags_ptr,
+                                      host_cache.tile_off_host.ctypes.data, 0, lay.ntiles, 8, epoch, s)
+            else:
+                lib.bz_stage_tiles_sm(host_cache.ptr, slab.ptr, slab.flags_ptr,
+                                      slab.tile_off.data_ptr(), 0, lay.ntiles, epoch, nctas, s)
+        outs = list(role.children)
+        if role.fanout:
+            outs.append(role.fanout[0])
+        if role.rep is not None:
+            sibs = plan.nvlink_fanout[role.rep]
+            i = sibs.index(node)
+            if i + 1 < len(sibs):
+                outs.append(sibs[i + 1])
+        if outs:
+            ptrs = ptr_array([slabs[n].ptr for n in outs])
+            flags = ptr_array([slabs[n].flags_ptr for n in outs])
+            lib.bz_push_tiles(slab.ptr, ptrs, flags, len(outs),
+                              slab.flags_ptr if role.receives else None, slab.tile_off.data_ptr(),
+                              0, lay.ntiles, epoch, nctas, engine, s)
+        if role.receives:
+            lib.bz_track_layers(slab.flags_ptr, slab.layer_tile.data_ptr(), lay.num_layers, epoch,
+                                slab.loaded.data_ptr(), slab.stamps.data_ptr(), s)
+
+
+def _topological(plan: ScalePlan) -> list[str]:
+    """Senders before receivers: plan edge order, then fan-out groups after their rep."""
+    order: list[str] = []
+    seen = set()
+
+    def add(n):
+        if n not in seen:
+            seen.add(n)
+            order.append(n)
+
+    for e in plan.edges:
+        add(e.src)
+        add(e.dst)
+        for rep in [e.dst]:
+            for s in plan.nvlink_fanout.get(rep, []):
+                add(s)
+    for rep, sibs in plan.nvlink_fanout.items():
+        add(rep)
+        for s in sibs:
+            add(s)
+    return order

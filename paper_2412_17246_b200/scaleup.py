@@ -1,0 +1,124 @@
+"""Scale-up sessions: the user-facing call that turns "add instances of model M
+on these GPUs" into a plan (reference API) and a measured transfer (B200 data plane).
+
+Mirrors the reference caller ``simcore.Simulation._scale_via_network``
+(simcore.py:676-750): sources from the parameter pool, ``build_scale_request``
+-> ``generate_plan`` -> ``estimate_completion``, then -- instead of pushing
+modeled ``transfer``/``layer`` events -- the plan is executed by
+``ScaleExecutor`` and the per-layer arrival stamps come back from the GPUs.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+from typing import Optional, Sequence
+
+import torch
+
+from .dataplane import ENGINE_VECTOR, DeviceSlab, Fabric, HostCache, ScaleExecutor
+from .planner import build_scale_request, estimate_completion, generate_plan
+from .slab import LlamaArch, SlabLayout, model_spec_for
+from .topology import FlowSet, load_topology
+
+
+@dataclass
+class ScaleUpResult:
+    epoch: int
+    elapsed_ms: float                       # this rank: launch -> its share done
+    kernel_ms: Optional[float] = None       # this rank's bulk mover (stream-event timed)
+    layer_ms: list[float] = field(default_factory=list)
+    verified: Optional[bool] = None
+
+
+def plan_for(arch: LlamaArch, sources: Sequence[str], targets: Sequence[str],
+             topo="b200-hgx", group: bool = True, tp: int = 1):
+    """Reference planning path for a real architecture (bytes = real shard size)."""
+    t = load_topology(topo)
+    flows = FlowSet(t)
+    model = model_spec_for(arch, tp=tp)
+    req = build_scale_request(model, list(sources), list(targets), t, flows)
+    plan = generate_plan(req, t, flows, group=group)
+    return plan, model, estimate_completion(plan, model, t, eta=1.0)
+
+
+def expected_fingerprints(layout: SlabLayout, device: int, seed: int) -> torch.Tensor:
+    """Fingerprints of the synthetic shard made from ``seed`` (regenerated locally)."""
+    tmp = DeviceSlab(layout, device)
+    tmp.fill_random(seed)
+    prints = tmp.fingerprints().cpu()
+    tmp.close()
+    return prints
+
+
+class ScaleUpSession:
+    """One rank's persistent scale-up machinery for a (plan, model) pair.
+
+    Construction is collective (all ranks): slabs are allocated, exported,
+    peer-mapped and multicast-bound once -- the connection pool.  ``run()``
+    executes one scale-up and blocks until this rank's share is done.  The
+    source shard is synthetic: random bits from ``seed`` (bf16 NaN/Inf
+    patterns included), on the source GPU or in the pinned host cache.
+    """
+
+    def __init__(self, fabric: Fabric, layout: SlabLayout, plan, node_rank: dict[str, int],
+                 host_cache: Optional[HostCache] = None, engine: int = ENGINE_VECTOR,
+                 nctas: int = 32, fanout_mode: str = "auto", seed: int = 241217,
+                 stage_engine: str = "ce"):
+        self.fabric = fabric
+        self.layout = layout
+        self.plan = plan
+        self.seed = seed
+        self.node_rank = node_rank
+        self.slab = DeviceSlab(layout, fabric.device)
+        node = {r: n for n, r in node_rank.items()}.get(fabric.rank)
+        self.node = node
+        self.is_source = node is not None and node not in plan.targets()
+        if self.is_source:
+            self.slab.fill_random(seed)
+        torch.cuda.synchronize()
+        self.executor = ScaleExecutor(fabric, plan, self.slab, node_rank, host_cache=host_cache,
+                                      engine=engine, nctas=nctas, fanout_mode=fanout_mode,
+                                      stage_engine=stage_engine)
+        self.receives = self.executor.role.receives
+        self._expected: Optional[torch.Tensor] = None
+
+    def run(self, verify: bool = False, time_kernel: bool = False) -> ScaleUpResult:
+        """Barrier, launch, wait; CUDA-event timed on this rank."""
+        self.fabric.barrier()
+        torch.cuda.synchronize()
+        cur = torch.cuda.current_stream()
+        start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        kev = None
+        if time_kernel:
+            kev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+        start.record(cur)
+        for s in self.executor.streams.values():
+            s.wait_stream(cur)
+        epoch = self.executor.launch(kernel_events=kev)
+        for s in self.executor.streams.values():
+            cur.wait_stream(s)
+        end.record(cur)
+        end.synchronize()
+        res = ScaleUpResult(epoch, start.elapsed_time(end))
+        if kev is not None and self.executor.dominant_stream() is not None:
+            res.kernel_ms = kev[0].elapsed_time(kev[1])
+        if self.receives:
+            res.layer_ms = self.executor.layer_arrivals_ms()
+        if verify:
+            res.verified = self.verify(epoch)
+        return res
+
+    def verify(self, epoch: int) -> bool:
+        """Bit-exactness of this rank's slab: tile fingerprints vs the regenerated
+        source, every tile flag at ``epoch``, every layer tracked."""
+        if not self.receives:
+            return True
+        if self._expected is None:
+            self._expected = expected_fingerprints(self.layout, self.fabric.device, self.seed)
+        ok = torch.equal(self.slab.fingerprints().cpu(), self._expected)
+        ok = ok and int(self.slab.flags.min()) == epoch and int(self.slab.flags.max()) == epoch
+        return ok and int(self.slab.loaded.item()) == self.layout.num_layers
+
+    def close(self):
+        self.executor.close()
+        self.slab.close()

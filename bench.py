@@ -39,6 +39,12 @@ NVLINK_PEAK_GBPS = 770.0     # B200_PROFILING.md: measured peer copy per directi
 NVLINK_NOMINAL_GBPS = 900.0
 PCIE_PEAK_GBPS = 63.0        # PCIe Gen5 x16 per direction, nominal
 METRIC = "scale-up delivered GB/s (Llama-2 7B bf16 shard into every new B200)"
+_T0 = time.perf_counter()
+
+
+def log(msg: str) -> None:
+    print(f"[bench r{os.environ.get('RANK', '0')} +{time.perf_counter() - _T0:7.1f}s] {msg}",
+          file=sys.stderr, flush=True)
 
 
 def parse_args():
@@ -56,6 +62,7 @@ def parse_args():
     p.add_argument("--stage-engine", default="ce", choices=["ce", "sm"])
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--cpu-sample-units", type=int, default=4)
+    p.add_argument("--watchdog-s", type=int, default=900)
     return p.parse_args()
 
 
@@ -251,11 +258,14 @@ def run_blitz(args):
         bound, peak, peak_src = "nvlink", NVLINK_PEAK_GBPS, "B200_PROFILING.md measured peer copy per direction (900 nominal)"
     receivers = len(plan.targets())
     delivered = payload * receivers
+    log(f"plan ready: {[(e.src, e.dst) for e in plan.edges]} fanout {plan.nvlink_fanout}")
     hc = host_cache_for(plan, "value")
+    log("host cache ready" if hc is not None else "no host cache on this rank")
     sess = ScaleUpSession(fabric, layout, plan, node_rank, host_cache=hc, engine=engine,
                           nctas=args.nctas, fanout_mode=args.fanout, seed=seed,
                           stage_engine=args.stage_engine)
 
+    log("session ready")
     # warm-up (first one verified bit-exact on every receiver)
     ok = True
     for w in range(max(args.warmup, 1)):
@@ -263,6 +273,7 @@ def run_blitz(args):
         if w == 0:
             ok = bool(r.verified)
     ok_all = dist_sum(0.0 if ok else 1.0, N) == 0.0
+    log(f"warm-up done, verified={ok_all}")
 
     clocks = ClockSampler(fabric.device)
     fabric.barrier()
@@ -281,6 +292,7 @@ def run_blitz(args):
     torch.cuda.synchronize()
     wall = time.perf_counter() - wall0
     clk = clocks.stop()
+    log(f"timed steps ms={steps} kernel_ms={kern}")
     step_ms = dist_max(steps, N)
     kern_ms = dist_max(kern, N)
     fl = dist_max([statistics.mean(first_layer) if first_layer else 0.0], N)[0]
@@ -300,6 +312,7 @@ def run_blitz(args):
     e2e = None
     if not args.no_e2e:
         e2e_plan, _, _ = plan_for(arch, ["mem0"], gpus)
+        log(f"e2e plan {[(e.src, e.dst) for e in e2e_plan.edges]} fanout {e2e_plan.nvlink_fanout}")
         hc2 = host_cache_for(e2e_plan, "e2e")
         sess2 = ScaleUpSession(fabric, layout, e2e_plan, node_rank, host_cache=hc2, engine=engine,
                                nctas=args.nctas, fanout_mode=args.fanout, seed=seed,
@@ -317,6 +330,7 @@ def run_blitz(args):
             stamps = sess2.slab.stamps.cpu()  # d2h: per-layer arrival stamps
             e2e_t.append(time.perf_counter() - t0)
         e2e_s = dist_max(e2e_t, N)
+        log(f"e2e steps s={e2e_t}")
         e2e_ok = dist_sum(0.0 if sess2.verify(sess2.executor.epoch) else 1.0, N) == 0.0
         h2d = payload  # one shard crosses PCIe per step
         d2h = int(stamps.numel() * 8) * N
@@ -332,7 +346,9 @@ def run_blitz(args):
 
     cpu = None
     if rank == 0:
+        log("cpu baseline")
         cpu = cpu_copy_baseline(plan, layout, args.cpu_sample_units, steps=1)
+        log(f"cpu baseline {cpu['value']:.2f} GB/s")
         cpu.pop("seconds", None)
 
     if rank == 0:
@@ -365,6 +381,8 @@ def run_blitz(args):
 
 def main():
     args = parse_args()
+    import faulthandler
+    faulthandler.dump_traceback_later(args.watchdog_s, exit=True)
     if args.impl == "reference":
         run_reference(args)
     else:

@@ -135,6 +135,10 @@ int bz_publish_layer(uint32_t* loaded, uint32_t value, uint64_t* stamp, void* st
 int bz_wait_layer(const uint32_t* loaded, uint32_t k, void* stream);
 /* Device gate kernel variant of the same (spins with ld.acquire.sys). */
 int bz_wait_flag_kernel(const uint32_t* flag, uint32_t value, void* stream);
+/* Every device-side wait is bounded: after `budget` ns it gives up and counts a
+ * timeout.  Returns the count for the current device (synchronous); a non-zero
+ * budget_ns replaces the budget (default 30 s). */
+int bz_wait_timeouts(uint64_t* count, uint64_t budget_ns);
 
 /* ---- payload + verification ---------------------------------------------------------- */
 /* Deterministic random bits: 64-bit word i = splitmix64(seed + i). */
@@ -147,7 +151,25 @@ int bz_tile_fingerprints(const void* base, const int64_t* tile_off, int t0, int 
 int bz_handoff(const void* src, void* dst, uint64_t bytes, uint32_t* flag, uint32_t value,
                int nctas, void* stream);
 
-/* ---- kernels timed by the caller ----------------------------------------------------- */
+/* ---- tensor-core GEMM (tcgen05 + TMEM + TMA) ----------------------------------------- */
+/* C[M,N] = A[M,K] . B[N,K]^T (+ residual[M,N]), all bf16 row-major, fp32 accumulate in
+ * TMEM.  B is a Linear weight [out, in].  K % 64 == 0, N % 8 == 0, leading dims % 8 == 0,
+ * 16-byte aligned pointers.  residual may be NULL.  max_ctas <= 0: one CTA per SM. */
+int bz_gemm_bf16(const void* A, const void* B, void* C, const void* residual, int M, int N, int K,
+                 int lda, int ldb, int ldc, int ldr, int max_ctas, void* stream);
+
+/* ---- Llama block glue (bf16 in/out, fp32 math) ---------------------------------------- */
+/* y = x * rsqrt(mean(x^2) + eps) * w per row; d % 8 == 0. */
+int bz_rmsnorm(const void* x, const void* w, void* y, int rows, int d, int ldx, int ldy, float eps,
+               void* stream);
+/* In-place rotate-half RoPE on the first n_rot_heads heads of each row of a fused
+ * [q | k | v] projection; positions[rows] int32. */
+int bz_rope(void* qkv, const int32_t* positions, int rows, int n_rot_heads, int head_dim, int ld,
+            float theta, void* stream);
+/* act[:, j] = silu(gu[:, j]) * gu[:, ffn + j]. */
+int bz_silu_mul(const void* gu, void* act, int rows, int ffn, int ldg, int lda, void* stream);
+
+/* ---- misc ------------------------------------------------------------------------------ */
 int bz_sm_count(int dev, int* n);
 
 #ifdef __cplusplus

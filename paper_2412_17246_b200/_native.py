@@ -121,9 +121,14 @@ _SIGNATURES = {
     "bz_publish_layer": [_P, _U32, _P, _P],
     "bz_wait_layer": [_P, _U32, _P],
     "bz_wait_flag_kernel": [_P, _U32, _P],
+    "bz_wait_timeouts": [_PU64, _U64],
     "bz_fill_random": [_P, _U64, _U64, _P],
     "bz_tile_fingerprints": [_P, _P, _I, _I, _P, _P],
     "bz_handoff": [_P, _P, _U64, _P, _U32, _I, _P],
+    "bz_gemm_bf16": [_P, _P, _P, _P, _I, _I, _I, _I, _I, _I, _I, _I, _P],
+    "bz_rmsnorm": [_P, _P, _P, _I, _I, _I, _I, ctypes.c_float, _P],
+    "bz_rope": [_P, _P, _I, _I, _I, _I, ctypes.c_float, _P],
+    "bz_silu_mul": [_P, _P, _I, _I, _I, _I, _P],
     "bz_sm_count": [_I, _PI],
 }
 

@@ -1,0 +1,120 @@
+"""ZigZag cooperative execution on real GPUs (cooperative-executor data path).
+
+Reference: the layer split ``(T_i, S_i)`` of livescale.py:4-14 solved by
+``configure_pipeline`` (livescale.py:113-181) and the target-side order
+rehearsed by ``zigzag_schedule`` (livescale.py:269-346); PAPER.md:585-589,
+786-895.  The reference only rehearses in abstract time units; this module
+executes the rehearsal:
+
+* the **target** (new instance, still receiving its slab) runs batch ``i``'s
+  layers ``1..T_i`` in the rehearsed (batch, layer) order, each gated on the
+  device readiness counter of its landing slab (``bz_wait_layer`` -- a
+  stream-side wait, no spinning kernel), then hands the hidden state to the
+  source (``bz_handoff``: a peer copy + release flag; K5 of SURVEY.md §2.2);
+* the **source** (overloaded instance, full weights) waits for batch ``i``'s
+  hand-off and runs layers ``T_i+1..L`` plus the LM head, FCFS (livescale.py:327-337).
+
+Both instances may share one GPU (two streams, stream-ordered events) or sit
+on two GPUs (handoff over NVLink into the source's buffer, cross-GPU flag).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+from typing import Optional, Sequence
+
+import torch
+
+from ._native import cuda_lib
+from .livescale import PipelineConfig, ZigzagTimeline
+from .llama import LlamaExecutor
+
+
+@dataclass
+class CoopResult:
+    logits: list[torch.Tensor]                 # per batch, fp32 [B, vocab]
+    executed_order: list[tuple[int, int]]      # (batch, layer) as enqueued on the target
+    handoff_bytes: int = 0
+    source_ms: Optional[float] = None
+    total_ms: Optional[float] = None
+
+
+class CooperativePair:
+    """A (source, target) pair on this process's GPU(s).
+
+    ``target_loaded`` is the target slab's device ``loaded_layers`` counter
+    (``DeviceSlab.loaded``): the target's block ``k`` (1-based) is enqueued
+    behind ``bz_wait_layer(target_loaded, k)``.
+    """
+
+    def __init__(self, source: LlamaExecutor, target: LlamaExecutor, target_loaded: torch.Tensor,
+                 handoff_ctas: int = 16):
+        self.src = source
+        self.tgt = target
+        self.loaded = target_loaded
+        self.lib = cuda_lib()
+        self.handoff_ctas = handoff_ctas
+        sdev = source.h.device
+        tdev = target.h.device
+        self.src_stream = torch.cuda.Stream(device=sdev)
+        self.tgt_stream = torch.cuda.Stream(device=tdev)
+        self.flag = torch.zeros(1, dtype=torch.int32, device=sdev)
+        self._handoffs = 0
+
+    @torch.no_grad()
+    def run(self, batches: Sequence[torch.Tensor], config: PipelineConfig,
+            timeline: ZigzagTimeline) -> CoopResult:
+        L = self.src.arch.n_layers
+        n = len(batches)
+        if config.batches != n:
+            raise ValueError("one split per batch")
+        shapes = [tuple(b.shape) for b in batches]
+        pos = [torch.arange(s, dtype=torch.int32, device=b.device).repeat(bsz)
+               for b, (bsz, s) in zip(batches, shapes)]
+        x: list[Optional[torch.Tensor]] = [None] * n
+        handed = [torch.cuda.Event() for _ in range(n)]
+        recv: list[Optional[torch.Tensor]] = [None] * n
+        order: list[tuple[int, int]] = []
+        nbytes = 0
+        start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        cur = torch.cuda.current_stream()
+        start.record(cur)
+        self.tgt_stream.wait_stream(cur)
+        self.src_stream.wait_stream(cur)
+        flag_base = int(self._handoffs)
+
+        # ---- target: the rehearsed zigzag order, gated per layer -------------------------
+        with torch.cuda.stream(self.tgt_stream):
+            for b, layer, _s, _e in timeline.target_intervals:
+                if x[b] is None:
+                    x[b] = self.tgt.embed(batches[b])
+                self.lib.bz_wait_layer(self.loaded.data_ptr(), layer, self.tgt_stream.cuda_stream)
+                x[b] = self.tgt.block(layer - 1, x[b], pos[b], shapes[b])
+                order.append((b, layer))
+                if layer == config.splits[b][0]:
+                    # hand the hidden state to the source (K5)
+                    recv[b] = torch.empty_like(x[b], device=self.src.h.device)
+                    self.lib.bz_handoff(x[b].data_ptr(), recv[b].data_ptr(), x[b].numel() * 2,
+                                        self.flag.data_ptr(), 0, self.handoff_ctas,
+                                        self.tgt_stream.cuda_stream)
+                    self._handoffs += self.handoff_ctas
+                    nbytes += x[b].numel() * 2
+                    handed[b].record(self.tgt_stream)
+
+        # ---- source: suffixes FCFS ---------------------------------------------------------
+        logits: list[Optional[torch.Tensor]] = [None] * n
+        with torch.cuda.stream(self.src_stream):
+            for i in range(n):
+                t_i, s_i = config.splits[i]
+                if t_i == 0:
+                    h = None
+                else:
+                    self.src_stream.wait_event(handed[i])
+                    h = recv[i]
+                logits[i] = self.src.forward(batches[i], first=t_i, last=L, x=h)
+        cur.wait_stream(self.src_stream)
+        cur.wait_stream(self.tgt_stream)
+        end.record(cur)
+        end.synchronize()
+        return CoopResult(logits=logits, executed_order=order, handoff_bytes=nbytes,
+                          total_ms=start.elapsed_time(end))

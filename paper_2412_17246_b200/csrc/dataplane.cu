@@ -67,11 +67,27 @@ __device__ __forceinline__ void mc_st16(int4* p, const int4& v) {
                : "memory");
 }
 
+// Bounded spin: a wait that outlives the budget gives up and counts a timeout
+// in g_wait_timeouts (read by bz_wait_timeouts) instead of hanging the GPU.
+__device__ unsigned long long g_wait_timeouts = 0;
+__constant__ uint64_t c_spin_budget_ns = 30ull * 1000 * 1000 * 1000;
+
+__device__ __forceinline__ bool spin_until_geq(const uint32_t* p, uint32_t v) {
+  if (ld_acquire_sys(p) >= v) return true;
+  const uint64_t t0 = globaltimer();
+  while (ld_acquire_sys(p) < v) {
+    __nanosleep(64);
+    if (globaltimer() - t0 > c_spin_budget_ns) {
+      atomicAdd(&g_wait_timeouts, 1ull);
+      return false;
+    }
+  }
+  return true;
+}
+
 // wait (thread 0) for an upstream tile flag, then release the CTA
 __device__ __forceinline__ void wait_tile(const uint32_t* flags, int t, uint32_t epoch) {
-  if (threadIdx.x == 0) {
-    while (ld_acquire_sys(flags + t) < epoch) __nanosleep(32);
-  }
+  if (threadIdx.x == 0) spin_until_geq(flags + t, epoch);
   __syncthreads();
 }
 
@@ -204,7 +220,7 @@ __global__ void __launch_bounds__(32) k_push_tiles_tma(PushArgs a) {
   uint32_t first = 0;  // running use count of the slot ring (slot = use % kTmaStages)
   for (int t = a.t0 + blockIdx.x; t < a.t1; t += gridDim.x) {
     if (kRelay) {
-      while (ld_acquire_sys(a.wait_flags + t) < a.epoch) __nanosleep(32);
+      spin_until_geq(a.wait_flags + t, a.epoch);
       // relayed bytes arrived through the generic proxy; TMA reads via the async proxy
       asm volatile("fence.proxy.async.global;" ::: "memory");
     }
@@ -253,9 +269,7 @@ __global__ void __launch_bounds__(32) k_track_layers(const uint32_t* flags, cons
                                                      uint64_t* stamps) {
   const int lane = threadIdx.x;
   for (int k = 0; k < nlayers; ++k) {
-    for (int t = layer_tile[k] + lane; t < layer_tile[k + 1]; t += 32) {
-      while (ld_acquire_sys(flags + t) < epoch) __nanosleep(64);
-    }
+    for (int t = layer_tile[k] + lane; t < layer_tile[k + 1]; t += 32) spin_until_geq(flags + t, epoch);
     __syncwarp();
     if (lane == 0) {
       stamps[k] = globaltimer();
@@ -272,9 +286,7 @@ __global__ void k_publish_layer(uint32_t* loaded, uint32_t value, uint64_t* stam
   st_release_sys(loaded, value);
 }
 
-__global__ void k_wait_flag(const uint32_t* flag, uint32_t value) {
-  while (ld_acquire_sys(flag) < value) __nanosleep(64);
-}
+__global__ void k_wait_flag(const uint32_t* flag, uint32_t value) { spin_until_geq(flag, value); }
 
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
@@ -445,6 +457,18 @@ extern "C" int bz_wait_layer(const uint32_t* loaded, uint32_t k, void* stream) {
   CUresult r = d->cuStreamWaitValue32(static_cast<CUstream>(stream), reinterpret_cast<CUdeviceptr>(loaded), k,
                                       CU_STREAM_WAIT_VALUE_GEQ);
   if (r != CUDA_SUCCESS) return bz_fail_cu(r, "cuStreamWaitValue32");
+  return BZ_OK;
+}
+
+extern "C" int bz_wait_timeouts(uint64_t* count, uint64_t budget_ns) {
+  unsigned long long v = 0;
+  cudaError_t e = cudaMemcpyFromSymbol(&v, g_wait_timeouts, sizeof(v));
+  if (e != cudaSuccess) return bz_fail_cuda(e, "read wait timeouts");
+  *count = v;
+  if (budget_ns) {
+    e = cudaMemcpyToSymbol(c_spin_budget_ns, &budget_ns, sizeof(budget_ns));
+    if (e != cudaSuccess) return bz_fail_cuda(e, "set spin budget");
+  }
   return BZ_OK;
 }
 

@@ -434,15 +434,19 @@ class ScaleExecutor:
         dom = self.dominant_stream()
         if kernel_events is not None and dom is not None:
             kernel_events[0].record(st[dom])
-        if self.role.receives and track:
-            # reset loaded_layers and stamp this rank's launch time, then track in order
+        staged = self.role.parent is not None and self.role.parent.startswith("mem")
+        if self.role.receives and (track or staged):
+            # reset loaded_layers and stamp this rank's launch time
+            stream = st["stage"] if staged and self.stage_engine == "ce" else st["track"]
             self.lib.bz_publish_layer(slab.loaded.data_ptr(), 0, slab.stamps.data_ptr()
-                                      + 8 * lay.num_layers, st["track"].cuda_stream)
+                                      + 8 * lay.num_layers, stream.cuda_stream)
+        if staged:
+            self._stage(e)
+        if self.role.receives and track and not (staged and self.stage_engine == "ce"):
+            # a peer (or a staging kernel) produces the tiles: one-warp in-order tracker
             self.lib.bz_track_layers(slab.flags_ptr, slab.layer_tile.data_ptr(), lay.num_layers, e,
                                      slab.loaded.data_ptr(), slab.stamps.data_ptr(),
                                      st["track"].cuda_stream)
-        if self.role.parent is not None and self.role.parent.startswith("mem"):
-            self._stage(e)
         dsts, relay = self._feeds()
         if dsts:
             ptrs = ptr_array([self.peers[n].ptr for n in dsts])
@@ -461,11 +465,19 @@ class ScaleExecutor:
     def kernels_per_launch(self) -> int:
         """Our kernels one ``launch`` enqueues on this rank (CE memcpys excluded)."""
         n = 0
+        staged = self.role.parent is not None and self.role.parent.startswith("mem")
         if self.role.receives:
-            n += 2  # publish + tracker
-        if self.role.parent is not None and self.role.parent.startswith("mem"):
-            n += (self.layout.ntiles + self.tiles_per_copy - 1) // self.tiles_per_copy \
-                if self.stage_engine == "ce" else 1
+            n += 1  # reset/publish
+            if not (staged and self.stage_engine == "ce"):
+                n += 1  # tracker
+        if staged:
+            if self.stage_engine == "ce":
+                lay = self.layout
+                for k in range(lay.num_layers):
+                    t0, t1 = lay.tiles_of_layer(k)
+                    n += (t1 - t0 + self.tiles_per_copy - 1) // self.tiles_per_copy + 1
+            else:
+                n += 1
         if self._unicast_targets():
             n += 1
         if self.fanout_mode == "nvls" and self.role.fanout:
@@ -478,9 +490,15 @@ class ScaleExecutor:
             raise RuntimeError(f"{self.node} is fed by {self.role.parent} but no host cache was given")
         s = self.streams["stage"].cuda_stream
         if self.stage_engine == "ce":
-            self.lib.bz_stage_tiles_ce(hc.ptr, slab.ptr, slab.flags_ptr,
-                                       hc.tile_off_host.ctypes.data, 0, lay.ntiles,
-                                       self.tiles_per_copy, e, s)
+            # copy engines, layer by layer; each layer is published in-stream right
+            # after its last tile (no spinning tracker on a locally produced slab)
+            for k in range(lay.num_layers):
+                t0, t1 = lay.tiles_of_layer(k)
+                self.lib.bz_stage_tiles_ce(hc.ptr, slab.ptr, slab.flags_ptr,
+                                           hc.tile_off_host.ctypes.data, t0, t1,
+                                           self.tiles_per_copy, e, s)
+                self.lib.bz_publish_layer(slab.loaded.data_ptr(), k + 1,
+                                          slab.stamps.data_ptr() + 8 * k, s)
         else:
             self.lib.bz_stage_tiles_sm(hc.ptr, slab.ptr, slab.flags_ptr, slab.tile_off.data_ptr(),
                                        0, lay.ntiles, e, self.nctas, s)

@@ -41,6 +41,25 @@ def plan_for(arch: LlamaArch, sources: Sequence[str], targets: Sequence[str],
     return plan, model, estimate_completion(plan, model, t, eta=1.0)
 
 
+class TransferTimeout(RuntimeError):
+    """A device-side wait gave up (its upstream never published)."""
+
+
+_seen_timeouts = 0
+
+
+def check_wait_timeouts() -> None:
+    global _seen_timeouts
+    import ctypes
+
+    n = ctypes.c_uint64()
+    from ._native import cuda_lib
+    cuda_lib().bz_wait_timeouts(ctypes.byref(n), 0)
+    if n.value > _seen_timeouts:
+        _seen_timeouts = n.value
+        raise TransferTimeout(f"{n.value} device-side waits timed out (upstream never published)")
+
+
 def expected_fingerprints(layout: SlabLayout, device: int, seed: int) -> torch.Tensor:
     """Fingerprints of the synthetic shard made from ``seed`` (regenerated locally)."""
     tmp = DeviceSlab(layout, device)
@@ -99,6 +118,7 @@ class ScaleUpSession:
             cur.wait_stream(s)
         end.record(cur)
         end.synchronize()
+        check_wait_timeouts()
         res = ScaleUpResult(epoch, start.elapsed_time(end))
         if kev is not None and self.executor.dominant_stream() is not None:
             res.kernel_ms = kev[0].elapsed_time(kev[1])

@@ -1,0 +1,73 @@
+"""tcgen05/TMEM/TMA GEMM numerics vs a plain PyTorch fp32 reference.
+
+C = A . B^T with bf16 inputs, fp32 accumulation: compared with the fp32 matmul
+of the same bf16 values; tolerance = bf16 output rounding (rel 1e-2 on the
+max-normalised error) -- the north star's cooperative-logit tolerance.
+"""
+
+import pytest
+import torch
+
+from paper_2412_17246_b200._native import cuda_lib
+
+pytestmark = pytest.mark.gpu
+
+
+def gemm(a, b, residual=None, max_ctas=0):
+    m, k = a.shape
+    n = b.shape[0]
+    c = torch.empty(m, n, dtype=torch.bfloat16, device=a.device)
+    cuda_lib().bz_gemm_bf16(a.data_ptr(), b.data_ptr(), c.data_ptr(),
+                            residual.data_ptr() if residual is not None else None,
+                            m, n, k, a.stride(0), b.stride(0), c.stride(0),
+                            residual.stride(0) if residual is not None else 0, max_ctas,
+                            torch.cuda.current_stream().cuda_stream)
+    return c
+
+
+def _check(c, ref):
+    err = (c.float() - ref).abs().max().item()
+    scale = ref.abs().max().item() + 1e-6
+    assert err / scale < 1e-2, (err, scale)
+
+
+@pytest.mark.parametrize("m,n,k", [
+    (128, 256, 64), (128, 256, 128), (256, 512, 512), (2000, 4096, 4096), (7, 24, 64),
+    (300, 1000, 192), (2000, 12288, 4096), (2000, 4096, 11008), (33, 32000, 256),
+])
+def test_gemm_matches_fp32(m, n, k):
+    torch.manual_seed(m * 7 + n + k)
+    a = (torch.randn(m, k, device="cuda") * 0.5).to(torch.bfloat16)
+    b = (torch.randn(n, k, device="cuda") * 0.02).to(torch.bfloat16)
+    c = gemm(a, b)
+    torch.cuda.synchronize()
+    _check(c, a.float() @ b.float().t())
+
+
+def test_gemm_residual_epilogue():
+    torch.manual_seed(1)
+    a = torch.randn(512, 1024, device="cuda").to(torch.bfloat16)
+    b = (torch.randn(768, 1024, device="cuda") * 0.03).to(torch.bfloat16)
+    r = torch.randn(512, 768, device="cuda").to(torch.bfloat16)
+    c = gemm(a, b, residual=r)
+    torch.cuda.synchronize()
+    _check(c, a.float() @ b.float().t() + r.float())
+
+
+def test_gemm_strided_operands_and_few_ctas():
+    torch.manual_seed(2)
+    big = torch.randn(256, 640, device="cuda").to(torch.bfloat16)
+    a = big[:, 64:576]                      # lda = 640
+    b = (torch.randn(384, 512, device="cuda") * 0.05).to(torch.bfloat16)
+    c = gemm(a, b, max_ctas=3)
+    torch.cuda.synchronize()
+    _check(c, a.float() @ b.float().t())
+
+
+def test_gemm_exact_small_integers():
+    """Integer-valued operands: fp32 accumulation must be exact."""
+    a = torch.randint(-3, 4, (256, 640), device="cuda").to(torch.bfloat16)
+    b = torch.randint(-3, 4, (512, 640), device="cuda").to(torch.bfloat16)
+    c = gemm(a, b)
+    torch.cuda.synchronize()
+    assert torch.equal(c, (a.float() @ b.float().t()).to(torch.bfloat16))

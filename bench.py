@@ -357,8 +357,8 @@ def run_blitz(args):
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "u8", "data": "synthetic",
             "config": {"workload": workload, "model": arch.name, "shard_bytes": payload,
-                       "receivers": receivers, "tile_bytes": layout.tile_off[1] - layout.tile_off[0]
-                       if layout.ntiles else 0, "ntiles": layout.ntiles, "nctas": args.nctas,
+                       "receivers": receivers, "tile_bytes": args.tile_kib * 1024,
+                       "ntiles": int(layout.ntiles), "nctas": args.nctas,
                        "engine": args.engine, "fanout": sess.executor.fanout_mode,
                        "stage_engine": args.stage_engine,
                        "l2": "inputs (13.48 GB shard) exceed the 126 MB L2; no flush needed",

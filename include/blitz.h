@@ -153,7 +153,8 @@ int bz_handoff(const void* src, void* dst, uint64_t bytes, uint32_t* flag, uint3
 
 /* ---- tensor-core GEMM (tcgen05 + TMEM + TMA) ----------------------------------------- */
 /* C[M,N] = A[M,K] . B[N,K]^T (+ residual[M,N]), all bf16 row-major, fp32 accumulate in
- * TMEM.  B is a Linear weight [out, in].  K % 64 == 0, N % 8 == 0, leading dims % 8 == 0,
+ * TMEM.  B is a Linear weight [out, in].  K % 8 == 0 (tails zero-filled by TMA), N % 8 == 0,
+ * leading dims % 8 == 0,
  * 16-byte aligned pointers.  residual may be NULL.  max_ctas <= 0: one CTA per SM. */
 int bz_gemm_bf16(const void* A, const void* B, void* C, const void* residual, int M, int N, int K,
                  int lda, int ldb, int ldc, int ldr, int max_ctas, void* stream);

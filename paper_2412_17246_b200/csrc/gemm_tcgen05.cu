@@ -143,7 +143,7 @@ __global__ void __launch_bounds__(THREADS, 1)
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const int num_tiles = p.m_tiles * p.n_tiles;
-  const int k_blocks = p.K / BK;
+  const int k_blocks = (p.K + BK - 1) / BK;
 
   if (warp == 0 && lane == 0) {
     prefetch_tmap(&map_a);
@@ -311,8 +311,10 @@ extern "C" int bz_gemm_bf16(const void* A, const void* B, void* C, const void* r
                             int lda, int ldb, int ldc, int ldr, int max_ctas, void* stream) {
   using namespace bz::gemm;
   if (!A || !B || !C || M <= 0 || N <= 0 || K <= 0) return bz_fail(BZ_EINVAL, "gemm: bad shape");
-  if (K % BK || lda % 8 || ldb % 8 || ldc % 8 || (residual && ldr % 8) || N % 8)
-    return bz_fail(BZ_EINVAL, "gemm: K must be a multiple of 64, N and leading dims multiples of 8");
+  // K tails are zero-filled by TMA (out-of-bounds box columns), so only the
+  // 16-byte stride/alignment rules of the tensor maps constrain K.
+  if (K % 8 || lda % 8 || ldb % 8 || ldc % 8 || (residual && ldr % 8) || N % 8)
+    return bz_fail(BZ_EINVAL, "gemm: K, N and leading dims must be multiples of 8");
   if ((reinterpret_cast<uintptr_t>(A) | reinterpret_cast<uintptr_t>(B) | reinterpret_cast<uintptr_t>(C)) & 15)
     return bz_fail(BZ_EINVAL, "gemm: operands must be 16-byte aligned");
   CUtensorMap ma, mb;

@@ -34,6 +34,7 @@ def _check(c, ref):
 @pytest.mark.parametrize("m,n,k", [
     (128, 256, 64), (128, 256, 128), (256, 512, 512), (2000, 4096, 4096), (7, 24, 64),
     (300, 1000, 192), (2000, 12288, 4096), (2000, 4096, 11008), (33, 32000, 256),
+    (64, 256, 688), (200, 1376, 256), (129, 264, 40),
 ])
 def test_gemm_matches_fp32(m, n, k):
     torch.manual_seed(m * 7 + n + k)

@@ -61,6 +61,7 @@ def parse_args():
     p.add_argument("--no-group", action="store_true", help="plan chains instead of NVLink fan-out")
     p.add_argument("--stage-engine", default="ce", choices=["ce", "sm"])
     p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg (sweeps only)")
     p.add_argument("--cpu-sample-units", type=int, default=4)
     p.add_argument("--watchdog-s", type=int, default=900)
     return p.parse_args()
@@ -345,7 +346,7 @@ def run_blitz(args):
             hc2.close()
 
     cpu = None
-    if rank == 0:
+    if rank == 0 and not args.no_cpu:
         log("cpu baseline")
         cpu = cpu_copy_baseline(plan, layout, args.cpu_sample_units, steps=1)
         log(f"cpu baseline {cpu['value']:.2f} GB/s")

@@ -54,6 +54,7 @@ def parse_args():
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", default="blitz", choices=["blitz", "reference"])
     p.add_argument("--arch", default="llama2-7b")
+    p.add_argument("--tp", type=int, default=1, help="GPUs per instance (C4: 13B TP=2, C5: 70B TP=4)")
     p.add_argument("--tile-kib", type=int, default=1024)
     p.add_argument("--nctas", type=int, default=32)
     p.add_argument("--engine", default="vector", choices=["vector", "tma"])
@@ -223,14 +224,18 @@ def run_blitz(args):
     from paper_2412_17246_b200 import slab as S
     from paper_2412_17246_b200.dataplane import (ENGINE_TMA, ENGINE_VECTOR, DeviceSlab, Fabric,
                                                  HostCache, plan_roles)
-    from paper_2412_17246_b200.scaleup import ScaleUpSession, plan_for
+    from paper_2412_17246_b200.scaleup import ScaleUpSession, plan_for, rank_plan
 
     fabric = Fabric.from_env()
     N, rank = fabric.world, fabric.rank
     arch = S.ARCHS[args.arch]
-    layout = S.SlabLayout.for_arch(arch, tile_bytes=args.tile_kib * 1024)
+    tp = args.tp
+    if N % tp:
+        raise SystemExit(f"--tp {tp} must divide the GPU count {N}")
+    layout = S.SlabLayout.for_arch(arch, tp=tp, tile_bytes=args.tile_kib * 1024)
     payload = layout.payload_bytes()
     gpus = [f"gpu{i}" for i in range(N)]
+    anchors = gpus[::tp]  # InstanceState.node = gpus[0] (simcore.py:142-144)
     node_rank = {g: i for i, g in enumerate(gpus)}
     engine = ENGINE_TMA if args.engine == "tma" else ENGINE_VECTOR
     seed = 241217
@@ -248,15 +253,17 @@ def run_blitz(args):
         tmp.close()
         return hc
 
-    if N == 1:
-        plan, model, est = plan_for(arch, ["mem0"], ["gpu0"])
-        workload = f"{arch.name} bf16 O(1) pinned host-cache load mem0->gpu0 (copy engines), per-layer readiness"
+    if len(anchors) == 1:
+        anchor_plan, model, est = plan_for(arch, ["mem0"], anchors, tp=tp)
+        workload = (f"{arch.name} bf16 TP={tp} O(1) pinned host-cache load mem0->{anchors} "
+                    f"(copy engines), per-layer readiness")
         bound, peak, peak_src = "pcie", PCIE_PEAK_GBPS, "PCIe Gen5 x16 nominal per direction"
     else:
-        plan, model, est = plan_for(arch, ["gpu0"], gpus[1:], group=not args.no_group)
-        workload = (f"{arch.name} bf16 live scale-up 1->{N}: plan "
-                    f"{[(e.src, e.dst) for e in plan.edges]} fan-out {plan.nvlink_fanout}")
+        anchor_plan, model, est = plan_for(arch, ["gpu0"], anchors[1:], group=not args.no_group, tp=tp)
+        workload = (f"{arch.name} bf16 TP={tp} live scale-up 1->{len(anchors)} instances: anchor plan "
+                    f"{[(e.src, e.dst) for e in anchor_plan.edges]} fan-out {anchor_plan.nvlink_fanout}")
         bound, peak, peak_src = "nvlink", NVLINK_PEAK_GBPS, "B200_PROFILING.md measured peer copy per direction (900 nominal)"
+    plan = rank_plan(anchor_plan, tp)
     receivers = len(plan.targets())
     delivered = payload * receivers
     log(f"plan ready: {[(e.src, e.dst) for e in plan.edges]} fanout {plan.nvlink_fanout}")
@@ -312,7 +319,8 @@ def run_blitz(args):
     # ---- e2e: public API, shard starts in pinned host memory ---------------------------------
     e2e = None
     if not args.no_e2e:
-        e2e_plan, _, _ = plan_for(arch, ["mem0"], gpus)
+        e2e_anchor, _, _ = plan_for(arch, ["mem0"], anchors, tp=tp)
+        e2e_plan = rank_plan(e2e_anchor, tp)
         log(f"e2e plan {[(e.src, e.dst) for e in e2e_plan.edges]} fanout {e2e_plan.nvlink_fanout}")
         hc2 = host_cache_for(e2e_plan, "e2e")
         sess2 = ScaleUpSession(fabric, layout, e2e_plan, node_rank, host_cache=hc2, engine=engine,
@@ -325,7 +333,8 @@ def run_blitz(args):
             fabric.barrier()
             t0 = time.perf_counter()
             # the user's call: plan (reference API) + execute + read readiness back
-            p, _, _ = plan_for(arch, ["mem0"], gpus)
+            p, _, _ = plan_for(arch, ["mem0"], anchors, tp=tp)
+            p = rank_plan(p, tp)
             assert p.edges == e2e_plan.edges and p.nvlink_fanout == e2e_plan.nvlink_fanout
             r = sess2.run()
             stamps = sess2.slab.stamps.cpu()  # d2h: per-layer arrival stamps
@@ -333,11 +342,11 @@ def run_blitz(args):
         e2e_s = dist_max(e2e_t, N)
         log(f"e2e steps s={e2e_t}")
         e2e_ok = dist_sum(0.0 if sess2.verify(sess2.executor.epoch) else 1.0, N) == 0.0
-        h2d = payload  # one shard crosses PCIe per step
+        h2d = payload * tp  # one shard per TP rank crosses PCIe per step
         d2h = int(stamps.numel() * 8) * N
         e2e = {"value": payload * len(e2e_plan.targets()) / statistics.mean(e2e_s) / 1e9,
                "unit": "GB/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-               "workload": f"public API: plan_for(mem0 -> {gpus}) + ScaleUpSession.run() + "
+               "workload": f"public API: plan_for(mem0 -> {anchors}, tp={tp}) + ScaleUpSession.run() + "
                            f"stamp readback; plan {[(e.src, e.dst, e.kind) for e in e2e_plan.edges]}"
                            f" fan-out {e2e_plan.nvlink_fanout}",
                "bit_exact": e2e_ok}
@@ -357,7 +366,7 @@ def run_blitz(args):
             "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": N, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "u8", "data": "synthetic",
-            "config": {"workload": workload, "model": arch.name, "shard_bytes": payload,
+            "config": {"workload": workload, "model": arch.name, "tp": tp, "shard_bytes": payload,
                        "receivers": receivers, "tile_bytes": args.tile_kib * 1024,
                        "ntiles": int(layout.ntiles), "nctas": args.nctas,
                        "engine": args.engine, "fanout": sess.executor.fanout_mode,

@@ -234,6 +234,48 @@ def run_pipeline_case(ss, case):
     return out
 
 
+SIM_TRACES = {
+    "c3-burst": ("burst", {"rate_per_s": 8, "duration_s": 30, "prompt_tokens": [512, 2048],
+                           "output_tokens": [16, 128],
+                           "bursts": [{"start_s": 10, "duration_s": 2, "multiplier": 5}]}, 1),
+    "poisson-small": ("poisson", {"rate_per_s": 6, "duration_s": 12, "prompt_tokens": [128, 1024],
+                                  "output_tokens": [2, 48]}, 3),
+    "burst-heavy": ("burst", {"rate_per_s": 14, "duration_s": 16, "prompt_tokens": [256, 2048],
+                              "output_tokens": [1, 64],
+                              "bursts": [{"start_s": 4, "duration_s": 2, "multiplier": 6}]}, 5),
+}
+
+SIM_CASES = [
+    # (topology doc key, model key, trace key, strategy)
+    ("b200-2x8", "llama2-7b", "c3-burst", "blitz-live"),
+    ("b200-2x8", "llama2-7b", "c3-burst", "blitz-stop"),
+    ("b200-2x8", "llama2-7b", "c3-burst", "allcache"),
+    ("b200-2x8", "llama2-7b", "c3-burst", "sllm"),
+    ("b200-2x8", "llama2-7b", "c3-burst", "static"),
+    ("cluster-A", "llama2-7b", "burst-heavy", "blitz-live"),
+    ("cluster-B", "llama2-7b", "burst-heavy", "blitz-live"),
+    ("cluster-B", "llama2-7b", "poisson-small", "sllm"),
+    ("shared-nic", "llama2-7b", "poisson-small", "blitz-live"),
+    ("b200-hgx", "llama2-7b", "burst-heavy", "blitz-live"),
+    ("p5.48xlarge", "llama2-70b", "c3-burst", "blitz-live"),
+]
+
+
+def run_sim_cases(ss):
+    simcore = importlib.import_module("scalesim.simcore")
+    out = []
+    for topo_key, model_key, trace_key, strategy in SIM_CASES:
+        kind, params, seed = SIM_TRACES[trace_key]
+        trace = ss.generate_trace(kind, params, seed)
+        topo = ss.load_topology(topo_docs()[topo_key])
+        model = ss.ModelSpec(**MODELS[model_key])
+        res = simcore.run_simulation(topo, [model], trace, simcore.SimPolicy(strategy=strategy))
+        summary = json.loads(json.dumps(res.summary()))
+        out.append(dict(topo=topo_key, model=model_key, trace=trace_key, strategy=strategy,
+                        summary=summary, series=json.loads(json.dumps(res.series))))
+    return out
+
+
 def main():
     ss = load_reference()
     OUT.mkdir(parents=True, exist_ok=True)
@@ -259,6 +301,7 @@ def main():
                                       allcache=ss.baseline_load_time("allcache", model, topo,
                                                                      eta=eta)))
     (OUT / "baseline_load.json").write_text(json.dumps(baselines, sort_keys=True))
+    (OUT / "simulations.json").write_text(json.dumps(run_sim_cases(ss), sort_keys=True))
     print(f"wrote {len(plans)} plan cases, {len(pipes)} pipeline cases to {OUT}")
 
 

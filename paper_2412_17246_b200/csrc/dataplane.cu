@@ -60,8 +60,10 @@ __device__ __forceinline__ void st16(int4* p, const int4& v) {
                "r"(v.z), "r"(v.w)
                : "memory");
 }
+// weak multicast store (plain STG.E.128 on the multicast VA); ordering to the
+// tile flag comes from the CTA barrier + fence.sys + release flag store
 __device__ __forceinline__ void mc_st16(int4* p, const int4& v) {
-  asm volatile("multimem.st.relaxed.sys.global.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(p),
+  asm volatile("multimem.st.global.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(p),
                "f"(__int_as_float(v.x)), "f"(__int_as_float(v.y)), "f"(__int_as_float(v.z)),
                "f"(__int_as_float(v.w))
                : "memory");

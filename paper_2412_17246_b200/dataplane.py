@@ -331,6 +331,17 @@ def expand_tp(plan: ScalePlan, tp: int) -> list[ScalePlan]:
     return out
 
 
+def merge_plans(plans: Sequence[ScalePlan]) -> ScalePlan:
+    """Union of node-disjoint per-TP-rank plans; every rank derives its role from it,
+    so collective setup (multicast groups) iterates the same list on every rank."""
+    edges, chains, fan = [], [], {}
+    for p in plans:
+        edges.extend(p.edges)
+        chains.extend(p.chains)
+        fan.update(p.nvlink_fanout)
+    return ScalePlan(edges=edges, chains=chains, nvlink_fanout=fan)
+
+
 # ---- executor -------------------------------------------------------------------------------
 
 
@@ -374,6 +385,7 @@ class ScaleExecutor:
         dev = torch.device("cuda", fabric.device)
         self.streams = {k: torch.cuda.Stream(device=dev) for k in ("copy", "fan", "track", "stage")}
         self.epoch = 0
+        self.writers = self._fanout_writers() if fanout_mode == "nvls" else {}
 
         # every rank exports its slab; peers it sends to are imported
         exports = fabric.allgather((self.node, slab.export()))
@@ -383,20 +395,45 @@ class ScaleExecutor:
             pid, fd, nbytes = exports[r][1]
             self.peers[n] = PeerSlab(fabric.device, pid, fd, nbytes, self.layout)
         fabric.barrier()
-        self.mc: Optional[MulticastGroup] = None
+        self.mc_out: list[MulticastGroup] = []     # groups this rank writes
+        self._mc_all: list[MulticastGroup] = []
         if self.fanout_mode == "nvls":
             # one multicast object per fan-out group, built collectively in plan order
-            for rep, sibs in plan.nvlink_fanout.items():
-                members = [self.node_rank[rep]] + [self.node_rank[s] for s in sibs]
-                grp = MulticastGroup(fabric, slab, members)
-                if self.node == rep:
-                    self.mc = grp
-                elif fabric.rank in members:
-                    self._member_group = grp
+            for rep, (writer, members) in self.writers.items():
+                ranks = [self.node_rank[n] for n in members]
+                grp = MulticastGroup(fabric, slab, ranks)
+                self._mc_all.append(grp)
+                if self.node == writer:
+                    self.mc_out.append(grp)
+
+    def _fanout_writers(self) -> dict[str, tuple[str, list[str]]]:
+        """rep -> (writer, multicast members) for every NVLink fan-out group.
+
+        NVLS replicates a multimem.st to every bound member, the writer included.
+        If the representative is fed over NVLink by a root source (1 -> N on one
+        box: ``gpu0 -> gpu1`` + ``gpu1 => {gpu2..}``), the source writes the group
+        {source, rep, siblings} itself: one stream out of the source, and the echo
+        lands on the source's idle ingress instead of doubling the rep's ingress.
+        Otherwise (rep staged from the host cache over PCIe, or a relayed rep) the
+        rep writes {rep, siblings} as it receives.
+        """
+        out = {}
+        for rep, sibs in self.plan.nvlink_fanout.items():
+            parent = self.roles[rep].parent
+            writer = rep
+            if parent is not None and parent.startswith("gpu"):
+                edge = next(e for e in self.plan.edges if e.dst == rep)
+                prole = self.roles[parent]
+                if edge.kind == "nvlink" and prole.parent is None and prole.rep is None:
+                    writer = parent
+            members = ([writer] if writer != rep else []) + [rep] + list(sibs)
+            out[rep] = (writer, members)
+        return out
 
     # chain children, plus siblings when the fan-out is served by unicast
     def _unicast_targets(self) -> list[str]:
-        out = list(self.role.children)
+        covered = {rep for rep, (w, _) in self.writers.items() if w == self.node and w != rep}
+        out = [c for c in self.role.children if c not in covered]
         if self.fanout_mode == "chain" and self.role.fanout:
             out.append(self.role.fanout[0])
         if self.fanout_mode == "chain" and self.role.rep is not None:
@@ -416,7 +453,7 @@ class ScaleExecutor:
         """Stream of this rank's bulk mover (for per-kernel timing), if any."""
         if self.role.parent is not None and self.role.parent.startswith("mem"):
             return "stage"
-        if self.fanout_mode == "nvls" and self.role.fanout:
+        if self.mc_out:
             return "fan"
         if self._unicast_targets():
             return "copy"
@@ -454,8 +491,8 @@ class ScaleExecutor:
             self.lib.bz_push_tiles(slab.ptr, ptrs, flags, len(dsts),
                                    slab.flags_ptr if relay else None, slab.tile_off.data_ptr(),
                                    0, lay.ntiles, e, self.nctas, self.engine, st["copy"].cuda_stream)
-        if self.fanout_mode == "nvls" and self.role.fanout:
-            self.lib.bz_multicast_tiles(slab.ptr, self.mc.ptr, self.mc.flags_ptr,
+        for grp in self.mc_out:
+            self.lib.bz_multicast_tiles(slab.ptr, grp.ptr, grp.flags_ptr,
                                         slab.flags_ptr if relay else None, slab.tile_off.data_ptr(),
                                         0, lay.ntiles, e, self.nctas, st["fan"].cuda_stream)
         if kernel_events is not None and dom is not None:
@@ -480,9 +517,7 @@ class ScaleExecutor:
                 n += 1
         if self._unicast_targets():
             n += 1
-        if self.fanout_mode == "nvls" and self.role.fanout:
-            n += 1
-        return n
+        return n + len(self.mc_out)
 
     def _stage(self, e: int):
         hc, slab, lay = self.host_cache, self.slab, self.layout
@@ -517,9 +552,8 @@ class ScaleExecutor:
         self.synchronize()
         for p in self.peers.values():
             p.close()
-        for grp in (self.mc, getattr(self, "_member_group", None)):
-            if grp is not None:
-                grp.close()
+        for grp in self._mc_all:
+            grp.close()
 
 
 # ---- loopback (several slabs driven by one process on one GPU) -------------------------------

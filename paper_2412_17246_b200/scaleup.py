@@ -32,13 +32,25 @@ class ScaleUpResult:
 
 def plan_for(arch: LlamaArch, sources: Sequence[str], targets: Sequence[str],
              topo="b200-hgx", group: bool = True, tp: int = 1):
-    """Reference planning path for a real architecture (bytes = real shard size)."""
+    """Reference planning path for a real architecture (bytes = real shard size).
+
+    Sources/targets are instance *anchors* (``InstanceState.node = gpus[0]``,
+    simcore.py:142-144); the returned plan is the anchor plan.  Use
+    ``rank_plan`` to expand it over the TP ranks of every instance.
+    """
     t = load_topology(topo)
     flows = FlowSet(t)
     model = model_spec_for(arch, tp=tp)
     req = build_scale_request(model, list(sources), list(targets), t, flows)
     plan = generate_plan(req, t, flows, group=group)
     return plan, model, estimate_completion(plan, model, t, eta=1.0)
+
+
+def rank_plan(anchor_plan, tp: int):
+    """Per-GPU plan: rank r of every instance talks to rank r of the others."""
+    from .dataplane import expand_tp, merge_plans
+
+    return anchor_plan if tp == 1 else merge_plans(expand_tp(anchor_plan, tp))
 
 
 class TransferTimeout(RuntimeError):

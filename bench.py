@@ -56,7 +56,7 @@ def parse_args():
     p.add_argument("--arch", default="llama2-7b")
     p.add_argument("--tp", type=int, default=1, help="GPUs per instance (C4: 13B TP=2, C5: 70B TP=4)")
     p.add_argument("--tile-kib", type=int, default=1024)
-    p.add_argument("--nctas", type=int, default=32)
+    p.add_argument("--nctas", type=int, default=48)
     p.add_argument("--engine", default="vector", choices=["vector", "tma"])
     p.add_argument("--fanout", default="auto", choices=["auto", "nvls", "chain", "star"])
     p.add_argument("--no-group", action="store_true", help="plan chains instead of NVLink fan-out")

@@ -1,0 +1,98 @@
+"""Measure the B200 costs the serving replay needs (prefill line, layer arrivals).
+
+``measure_prefill`` times real Llama prefill passes of the tcgen05 executor
+(one block at each token count, scaled by the layer count, plus the head), and
+``c3_report`` replays the C3 burst trace through ``simcore`` twice -- with the
+reference's analytic costs and with the measured ones -- for each strategy.
+"""
+
+from __future__ import annotations
+
+import time
+from typing import Optional, Sequence
+
+import torch
+
+from .costs import MeasuredCosts, fit_line
+from .slab import LlamaArch, SlabLayout
+
+
+def measure_prefill(arch: LlamaArch, token_counts: Sequence[int] = (256, 512, 1024, 2048),
+                    seq_len: int = 512, iters: int = 5, device: int = 0) -> dict:
+    """ms of a full-model prefill at each token count (B sequences of <= seq_len)."""
+    from .dataplane import DeviceSlab
+    from .llama import LlamaExecutor, SlabWeights
+
+    probe = LlamaArch(arch.name + "-probe", arch.d_model, 1, arch.n_heads, arch.n_kv_heads,
+                      arch.ffn, arch.vocab, arch.norm_eps, arch.rope_theta)
+    lay = SlabLayout.for_arch(probe, tile_bytes=1 << 20)
+    slab = DeviceSlab(lay, device)
+    w = SlabWeights(probe, lay, slab.data)
+    w.init_random(seed=0)
+    ex = LlamaExecutor(w, max_tokens=max(token_counts), device=torch.device("cuda", device))
+    out = {}
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+    for n in token_counts:
+        s = min(seq_len, n)
+        b = max(1, n // s)
+        toks = torch.randint(0, arch.vocab, (b, s), device=f"cuda:{device}")
+        pos = torch.arange(s, dtype=torch.int32, device=toks.device).repeat(b)
+        x = ex.embed(toks)
+        for _ in range(2):
+            ex.block(0, x, pos, (b, s))
+            ex.head(x, (b, s))
+        torch.cuda.synchronize()
+        ev[0].record()
+        for _ in range(iters):
+            ex.block(0, x, pos, (b, s))
+        ev[1].record()
+        for _ in range(iters):
+            ex.head(x, (b, s))
+        ev[2].record()
+        ev[2].synchronize()
+        block_ms = ev[0].elapsed_time(ev[1]) / iters
+        head_ms = ev[1].elapsed_time(ev[2]) / iters
+        out[b * s] = block_ms * arch.n_layers + head_ms
+    slab.close()
+    return out
+
+
+def build_costs(prefill: Optional[dict] = None, nvlink_layer_ms=None, host_layer_ms=None,
+                source: Optional[dict] = None) -> MeasuredCosts:
+    a = b = None
+    if prefill:
+        xs = sorted(prefill)
+        a, b = fit_line(xs, [prefill[x] for x in xs])
+    return MeasuredCosts(prefill_alpha_ms=a, prefill_beta_ms=b, nvlink_layer_ms=nvlink_layer_ms,
+                         host_layer_ms=host_layer_ms, source=source or {})
+
+
+def c3_report(costs: MeasuredCosts, topo_name: str = "b200-hgx-2x8",
+              strategies: Sequence[str] = ("blitz-live", "blitz-stop", "allcache", "sllm")) -> dict:
+    """C3: Llama-2 7B under the 5x-burst trace; p99 TTFT/TBT with modeled and measured costs."""
+    from . import simcore
+    from .parampool import ModelSpec
+    from .slab import LLAMA2_7B, model_spec_for
+    from .topology import load_topology
+    from .traces import generate_trace
+
+    trace = generate_trace("burst", {"rate_per_s": 20, "duration_s": 30, "prompt_tokens": [512, 2048],
+                                     "output_tokens": [16, 128],
+                                     "bursts": [{"start_s": 10, "duration_s": 2, "multiplier": 5}]},
+                           seed=1)
+    spec = model_spec_for(LLAMA2_7B)
+    topo = load_topology(topo_name)
+    out = {"trace": f"burst 20 req/s x 30 s, 5x for 2 s at t=10 s, seed 1 ({len(trace)} requests)",
+           "topology": topo_name, "model": spec.name, "costs": costs.describe(), "strategies": {}}
+    for strat in strategies:
+        row = {}
+        for label, c in (("modeled", simcore.ReferenceCosts()), ("measured", costs)):
+            t0 = time.perf_counter()
+            res = simcore.run_simulation(topo, [spec], trace, simcore.SimPolicy(strategy=strat), costs=c)
+            s = res.summary()
+            row[label] = {"p99_ttft_ms": s["ttft_ms"]["p99"], "p50_ttft_ms": s["ttft_ms"]["p50"],
+                          "p99_tbt_ms": s["tbt_ms"]["p99"], "slo_attainment": s["slo_attainment"],
+                          "scale_ups": s["counters"]["scale_ups"],
+                          "replay_cpu_s": time.perf_counter() - t0}
+        out["strategies"][strat] = row
+    return out

@@ -380,7 +380,9 @@ class ScaleExecutor:
         self.tiles_per_copy = tiles_per_copy
         self.lib = cuda_lib()
         if fanout_mode == "auto":
-            fanout_mode = "nvls" if fabric.multicast_supported and fabric.world > 1 else "chain"
+            # measured on 4x B200 (profiles/r1_sweep4.txt): a pipelined sibling chain
+            # delivers ~650 GB/s per destination, the NVLS multicast stream ~530 GB/s
+            fanout_mode = "chain"
         self.fanout_mode = fanout_mode
         dev = torch.device("cuda", fabric.device)
         self.streams = {k: torch.cuda.Stream(device=dev) for k in ("copy", "fan", "track", "stage")}

@@ -63,6 +63,7 @@ def parse_args():
     p.add_argument("--stage-engine", default="ce", choices=["ce", "sm"])
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg (sweeps only)")
+    p.add_argument("--no-c3", action="store_true", help="skip the C3 serving replay")
     p.add_argument("--cpu-sample-units", type=int, default=4)
     p.add_argument("--watchdog-s", type=int, default=900)
     return p.parse_args()
@@ -288,6 +289,7 @@ def run_blitz(args):
     torch.cuda.synchronize()
     clocks.start()
     steps, kern, first_layer, last_layer = [], [], [], []
+    layers_value, layers_host = None, None
     wall0 = time.perf_counter()
     for _ in range(args.steps):
         r = sess.run(time_kernel=True)
@@ -296,6 +298,7 @@ def run_blitz(args):
         if r.layer_ms:
             first_layer.append(r.layer_ms[0])
             last_layer.append(r.layer_ms[-1])
+            layers_value = r.layer_ms
     fabric.barrier()
     torch.cuda.synchronize()
     wall = time.perf_counter() - wall0
@@ -339,6 +342,8 @@ def run_blitz(args):
             r = sess2.run()
             stamps = sess2.slab.stamps.cpu()  # d2h: per-layer arrival stamps
             e2e_t.append(time.perf_counter() - t0)
+            if r.layer_ms:
+                layers_host = r.layer_ms
         e2e_s = dist_max(e2e_t, N)
         log(f"e2e steps s={e2e_t}")
         e2e_ok = dist_sum(0.0 if sess2.verify(sess2.executor.epoch) else 1.0, N) == 0.0
@@ -353,6 +358,30 @@ def run_blitz(args):
         sess2.close()
         if hc2 is not None:
             hc2.close()
+
+    # ---- C3: serving replay of the 5x burst with the times measured above -------------------------
+    c3 = None
+    if not args.no_c3 and tp == 1:
+        roles_v = plan_roles(plan)
+        e2e_roles = plan_roles(e2e_plan) if not args.no_e2e else {}
+        mine = {"node": my, "value": layers_value, "host": layers_host,
+                "value_parent": roles_v[my].parent if my in roles_v else None,
+                "host_parent": e2e_roles[my].parent if my in e2e_roles else None}
+        allm = fabric.allgather(mine)
+        if rank == 0:
+            nv = next((m["value"] for m in allm if m["value"] and m["value_parent"] == "gpu0"), None)
+            host = next((m["host"] for m in allm if m["host"] and (m["host_parent"] or "").startswith("mem")),
+                        None)
+            if N == 1 and host is None:
+                host = layers_value
+            from paper_2412_17246_b200.calibrate import build_costs, c3_report, measure_prefill
+            log("c3: measuring prefill")
+            pre = measure_prefill(arch, device=fabric.device)
+            costs = build_costs(prefill=pre, nvlink_layer_ms=nv, host_layer_ms=host,
+                                source={"prefill_points_ms": pre,
+                                        "measured_in": "this bench run"})
+            c3 = c3_report(costs)
+            log(f"c3 done: { {k: v['measured']['p99_ttft_ms'] for k, v in c3['strategies'].items()} }")
 
     cpu = None
     if rank == 0 and not args.no_cpu:
@@ -383,7 +412,7 @@ def run_blitz(args):
                          "frac_of_nominal": (achieved / (NVLINK_NOMINAL_GBPS if bound == "nvlink"
                                                          else PCIE_PEAK_GBPS)) if achieved else None},
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
-            "clocks": clk, "wall_s": wall,
+            "clocks": clk, "wall_s": wall, "c3": c3,
         }
         print(json.dumps(line), flush=True)
     fabric.barrier()

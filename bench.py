@@ -64,6 +64,7 @@ def parse_args():
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg (sweeps only)")
     p.add_argument("--no-c3", action="store_true", help="skip the C3 serving replay")
+    p.add_argument("--no-coop", action="store_true", help="skip the C1 cooperative-execution block")
     p.add_argument("--cpu-sample-units", type=int, default=4)
     p.add_argument("--watchdog-s", type=int, default=900)
     return p.parse_args()
@@ -176,6 +177,132 @@ def cpu_copy_baseline(plan, layout, units: int, steps: int = 1) -> dict:
                       f"to {len(plan.targets())} destination buffer(s)), torch CPU copy_ along "
                       f"the plan edges, best of {steps}",
             "seconds": secs}
+
+
+# ---- decision path (our API) next to the reference's timings ------------------------------------
+
+
+def decision_timings() -> dict:
+    """SURVEY.md §8(d) item 1 on our API (single thread), with the reference's own
+    timings of the same calls (tests/golden/reference_timings.json, measured in the
+    build container by oracle/gen_golden.py -- the reference cannot run on the box)."""
+    import paper_2412_17246_b200 as ss
+    from paper_2412_17246_b200 import simcore
+    from paper_2412_17246_b200.slab import LLAMA2_7B, model_spec_for
+
+    model = model_spec_for(LLAMA2_7B)
+    topo = ss.load_topology("b200-hgx")
+    flows = ss.FlowSet(topo)
+    topo2 = ss.load_topology("b200-hgx-2x8")
+    trace = ss.generate_trace("burst", {"rate_per_s": 20, "duration_s": 30, "prompt_tokens": [512, 2048],
+                                        "output_tokens": [16, 128],
+                                        "bursts": [{"start_s": 10, "duration_s": 2, "multiplier": 5}]}, 1)
+
+    def plan_1to8():
+        req = ss.build_scale_request(model, ["gpu0"], [f"gpu{i}" for i in range(1, 8)], topo, flows)
+        ss.estimate_completion(ss.generate_plan(req, topo, flows), model, topo, eta=1.0)
+
+    def pipeline(n, L):
+        return lambda: ss.zigzag_schedule(ss.configure_pipeline(n, L, 1.0))
+
+    work = {
+        "plan+estimate 1->8 (a1,a4,a6)": plan_1to8,
+        "configure_pipeline+zigzag N=16 L=32 time_l=1 (a17,a19)": pipeline(16, 32),
+        "configure_pipeline+zigzag N=16 L=80 time_l=1 (a17,a19)": pipeline(16, 80),
+        "run_simulation C3 730 req blitz-live (b200 2x8)":
+            lambda: simcore.run_simulation(topo2, [model], trace, simcore.SimPolicy("blitz-live")),
+    }
+    ref_path = ROOT / "tests" / "golden" / "reference_timings.json"
+    ref = json.loads(ref_path.read_text())["seconds"] if ref_path.exists() else {}
+    out = {}
+    for name, fn in work.items():
+        best = float("inf")
+        for _ in range(5):
+            t0 = time.perf_counter()
+            fn()
+            best = min(best, time.perf_counter() - t0)
+        out[name] = {"ours_ms": best * 1e3,
+                     "reference_ms": ref[name] * 1e3 if name in ref else None}
+    return out
+
+
+# ---- C1 cooperative execution (ZigZag) on this GPU vs the CPU fp32 oracle -----------------------
+
+
+def coop_c1(device: int, n_batches: int = 8, seqs: int = 2, seq_len: int = 1000) -> dict:
+    """C1: tiny 4-layer Llama (d=256) scaled 1->2 on one GPU.  The new instance's slab
+    streams in from the pinned host cache (copy engines, per-layer publish) while the
+    pair serves 8 x 2000-token prefill batches with the configure_pipeline split and
+    the zigzag_schedule order; logits vs the fp32 CPU oracle; CPU oracle tokens/s."""
+    import torch
+    import paper_2412_17246_b200 as ss
+    from paper_2412_17246_b200 import slab as S
+    from paper_2412_17246_b200.coop import CooperativePair
+    from paper_2412_17246_b200.dataplane import DeviceSlab, Fabric, HostCache, ScaleExecutor
+    from paper_2412_17246_b200.llama import LlamaExecutor, SlabWeights
+    from oracle.forward_ref import forward_fp32, weights_to_cpu_fp32
+
+    arch = S.TINY_4L
+    lay = S.SlabLayout.for_arch(arch, tile_bytes=256 * 1024)
+    src = DeviceSlab(lay, device)
+    w = SlabWeights(arch, lay, src.data)
+    w.init_random(seed=0)
+    hc = HostCache(lay)
+    hc.tensor.copy_(src.data.cpu())
+    tgt = DeviceSlab(lay, device)
+    fabric = Fabric(device)
+    plan = ss.ScalePlan(edges=[ss.planner.PlanEdge("mem0", "gpu0", 512.0, "pcie")],
+                        chains=[["mem0", "gpu0"]])
+    ex = ScaleExecutor(fabric, plan, tgt, {"gpu0": 0}, host_cache=hc)
+    g = torch.Generator().manual_seed(3)
+    batches = [torch.randint(0, arch.vocab, (seqs, seq_len), generator=g).to(f"cuda:{device}")
+               for _ in range(n_batches)]
+    source = LlamaExecutor(w, max_tokens=seqs * seq_len, device=f"cuda:{device}")
+    target = LlamaExecutor(SlabWeights(arch, lay, tgt.data), max_tokens=seqs * seq_len,
+                           device=f"cuda:{device}")
+    # measured time_l = one unit's load time / one block's execution time
+    ex.launch()
+    ex.synchronize()
+    load_ms = ex.layer_arrivals_ms()
+    pos = torch.arange(seq_len, dtype=torch.int32, device=f"cuda:{device}").repeat(seqs)
+    x = source.embed(batches[0])
+    s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    source.block(0, x, pos, (seqs, seq_len))
+    s0.record()
+    for _ in range(5):
+        source.block(0, x, pos, (seqs, seq_len))
+    s1.record()
+    s1.synchronize()
+    block_ms = s0.elapsed_time(s1) / 5
+    unit_ms = (load_ms[-1] - load_ms[0]) / max(1, arch.n_layers - 1) if arch.n_layers > 1 else load_ms[0]
+    time_l = max(unit_ms, 1e-6) / block_ms
+    cfg = ss.configure_pipeline(n_batches, arch.n_layers, time_l)
+    tl = ss.zigzag_schedule(cfg)
+    pair = CooperativePair(source, target, tgt.loaded)
+    ex.launch()                       # fresh transfer: layers arrive while the pair serves
+    res = pair.run(batches, cfg, tl)
+    ex.synchronize()
+    tokens = n_batches * seqs * seq_len
+    ref_w = weights_to_cpu_fp32(w)
+    torch.set_num_threads(os.cpu_count() or 1)
+    t0 = time.perf_counter()
+    ref0 = forward_fp32(arch, ref_w, batches[0].cpu())
+    cpu_s = time.perf_counter() - t0
+    got = res.logits[0].cpu()
+    rel = float((got - ref0).abs().max() / (ref0.abs().max() + 1e-6))
+    greedy = bool(torch.equal(got.argmax(-1), ref0.argmax(-1)))
+    out = {"workload": f"C1 tiny-4l d=256, 1->2 on one GPU, {n_batches} x {seqs * seq_len}-token prefill "
+                       f"batches served while the new slab streams from the pinned host cache",
+           "time_l_measured": time_l, "splits": cfg.splits, "objective": cfg.objective(),
+           "pair_ms": res.total_ms, "tokens_per_s": tokens / (res.total_ms / 1e3),
+           "handoff_bytes": res.handoff_bytes, "max_rel_err_vs_fp32": rel, "greedy_equal": greedy,
+           "cpu_fp32_oracle_tokens_per_s": seqs * seq_len / cpu_s,
+           "cpu_cores": os.cpu_count()}
+    ex.close()
+    hc.close()
+    tgt.close()
+    src.close()
+    return out
 
 
 # ---- reference arm ------------------------------------------------------------------------------
@@ -315,22 +442,31 @@ def run_blitz(args):
     achieved = payload / (dom_kernel_ms / 1e3) / 1e9 if dom_kernel_ms > 0 else None
     final_ok = sess.verify(sess.executor.epoch)
     final_all = dist_sum(0.0 if final_ok else 1.0, N) == 0.0
-    sess.close()
-    if hc is not None:
-        hc.close()
 
     # ---- e2e: public API, shard starts in pinned host memory ---------------------------------
     e2e = None
+    e2e_plan = None
     if not args.no_e2e:
         e2e_anchor, _, _ = plan_for(arch, ["mem0"], anchors, tp=tp)
         e2e_plan = rank_plan(e2e_anchor, tp)
-        log(f"e2e plan {[(e.src, e.dst) for e in e2e_plan.edges]} fanout {e2e_plan.nvlink_fanout}")
-        hc2 = host_cache_for(e2e_plan, "e2e")
-        sess2 = ScaleUpSession(fabric, layout, e2e_plan, node_rank, host_cache=hc2, engine=engine,
-                               nctas=args.nctas, fanout_mode=args.fanout, seed=seed,
-                               stage_engine=args.stage_engine)
-        for w in range(max(1, min(args.warmup, 2))):
-            sess2.run(verify=(w == 0))
+    reuse = e2e_plan is not None and e2e_plan.edges == plan.edges and \
+        e2e_plan.nvlink_fanout == plan.nvlink_fanout
+    if not reuse:
+        sess.close()
+        if hc is not None:
+            hc.close()
+    if e2e_plan is not None:
+        log(f"e2e plan {[(e.src, e.dst) for e in e2e_plan.edges]} fanout {e2e_plan.nvlink_fanout}"
+            f"{' (same session as value)' if reuse else ''}")
+        if reuse:
+            hc2, sess2 = hc, sess
+        else:
+            hc2 = host_cache_for(e2e_plan, "e2e")
+            sess2 = ScaleUpSession(fabric, layout, e2e_plan, node_rank, host_cache=hc2, engine=engine,
+                                   nctas=args.nctas, fanout_mode=args.fanout, seed=seed,
+                                   stage_engine=args.stage_engine)
+            for w in range(max(1, min(args.warmup, 2))):
+                sess2.run(verify=(w == 0))
         e2e_t = []
         for _ in range(args.steps):
             fabric.barrier()
@@ -363,7 +499,7 @@ def run_blitz(args):
     c3 = None
     if not args.no_c3 and tp == 1:
         roles_v = plan_roles(plan)
-        e2e_roles = plan_roles(e2e_plan) if not args.no_e2e else {}
+        e2e_roles = plan_roles(e2e_plan) if e2e_plan is not None else {}
         mine = {"node": my, "value": layers_value, "host": layers_host,
                 "value_parent": roles_v[my].parent if my in roles_v else None,
                 "host_parent": e2e_roles[my].parent if my in e2e_roles else None}
@@ -382,6 +518,13 @@ def run_blitz(args):
                                         "measured_in": "this bench run"})
             c3 = c3_report(costs)
             log(f"c3 done: { {k: v['measured']['p99_ttft_ms'] for k, v in c3['strategies'].items()} }")
+
+    decisions = decision_timings() if rank == 0 else None
+    coop = None
+    if rank == 0 and not args.no_coop:
+        log("c1 cooperative execution")
+        coop = coop_c1(fabric.device)
+        log(f"c1 done {coop['tokens_per_s']:.0f} tok/s rel_err {coop['max_rel_err_vs_fp32']:.2e}")
 
     cpu = None
     if rank == 0 and not args.no_cpu:
@@ -412,7 +555,7 @@ def run_blitz(args):
                          "frac_of_nominal": (achieved / (NVLINK_NOMINAL_GBPS if bound == "nvlink"
                                                          else PCIE_PEAK_GBPS)) if achieved else None},
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
-            "clocks": clk, "wall_s": wall, "c3": c3,
+            "clocks": clk, "wall_s": wall, "c3": c3, "decisions": decisions, "coop_c1": coop,
         }
         print(json.dumps(line), flush=True)
     fabric.barrier()

@@ -276,6 +276,50 @@ def run_sim_cases(ss):
     return out
 
 
+def decision_workloads(ss, simcore_mod):
+    """The reference decision-path items of SURVEY.md §8(d) item 1, as callables
+    (used both to time the reference here and our package on the GPU box)."""
+    b200 = topo_docs()["b200-hgx"]
+    model = ss.ModelSpec(**MODELS["llama2-7b-real"])
+    topo = ss.load_topology(b200)
+    flows = ss.FlowSet(topo)
+    kind, params, seed = SIM_TRACES["c3-burst"]
+    trace = ss.generate_trace(kind, {**params, "rate_per_s": 20}, seed)
+    topo2 = ss.load_topology(topo_docs()["b200-2x8"])
+    targets = [f"gpu{i}" for i in range(1, 8)]
+
+    def plan_1to8():
+        req = ss.build_scale_request(model, ["gpu0"], targets, topo, flows)
+        plan = ss.generate_plan(req, topo, flows)
+        ss.estimate_completion(plan, model, topo, eta=1.0)
+
+    def pipeline(n, L, tl):
+        def f():
+            cfg = ss.configure_pipeline(n, L, tl)
+            ss.zigzag_schedule(cfg)
+        return f
+
+    def sim():
+        simcore_mod.run_simulation(topo2, [model], trace, simcore_mod.SimPolicy(strategy="blitz-live"))
+
+    return {
+        "plan+estimate 1->8 (a1,a4,a6)": plan_1to8,
+        "configure_pipeline+zigzag N=16 L=32 time_l=1 (a17,a19)": pipeline(16, 32, 1.0),
+        "configure_pipeline+zigzag N=16 L=80 time_l=1 (a17,a19)": pipeline(16, 80, 1.0),
+        "run_simulation C3 730 req blitz-live (b200 2x8)": sim,
+    }
+
+
+def time_best(fn, reps=5):
+    import time as _t
+    best = math.inf
+    for _ in range(reps):
+        t0 = _t.perf_counter()
+        fn()
+        best = min(best, _t.perf_counter() - t0)
+    return best
+
+
 def main():
     ss = load_reference()
     OUT.mkdir(parents=True, exist_ok=True)
@@ -302,6 +346,14 @@ def main():
                                                                      eta=eta)))
     (OUT / "baseline_load.json").write_text(json.dumps(baselines, sort_keys=True))
     (OUT / "simulations.json").write_text(json.dumps(run_sim_cases(ss), sort_keys=True))
+    import os
+    timings = {name: time_best(fn) for name, fn in
+               decision_workloads(ss, importlib.import_module("scalesim.simcore")).items()}
+    (OUT / "reference_timings.json").write_text(json.dumps({
+        "what": "reference scalesim decision path, best of 5, single thread (GIL), this build container",
+        "cpu": open("/proc/cpuinfo").read().split("model name")[1].split("\n")[0].strip(": ")
+        if os.path.exists("/proc/cpuinfo") else "?",
+        "seconds": timings}, indent=1, sort_keys=True))
     print(f"wrote {len(plans)} plan cases, {len(pipes)} pipeline cases to {OUT}")
 
 

@@ -17,6 +17,7 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 #include "../../include/blitz.h"
 #include "common.cuh"
@@ -25,17 +26,28 @@ namespace bz {
 namespace gemm {
 
 constexpr int BM = 128;
-constexpr int BN = 256;
 constexpr int BK = 64;  // 64 bf16 = 128 B = one swizzle-128B row
-constexpr int STAGES = 4;
 constexpr int UMMA_K = 16;
 constexpr int A_BYTES = BM * BK * 2;  // 16 KiB
-constexpr int B_BYTES = BN * BK * 2;  // 32 KiB
-constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-constexpr int ACC_COLS = BN;          // fp32 accumulator columns per buffer
-constexpr int TMEM_COLS = 2 * ACC_COLS;
 constexpr int THREADS = 256;
-constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align slack*/ + 256 /*barriers*/;
+constexpr int SMEM_LIMIT = 232448;    // 227 KiB dynamic shared memory per CTA
+
+// Tile width N is a template parameter (128 / 192 / 256): the host picks the one
+// that best fills 148 SMs for the problem's tile count; narrower tiles leave room
+// for a deeper smem ring.
+template <int BN_>
+struct Cfg {
+  static constexpr int BN = BN_;
+  static constexpr int B_BYTES = BN * BK * 2;
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int STAGES_FIT = (SMEM_LIMIT - 2048) / STAGE_BYTES;
+  static constexpr int STAGES = STAGES_FIT > 8 ? 8 : STAGES_FIT;
+  static constexpr int ACC_COLS = BN;  // fp32 accumulator columns per buffer
+  static constexpr int TMEM_COLS = 2 * BN <= 256 ? 256 : 512;  // power-of-two allocation
+  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align slack*/ + 256 /*barriers*/;
+  static_assert(BN % 32 == 0 && BN <= 256, "tile N");
+  static_assert(SMEM_BYTES <= SMEM_LIMIT, "smem");
+};
 
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
@@ -128,8 +140,12 @@ struct Params {
   int m_tiles, n_tiles;
 };
 
+template <int BN_>
 __global__ void __launch_bounds__(THREADS, 1)
     k_gemm_bf16(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b, Params p) {
+  using C = Cfg<BN_>;
+  constexpr int BN = C::BN, STAGES = C::STAGES, B_BYTES = C::B_BYTES, STAGE_BYTES = C::STAGE_BYTES;
+  constexpr int ACC_COLS = C::ACC_COLS, TMEM_COLS = C::TMEM_COLS;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sa = smem;                         // STAGES x A tiles
@@ -302,6 +318,65 @@ static int encode_kmajor(CUtensorMap* map, const void* ptr, int rows, int k, int
   return BZ_OK;
 }
 
+// BZ_GEMM_BN=128|192|256 pins the tile width (tests/benchmarks); 0 = automatic
+static int bn_override() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("BZ_GEMM_BN");
+    v = e ? atoi(e) : 0;
+    if (v != 128 && v != 192 && v != 256) v = 0;
+  }
+  return v;
+}
+
+// Tile width for a problem: maximise (useful columns / padded columns) x
+// (tiles / (waves x SMs)) x a small per-width efficiency prior.
+static int pick_bn(int M, int N, int ctas) {
+  const int widths[3] = {256, 192, 128};
+  const double prior[3] = {1.0, 0.985, 0.95};
+  int best = 256;
+  double best_score = -1.0;
+  const int mt = (M + BM - 1) / BM;
+  for (int i = 0; i < 3; ++i) {
+    const int bn = widths[i];
+    const int nt = (N + bn - 1) / bn;
+    const long tiles = static_cast<long>(mt) * nt;
+    const long waves = (tiles + ctas - 1) / ctas;
+    const double fill = static_cast<double>(tiles) / static_cast<double>(waves * ctas);
+    const double cols = static_cast<double>(N) / (static_cast<double>(nt) * bn);
+    const double score = fill * cols * prior[i];
+    if (score > best_score + 1e-9) {
+      best_score = score;
+      best = bn;
+    }
+  }
+  return best;
+}
+
+template <int BN_>
+static int launch(const CUtensorMap& ma, const void* B, int N, int K, int ldb, Params p, int max_ctas,
+                  cudaStream_t stream) {
+  using Cf = Cfg<BN_>;
+  CUtensorMap mb;
+  if (int rc = encode_kmajor(&mb, B, N, K, ldb, BN_)) return rc;
+  p.n_tiles = (N + BN_ - 1) / BN_;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  int grid = p.m_tiles * p.n_tiles;
+  const int cap = max_ctas > 0 ? tmin(max_ctas, sms) : sms;
+  if (grid > cap) grid = cap;
+  static bool attr_set[64] = {};
+  if (dev < 64 && !attr_set[dev]) {
+    cudaError_t e =
+        cudaFuncSetAttribute(k_gemm_bf16<BN_>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cf::SMEM_BYTES);
+    if (e != cudaSuccess) return bz_fail_cuda(e, "gemm smem attribute");
+    attr_set[dev] = true;
+  }
+  k_gemm_bf16<BN_><<<grid, THREADS, Cf::SMEM_BYTES, stream>>>(ma, mb, p);
+  return bz_check_launch("bz_gemm_bf16");
+}
+
 }  // namespace gemm
 }  // namespace bz
 
@@ -317,9 +392,12 @@ extern "C" int bz_gemm_bf16(const void* A, const void* B, void* C, const void* r
     return bz_fail(BZ_EINVAL, "gemm: K, N and leading dims must be multiples of 8");
   if ((reinterpret_cast<uintptr_t>(A) | reinterpret_cast<uintptr_t>(B) | reinterpret_cast<uintptr_t>(C)) & 15)
     return bz_fail(BZ_EINVAL, "gemm: operands must be 16-byte aligned");
-  CUtensorMap ma, mb;
+  CUtensorMap ma;
   if (int rc = encode_kmajor(&ma, A, M, K, lda, BM)) return rc;
-  if (int rc = encode_kmajor(&mb, B, N, K, ldb, BN)) return rc;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int ctas = max_ctas > 0 ? tmin(max_ctas, sms) : sms;
   Params p;
   p.C = static_cast<__nv_bfloat16*>(C);
   p.R = static_cast<const __nv_bfloat16*>(residual);
@@ -329,19 +407,16 @@ extern "C" int bz_gemm_bf16(const void* A, const void* B, void* C, const void* r
   p.ldc = ldc;
   p.ldr = ldr;
   p.m_tiles = (M + BM - 1) / BM;
-  p.n_tiles = (N + BN - 1) / BN;
-  int dev = 0, sms = 148;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  int grid = p.m_tiles * p.n_tiles;
-  const int cap = max_ctas > 0 ? tmin(max_ctas, sms) : sms;
-  if (grid > cap) grid = cap;
-  static bool attr_set[64] = {};
-  if (dev < 64 && !attr_set[dev]) {
-    cudaError_t e = cudaFuncSetAttribute(k_gemm_bf16, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
-    if (e != cudaSuccess) return bz_fail_cuda(e, "gemm smem attribute");
-    attr_set[dev] = true;
+  p.n_tiles = 0;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const int forced = bn_override();
+  const int bn = forced ? forced : pick_bn(M, N, ctas);
+  switch (bn) {
+    case 128:
+      return launch<128>(ma, B, N, K, ldb, p, max_ctas, s);
+    case 192:
+      return launch<192>(ma, B, N, K, ldb, p, max_ctas, s);
+    default:
+      return launch<256>(ma, B, N, K, ldb, p, max_ctas, s);
   }
-  k_gemm_bf16<<<grid, THREADS, SMEM_BYTES, static_cast<cudaStream_t>(stream)>>>(ma, mb, p);
-  return bz_check_launch("bz_gemm_bf16");
 }

@@ -1,0 +1,80 @@
+"""Multi-process (one process per GPU) parity of the data plane.
+
+GPU path: spawns ``torchrun`` over every visible GPU (needs >= 2) running
+scripts/mgpu_check.py -- grouped/NVLS, grouped/chain, chain (vector + TMA
+engines) and host-cache fan-out plans, each verified bit-exact on every
+receiver.  CPU path: the control plane (fd-exchange allgather, barriers, role
+derivation) over a 2-process gloo group.
+"""
+
+import json
+import os
+import subprocess
+import sys
+from pathlib import Path
+
+import pytest
+
+ROOT = Path(__file__).resolve().parent.parent
+
+
+def _gpus():
+    try:
+        import torch
+        return torch.cuda.device_count() if torch.cuda.is_available() else 0
+    except Exception:
+        return 0
+
+
+@pytest.mark.gpu
+@pytest.mark.multigpu
+@pytest.mark.skipif(_gpus() < 2, reason="needs >= 2 GPUs")
+def test_torchrun_scaleup_bit_exact():
+    n = min(_gpus(), 8)
+    env = dict(os.environ, BZ_WATCHDOG_S="240")
+    proc = subprocess.run(
+        [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+         "--master-addr", "127.0.0.1", "--master-port", "29651", str(ROOT / "scripts" / "mgpu_check.py")],
+        capture_output=True, text=True, timeout=600, env=env, cwd=str(ROOT))
+    lines = [json.loads(l) for l in proc.stdout.splitlines() if l.startswith("{")]
+    assert proc.returncode == 0, proc.stdout[-2000:] + proc.stderr[-3000:]
+    assert len(lines) == 5 and all(l["ok"] for l in lines), lines
+
+
+_WORKER = r"""
+import os, sys, json
+sys.path.insert(0, {root!r})
+import torch.distributed as dist
+dist.init_process_group("gloo", rank=int(sys.argv[1]), world_size=2,
+                        init_method="tcp://127.0.0.1:29652")
+import paper_2412_17246_b200 as ss
+from paper_2412_17246_b200 import slab as S
+from paper_2412_17246_b200.dataplane import plan_roles
+from paper_2412_17246_b200.scaleup import plan_for, rank_plan
+# every rank derives the same plan and roles, and the allgather carries (pid, fd)
+plan, _, _ = plan_for(S.LLAMA2_13B, ["gpu0"], ["gpu2", "gpu4", "gpu6"], tp=2)
+per_rank = rank_plan(plan, 2)
+roles = plan_roles(per_rank)
+out = [None, None]
+dist.all_gather_object(out, (os.getpid(), 100 + dist.get_rank(), sorted(roles)))
+dist.barrier()
+if dist.get_rank() == 0:
+    print(json.dumps({{"pids": [o[0] for o in out], "fds": [o[1] for o in out],
+                      "roles_equal": out[0][2] == out[1][2],
+                      "edges": [(e.src, e.dst) for e in per_rank.edges],
+                      "fanout": per_rank.nvlink_fanout}}))
+dist.destroy_process_group()
+"""
+
+
+def test_control_plane_two_process_gloo(tmp_path):
+    script = tmp_path / "w.py"
+    script.write_text(_WORKER.format(root=str(ROOT)))
+    procs = [subprocess.Popen([sys.executable, str(script), str(r)], stdout=subprocess.PIPE,
+                              stderr=subprocess.PIPE, text=True) for r in range(2)]
+    outs = [p.communicate(timeout=120) for p in procs]
+    assert all(p.returncode == 0 for p in procs), [o[1][-1500:] for o in outs]
+    res = json.loads(outs[0][0].strip().splitlines()[-1])
+    assert res["roles_equal"] and len(set(res["pids"])) == 2 and res["fds"] == [100, 101]
+    assert res["edges"] == [["gpu0", "gpu2"], ["gpu1", "gpu3"]]
+    assert res["fanout"] == {"gpu2": ["gpu4", "gpu6"], "gpu3": ["gpu5", "gpu7"]}

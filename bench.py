@@ -290,12 +290,18 @@ def coop_c1(device: int, n_batches: int = 8, seqs: int = 2, seq_len: int = 1000)
     cpu_s = time.perf_counter() - t0
     got = res.logits[0].cpu()
     rel = float((got - ref0).abs().max() / (ref0.abs().max() + 1e-6))
-    greedy = bool(torch.equal(got.argmax(-1), ref0.argmax(-1)))
+    # greedy tokens must agree wherever the oracle's top-2 margin exceeds the tolerance
+    top2 = ref0.topk(2, dim=-1).values
+    decisive = (top2[:, 0] - top2[:, 1]) > 2e-2 * ref0.abs().max()
+    greedy = bool(torch.equal(got.argmax(-1)[decisive], ref0.argmax(-1)[decisive]))
+    ties = int((~decisive).sum())
     out = {"workload": f"C1 tiny-4l d=256, 1->2 on one GPU, {n_batches} x {seqs * seq_len}-token prefill "
                        f"batches served while the new slab streams from the pinned host cache",
            "time_l_measured": time_l, "splits": cfg.splits, "objective": cfg.objective(),
            "pair_ms": res.total_ms, "tokens_per_s": tokens / (res.total_ms / 1e3),
-           "handoff_bytes": res.handoff_bytes, "max_rel_err_vs_fp32": rel, "greedy_equal": greedy,
+           "handoff_bytes": res.handoff_bytes, "max_rel_err_vs_fp32": rel,
+           "greedy_equal_where_decisive": greedy, "near_tie_rows": ties,
+           "rows": int(ref0.shape[0]),
            "cpu_fp32_oracle_tokens_per_s": seqs * seq_len / cpu_s,
            "cpu_cores": os.cpu_count()}
     ex.close()

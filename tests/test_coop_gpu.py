@@ -82,6 +82,41 @@ def test_zigzag_split_matches_oracle(model, n, time_l):
     tgt.close()
 
 
+@pytest.mark.multigpu
+@pytest.mark.skipif(torch.cuda.device_count() < 2, reason="needs 2 GPUs")
+def test_cross_gpu_zigzag_handoff_over_nvlink(model):
+    """Source on cuda:0, target on cuda:1 loading from the host cache; the hidden
+    states cross NVLink through bz_handoff (peer access), logits vs the oracle."""
+    from paper_2412_17246_b200._native import cuda_lib
+    lay, src, w, ref_w = model
+    lib = cuda_lib()
+    lib.bz_enable_peer_mesh(0)
+    lib.bz_enable_peer_mesh(1)
+    hc = HostCache(lay)
+    hc.tensor.copy_(src.data.cpu())
+    with torch.cuda.device(1):
+        tgt = DeviceSlab(lay, 1)
+        plan = ss.ScalePlan(edges=[ss.planner.PlanEdge("mem0", "gpu1", 512.0, "pcie")],
+                            chains=[["mem0", "gpu1"]])
+        ex = ScaleExecutor(Fabric(1), plan, tgt, {"gpu1": 0}, host_cache=hc)
+        target = LlamaExecutor(SlabWeights(ARCH, lay, tgt.data), max_tokens=64, device="cuda:1")
+    source = LlamaExecutor(w, max_tokens=64, device="cuda:0")
+    cfg = ss.configure_pipeline(4, ARCH.n_layers, 1.0)
+    tl = ss.zigzag_schedule(cfg)
+    pair = CooperativePair(source, target, tgt.loaded)
+    batches = _tokens(4, 2, 32, 13)
+    with torch.cuda.device(1):
+        ex.launch()
+    res = pair.run(batches, cfg, tl)
+    ex.synchronize()
+    for b, logits in zip(batches, res.logits):
+        assert logits.device.index == 0
+        _check_logits(logits, forward_fp32(ARCH, ref_w, b.cpu()))
+    ex.close()
+    hc.close()
+    tgt.close()
+
+
 def test_serving_overlaps_host_staging(model):
     """Target slab streams in from the pinned host cache (copy engines, per-layer
     publish) while the cooperative pair is already executing layer-gated work."""

@@ -158,6 +158,13 @@ int bz_handoff(const void* src, void* dst, uint64_t bytes, uint32_t* flag, uint3
  * 16-byte aligned pointers.  residual may be NULL.  max_ctas <= 0: one CTA per SM. */
 int bz_gemm_bf16(const void* A, const void* B, void* C, const void* residual, int M, int N, int K,
                  int lda, int ldb, int ldc, int ldr, int max_ctas, void* stream);
+/* Fused GEMM -> hand-off: same GEMM, C may be a peer (NVLink) mapping of the
+ * receiving instance's buffer; every CTA, after storing its tiles, adds 1 to
+ * *signal with a system-scope release.  *ctas_out = number of CTAs launched, so
+ * the receiver gates on (*signal >= previous + ctas_out) (bz_wait_layer). */
+int bz_gemm_bf16_signal(const void* A, const void* B, void* C, const void* residual, int M, int N,
+                        int K, int lda, int ldb, int ldc, int ldr, int max_ctas, uint32_t* signal,
+                        int* ctas_out, void* stream);
 
 /* ---- Llama block glue (bf16 in/out, fp32 math) ---------------------------------------- */
 /* y = x * rsqrt(mean(x^2) + eps) * w per row; d % 8 == 0. */

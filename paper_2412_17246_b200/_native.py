@@ -126,6 +126,7 @@ _SIGNATURES = {
     "bz_tile_fingerprints": [_P, _P, _I, _I, _P, _P],
     "bz_handoff": [_P, _P, _U64, _P, _U32, _I, _P],
     "bz_gemm_bf16": [_P, _P, _P, _P, _I, _I, _I, _I, _I, _I, _I, _I, _P],
+    "bz_gemm_bf16_signal": [_P, _P, _P, _P, _I, _I, _I, _I, _I, _I, _I, _I, _P, _PI, _P],
     "bz_rmsnorm": [_P, _P, _P, _I, _I, _I, _I, ctypes.c_float, _P],
     "bz_rope": [_P, _P, _I, _I, _I, _I, ctypes.c_float, _P],
     "bz_silu_mul": [_P, _P, _I, _I, _I, _I, _P],

@@ -48,12 +48,15 @@ class CooperativePair:
     """
 
     def __init__(self, source: LlamaExecutor, target: LlamaExecutor, target_loaded: torch.Tensor,
-                 handoff_ctas: int = 16):
+                 handoff_ctas: int = 16, fused_handoff: bool = True):
         self.src = source
         self.tgt = target
         self.loaded = target_loaded
         self.lib = cuda_lib()
         self.handoff_ctas = handoff_ctas
+        # fused: the target's last down-projection GEMM stores straight into the
+        # source's buffer (peer mapping) and signals; otherwise a bz_handoff copy
+        self.fused = fused_handoff
         sdev = source.h.device
         tdev = target.h.device
         self.src_stream = torch.cuda.Stream(device=sdev)
@@ -72,8 +75,12 @@ class CooperativePair:
         pos = [torch.arange(s, dtype=torch.int32, device=b.device).repeat(bsz)
                for b, (bsz, s) in zip(batches, shapes)]
         x: list[Optional[torch.Tensor]] = [None] * n
-        handed = [torch.cuda.Event() for _ in range(n)]
+        handed_at = [0] * n          # cumulative signal value that releases batch i
         recv: list[Optional[torch.Tensor]] = [None] * n
+        for i, (t_i, _) in enumerate(config.splits):
+            if t_i > 0:  # receive buffers live with the source
+                recv[i] = torch.empty(batches[i].numel(), self.src.arch.d_model,
+                                      dtype=torch.bfloat16, device=self.src.h.device)
         order: list[tuple[int, int]] = []
         nbytes = 0
         start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -81,27 +88,30 @@ class CooperativePair:
         start.record(cur)
         self.tgt_stream.wait_stream(cur)
         self.src_stream.wait_stream(cur)
-        flag_base = int(self._handoffs)
-
         # ---- target: the rehearsed zigzag order, gated per layer -------------------------
         with torch.cuda.stream(self.tgt_stream):
             for b, layer, _s, _e in timeline.target_intervals:
                 if x[b] is None:
                     x[b] = self.tgt.embed(batches[b])
                 self.lib.bz_wait_layer(self.loaded.data_ptr(), layer, self.tgt_stream.cuda_stream)
-                x[b] = self.tgt.block(layer - 1, x[b], pos[b], shapes[b])
+                last = layer == config.splits[b][0]
+                if last and self.fused:
+                    # K5 fused into the GEMM epilogue: tiles land in the source's buffer
+                    self.tgt.block(layer - 1, x[b], pos[b], shapes[b], out=recv[b], signal=self.flag)
+                    self._handoffs += self.tgt.last_signal_ctas
+                else:
+                    x[b] = self.tgt.block(layer - 1, x[b], pos[b], shapes[b])
+                    if last:
+                        self.lib.bz_handoff(x[b].data_ptr(), recv[b].data_ptr(), x[b].numel() * 2,
+                                            self.flag.data_ptr(), 0, self.handoff_ctas,
+                                            self.tgt_stream.cuda_stream)
+                        self._handoffs += self.handoff_ctas
                 order.append((b, layer))
-                if layer == config.splits[b][0]:
-                    # hand the hidden state to the source (K5)
-                    recv[b] = torch.empty_like(x[b], device=self.src.h.device)
-                    self.lib.bz_handoff(x[b].data_ptr(), recv[b].data_ptr(), x[b].numel() * 2,
-                                        self.flag.data_ptr(), 0, self.handoff_ctas,
-                                        self.tgt_stream.cuda_stream)
-                    self._handoffs += self.handoff_ctas
-                    nbytes += x[b].numel() * 2
-                    handed[b].record(self.tgt_stream)
+                if last:
+                    nbytes += recv[b].numel() * 2
+                    handed_at[b] = self._handoffs
 
-        # ---- source: suffixes FCFS ---------------------------------------------------------
+        # ---- source: suffixes FCFS, each gated on its hand-off counter -----------------------
         logits: list[Optional[torch.Tensor]] = [None] * n
         with torch.cuda.stream(self.src_stream):
             for i in range(n):
@@ -109,7 +119,8 @@ class CooperativePair:
                 if t_i == 0:
                     h = None
                 else:
-                    self.src_stream.wait_event(handed[i])
+                    self.lib.bz_wait_layer(self.flag.data_ptr(), handed_at[i],
+                                           self.src_stream.cuda_stream)
                     h = recv[i]
                 logits[i] = self.src.forward(batches[i], first=t_i, last=L, x=h)
         cur.wait_stream(self.src_stream)

@@ -138,6 +138,7 @@ struct Params {
   const __nv_bfloat16* R;  // optional residual added in the epilogue (same layout as C)
   int M, N, K, ldc, ldr;
   int m_tiles, n_tiles;
+  uint32_t* signal;  // optional: +1 (release, system scope) per CTA when its tiles are stored
 };
 
 template <int BN_>
@@ -301,6 +302,11 @@ __global__ void __launch_bounds__(THREADS, 1)
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "n"(TMEM_COLS));
   }
+  if (p.signal != nullptr && threadIdx.x == 0) {
+    // fused hand-off: C may be a peer (NVLink) mapping; publish this CTA's tiles
+    __threadfence_system();
+    asm volatile("red.release.sys.global.add.u32 [%0], 1;" ::"l"(p.signal) : "memory");
+  }
 }
 
 static int encode_kmajor(CUtensorMap* map, const void* ptr, int rows, int k, int ld, int box_rows) {
@@ -355,7 +361,7 @@ static int pick_bn(int M, int N, int ctas) {
 
 template <int BN_>
 static int launch(const CUtensorMap& ma, const void* B, int N, int K, int ldb, Params p, int max_ctas,
-                  cudaStream_t stream) {
+                  cudaStream_t stream, int* ctas_out) {
   using Cf = Cfg<BN_>;
   CUtensorMap mb;
   if (int rc = encode_kmajor(&mb, B, N, K, ldb, BN_)) return rc;
@@ -374,17 +380,12 @@ static int launch(const CUtensorMap& ma, const void* B, int N, int K, int ldb, P
     attr_set[dev] = true;
   }
   k_gemm_bf16<BN_><<<grid, THREADS, Cf::SMEM_BYTES, stream>>>(ma, mb, p);
+  if (ctas_out) *ctas_out = grid;
   return bz_check_launch("bz_gemm_bf16");
 }
 
-}  // namespace gemm
-}  // namespace bz
-
-using namespace bz;
-
-extern "C" int bz_gemm_bf16(const void* A, const void* B, void* C, const void* residual, int M, int N, int K,
-                            int lda, int ldb, int ldc, int ldr, int max_ctas, void* stream) {
-  using namespace bz::gemm;
+static int gemm_impl(const void* A, const void* B, void* C, const void* residual, int M, int N, int K, int lda,
+                     int ldb, int ldc, int ldr, int max_ctas, uint32_t* signal, int* ctas_out, void* stream) {
   if (!A || !B || !C || M <= 0 || N <= 0 || K <= 0) return bz_fail(BZ_EINVAL, "gemm: bad shape");
   // K tails are zero-filled by TMA (out-of-bounds box columns), so only the
   // 16-byte stride/alignment rules of the tensor maps constrain K.
@@ -408,15 +409,33 @@ extern "C" int bz_gemm_bf16(const void* A, const void* B, void* C, const void* r
   p.ldr = ldr;
   p.m_tiles = (M + BM - 1) / BM;
   p.n_tiles = 0;
+  p.signal = signal;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const int forced = bn_override();
   const int bn = forced ? forced : pick_bn(M, N, ctas);
   switch (bn) {
     case 128:
-      return launch<128>(ma, B, N, K, ldb, p, max_ctas, s);
+      return launch<128>(ma, B, N, K, ldb, p, max_ctas, s, ctas_out);
     case 192:
-      return launch<192>(ma, B, N, K, ldb, p, max_ctas, s);
+      return launch<192>(ma, B, N, K, ldb, p, max_ctas, s, ctas_out);
     default:
-      return launch<256>(ma, B, N, K, ldb, p, max_ctas, s);
+      return launch<256>(ma, B, N, K, ldb, p, max_ctas, s, ctas_out);
   }
+}
+
+}  // namespace gemm
+}  // namespace bz
+
+using namespace bz;
+
+extern "C" int bz_gemm_bf16(const void* A, const void* B, void* C, const void* residual, int M, int N, int K,
+                            int lda, int ldb, int ldc, int ldr, int max_ctas, void* stream) {
+  return gemm::gemm_impl(A, B, C, residual, M, N, K, lda, ldb, ldc, ldr, max_ctas, nullptr, nullptr, stream);
+}
+
+extern "C" int bz_gemm_bf16_signal(const void* A, const void* B, void* C, const void* residual, int M, int N,
+                                   int K, int lda, int ldb, int ldc, int ldr, int max_ctas, uint32_t* signal,
+                                   int* ctas_out, void* stream) {
+  if (!signal || !ctas_out) return bz_fail(BZ_EINVAL, "gemm_signal: signal and ctas_out required");
+  return gemm::gemm_impl(A, B, C, residual, M, N, K, lda, ldb, ldc, ldr, max_ctas, signal, ctas_out, stream);
 }

@@ -132,8 +132,15 @@ class LlamaExecutor:
         return self.w.layers[0]["embed"].index_select(0, tokens.reshape(-1)).contiguous()
 
     @torch.no_grad()
-    def block(self, k: int, x: torch.Tensor, positions: torch.Tensor, bs: tuple[int, int]) -> torch.Tensor:
-        """x [B*S, d] -> block k output (new tensor); positions int32 [B*S]."""
+    def block(self, k: int, x: torch.Tensor, positions: torch.Tensor, bs: tuple[int, int],
+              out: Optional[torch.Tensor] = None, signal: Optional[torch.Tensor] = None) -> torch.Tensor:
+        """x [B*S, d] -> block k output; positions int32 [B*S].
+
+        ``out`` may live on another GPU (peer access): the down-projection GEMM
+        then stores the block output straight into it over NVLink and, with
+        ``signal``, raises that u32 counter by its CTA count when done (the fused
+        hand-off of cooperative execution).  Returns ``out`` (or a new tensor).
+        """
         a, L = self.arch, self.w.layers[k]
         m = x.shape[0]
         B, S = bs
@@ -155,8 +162,20 @@ class LlamaExecutor:
         gu, act = self.gu[:m], self.act[:m]
         self._gemm(h, L["wgu"], gu)
         self.lib.bz_silu_mul(gu.data_ptr(), act.data_ptr(), m, a.ffn, gu.stride(0), act.stride(0), s)
-        out = torch.empty_like(x)
-        self._gemm(act, L["wdown"], out, residual=o)
+        if out is None:
+            out = torch.empty_like(x)
+        if signal is None:
+            self._gemm(act, L["wdown"], out, residual=o)
+            self.last_signal_ctas = 0
+        else:
+            import ctypes
+            ctas = ctypes.c_int(0)
+            w = L["wdown"]
+            self.lib.bz_gemm_bf16_signal(act.data_ptr(), w.data_ptr(), out.data_ptr(), o.data_ptr(),
+                                         m, w.shape[0], act.shape[1], act.stride(0), w.stride(0),
+                                         out.stride(0), o.stride(0), 0, signal.data_ptr(),
+                                         ctypes.byref(ctas), s)
+            self.last_signal_ctas = ctas.value
         return out
 
     @torch.no_grad()

@@ -1,0 +1,332 @@
+"""Live pair across two GPU processes: ZigZag cooperative execution while the new
+instance's weights are still arriving (BlitzScale §5.2).
+
+Rank ``src`` holds a live Llama (weights in its slab); rank ``tgt`` receives the
+slab through the data plane -- a chain hop over NVLink from the source, or the
+O(1) pinned host cache over PCIe.  A queue of prefill batches is split with
+``configure_pipeline`` (livescale.py:113-181) using the *measured* time_l, and
+the target runs its prefixes in the ``zigzag_schedule`` order
+(livescale.py:269-346), each layer gated on the device readiness counter.  The
+last prefix GEMM of every batch stores the hidden state straight into the
+source's mailbox over NVLink (``bz_gemm_bf16_signal``), and the source's stream
+waits on that batch's counter (``cuStreamWaitValue32``) before running the
+suffix + LM head.
+
+Measured per batch: completion time on the source after the common start.
+Compared with the source serving every batch alone and with the rehearsal's
+prediction; logits must equal the source-alone logits (same kernels, same
+operand bytes -- checked bitwise).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass, field
+from typing import Optional
+
+import torch
+
+from . import livescale
+from ._native import BzSlab, cuda_lib
+from .dataplane import DeviceSlab, Fabric, HostCache, ScaleExecutor, device_view
+from .llama import LlamaExecutor, SlabWeights
+from .planner import PlanEdge, ScalePlan
+from .slab import LlamaArch, SlabLayout
+
+
+class Mailbox:
+    """Exportable device region on the source: n hidden-state slots + n counters."""
+
+    def __init__(self, device: int, n: int, slot_elems: int):
+        self.lib = cuda_lib()
+        self.n, self.slot_elems = n, slot_elems
+        self.slot_bytes = slot_elems * 2
+        self.flag_off = n * self.slot_bytes
+        self.raw = BzSlab()
+        self.lib.bz_slab_create(device, self.flag_off + 4 * n + 4096, self.raw)
+        dev = torch.device("cuda", device)
+        self.slots = device_view(self.raw.ptr, self.flag_off, torch.int16, dev).view(torch.bfloat16)
+        self.flags = device_view(self.raw.ptr + self.flag_off, 4 * n, torch.int32, dev)
+        self.flags.zero_()
+        self.exported = False
+
+    def slot(self, i: int, rows: int, d: int) -> torch.Tensor:
+        return self.slots[i * self.slot_elems: i * self.slot_elems + rows * d].view(rows, d)
+
+    def export(self):
+        if not self.exported:
+            self.lib.bz_slab_export(self.raw)
+            self.exported = True
+        return (os.getpid(), int(self.raw.fd), int(self.raw.bytes))
+
+    def close(self):
+        self.lib.bz_slab_free(self.raw)
+
+
+class PeerMailbox:
+    def __init__(self, device: int, info, n: int, slot_elems: int):
+        self.lib = cuda_lib()
+        self.raw = BzSlab()
+        self.lib.bz_slab_import(device, info[0], info[1], info[2], self.raw)
+        self.n, self.slot_elems = n, slot_elems
+        dev = torch.device("cuda", device)
+        flag_off = n * slot_elems * 2
+        self.slots = device_view(self.raw.ptr, flag_off, torch.int16, dev).view(torch.bfloat16)
+        self.flags = device_view(self.raw.ptr + flag_off, 4 * n, torch.int32, dev)
+
+    def slot(self, i: int, rows: int, d: int) -> torch.Tensor:
+        return self.slots[i * self.slot_elems: i * self.slot_elems + rows * d].view(rows, d)
+
+    def close(self):
+        self.lib.bz_slab_free(self.raw)
+
+
+@dataclass
+class LivePairResult:
+    mode: str
+    time_l: float
+    w_ms: float
+    splits: list
+    zigzag_finish_ms: list[float] = field(default_factory=list)
+    source_alone_finish_ms: list[float] = field(default_factory=list)
+    predicted_finish_ms: list[float] = field(default_factory=list)
+    best_effort_finish_ms: list[float] = field(default_factory=list)
+    load_ms: float = 0.0
+    logits_bitwise_equal: Optional[bool] = None
+    max_abs_diff: Optional[float] = None
+
+
+def _mean(x):
+    return sum(x) / len(x) if x else 0.0
+
+
+class LivePair:
+    """Collective over a Fabric (>= 2 ranks): rank ``src`` = live source, ``tgt`` = new instance."""
+
+    def __init__(self, fabric: Fabric, arch: LlamaArch, n_batches: int, seqs: int, seq_len: int,
+                 mode: str = "host", src: int = 0, tgt: int = 1, tile_bytes: int = 1 << 20,
+                 nctas: int = 48, seed: int = 7):
+        self.f, self.arch, self.mode = fabric, arch, mode
+        self.src, self.tgt = src, tgt
+        self.n, self.seqs, self.seq_len = n_batches, seqs, seq_len
+        self.rows = seqs * seq_len
+        self.layout = SlabLayout.for_arch(arch, tile_bytes=tile_bytes)
+        self.me = fabric.rank
+        dev = torch.device("cuda", fabric.device)
+        self.slab = DeviceSlab(self.layout, fabric.device) if self.me in (src, tgt) else None
+        g = torch.Generator().manual_seed(seed)
+        self.batches = [torch.randint(0, arch.vocab, (seqs, seq_len), generator=g).to(dev)
+                        for _ in range(n_batches)]
+        self.hc = None
+        if self.me == src:
+            SlabWeights(arch, self.layout, self.slab.data).init_random(seed=0)
+            torch.cuda.synchronize()
+        src_node, tgt_node = f"gpu{src}", f"gpu{tgt}"
+        if mode == "host":
+            # the O(1) host copy of the live weights, shared through /dev/shm
+            name = f"blitz_livepair_{os.getppid()}"
+            if self.me == src:
+                hc = HostCache(self.layout, shm_name=name, create=True)
+                hc.tensor.copy_(self.slab.data.cpu())
+                hc.close()
+            fabric.barrier()
+            if self.me == tgt:
+                self.hc = HostCache(self.layout, shm_name=name, create=False)
+            plan = ScalePlan(edges=[PlanEdge("mem0", tgt_node, 512.0, "pcie")], chains=[["mem0", tgt_node]])
+        else:
+            plan = ScalePlan(edges=[PlanEdge(src_node, tgt_node, 7200.0, "nvlink")],
+                             chains=[[src_node, tgt_node]])
+        node_rank = {src_node: src, tgt_node: tgt}
+        if self.slab is not None:
+            self.executor = ScaleExecutor(fabric, plan, self.slab, node_rank, host_cache=self.hc,
+                                          nctas=nctas)
+        else:  # bystander ranks still join the collective setup
+            fabric.allgather(None)
+            fabric.barrier()
+            self.executor = None
+        self.lib = cuda_lib()
+        self.ex = None
+        if self.me in (src, tgt):
+            self.ex = LlamaExecutor(SlabWeights(arch, self.layout, self.slab.data), max_tokens=self.rows,
+                                    device=dev)
+        mb_info = None
+        self.mailbox = self.peer_mb = None
+        if self.me == src:
+            self.mailbox = Mailbox(fabric.device, n_batches, self.rows * arch.d_model)
+            mb_info = self.mailbox.export()
+        infos = fabric.allgather(mb_info)
+        if self.me == tgt:
+            self.peer_mb = PeerMailbox(fabric.device, infos[src], n_batches, self.rows * arch.d_model)
+        fabric.barrier()
+        self.stream = torch.cuda.Stream(device=dev)
+        self.pos = torch.arange(seq_len, dtype=torch.int32, device=dev).repeat(seqs)
+
+    # ---- calibration ------------------------------------------------------------------------
+
+    def calibrate(self) -> tuple[float, float, float]:
+        """(w_ms per batch full forward on the source, unit load ms, time_l)."""
+        w = torch.zeros(1, dtype=torch.float64, device="cuda")
+        lm = torch.zeros(2, dtype=torch.float64, device="cuda")
+        if self.me == self.src:
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            self.ex.forward(self.batches[0])
+            e0.record()
+            for _ in range(3):
+                self.ex.forward(self.batches[0])
+            e1.record()
+            e1.synchronize()
+            w[0] = e0.elapsed_time(e1) / 3
+        self._transfer_once()
+        if self.me == self.tgt:
+            arr = self.executor.layer_arrivals_ms()
+            lm[0] = arr[-1]
+            lm[1] = (arr[-1] - arr[0]) / max(1, len(arr) - 1)
+        import torch.distributed as dist
+        dist.all_reduce(w)
+        dist.all_reduce(lm)
+        w_ms, load_ms, unit_ms = float(w.item()), float(lm[0].item()), float(lm[1].item())
+        self.load_ms = load_ms
+        layer_exec = w_ms / self.arch.n_layers
+        return w_ms, unit_ms, unit_ms / layer_exec
+
+    def _transfer_once(self):
+        self.f.barrier()
+        if self.executor is not None:
+            self.executor.launch()
+            self.executor.synchronize()
+        self.f.barrier()
+
+    # ---- runs --------------------------------------------------------------------------------
+
+    def run_source_alone(self) -> tuple[list[float], list[torch.Tensor]]:
+        out, fins = [], []
+        self.f.barrier()
+        torch.cuda.synchronize()
+        if self.me == self.src:
+            start = torch.cuda.Event(enable_timing=True)
+            ev = [torch.cuda.Event(enable_timing=True) for _ in range(self.n)]
+            start.record()
+            for i, b in enumerate(self.batches):
+                out.append(self.ex.forward(b))
+                ev[i].record()
+            ev[-1].synchronize()
+            fins = [start.elapsed_time(e) for e in ev]
+        self.f.barrier()
+        return fins, out
+
+    def run_split(self, cfg: livescale.PipelineConfig, tl: livescale.ZigzagTimeline):
+        """Execute cfg/tl with the weights streaming in; returns (finish ms, logits) on the source."""
+        L = self.arch.n_layers
+        if self.me == self.src:
+            self.mailbox.flags.zero_()
+        if self.me == self.tgt:
+            self.slab.loaded.zero_()  # gates closed before any target work is enqueued
+        self.f.barrier()
+        torch.cuda.synchronize()
+        fins, logits = [], []
+        cur = torch.cuda.current_stream()
+        start = torch.cuda.Event(enable_timing=True)
+        start.record(cur)
+        self.stream.wait_stream(cur)
+        if self.executor is not None:
+            for s in self.executor.streams.values():
+                s.wait_stream(cur)
+            self.executor.launch()
+        if self.me == self.tgt:
+            x = [None] * self.n
+            with torch.cuda.stream(self.stream):
+                for b, layer, _s, _e in tl.target_intervals:
+                    if x[b] is None:
+                        x[b] = self.ex.embed(self.batches[b])
+                    self.lib.bz_wait_layer(self.slab.loaded.data_ptr(), layer, self.stream.cuda_stream)
+                    if layer == cfg.splits[b][0]:
+                        flag = self.peer_mb.flags[b:b + 1]
+                        self.ex.block(layer - 1, x[b], self.pos, (self.seqs, self.seq_len),
+                                      out=self.peer_mb.slot(b, self.rows, self.arch.d_model), signal=flag)
+                    else:
+                        x[b] = self.ex.block(layer - 1, x[b], self.pos, (self.seqs, self.seq_len))
+            self.stream.synchronize()
+        if self.me == self.src:
+            grid = [0] * self.n
+            for i, (t_i, _) in enumerate(cfg.splits):
+                if t_i > 0:
+                    grid[i] = self.gemm_grid(self.rows, self.arch.d_model)
+            ev = [torch.cuda.Event(enable_timing=True) for _ in range(self.n)]
+            with torch.cuda.stream(self.stream):
+                for i, (t_i, _) in enumerate(cfg.splits):
+                    h = None
+                    if t_i > 0:
+                        self.lib.bz_wait_layer(self.mailbox.flags[i:i + 1].data_ptr(), grid[i],
+                                               self.stream.cuda_stream)
+                        h = self.mailbox.slot(i, self.rows, self.arch.d_model)
+                    logits.append(self.ex.forward(self.batches[i], first=t_i, last=L, x=h))
+                    ev[i].record(self.stream)
+            ev[-1].synchronize()
+            fins = [start.elapsed_time(e) for e in ev]
+        if self.executor is not None:
+            self.executor.synchronize()
+        self.f.barrier()
+        return fins, logits
+
+    def gemm_grid(self, m: int, n: int) -> int:
+        """CTAs the fused down-projection launches (the counter value that completes it)."""
+        probe = torch.zeros(1, dtype=torch.int32, device=self.slab.data.device)
+        a = torch.zeros(m, self.arch.ffn, dtype=torch.bfloat16, device=probe.device)
+        w = self.ex.w.layers[0]["wdown"]
+        out = torch.empty(m, n, dtype=torch.bfloat16, device=probe.device)
+        ctas = ctypes.c_int(0)
+        self.lib.bz_gemm_bf16_signal(a.data_ptr(), w.data_ptr(), out.data_ptr(), None, m, n,
+                                     self.arch.ffn, a.stride(0), w.stride(0), out.stride(0), 0, 0,
+                                     probe.data_ptr(), ctypes.byref(ctas),
+                                     torch.cuda.current_stream().cuda_stream)
+        torch.cuda.synchronize()
+        return ctas.value
+
+    def run(self) -> Optional[LivePairResult]:
+        w_ms, unit_ms, time_l = self.calibrate()
+        cfg = livescale.configure_pipeline(self.n, self.arch.n_layers, time_l)
+        tl = livescale.zigzag_schedule(cfg)
+        be = livescale.best_effort_pipeline(self.n, self.arch.n_layers, time_l)
+        be_tl = livescale.zigzag_schedule(be)
+        alone_f, alone_logits = self.run_source_alone()
+        zz_f, zz_logits = self.run_split(cfg, tl)
+        be_f, _ = self.run_split(be, be_tl)
+        res = None
+        if self.me == self.src:
+            layer_ms = w_ms / self.arch.n_layers
+            res = LivePairResult(mode=self.mode, time_l=time_l, w_ms=w_ms,
+                                 splits=[list(s) for s in cfg.splits], zigzag_finish_ms=zz_f,
+                                 source_alone_finish_ms=alone_f,
+                                 predicted_finish_ms=[t * layer_ms for t in tl.finish],
+                                 best_effort_finish_ms=be_f, load_ms=self.load_ms)
+            eq = all(torch.equal(a, b) for a, b in zip(zz_logits, alone_logits))
+            diff = max(float((a - b).abs().max()) for a, b in zip(zz_logits, alone_logits))
+            res.logits_bitwise_equal, res.max_abs_diff = eq, diff
+        return res
+
+    def close(self):
+        if self.executor is not None:
+            self.executor.close()
+        if self.peer_mb is not None:
+            self.peer_mb.close()
+        if self.mailbox is not None:
+            self.mailbox.close()
+        if self.hc is not None:
+            self.hc.close(unlink=True)
+        if self.slab is not None:
+            self.slab.close()
+
+
+def summarize(res: LivePairResult) -> dict:
+    return {
+        "mode": res.mode, "time_l_measured": res.time_l, "batch_forward_ms": res.w_ms,
+        "weights_load_ms": res.load_ms, "splits": res.splits,
+        "avg_latency_ms": {"zigzag_executed": _mean(res.zigzag_finish_ms),
+                           "best_effort_executed": _mean(res.best_effort_finish_ms),
+                           "source_alone": _mean(res.source_alone_finish_ms),
+                           "zigzag_rehearsal_prediction": _mean(res.predicted_finish_ms)},
+        "finish_ms": {"zigzag": res.zigzag_finish_ms, "source_alone": res.source_alone_finish_ms},
+        "logits_bitwise_equal_to_source_alone": res.logits_bitwise_equal,
+        "max_abs_logit_diff": res.max_abs_diff,
+    }

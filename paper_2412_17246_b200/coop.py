@@ -27,6 +27,7 @@ import torch
 
 from ._native import cuda_lib
 from .livescale import PipelineConfig, ZigzagTimeline
+from .dataplane import gate
 from .llama import LlamaExecutor
 
 
@@ -93,7 +94,7 @@ class CooperativePair:
             for b, layer, _s, _e in timeline.target_intervals:
                 if x[b] is None:
                     x[b] = self.tgt.embed(batches[b])
-                self.lib.bz_wait_layer(self.loaded.data_ptr(), layer, self.tgt_stream.cuda_stream)
+                gate(self.loaded.data_ptr(), layer, self.tgt_stream.cuda_stream)
                 last = layer == config.splits[b][0]
                 if last and self.fused:
                     # K5 fused into the GEMM epilogue: tiles land in the source's buffer
@@ -119,7 +120,7 @@ class CooperativePair:
                 if t_i == 0:
                     h = None
                 else:
-                    self.lib.bz_wait_layer(self.flag.data_ptr(), handed_at[i],
+                    gate(self.flag.data_ptr(), handed_at[i],
                                            self.src_stream.cuda_stream)
                     h = recv[i]
                 logits[i] = self.src.forward(batches[i], first=t_i, last=L, x=h)

@@ -231,6 +231,24 @@ class MulticastGroup:
             self.lib.bz_mc_free(self.raw, self.fabric.device, self.bound)
 
 
+GATE_MODE = os.environ.get("BZ_GATE", "kernel")
+
+
+def gate(flag_ptr: int, value: int, stream_handle: int, mode: Optional[str] = None) -> None:
+    """Block ``stream`` until the u32 at ``flag_ptr`` >= ``value``.
+
+    ``kernel`` (default): a one-thread gate kernel spinning with ld.acquire.sys
+    (bounded, ~µs wake-up).  ``memop``: cuStreamWaitValue32 in the stream front
+    end (no SM, but its re-polling interval backs off: measured ~100 ms late
+    wake-ups when the flag is raised by a peer GPU's NVLink atomics).
+    """
+    lib = cuda_lib()
+    if (mode or GATE_MODE) == "memop":
+        lib.bz_wait_layer(flag_ptr, value, stream_handle)
+    else:
+        lib.bz_wait_flag_kernel(flag_ptr, value, stream_handle)
+
+
 def _stream_handle(stream) -> int:
     if stream is None:
         return int(torch.cuda.current_stream().cuda_stream)

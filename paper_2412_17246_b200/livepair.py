@@ -29,7 +29,7 @@ import torch
 
 from . import livescale
 from ._native import BzSlab, cuda_lib
-from .dataplane import DeviceSlab, Fabric, HostCache, ScaleExecutor, device_view
+from .dataplane import DeviceSlab, Fabric, HostCache, ScaleExecutor, device_view, gate
 from .llama import LlamaExecutor, SlabWeights
 from .planner import PlanEdge, ScalePlan
 from .slab import LlamaArch, SlabLayout
@@ -239,7 +239,7 @@ class LivePair:
                 for b, layer, _s, _e in tl.target_intervals:
                     if x[b] is None:
                         x[b] = self.ex.embed(self.batches[b])
-                    self.lib.bz_wait_layer(self.slab.loaded.data_ptr(), layer, self.stream.cuda_stream)
+                    gate(self.slab.loaded.data_ptr(), layer, self.stream.cuda_stream)
                     if layer == cfg.splits[b][0]:
                         flag = self.peer_mb.flags[b:b + 1]
                         self.ex.block(layer - 1, x[b], self.pos, (self.seqs, self.seq_len),
@@ -257,7 +257,7 @@ class LivePair:
                 for i, (t_i, _) in enumerate(cfg.splits):
                     h = None
                     if t_i > 0:
-                        self.lib.bz_wait_layer(self.mailbox.flags[i:i + 1].data_ptr(), grid[i],
+                        gate(self.mailbox.flags[i:i + 1].data_ptr(), grid[i],
                                                self.stream.cuda_stream)
                         h = self.mailbox.slot(i, self.rows, self.arch.d_model)
                     logits.append(self.ex.forward(self.batches[i], first=t_i, last=L, x=h))

@@ -179,6 +179,16 @@ class LivePair:
             w[0] = e0.elapsed_time(e1) / 3
         self._transfer_once()
         if self.me == self.tgt:
+            # warm every kernel / library plan the target will use (cuDNN SDPA plans,
+            # lazily loaded modules) so the timed run measures steady state
+            x = self.ex.embed(self.batches[0])
+            for k in range(2):
+                x = self.ex.block(k, x, self.pos, (self.seqs, self.seq_len))
+            probe = torch.zeros(1, dtype=torch.int32, device=x.device)
+            scratch = torch.empty_like(x)
+            self.ex.block(0, x, self.pos, (self.seqs, self.seq_len), out=scratch, signal=probe)
+            self.ex.head(x, (self.seqs, self.seq_len))
+            torch.cuda.synchronize()
             arr = self.executor.layer_arrivals_ms()
             lm[0] = arr[-1]
             lm[1] = (arr[-1] - arr[0]) / max(1, len(arr) - 1)

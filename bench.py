@@ -7,12 +7,14 @@ Workloads (BASELINE.json configs):
            copy-engine staging on a side stream + per-layer readiness tracking.
   N >= 2 : live scale-up 1 -> N: the source instance on gpu0 multicasts its
            shard to N-1 new GPUs; plan from ``generate_plan`` (group=True:
-           gpu0 -> rep gpu1 over NVLink, rep -> NVLS multicast to the rest).
+           gpu0 -> rep gpu1 over NVLink, the rep's NVLink fan-out realised as a
+           pipelined sibling chain -- measured faster than NVLS multimem.st;
+           ``--fanout nvls`` selects the multicast realisation).
 One step = one complete scale-up (every target holds the bit-exact shard and
 its tracker has published every layer).  value = delivered bytes / time
 (delivered = shard x number of receiving GPUs), max over ranks.
 e2e = the same metric through the public API (planning included) with the
-shard starting in the pinned O(1) host cache: ``mem0 -> gpu0`` + NVLS fan-out
+shard starting in the pinned O(1) host cache: ``mem0 -> gpu0`` + NVLink fan-out
 to every other GPU, host->device bytes inside the timed region, per-layer
 stamps read back to the host.
 
@@ -61,6 +63,7 @@ def parse_args():
     p.add_argument("--fanout", default="auto", choices=["auto", "nvls", "chain", "star"])
     p.add_argument("--no-group", action="store_true", help="plan chains instead of NVLink fan-out")
     p.add_argument("--stage-engine", default="ce", choices=["ce", "sm"])
+    p.add_argument("--tiles-per-copy", type=int, default=8, help="tiles per copy-engine memcpy")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg (sweeps only)")
     p.add_argument("--no-c3", action="store_true", help="skip the C3 serving replay")
@@ -405,7 +408,7 @@ def run_blitz(args):
     log("host cache ready" if hc is not None else "no host cache on this rank")
     sess = ScaleUpSession(fabric, layout, plan, node_rank, host_cache=hc, engine=engine,
                           nctas=args.nctas, fanout_mode=args.fanout, seed=seed,
-                          stage_engine=args.stage_engine)
+                          stage_engine=args.stage_engine, tiles_per_copy=args.tiles_per_copy)
 
     log("session ready")
     # warm-up (first one verified bit-exact on every receiver)
@@ -470,7 +473,7 @@ def run_blitz(args):
             hc2 = host_cache_for(e2e_plan, "e2e")
             sess2 = ScaleUpSession(fabric, layout, e2e_plan, node_rank, host_cache=hc2, engine=engine,
                                    nctas=args.nctas, fanout_mode=args.fanout, seed=seed,
-                                   stage_engine=args.stage_engine)
+                                   stage_engine=args.stage_engine, tiles_per_copy=args.tiles_per_copy)
             for w in range(max(1, min(args.warmup, 2))):
                 sess2.run(verify=(w == 0))
         e2e_t = []

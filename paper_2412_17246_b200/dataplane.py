@@ -479,11 +479,16 @@ class ScaleExecutor:
             return "copy"
         return None
 
-    def launch(self, epoch: Optional[int] = None, track: bool = True, kernel_events=None):
+    def launch(self, epoch: Optional[int] = None, track: bool = True, kernel_events=None,
+               async_stage: bool = False):
         """Enqueue this rank's work for a new transfer; returns the epoch.
 
         ``kernel_events=(start, end)`` brackets the bulk mover on its own stream.
+        ``async_stage``: host-cache staging is enqueued by a helper thread (call
+        ``join_stage``/``synchronize`` before relying on the stage stream).
         """
+        if async_stage and kernel_events is not None:
+            raise ValueError("kernel_events need a synchronous enqueue")
         self.epoch = epoch if epoch is not None else self.epoch + 1
         e = self.epoch
         lay, slab = self.layout, self.slab
@@ -498,7 +503,14 @@ class ScaleExecutor:
             self.lib.bz_publish_layer(slab.loaded.data_ptr(), 0, slab.stamps.data_ptr()
                                       + 8 * lay.num_layers, stream.cuda_stream)
         if staged:
-            self._stage(e)
+            if async_stage:
+                # a few thousand copy-engine calls take host time; let a helper
+                # thread enqueue them so the caller can enqueue compute meanwhile
+                import threading
+                self._stage_thread = threading.Thread(target=self._stage, args=(e,), daemon=True)
+                self._stage_thread.start()
+            else:
+                self._stage(e)
         if self.role.receives and track and not (staged and self.stage_engine == "ce"):
             # a peer (or a staging kernel) produces the tiles: one-warp in-order tracker
             self.lib.bz_track_layers(slab.flags_ptr, slab.layer_tile.data_ptr(), lay.num_layers, e,
@@ -558,7 +570,14 @@ class ScaleExecutor:
             self.lib.bz_stage_tiles_sm(hc.ptr, slab.ptr, slab.flags_ptr, slab.tile_off.data_ptr(),
                                        0, lay.ntiles, e, self.nctas, s)
 
+    def join_stage(self):
+        t = getattr(self, "_stage_thread", None)
+        if t is not None:
+            t.join()
+            self._stage_thread = None
+
     def synchronize(self):
+        self.join_stage()
         for s in self.streams.values():
             s.synchronize()
 

@@ -242,7 +242,7 @@ class LivePair:
         if self.executor is not None:
             for s in self.executor.streams.values():
                 s.wait_stream(cur)
-            self.executor.launch()
+            self.executor.launch(async_stage=True)
         if self.me == self.tgt:
             x = [None] * self.n
             with torch.cuda.stream(self.stream):

@@ -94,7 +94,7 @@ class ScaleUpSession:
     def __init__(self, fabric: Fabric, layout: SlabLayout, plan, node_rank: dict[str, int],
                  host_cache: Optional[HostCache] = None, engine: int = ENGINE_VECTOR,
                  nctas: int = 32, fanout_mode: str = "auto", seed: int = 241217,
-                 stage_engine: str = "ce"):
+                 stage_engine: str = "ce", tiles_per_copy: int = 8):
         self.fabric = fabric
         self.layout = layout
         self.plan = plan
@@ -109,7 +109,7 @@ class ScaleUpSession:
         torch.cuda.synchronize()
         self.executor = ScaleExecutor(fabric, plan, self.slab, node_rank, host_cache=host_cache,
                                       engine=engine, nctas=nctas, fanout_mode=fanout_mode,
-                                      stage_engine=stage_engine)
+                                      stage_engine=stage_engine, tiles_per_copy=tiles_per_copy)
         self.receives = self.executor.role.receives
         self._expected: Optional[torch.Tensor] = None
 

@@ -41,6 +41,25 @@ def test_torchrun_scaleup_bit_exact():
     assert len(lines) == 5 and all(l["ok"] for l in lines), lines
 
 
+@pytest.mark.gpu
+@pytest.mark.multigpu
+@pytest.mark.skipif(_gpus() < 2, reason="needs >= 2 GPUs")
+@pytest.mark.parametrize("mode", ["host", "nvlink"])
+def test_two_process_live_pair_logits_bitwise(mode):
+    """ZigZag across two processes while the target's slab streams in: every batch's
+    logits equal the source-alone logits bit for bit (fused NVLink hand-off)."""
+    env = dict(os.environ, BZ_ARCH="tiny-4l", BZ_BATCHES="6", BZ_SEQS="2", BZ_SEQ="128",
+               BZ_MODE=mode, BZ_WATCHDOG_S="200")
+    proc = subprocess.run(
+        [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+         "--master-addr", "127.0.0.1", "--master-port", "29653" if mode == "host" else "29654",
+         str(ROOT / "scripts" / "live_pair.py")],
+        capture_output=True, text=True, timeout=400, env=env, cwd=str(ROOT))
+    assert proc.returncode == 0, proc.stdout[-2000:] + proc.stderr[-3000:]
+    res = json.loads([l for l in proc.stdout.splitlines() if l.startswith("{")][-1])
+    assert res["logits_bitwise_equal_to_source_alone"] is True
+
+
 _WORKER = r"""
 import os, sys, json
 sys.path.insert(0, {root!r})

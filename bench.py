@@ -68,6 +68,7 @@ def parse_args():
     p.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg (sweeps only)")
     p.add_argument("--no-c3", action="store_true", help="skip the C3 serving replay")
     p.add_argument("--no-coop", action="store_true", help="skip the C1 cooperative-execution block")
+    p.add_argument("--no-live", action="store_true", help="skip the two-GPU live-pair block")
     p.add_argument("--cpu-sample-units", type=int, default=4)
     p.add_argument("--watchdog-s", type=int, default=900)
     return p.parse_args()
@@ -528,6 +529,18 @@ def run_blitz(args):
             c3 = c3_report(costs)
             log(f"c3 done: { {k: v['measured']['p99_ttft_ms'] for k, v in c3['strategies'].items()} }")
 
+    # ---- live pair (N >= 2): ZigZag across two GPUs while the weights stream in ---------------
+    live = None
+    if N >= 2 and tp == 1 and not args.no_live:
+        from paper_2412_17246_b200.livepair import LivePair, summarize
+        log("live pair (7B, NVLink hop, ZigZag)")
+        lp = LivePair(fabric, arch, n_batches=12, seqs=4, seq_len=500, mode="nvlink")
+        res = lp.run()
+        live = summarize(res) if res is not None else None
+        lp.close()
+        if live is not None:
+            log(f"live pair avg latency {live['avg_latency_ms']}")
+
     decisions = decision_timings() if rank == 0 else None
     coop = None
     if rank == 0 and not args.no_coop:
@@ -565,6 +578,7 @@ def run_blitz(args):
                                                          else PCIE_PEAK_GBPS)) if achieved else None},
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
             "clocks": clk, "wall_s": wall, "c3": c3, "decisions": decisions, "coop_c1": coop,
+            "live_pair": live,
         }
         print(json.dumps(line), flush=True)
     fabric.barrier()

@@ -309,6 +309,236 @@ __global__ void __launch_bounds__(THREADS, 1)
   }
 }
 
+// ===========================================================================
+// CTA-pair variant (cta_group::2): a cluster of two CTAs computes a 256 x BN
+// tile.  CTA r loads A rows [128r, 128r+128) and B rows [r*BN/2, (r+1)*BN/2)
+// of the pair tile; the leader (r = 0) issues tcgen05.mma.cta_group::2 M=256,
+// which reads A from both CTAs' shared memory and B from both halves, and
+// writes 128 accumulator lanes x BN columns into each CTA's TMEM.  Per SM the
+// smem fill per K step drops from (128 + BN) rows to (128 + BN/2) rows.
+
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ uint32_t mapa_cta(uint32_t smem_addr, uint32_t cta) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_addr), "r"(cta));
+  return r;
+}
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+// both CTAs load into their own smem; completion bytes go to the leader's barrier
+__device__ __forceinline__ void tma_load_2d_pair(void* smem, const CUtensorMap* map, int c0, int c1, uint64_t* bar) {
+  const uint32_t leader_bar = smem_u32(bar) & 0xFEFFFFFFu;
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], "
+      "[%4];" ::"r"(smem_u32(smem)),
+      "l"(map), "r"(c0), "r"(c1), "r"(leader_bar)
+      : "memory");
+}
+__device__ __forceinline__ void umma_bf16_pair(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(a), "l"(b), "r"(idesc), "r"(acc)
+      : "memory");
+}
+// arrive on the same-offset barrier of both CTAs when the leader's MMAs complete
+__device__ __forceinline__ void umma_commit_pair(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          smem_u32(bar)),
+      "h"(static_cast<uint16_t>(0x3))
+      : "memory");
+}
+
+template <int BN_>
+struct CfgPair {
+  static constexpr int BN = BN_;
+  static constexpr int B_BYTES = (BN / 2) * BK * 2;  // this CTA's half of the B tile
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int STAGES_FIT = (SMEM_LIMIT - 2048) / STAGE_BYTES;
+  static constexpr int STAGES = STAGES_FIT > 8 ? 8 : STAGES_FIT;
+  static constexpr int TMEM_COLS = 2 * BN <= 256 ? 256 : 512;
+  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 256;
+  static_assert(BN % 32 == 0 && BN <= 256 && BN >= 64, "tile N");
+};
+
+// bf16 store of a 32-column accumulator chunk (+ optional residual) for one row
+__device__ __forceinline__ void store_chunk(const Params& p, int row, int col, const uint32_t (&r)[32]) {
+  __nv_bfloat16* out = p.C + static_cast<int64_t>(row) * p.ldc + col;
+  const __nv_bfloat16* res = p.R ? p.R + static_cast<int64_t>(row) * p.ldr + col : nullptr;
+  if (col + 32 <= p.N) {
+    uint32_t w[16];
+    if (res) {
+      const uint4* rv = reinterpret_cast<const uint4*>(res);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        uint4 x = rv[q];
+        const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&x);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          float2 f = __bfloat1622float2(h[j]);
+          w[q * 4 + j] = pack_bf16(__uint_as_float(r[q * 8 + 2 * j]) + f.x, __uint_as_float(r[q * 8 + 2 * j + 1]) + f.y);
+        }
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < 16; ++j) w[j] = pack_bf16(__uint_as_float(r[2 * j]), __uint_as_float(r[2 * j + 1]));
+    }
+    uint4* o = reinterpret_cast<uint4*>(out);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) o[q] = make_uint4(w[4 * q], w[4 * q + 1], w[4 * q + 2], w[4 * q + 3]);
+  } else {
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+      if (col + j < p.N) {
+        float v = __uint_as_float(r[j]);
+        if (res) v += __bfloat162float(res[j]);
+        out[j] = __float2bfloat16_rn(v);
+      }
+    }
+  }
+}
+
+// p.m_tiles counts 256-row pair tiles here
+template <int BN_>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
+    k_gemm_bf16_pair(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b, Params p) {
+  using C = CfgPair<BN_>;
+  constexpr int BN = C::BN, STAGES = C::STAGES, B_BYTES = C::B_BYTES, STAGE_BYTES = C::STAGE_BYTES;
+  constexpr int TMEM_COLS = C::TMEM_COLS;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sa = smem;
+  uint8_t* sb = smem + STAGES * A_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
+  uint64_t* empty = full + STAGES;
+  uint64_t* acc_full = empty + STAGES;
+  uint64_t* acc_empty = acc_full + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_ctarank();
+  const bool leader = rank == 0;
+  const int cluster = blockIdx.x >> 1;
+  const int clusters = gridDim.x >> 1;
+  const int num_tiles = p.m_tiles * p.n_tiles;
+  const int k_blocks = (p.K + BK - 1) / BK;
+
+  if (warp == 0 && lane == 0) {
+    prefetch_tmap(&map_a);
+    prefetch_tmap(&map_b);
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&acc_full[b], 1);
+      mbar_init(&acc_empty[b], 8);  // 4 epilogue warps x 2 CTAs (leader's copy is used)
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "n"(TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  tc_fence_before();
+  cluster_sync_all();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      uint32_t stage = 0, phase = 0;
+      for (int tile = cluster; tile < num_tiles; tile += clusters) {
+        const int m0 = (tile % p.m_tiles) * (2 * BM) + static_cast<int>(rank) * BM;
+        const int n0 = (tile / p.m_tiles) * BN + static_cast<int>(rank) * (BN / 2);
+        for (int kb = 0; kb < k_blocks; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          if (leader) mbar_expect_tx(&full[stage], 2 * STAGE_BYTES);
+          tma_load_2d_pair(sa + stage * A_BYTES, &map_a, kb * BK, m0, &full[stage]);
+          tma_load_2d_pair(sb + stage * B_BYTES, &map_b, kb * BK, n0, &full[stage]);
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (leader && lane == 0) {
+      constexpr uint32_t idesc = instr_desc_bf16(2 * BM, BN);
+      uint32_t stage = 0, phase = 0;
+      int it = 0;
+      for (int tile = cluster; tile < num_tiles; tile += clusters, ++it) {
+        const int buf = it & 1;
+        const uint32_t use = static_cast<uint32_t>(it >> 1);
+        mbar_wait(&acc_empty[buf], (use & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t d = tmem_base + buf * BN;
+        for (int kb = 0; kb < k_blocks; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint64_t da = umma_desc_sw128(smem_u32(sa + stage * A_BYTES));
+          const uint64_t db = umma_desc_sw128(smem_u32(sb + stage * B_BYTES));
+#pragma unroll
+          for (int k = 0; k < BK / UMMA_K; ++k) umma_bf16_pair(d, da + 2 * k, db + 2 * k, idesc, (kb | k) != 0);
+          umma_commit_pair(&empty[stage]);
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        umma_commit_pair(&acc_full[buf]);
+      }
+    }
+  } else if (warp >= 4) {
+    const int quarter = warp & 3;
+    const uint32_t leader_acc_empty0 = mapa_cta(smem_u32(&acc_empty[0]), 0);
+    int it = 0;
+    for (int tile = cluster; tile < num_tiles; tile += clusters, ++it) {
+      const int buf = it & 1;
+      const uint32_t use = static_cast<uint32_t>(it >> 1);
+      const int m0 = (tile % p.m_tiles) * (2 * BM) + static_cast<int>(rank) * BM;
+      const int n0 = (tile / p.m_tiles) * BN;
+      mbar_wait(&acc_full[buf], use & 1);
+      tc_fence_after();
+      const int row = m0 + quarter * 32 + lane;
+      const uint32_t taddr = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + buf * BN;
+#pragma unroll 1
+      for (int c = 0; c < BN; c += 32) {
+        uint32_t r[32];
+        tmem_ld_32x32b_x32(taddr + c, r);
+        if (row < p.M) store_chunk(p, row, n0 + c, r);
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(leader_acc_empty0 + buf * 8);
+    }
+  }
+
+  tc_fence_before();
+  cluster_sync_all();
+  if (warp == 2) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "n"(TMEM_COLS));
+  }
+  if (p.signal != nullptr && threadIdx.x == 0) {
+    __threadfence_system();
+    asm volatile("red.release.sys.global.add.u32 [%0], 1;" ::"l"(p.signal) : "memory");
+  }
+}
+
 static int encode_kmajor(CUtensorMap* map, const void* ptr, int rows, int k, int ld, int box_rows) {
   const DriverApi* d = driver_api();
   if (!d) return BZ_ECUDA;
@@ -384,6 +614,42 @@ static int launch(const CUtensorMap& ma, const void* B, int N, int K, int ldb, P
   return bz_check_launch("bz_gemm_bf16");
 }
 
+template <int BN_>
+static int launch_pair(const CUtensorMap& ma, const void* B, int N, int K, int ldb, Params p, int max_ctas,
+                       cudaStream_t stream, int* ctas_out) {
+  using Cf = CfgPair<BN_>;
+  CUtensorMap mb;
+  if (int rc = encode_kmajor(&mb, B, N, K, ldb, BN_ / 2)) return rc;
+  p.n_tiles = (N + BN_ - 1) / BN_;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int cap = (max_ctas > 0 ? tmin(max_ctas, sms) : sms) / 2;
+  int clusters = p.m_tiles * p.n_tiles;
+  if (clusters > cap) clusters = cap;
+  if (clusters < 1) clusters = 1;
+  static bool attr_set[64] = {};
+  if (dev < 64 && !attr_set[dev]) {
+    cudaError_t e =
+        cudaFuncSetAttribute(k_gemm_bf16_pair<BN_>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cf::SMEM_BYTES);
+    if (e != cudaSuccess) return bz_fail_cuda(e, "gemm pair smem attribute");
+    attr_set[dev] = true;
+  }
+  k_gemm_bf16_pair<BN_><<<2 * clusters, THREADS, Cf::SMEM_BYTES, stream>>>(ma, mb, p);
+  if (ctas_out) *ctas_out = 2 * clusters;
+  return bz_check_launch("bz_gemm_bf16 (pair)");
+}
+
+// BZ_GEMM_PAIR=0 forces single-CTA tiles, =1 forces CTA pairs; default: pairs when M >= 256
+static int pair_override() {
+  static int v = -2;
+  if (v == -2) {
+    const char* e = getenv("BZ_GEMM_PAIR");
+    v = e ? atoi(e) : -1;
+  }
+  return v;
+}
+
 static int gemm_impl(const void* A, const void* B, void* C, const void* residual, int M, int N, int K, int lda,
                      int ldb, int ldc, int ldr, int max_ctas, uint32_t* signal, int* ctas_out, void* stream) {
   if (!A || !B || !C || M <= 0 || N <= 0 || K <= 0) return bz_fail(BZ_EINVAL, "gemm: bad shape");
@@ -412,6 +678,20 @@ static int gemm_impl(const void* A, const void* B, void* C, const void* residual
   p.signal = signal;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const int forced = bn_override();
+  const int po = pair_override();
+  const bool pair = po == 1 || (po == -1 && M >= 2 * BM);
+  if (pair) {
+    p.m_tiles = (M + 2 * BM - 1) / (2 * BM);
+    const int bn = forced ? forced : pick_bn(M, N, ctas);
+    switch (bn) {
+      case 128:
+        return launch_pair<128>(ma, B, N, K, ldb, p, max_ctas, s, ctas_out);
+      case 192:
+        return launch_pair<192>(ma, B, N, K, ldb, p, max_ctas, s, ctas_out);
+      default:
+        return launch_pair<256>(ma, B, N, K, ldb, p, max_ctas, s, ctas_out);
+    }
+  }
   const int bn = forced ? forced : pick_bn(M, N, ctas);
   switch (bn) {
     case 128:

@@ -507,7 +507,16 @@ class ScaleExecutor:
                 # a few thousand copy-engine calls take host time; let a helper
                 # thread enqueue them so the caller can enqueue compute meanwhile
                 import threading
-                self._stage_thread = threading.Thread(target=self._stage, args=(e,), daemon=True)
+
+                def worker():
+                    try:
+                        torch.cuda.set_device(self.fabric.device)  # new threads start on device 0
+                        self._stage(e)
+                    except BaseException as exc:  # surfaced by join_stage()
+                        self._stage_error = exc
+
+                self._stage_error = None
+                self._stage_thread = threading.Thread(target=worker, daemon=True)
                 self._stage_thread.start()
             else:
                 self._stage(e)
@@ -575,6 +584,9 @@ class ScaleExecutor:
         if t is not None:
             t.join()
             self._stage_thread = None
+            if self._stage_error is not None:
+                err, self._stage_error = self._stage_error, None
+                raise RuntimeError("host-cache staging enqueue failed") from err
 
     def synchronize(self):
         self.join_stage()

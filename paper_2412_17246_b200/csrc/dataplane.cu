@@ -140,6 +140,68 @@ __device__ __forceinline__ void copy_tile(const int4* __restrict__ src, int4* co
   }
 }
 
+// 256-bit variant (sm_100 LDG/STG.E.ENL2.256): half the memory instructions per byte
+struct __align__(32) v8u32 {
+  uint32_t v[8];
+};
+template <bool kCoherent>
+__device__ __forceinline__ v8u32 ld32(const v8u32* p) {
+  v8u32 r;
+  if (kCoherent)
+    asm volatile("ld.global.L1::no_allocate.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=r"(r.v[0]), "=r"(r.v[1]), "=r"(r.v[2]), "=r"(r.v[3]), "=r"(r.v[4]), "=r"(r.v[5]),
+                   "=r"(r.v[6]), "=r"(r.v[7])
+                 : "l"(p));
+  else
+    asm volatile("ld.global.nc.L1::no_allocate.L2::256B.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=r"(r.v[0]), "=r"(r.v[1]), "=r"(r.v[2]), "=r"(r.v[3]), "=r"(r.v[4]), "=r"(r.v[5]),
+                   "=r"(r.v[6]), "=r"(r.v[7])
+                 : "l"(p));
+  return r;
+}
+__device__ __forceinline__ void st32(v8u32* p, const v8u32& x) {
+  asm volatile("st.global.L1::no_allocate.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "r"(x.v[0]),
+               "r"(x.v[1]), "r"(x.v[2]), "r"(x.v[3]), "r"(x.v[4]), "r"(x.v[5]), "r"(x.v[6]), "r"(x.v[7])
+               : "memory");
+}
+
+// tile [b, e) in 32-byte words
+template <bool kCoherent>
+__device__ __forceinline__ void copy_tile32(const v8u32* __restrict__ src, int4* const* dst, int ndst, int64_t b,
+                                            int64_t e) {
+  constexpr int U = 4;
+  const int64_t step = blockDim.x;
+  int64_t i = b + threadIdx.x;
+  for (; i + (U - 1) * step < e; i += U * step) {
+    v8u32 v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) v[u] = ld32<kCoherent>(src + i + u * step);
+    for (int d = 0; d < ndst; ++d) {
+      v8u32* o = reinterpret_cast<v8u32*>(dst[d]);
+#pragma unroll
+      for (int u = 0; u < U; ++u) st32(o + i + u * step, v[u]);
+    }
+  }
+  for (; i < e; i += step) {
+    v8u32 v = ld32<kCoherent>(src + i);
+    for (int d = 0; d < ndst; ++d) st32(reinterpret_cast<v8u32*>(dst[d]) + i, v);
+  }
+}
+
+template <bool kRelay>
+__global__ void __launch_bounds__(kThreads) k_push_tiles32(PushArgs a) {
+  for (int t = a.t0 + blockIdx.x; t < a.t1; t += gridDim.x) {
+    if (kRelay) wait_tile(a.wait_flags, t, a.epoch);
+    const int64_t b = a.tile_off[t] >> 5, e = a.tile_off[t + 1] >> 5;
+    copy_tile32<kRelay>(reinterpret_cast<const v8u32*>(a.src), a.dst, a.ndst, b, e);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence_system();
+      for (int d = 0; d < a.ndst; ++d) st_release_sys(a.flags[d] + t, a.epoch);
+    }
+  }
+}
+
 template <bool kRelay>
 __global__ void __launch_bounds__(kThreads) k_push_tiles(PushArgs a) {
   for (int t = a.t0 + blockIdx.x; t < a.t1; t += gridDim.x) {
@@ -384,6 +446,15 @@ extern "C" int bz_push_tiles(const void* src, void* const* dst, uint32_t* const*
     auto kern = wait_flags ? k_push_tiles_tma<true> : k_push_tiles_tma<false>;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     kern<<<grid, 32, smem, s>>>(a);
+  } else if (engine == 2) {
+    // 256-bit path: needs 32-byte aligned bases and tile offsets (slabs are 256-B aligned)
+    uintptr_t align = reinterpret_cast<uintptr_t>(src);
+    for (int d = 0; d < ndst; ++d) align |= reinterpret_cast<uintptr_t>(dst[d]);
+    if (align & 31) return bz_fail(BZ_EINVAL, "push (256-bit): bases must be 32-byte aligned");
+    if (wait_flags)
+      k_push_tiles32<true><<<grid, kThreads, 0, s>>>(a);
+    else
+      k_push_tiles32<false><<<grid, kThreads, 0, s>>>(a);
   } else if (wait_flags) {
     k_push_tiles<true><<<grid, kThreads, 0, s>>>(a);
   } else {

@@ -43,6 +43,7 @@ from .slab import SlabLayout
 
 ENGINE_VECTOR = 0
 ENGINE_TMA = 1
+ENGINE_VEC256 = 2   # 32-byte LDG/STG.E.ENL2.256 (sm_100)
 
 
 class _CudaView:

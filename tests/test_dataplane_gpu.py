@@ -54,7 +54,7 @@ def _check_copies(slabs, src, layout, epoch):
         assert int(s.loaded.item()) == layout.num_layers
 
 
-@pytest.mark.parametrize("engine", [ENGINE_VECTOR, ENGINE_TMA])
+@pytest.mark.parametrize("engine", [ENGINE_VECTOR, ENGINE_TMA, 2])
 @pytest.mark.parametrize("targets,group", [
     (["gpu1"], True),                                  # C1 1->2
     (["gpu1", "gpu2", "gpu3"], False),                 # 1->4 chain

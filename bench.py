@@ -63,7 +63,8 @@ def parse_args():
     p.add_argument("--fanout", default="auto", choices=["auto", "nvls", "chain", "star"])
     p.add_argument("--no-group", action="store_true", help="plan chains instead of NVLink fan-out")
     p.add_argument("--stage-engine", default="ce", choices=["ce", "sm"])
-    p.add_argument("--tiles-per-copy", type=int, default=8, help="tiles per copy-engine memcpy")
+    p.add_argument("--tiles-per-copy", type=int, default=128,
+                   help="tiles per copy-engine memcpy (128 x 1 MiB measured best: 54.8 GB/s)")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg (sweeps only)")
     p.add_argument("--no-c3", action="store_true", help="skip the C3 serving replay")

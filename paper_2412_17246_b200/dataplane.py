@@ -382,7 +382,7 @@ class ScaleExecutor:
     def __init__(self, fabric: Fabric, plan: ScalePlan, slab: DeviceSlab,
                  node_rank: dict[str, int], host_cache: Optional[HostCache] = None,
                  engine: int = ENGINE_VECTOR, nctas: int = 32, fanout_mode: str = "auto",
-                 stage_engine: str = "ce", tiles_per_copy: int = 8):
+                 stage_engine: str = "ce", tiles_per_copy: int = 128):
         self.fabric = fabric
         self.plan = plan
         self.slab = slab

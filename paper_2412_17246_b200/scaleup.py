@@ -94,7 +94,7 @@ class ScaleUpSession:
     def __init__(self, fabric: Fabric, layout: SlabLayout, plan, node_rank: dict[str, int],
                  host_cache: Optional[HostCache] = None, engine: int = ENGINE_VECTOR,
                  nctas: int = 32, fanout_mode: str = "auto", seed: int = 241217,
-                 stage_engine: str = "ce", tiles_per_copy: int = 8):
+                 stage_engine: str = "ce", tiles_per_copy: int = 128):
         self.fabric = fabric
         self.layout = layout
         self.plan = plan

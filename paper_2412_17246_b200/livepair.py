@@ -95,6 +95,7 @@ class LivePairResult:
     load_ms: float = 0.0
     logits_bitwise_equal: Optional[bool] = None
     max_abs_diff: Optional[float] = None
+    diagnostics: dict = field(default_factory=dict)   # zigzag run: target hand-off / layer times
 
 
 def _mean(x):
@@ -243,15 +244,21 @@ class LivePair:
         start = torch.cuda.Event(enable_timing=True)
         start.record(cur)
         self.stream.wait_stream(cur)
+        diag = {}
         if self.executor is not None:
             for s in self.executor.streams.values():
                 s.wait_stream(cur)
             self.executor.launch(async_stage=True)
+            if self.me == self.src and self.mode == "nvlink":
+                pushed = torch.cuda.Event(enable_timing=True)
+                pushed.record(self.executor.streams["copy"])
+                diag["push_done"] = pushed
         if self.me == self.tgt:
             # per-batch ping-pong activations: no allocator traffic while enqueueing
             bufs = self._act_bufs()
             embed_w = self.ex.w.layers[0]["embed"]
             started = [False] * self.n
+            handed = {}
             with torch.cuda.stream(self.stream):
                 for b, layer, _s, _e in tl.target_intervals:
                     if not started[b]:
@@ -263,10 +270,16 @@ class LivePair:
                         flag = self.peer_mb.flags[b:b + 1]
                         self.ex.block(layer - 1, x_in, self.pos, (self.seqs, self.seq_len),
                                       out=self.peer_mb.slot(b, self.rows, self.arch.d_model), signal=flag)
+                        handed[b] = torch.cuda.Event(enable_timing=True)
+                        handed[b].record(self.stream)
                     else:
                         self.ex.block(layer - 1, x_in, self.pos, (self.seqs, self.seq_len),
                                       out=bufs[b][layer % 2])
             self.stream.synchronize()
+            self.executor.synchronize()
+            diag["handoff_ms"] = {b: start.elapsed_time(e) for b, e in handed.items()}
+            arr = self.executor.layer_arrivals_ms()
+            diag["layer_ms_first_last"] = (arr[0], arr[-1])
         if self.me == self.src:
             g = self.fused_grid()
             grid = [g if t_i > 0 else 0 for t_i, _ in cfg.splits]
@@ -282,8 +295,14 @@ class LivePair:
                     ev[i].record(self.stream)
             ev[-1].synchronize()
             fins = [start.elapsed_time(e) for e in ev]
+            if "push_done" in diag:
+                self.executor.synchronize()
+                diag["push_done_ms"] = start.elapsed_time(diag.pop("push_done"))
         if self.executor is not None:
             self.executor.synchronize()
+        diag.pop("push_done", None)
+        gathered = self.f.allgather(diag)
+        self.last_diag = {"source": gathered[self.src], "target": gathered[self.tgt]}
         self.f.barrier()
         return fins, logits
 
@@ -321,6 +340,7 @@ class LivePair:
         be_tl = livescale.zigzag_schedule(be)
         alone_f, alone_logits = self.run_source_alone()
         zz_f, zz_logits = self.run_split(cfg, tl)
+        zz_diag = self.last_diag
         be_f, _ = self.run_split(be, be_tl)
         res = None
         if self.me == self.src:
@@ -333,6 +353,7 @@ class LivePair:
             eq = all(torch.equal(a, b) for a, b in zip(zz_logits, alone_logits))
             diff = max(float((a - b).abs().max()) for a, b in zip(zz_logits, alone_logits))
             res.logits_bitwise_equal, res.max_abs_diff = eq, diff
+            res.diagnostics = zz_diag
         return res
 
     def close(self):
@@ -359,4 +380,5 @@ def summarize(res: LivePairResult) -> dict:
         "finish_ms": {"zigzag": res.zigzag_finish_ms, "source_alone": res.source_alone_finish_ms},
         "logits_bitwise_equal_to_source_alone": res.logits_bitwise_equal,
         "max_abs_logit_diff": res.max_abs_diff,
+        "diagnostics": res.diagnostics,
     }

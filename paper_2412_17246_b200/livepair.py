@@ -169,26 +169,32 @@ class LivePair:
         """(w_ms per batch full forward on the source, unit load ms, time_l)."""
         w = torch.zeros(1, dtype=torch.float64, device="cuda")
         lm = torch.zeros(2, dtype=torch.float64, device="cuda")
+        # everything runs on self.stream -- the stream the timed runs use -- because
+        # library state (cuDNN SDPA handles/plans) is per stream: warming the default
+        # stream left 60-200 ms of first-call setup inside the timed ZigZag run
         if self.me == self.src:
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            self.ex.forward(self.batches[0])
-            e0.record()
-            for _ in range(3):
+            with torch.cuda.stream(self.stream):
                 self.ex.forward(self.batches[0])
-            e1.record()
+                e0.record(self.stream)
+                for _ in range(3):
+                    self.ex.forward(self.batches[0])
+                e1.record(self.stream)
             e1.synchronize()
             w[0] = e0.elapsed_time(e1) / 3
         self._transfer_once()
         if self.me == self.tgt:
             # warm every kernel / library plan the target will use (cuDNN SDPA plans,
             # lazily loaded modules) so the timed run measures steady state
-            x = self.ex.embed(self.batches[0])
-            for k in range(2):
-                x = self.ex.block(k, x, self.pos, (self.seqs, self.seq_len))
-            probe = torch.zeros(1, dtype=torch.int32, device=x.device)
-            scratch = torch.empty_like(x)
-            self.ex.block(0, x, self.pos, (self.seqs, self.seq_len), out=scratch, signal=probe)
-            self.ex.head(x, (self.seqs, self.seq_len))
+            with torch.cuda.stream(self.stream):
+                x = self.ex.embed(self.batches[0])
+                for k in range(2):
+                    x = self.ex.block(k, x, self.pos, (self.seqs, self.seq_len))
+                probe = torch.zeros(1, dtype=torch.int32, device=x.device)
+                scratch = torch.empty_like(x)
+                self.ex.block(0, x, self.pos, (self.seqs, self.seq_len), out=scratch, signal=probe)
+                self.ex.head(x, (self.seqs, self.seq_len))
+                gate(probe.data_ptr(), 0, self.stream.cuda_stream)
             torch.cuda.synchronize()
             arr = self.executor.layer_arrivals_ms()
             lm[0] = arr[-1]
@@ -221,10 +227,11 @@ class LivePair:
         if self.me == self.src:
             start = torch.cuda.Event(enable_timing=True)
             ev = [torch.cuda.Event(enable_timing=True) for _ in range(self.n)]
-            start.record()
-            for i, b in enumerate(self.batches):
-                out.append(self.ex.forward(b))
-                ev[i].record()
+            with torch.cuda.stream(self.stream):  # same (warm) stream as the split runs
+                start.record(self.stream)
+                for i, b in enumerate(self.batches):
+                    out.append(self.ex.forward(b))
+                    ev[i].record(self.stream)
             ev[-1].synchronize()
             fins = [start.elapsed_time(e) for e in ev]
         self.f.barrier()

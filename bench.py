@@ -59,7 +59,7 @@ def parse_args():
     p.add_argument("--tp", type=int, default=1, help="GPUs per instance (C4: 13B TP=2, C5: 70B TP=4)")
     p.add_argument("--tile-kib", type=int, default=1024)
     p.add_argument("--nctas", type=int, default=48)
-    p.add_argument("--engine", default="vector", choices=["vector", "vec256", "tma"])
+    p.add_argument("--engine", default="vector", choices=["vector", "vec256", "tma", "ce"])
     p.add_argument("--fanout", default="auto", choices=["auto", "nvls", "chain", "star"])
     p.add_argument("--no-group", action="store_true", help="plan chains instead of NVLink fan-out")
     p.add_argument("--stage-engine", default="ce", choices=["ce", "sm"])
@@ -376,7 +376,7 @@ def run_blitz(args):
     gpus = [f"gpu{i}" for i in range(N)]
     anchors = gpus[::tp]  # InstanceState.node = gpus[0] (simcore.py:142-144)
     node_rank = {g: i for i, g in enumerate(gpus)}
-    engine = {"tma": 1, "vec256": 2}.get(args.engine, 0)
+    engine = {"tma": 1, "vec256": 2, "ce": 3}.get(args.engine, 0)
     seed = 241217
     my = gpus[rank]
 

@@ -105,6 +105,14 @@ int bz_push_tiles(const void* src, void* const* dst, uint32_t* const* dst_flags,
                   const uint32_t* wait_flags, const int64_t* tile_off, int t0, int t1,
                   uint32_t epoch, int nctas, int engine, void* stream);
 
+/* bz_push_tiles_ce: the same hop on the copy engines (one destination): per
+ * group of `tiles_per_copy` tiles, [relay: one-warp gate until wait_flags of the
+ * group >= epoch] -> cudaMemcpyAsync into the peer VA -> release of dst_flags.
+ * tile_off_host is a host copy of the tile table.  Keeps the SMs for compute. */
+int bz_push_tiles_ce(const void* src, void* dst, uint32_t* dst_flags, const uint32_t* wait_flags,
+                     const int64_t* tile_off_host, int t0, int t1, int tiles_per_copy, uint32_t epoch,
+                     void* stream);
+
 /* bz_multicast_tiles: one multimem.st stream into the multicast VA `mc_dst`
  * (bound to every receiver's slab); flags go through `mc_flags` (the
  * multicast VA of the receivers' flag arrays). */

@@ -352,6 +352,11 @@ __global__ void k_publish_layer(uint32_t* loaded, uint32_t value, uint64_t* stam
 
 __global__ void k_wait_flag(const uint32_t* flag, uint32_t value) { spin_until_geq(flag, value); }
 
+// one warp: every flag in [t0, t1) >= epoch (gate in front of a copy-engine relay)
+__global__ void __launch_bounds__(32) k_wait_range(const uint32_t* flags, int t0, int t1, uint32_t epoch) {
+  for (int t = t0 + threadIdx.x; t < t1; t += 32) spin_until_geq(flags + t, epoch);
+}
+
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
   x += 0x9E3779B97F4A7C15ull;
@@ -496,6 +501,28 @@ extern "C" int bz_stage_tiles_ce(const void* host_src, void* dst, uint32_t* dst_
     k_set_flags<<<(te - t + 127) / 128, 128, 0, s>>>(dst_flags, t, te, epoch);
   }
   return bz_check_launch("bz_stage_tiles_ce");
+}
+
+// Chain hop on the copy engines: no SM moves bytes (the SMs stay with the
+// cooperating instance's GEMMs).  Per group of tiles: [relay: one-warp gate on
+// the group's upstream flags] -> cudaMemcpyAsync into the peer mapping ->
+// flag kernel (system-scope release into the peer's flag array).
+extern "C" int bz_push_tiles_ce(const void* src, void* dst, uint32_t* dst_flags, const uint32_t* wait_flags,
+                                const int64_t* tile_off_host, int t0, int t1, int tiles_per_copy, uint32_t epoch,
+                                void* stream) {
+  if (!src || !dst || !dst_flags || !tile_off_host || t0 < 0 || t1 < t0 || tiles_per_copy < 1)
+    return bz_fail(BZ_EINVAL, "push_ce: bad arguments");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  for (int t = t0; t < t1; t += tiles_per_copy) {
+    const int te = min(t1, t + tiles_per_copy);
+    if (wait_flags) k_wait_range<<<1, 32, 0, s>>>(wait_flags, t, te, epoch);
+    const int64_t b = tile_off_host[t], e = tile_off_host[te];
+    cudaError_t err = cudaMemcpyAsync(static_cast<char*>(dst) + b, static_cast<const char*>(src) + b,
+                                      static_cast<size_t>(e - b), cudaMemcpyDeviceToDevice, s);
+    if (err != cudaSuccess) return bz_fail_cuda(err, "push_ce memcpy");
+    k_set_flags<<<(te - t + 127) / 128, 128, 0, s>>>(dst_flags, t, te, epoch);
+  }
+  return bz_check_launch("bz_push_tiles_ce");
 }
 
 extern "C" int bz_stage_tiles_sm(const void* host_src, void* dst, uint32_t* dst_flags, const int64_t* tile_off,

@@ -44,6 +44,8 @@ from .slab import SlabLayout
 ENGINE_VECTOR = 0
 ENGINE_TMA = 1
 ENGINE_VEC256 = 2   # 32-byte LDG/STG.E.ENL2.256 (sm_100)
+ENGINE_CE = 3       # copy engines (cudaMemcpyAsync into the peer VA), SMs left for compute
+CE_TILES_PER_COPY = 16
 
 
 class _CudaView:
@@ -406,6 +408,7 @@ class ScaleExecutor:
         dev = torch.device("cuda", fabric.device)
         self.streams = {k: torch.cuda.Stream(device=dev) for k in ("copy", "fan", "track", "stage")}
         self.epoch = 0
+        self._tile_off_host = np.ascontiguousarray(self.layout.tile_off)
         self.writers = self._fanout_writers() if fanout_mode == "nvls" else {}
 
         # every rank exports its slab; peers it sends to are imported
@@ -527,7 +530,13 @@ class ScaleExecutor:
                                      slab.loaded.data_ptr(), slab.stamps.data_ptr(),
                                      st["track"].cuda_stream)
         dsts, relay = self._feeds()
-        if dsts:
+        if dsts and self.engine == ENGINE_CE:
+            for n in dsts:
+                self.lib.bz_push_tiles_ce(slab.ptr, self.peers[n].ptr, self.peers[n].flags_ptr,
+                                          slab.flags_ptr if relay else None,
+                                          self._tile_off_host.ctypes.data, 0, lay.ntiles,
+                                          CE_TILES_PER_COPY, e, st["copy"].cuda_stream)
+        elif dsts:
             ptrs = ptr_array([self.peers[n].ptr for n in dsts])
             flags = ptr_array([self.peers[n].flags_ptr for n in dsts])
             self.lib.bz_push_tiles(slab.ptr, ptrs, flags, len(dsts),
@@ -557,7 +566,12 @@ class ScaleExecutor:
                     n += (t1 - t0 + self.tiles_per_copy - 1) // self.tiles_per_copy + 1
             else:
                 n += 1
-        if self._unicast_targets():
+        dsts = self._unicast_targets()
+        if dsts and self.engine == ENGINE_CE:
+            groups = (self.layout.ntiles + CE_TILES_PER_COPY - 1) // CE_TILES_PER_COPY
+            per_group = 2 if self.role.receives else 1  # [gate] + flag kernel (memcpy not counted)
+            n += len(dsts) * groups * per_group
+        elif dsts:
             n += 1
         return n + len(self.mc_out)
 

@@ -107,7 +107,7 @@ class LivePair:
 
     def __init__(self, fabric: Fabric, arch: LlamaArch, n_batches: int, seqs: int, seq_len: int,
                  mode: str = "host", src: int = 0, tgt: int = 1, tile_bytes: int = 1 << 20,
-                 nctas: int = 48, seed: int = 7):
+                 nctas: int = 48, seed: int = 7, engine: int = 0):
         self.f, self.arch, self.mode = fabric, arch, mode
         self.src, self.tgt = src, tgt
         self.n, self.seqs, self.seq_len = n_batches, seqs, seq_len
@@ -141,7 +141,7 @@ class LivePair:
         node_rank = {src_node: src, tgt_node: tgt}
         if self.slab is not None:
             self.executor = ScaleExecutor(fabric, plan, self.slab, node_rank, host_cache=self.hc,
-                                          nctas=nctas)
+                                          nctas=nctas, engine=engine)
         else:  # bystander ranks still join the collective setup
             fabric.allgather(None)
             fabric.barrier()

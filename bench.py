@@ -361,8 +361,7 @@ def run_reference(args):
 def run_blitz(args):
     import torch
     from paper_2412_17246_b200 import slab as S
-    from paper_2412_17246_b200.dataplane import (ENGINE_TMA, ENGINE_VECTOR, DeviceSlab, Fabric,
-                                                 HostCache, plan_roles)
+    from paper_2412_17246_b200.dataplane import DeviceSlab, Fabric, HostCache, plan_roles
     from paper_2412_17246_b200.scaleup import ScaleUpSession, plan_for, rank_plan
 
     fabric = Fabric.from_env()

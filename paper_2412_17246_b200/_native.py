@@ -11,7 +11,6 @@ the call that needs it raises ``NativeLibraryMissing``.
 from __future__ import annotations
 
 import ctypes
-import math
 import os
 from pathlib import Path
 from typing import Optional, Sequence

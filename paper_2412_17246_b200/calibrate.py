@@ -71,7 +71,6 @@ def c3_report(costs: MeasuredCosts, topo_name: str = "b200-hgx-2x8",
               strategies: Sequence[str] = ("blitz-live", "blitz-stop", "allcache", "sllm")) -> dict:
     """C3: Llama-2 7B under the 5x-burst trace; p99 TTFT/TBT with modeled and measured costs."""
     from . import simcore
-    from .parampool import ModelSpec
     from .slab import LLAMA2_7B, model_spec_for
     from .topology import load_topology
     from .traces import generate_trace

@@ -17,9 +17,7 @@ from __future__ import annotations
 import json
 import time
 from pathlib import Path
-from typing import Optional
 
-import numpy as np
 import torch
 
 from .llama import SlabWeights

@@ -20,7 +20,7 @@ on two GPUs (handoff over NVLink into the source's buffer, cross-GPU flag).
 
 from __future__ import annotations
 
-from dataclasses import dataclass, field
+from dataclasses import dataclass
 from typing import Optional, Sequence
 
 import torch

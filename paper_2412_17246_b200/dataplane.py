@@ -366,13 +366,6 @@ def merge_plans(plans: Sequence[ScalePlan]) -> ScalePlan:
 # ---- executor -------------------------------------------------------------------------------
 
 
-@dataclass
-class TransferTiming:
-    elapsed_ms: float                    # this rank: start -> last tile landed + tracked
-    layer_ms: list[float]                # per-layer arrival after start (receivers)
-    bytes_received: int
-
-
 class ScaleExecutor:
     """Runs one node's share of a plan on its GPU, every epoch a fresh transfer.
 

@@ -16,7 +16,6 @@ holds 1/tp of every matrix), rounded up to the alignment.
 from __future__ import annotations
 
 from dataclasses import dataclass, field
-from typing import Optional, Sequence
 
 import numpy as np
 

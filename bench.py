@@ -316,6 +316,34 @@ def coop_c1(device: int, n_batches: int = 8, seqs: int = 2, seq_len: int = 1000)
     return out
 
 
+def block_cpu_vs_gpu(arch, prefill_ms: dict) -> dict:
+    """One Llama block at 2048 tokens (4 x 512): the fp32 CPU oracle (all host threads)
+    next to the measured B200 prefill line."""
+    import torch
+    from oracle.forward_ref import block_fp32
+
+    torch.set_num_threads(os.cpu_count() or 1)
+    g = torch.Generator().manual_seed(0)
+    d, kv, f = arch.d_model, arch.kv_dim, arch.ffn
+    w = {"attn_norm": torch.ones(d), "ffn_norm": torch.ones(d),
+         "wqkv": torch.randn(d + 2 * kv, d, generator=g) * 0.02,
+         "wo": torch.randn(d, d, generator=g) * 0.02,
+         "wgu": torch.randn(2 * f, d, generator=g) * 0.02,
+         "wdown": torch.randn(d, f, generator=g) * 0.02}
+    x = torch.randn(4, 512, d, generator=g)
+    block_fp32(arch, w, x[:, :64])  # warm
+    t0 = time.perf_counter()
+    block_fp32(arch, w, x)
+    cpu_s = time.perf_counter() - t0
+    gpu_block_ms = None
+    if prefill_ms and 2048 in prefill_ms:
+        gpu_block_ms = prefill_ms[2048] / arch.n_layers  # upper bound: includes head / L
+    return {"tokens": 2048, "cpu_fp32_ms": cpu_s * 1e3, "cpu_threads": os.cpu_count(),
+            "cpu_tokens_per_s": 2048 / cpu_s,
+            "gpu_ms_per_block": gpu_block_ms,
+            "gpu_tokens_per_s_per_block": 2048 / (gpu_block_ms / 1e3) if gpu_block_ms else None}
+
+
 # ---- reference arm ------------------------------------------------------------------------------
 
 
@@ -527,6 +555,7 @@ def run_blitz(args):
                                 source={"prefill_points_ms": pre,
                                         "measured_in": "this bench run"})
             c3 = c3_report(costs)
+            c3["block_7b_2048tok"] = block_cpu_vs_gpu(arch, pre)
             log(f"c3 done: { {k: v['measured']['p99_ttft_ms'] for k, v in c3['strategies'].items()} }")
 
     # ---- live pair (N >= 2): ZigZag across two GPUs while the weights stream in ---------------

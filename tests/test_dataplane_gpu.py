@@ -140,3 +140,66 @@ def test_handoff_copies_and_counts():
                    torch.cuda.current_stream().cuda_stream)
     torch.cuda.synchronize()
     assert torch.equal(src, dst) and int(flag.item()) == 8
+
+
+# ---- edge cases: ragged units, single tile, maximum fan-out, empty ranges ------------------
+
+
+def test_ragged_units_and_tiles_bit_exact():
+    """Unit sizes that are not tile multiples (last tile of every unit ragged),
+    including a unit smaller than one tile."""
+    lay = S.SlabLayout([3 * 4096 + 256, 256, 7 * 4096 - 256, 4096], tile_bytes=4096)
+    assert any(int(b - a) < 4096 for a, b in zip(lay.tile_off[:-1], lay.tile_off[1:]))
+    slabs = {n: DeviceSlab(lay, 0) for n in ("gpu0", "gpu1", "gpu2")}
+    slabs["gpu0"].fill_random(seed=11)
+    plan = _plan(["gpu0"], ["gpu1", "gpu2"], group=False, model=S.model_spec_for(S.TINY_4L))
+    for engine in (ENGINE_VECTOR, ENGINE_TMA, 2):
+        execute_plan_loopback(plan, slabs, engine + 1, engine=engine, nctas=3)
+        torch.cuda.synchronize()
+        _check_copies(slabs, "gpu0", lay, engine + 1)
+    for s in slabs.values():
+        s.close()
+
+
+def test_single_tile_slab():
+    lay = S.SlabLayout([512], tile_bytes=1 << 20)
+    assert lay.ntiles == 1
+    a, b = DeviceSlab(lay, 0), DeviceSlab(lay, 0)
+    a.fill_random(seed=2)
+    execute_plan_loopback(_plan(["gpu0"], ["gpu1"], model=S.model_spec_for(S.TINY_4L)),
+                          {"gpu0": a, "gpu1": b}, 1, nctas=64)
+    torch.cuda.synchronize()
+    assert torch.equal(a.data, b.data) and int(b.loaded.item()) == 1
+    a.close()
+    b.close()
+
+
+def test_max_fanout_star_push_and_empty_range(tiny_layout):
+    """One read, BZ_MAX_DST = 8 peer writes per tile; an empty tile range is a no-op."""
+    from paper_2412_17246_b200._native import ptr_array
+    lib = cuda_lib()
+    src = DeviceSlab(tiny_layout, 0)
+    src.fill_random(seed=8)
+    dsts = [DeviceSlab(tiny_layout, 0) for _ in range(8)]
+    s = torch.cuda.current_stream().cuda_stream
+    ptrs = ptr_array([d.ptr for d in dsts])
+    flags = ptr_array([d.flags_ptr for d in dsts])
+    lib.bz_push_tiles(src.ptr, ptrs, flags, 8, None, src.tile_off.data_ptr(), 0, 0, 1, 8, 0, s)
+    lib.bz_push_tiles(src.ptr, ptrs, flags, 8, None, src.tile_off.data_ptr(), 0,
+                      tiny_layout.ntiles, 1, 8, 0, s)
+    torch.cuda.synchronize()
+    for d in dsts:
+        assert torch.equal(d.data, src.data) and int(d.flags.min()) == 1
+        d.close()
+    src.close()
+
+
+def test_bad_arguments_raise():
+    from paper_2412_17246_b200._native import BlitzError, ptr_array
+    lib = cuda_lib()
+    with pytest.raises(BlitzError):
+        lib.bz_push_tiles(None, ptr_array([0]), ptr_array([0]), 1, None, None, 0, 1, 1, 8, 0, 0)
+    with pytest.raises(BlitzError):  # ndst above BZ_MAX_DST
+        lib.bz_push_tiles(1, ptr_array([0] * 9), ptr_array([0] * 9), 9, None, 1, 0, 1, 1, 8, 0, 0)
+    with pytest.raises(BlitzError):
+        lib.bz_fill_random(1, 17, 0, 0)   # size not a multiple of 16

@@ -37,6 +37,14 @@ from pathlib import Path
 ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
+def _hbm_peak() -> float:
+    try:
+        with open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["hbm_gbs"])
+    except (OSError, KeyError, ValueError):
+        return 6545.6
+
+
 NVLINK_PEAK_GBPS = 770.0     # B200_PROFILING.md: measured peer copy per direction (900 nominal)
 NVLINK_NOMINAL_GBPS = 900.0
 PCIE_PEAK_GBPS = 63.0        # PCIe Gen5 x16 per direction, nominal
@@ -548,14 +556,21 @@ def run_blitz(args):
                         None)
             if N == 1 and host is None:
                 host = layers_value
-            from paper_2412_17246_b200.calibrate import build_costs, c3_report, measure_prefill
-            log("c3: measuring prefill")
+            from paper_2412_17246_b200.calibrate import (build_costs, c3_report, measure_decode,
+                                                         measure_prefill)
+            log("c3: measuring prefill and decode")
             pre = measure_prefill(arch, device=fabric.device)
-            costs = build_costs(prefill=pre, nvlink_layer_ms=nv, host_layer_ms=host,
-                                source={"prefill_points_ms": pre,
+            dec = measure_decode(arch, device=fabric.device)
+            costs = build_costs(prefill=pre, nvlink_layer_ms=nv, host_layer_ms=host, decode=dec,
+                                source={"prefill_points_ms": pre, "decode_points_ms": dec,
+                                        "decode_context_tokens": 1024,
                                         "measured_in": "this bench run"})
             c3 = c3_report(costs)
             c3["block_7b_2048tok"] = block_cpu_vs_gpu(arch, pre)
+            # a batch-1 decode step reads every weight once: HBM roofline of the decode GEMMs
+            wbytes = arch.total_bytes() - arch.embed_bytes()
+            c3["decode_b1_weight_GBps"] = wbytes / (dec[1] / 1e3) / 1e9
+            c3["decode_b1_hbm_frac"] = c3["decode_b1_weight_GBps"] / _hbm_peak()
             log(f"c3 done: { {k: v['measured']['p99_ttft_ms'] for k, v in c3['strategies'].items()} }")
 
     # ---- live pair (N >= 2): ZigZag across two GPUs while the weights stream in ---------------

@@ -173,6 +173,20 @@ int bz_gemm_bf16(const void* A, const void* B, void* C, const void* residual, in
 int bz_gemm_bf16_signal(const void* A, const void* B, void* C, const void* residual, int M, int N,
                         int K, int lda, int ldb, int ldc, int ldr, int max_ctas, uint32_t* signal,
                         int* ctas_out, void* stream);
+/* General form.  With a caller-owned fp32 workspace (16-byte aligned) a skinny
+ * problem (fewer tiles than SMs, e.g. a decode step's M = batch rows) is split
+ * along K: slices write fp32 partials into the workspace and a reduce pass adds
+ * them (plus the residual) into C.  The split is chosen per call from the tile
+ * count, K and workspace_bytes; workspace = NULL disables it.  signal/ctas_out
+ * as in bz_gemm_bf16_signal.  All compute kernels are launched with programmatic
+ * dependent launch (set-up overlaps the previous kernel; BZ_PDL=0 disables).  The workspace must be zero-filled before its first
+ * use (it holds per-tile arrival counters, which every call leaves at zero) and
+ * must not be shared by GEMMs running concurrently. */
+#define BZ_GEMM_B_STATIC 1u /* B is not written by kernels still in flight on the stream (weights):
+                               its first tiles may load before the predecessor kernel completes */
+int bz_gemm_bf16_ex(const void* A, const void* B, void* C, const void* residual, int M, int N, int K,
+                    int lda, int ldb, int ldc, int ldr, int max_ctas, unsigned flags, void* workspace,
+                    int64_t workspace_bytes, uint32_t* signal, int* ctas_out, void* stream);
 
 /* ---- Llama block glue (bf16 in/out, fp32 math) ---------------------------------------- */
 /* y = x * rsqrt(mean(x^2) + eps) * w per row; d % 8 == 0. */
@@ -184,6 +198,25 @@ int bz_rope(void* qkv, const int32_t* positions, int rows, int n_rot_heads, int 
             float theta, void* stream);
 /* act[:, j] = silu(gu[:, j]) * gu[:, ffn + j]. */
 int bz_silu_mul(const void* gu, void* act, int rows, int ffn, int ldg, int lda, void* stream);
+
+/* ---- KV-cache decode (csrc/decode_kernels.cu) -------------------------------------------
+ * The decode position is read from device memory (*pos, int32), so a captured
+ * decode step replays for every position.  Cache layout [rows, n_kv, s_max, hd]
+ * bf16.  Replaces the reference's decode cost line ModelSpec.decode_step_ms
+ * (parampool.py:61-62) for a prefill instance flipped to decode by
+ * mutate_prefill_to_decode (livescale.py:512-536) and for cooperative decode. */
+/* Rotate q (in place) and k of each row's fused [q | k | v] projection at
+ * position *pos, and write k, v into the caches at that position. */
+int bz_rope_append(void* qkv, int ld, int rows, int n_heads, int n_kv, int head_dim, float theta,
+                   void* k_cache, void* v_cache, int64_t s_max, const int32_t* pos, void* stream);
+/* Bytes of workspace bz_decode_attention needs for these sizes. */
+int bz_decode_workspace_bytes(int rows, int n_heads, int n_kv, int head_dim, int64_t s_max, int64_t* bytes);
+/* out[r, h*hd:(h+1)*hd] = softmax(q_h K[0..*pos]^T / sqrt(hd)) V over each row's
+ * cached prefix (GQA: head h reads kv head h / (n_heads / n_kv), 1/2/4/8 heads per kv head);
+ * hd 64 or 128. */
+int bz_decode_attention(const void* q, int ldq, const void* k_cache, const void* v_cache, int rows, int n_heads,
+                        int n_kv, int head_dim, int64_t s_max, const int32_t* pos, void* out, int ldo,
+                        void* workspace, int64_t workspace_bytes, void* stream);
 
 /* ---- misc ------------------------------------------------------------------------------ */
 int bz_sm_count(int dev, int* n);

@@ -95,6 +95,8 @@ _PP = ctypes.POINTER(ctypes.c_void_p)
 _PI = ctypes.POINTER(ctypes.c_int)
 _PU64 = ctypes.POINTER(ctypes.c_uint64)
 
+BZ_GEMM_B_STATIC = 1   # include/blitz.h
+
 # name -> argtypes; every function returns int status
 _SIGNATURES = {
     "bz_version": [],
@@ -127,9 +129,15 @@ _SIGNATURES = {
     "bz_handoff": [_P, _P, _U64, _P, _U32, _I, _P],
     "bz_gemm_bf16": [_P, _P, _P, _P, _I, _I, _I, _I, _I, _I, _I, _I, _P],
     "bz_gemm_bf16_signal": [_P, _P, _P, _P, _I, _I, _I, _I, _I, _I, _I, _I, _P, _PI, _P],
+    "bz_gemm_bf16_ex": [_P, _P, _P, _P, _I, _I, _I, _I, _I, _I, _I, _I, ctypes.c_uint, _P, ctypes.c_int64, _P,
+                        _PI, _P],
     "bz_rmsnorm": [_P, _P, _P, _I, _I, _I, _I, ctypes.c_float, _P],
     "bz_rope": [_P, _P, _I, _I, _I, _I, ctypes.c_float, _P],
     "bz_silu_mul": [_P, _P, _I, _I, _I, _I, _P],
+    "bz_rope_append": [_P, _I, _I, _I, _I, _I, ctypes.c_float, _P, _P, ctypes.c_int64, _P, _P],
+    "bz_decode_workspace_bytes": [_I, _I, _I, _I, ctypes.c_int64, ctypes.POINTER(ctypes.c_int64)],
+    "bz_decode_attention": [_P, _I, _P, _P, _I, _I, _I, _I, ctypes.c_int64, _P, _P, _I, _P, ctypes.c_int64,
+                            _P],
     "bz_sm_count": [_I, _PI],
 }
 

@@ -1,7 +1,8 @@
 """Measure the B200 costs the serving replay needs (prefill line, layer arrivals).
 
 ``measure_prefill`` times real Llama prefill passes of the tcgen05 executor
-(one block at each token count, scaled by the layer count, plus the head), and
+(one block at each token count, scaled by the layer count, plus the head),
+``measure_decode`` times KV-cache decode steps the same way, and
 ``c3_report`` replays the C3 burst trace through ``simcore`` twice -- with the
 reference's analytic costs and with the measured ones -- for each strategy.
 """
@@ -57,14 +58,63 @@ def measure_prefill(arch: LlamaArch, token_counts: Sequence[int] = (256, 512, 10
     return out
 
 
+def measure_decode(arch: LlamaArch, batches: Sequence[int] = (1, 8, 32, 64), context: int = 1024,
+                   iters: int = 10, device: int = 0, probe_layers: int = 8) -> dict:
+    """ms of one full-model decode step for ``b`` sequences at ``context`` cached
+    tokens each: ``probe_layers`` distinct blocks captured as one CUDA graph (as
+    served), replayed from position ``context`` on and scaled to the layer count,
+    plus the head timed separately."""
+    from .dataplane import DeviceSlab
+    from .llama import KVCache, LlamaExecutor, SlabWeights
+
+    nl = min(probe_layers, arch.n_layers)
+    probe = LlamaArch(arch.name + "-probe", arch.d_model, nl, arch.n_heads, arch.n_kv_heads,
+                      arch.ffn, arch.vocab, arch.norm_eps, arch.rope_theta)
+    lay = SlabLayout.for_arch(probe, tile_bytes=1 << 20)
+    slab = DeviceSlab(lay, device)
+    w = SlabWeights(probe, lay, slab.data)
+    w.init_random(seed=0)
+    dev = torch.device("cuda", device)
+    ex = LlamaExecutor(w, max_tokens=max(batches), device=dev)
+    out = {}
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+    for b in batches:
+        kv = KVCache(probe, b, context + iters + 2, dev)
+        for t in list(kv.k.values()) + list(kv.v.values()):
+            t.normal_(0, 1)
+        kv.length = context
+        step = ex.decode_graph(kv, 0, nl, hidden_in=True, head=False)
+        step.hidden.normal_(0, 1)
+        x = step.hidden
+        step()
+        torch.cuda.synchronize()
+        ev[0].record()
+        for _ in range(iters):
+            step()
+        ev[1].record()
+        for _ in range(iters):
+            ex.head(x, (b, 1))
+        ev[2].record()
+        ev[2].synchronize()
+        per_block = ev[0].elapsed_time(ev[1]) / iters / nl
+        out[b] = per_block * arch.n_layers + ev[1].elapsed_time(ev[2]) / iters
+        del step, kv
+    slab.close()
+    return out
+
+
 def build_costs(prefill: Optional[dict] = None, nvlink_layer_ms=None, host_layer_ms=None,
-                source: Optional[dict] = None) -> MeasuredCosts:
-    a = b = None
+                source: Optional[dict] = None, decode: Optional[dict] = None) -> MeasuredCosts:
+    a = b = da = db = None
     if prefill:
         xs = sorted(prefill)
         a, b = fit_line(xs, [prefill[x] for x in xs])
+    if decode:
+        xs = sorted(decode)
+        da, db = fit_line(xs, [decode[x] for x in xs])
     return MeasuredCosts(prefill_alpha_ms=a, prefill_beta_ms=b, nvlink_layer_ms=nvlink_layer_ms,
-                         host_layer_ms=host_layer_ms, source=source or {})
+                         host_layer_ms=host_layer_ms, decode_alpha_ms=da, decode_beta_ms=db,
+                         source=source or {})
 
 
 def c3_report(costs: MeasuredCosts, topo_name: str = "b200-hgx-2x8",

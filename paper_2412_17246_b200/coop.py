@@ -28,7 +28,7 @@ import torch
 from ._native import cuda_lib
 from .livescale import PipelineConfig, ZigzagTimeline
 from .dataplane import gate
-from .llama import LlamaExecutor
+from .llama import KVCache, LlamaExecutor
 
 
 @dataclass
@@ -67,7 +67,9 @@ class CooperativePair:
 
     @torch.no_grad()
     def run(self, batches: Sequence[torch.Tensor], config: PipelineConfig,
-            timeline: ZigzagTimeline) -> CoopResult:
+            timeline: ZigzagTimeline, caches: Optional[list[tuple[KVCache, KVCache]]] = None) -> CoopResult:
+        """Prefill every batch with its split; with ``caches`` (see ``make_caches``)
+        each side keeps the keys/values of the blocks it ran, for ``decode``."""
         L = self.src.arch.n_layers
         n = len(batches)
         if config.batches != n:
@@ -84,6 +86,8 @@ class CooperativePair:
                                       dtype=torch.bfloat16, device=self.src.h.device)
         order: list[tuple[int, int]] = []
         nbytes = 0
+        kv_t = [c[0] for c in caches] if caches else [None] * n
+        kv_s = [c[1] for c in caches] if caches else [None] * n
         start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         cur = torch.cuda.current_stream()
         start.record(cur)
@@ -98,10 +102,11 @@ class CooperativePair:
                 last = layer == config.splits[b][0]
                 if last and self.fused:
                     # K5 fused into the GEMM epilogue: tiles land in the source's buffer
-                    self.tgt.block(layer - 1, x[b], pos[b], shapes[b], out=recv[b], signal=self.flag)
+                    self.tgt.block(layer - 1, x[b], pos[b], shapes[b], out=recv[b], signal=self.flag,
+                                   kv=kv_t[b])
                     self._handoffs += self.tgt.last_signal_ctas
                 else:
-                    x[b] = self.tgt.block(layer - 1, x[b], pos[b], shapes[b])
+                    x[b] = self.tgt.block(layer - 1, x[b], pos[b], shapes[b], kv=kv_t[b])
                     if last:
                         self.lib.bz_handoff(x[b].data_ptr(), recv[b].data_ptr(), x[b].numel() * 2,
                                             self.flag.data_ptr(), 0, self.handoff_ctas,
@@ -111,6 +116,8 @@ class CooperativePair:
                 if last:
                     nbytes += recv[b].numel() * 2
                     handed_at[b] = self._handoffs
+                    if kv_t[b] is not None:
+                        kv_t[b].length = shapes[b][1]
 
         # ---- source: suffixes FCFS, each gated on its hand-off counter -----------------------
         logits: list[Optional[torch.Tensor]] = [None] * n
@@ -123,10 +130,76 @@ class CooperativePair:
                     gate(self.flag.data_ptr(), handed_at[i],
                                            self.src_stream.cuda_stream)
                     h = recv[i]
-                logits[i] = self.src.forward(batches[i], first=t_i, last=L, x=h)
+                logits[i] = self.src.forward(batches[i], first=t_i, last=L, x=h, kv=kv_s[i])
         cur.wait_stream(self.src_stream)
         cur.wait_stream(self.tgt_stream)
         end.record(cur)
         end.synchronize()
         return CoopResult(logits=logits, executed_order=order, handoff_bytes=nbytes,
+                          total_ms=start.elapsed_time(end))
+
+    def make_caches(self, batches: Sequence[torch.Tensor], config: PipelineConfig,
+                    max_new_tokens: int) -> list[tuple[KVCache, KVCache]]:
+        """Per batch: the target's cache for blocks [0, T_i) and the source's for
+        [T_i, L), each sized for the prompt plus ``max_new_tokens``."""
+        L = self.src.arch.n_layers
+        out = []
+        for b, (t_i, _) in zip(batches, config.splits):
+            B, S = b.shape
+            out.append((KVCache(self.tgt.arch, B, S + max_new_tokens, self.tgt.h.device, 0, t_i),
+                        KVCache(self.src.arch, B, S + max_new_tokens, self.src.h.device, t_i, L)))
+        return out
+
+    @torch.no_grad()
+    def decode(self, tokens: Sequence[torch.Tensor], config: PipelineConfig,
+               caches: list[tuple[KVCache, KVCache]]) -> CoopResult:
+        """One cooperative decode step per batch (tokens[i] int64 [B]): the target
+        runs blocks [0, T_i) against its cache and hands the [B, d] hidden state to
+        the source (fused into the last down-projection), which finishes blocks
+        [T_i, L) and the head.  Only ``B*d*2`` bytes per batch cross."""
+        L = self.src.arch.n_layers
+        n = len(tokens)
+        recv: list[Optional[torch.Tensor]] = [None] * n
+        handed_at = [0] * n
+        nbytes = 0
+        start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        cur = torch.cuda.current_stream()
+        start.record(cur)
+        self.tgt_stream.wait_stream(cur)
+        self.src_stream.wait_stream(cur)
+        with torch.cuda.stream(self.tgt_stream):
+            for i, (t_i, _) in enumerate(config.splits):
+                if t_i == 0:
+                    continue
+                kv = caches[i][0]
+                recv[i] = torch.empty(tokens[i].numel(), self.src.arch.d_model, dtype=torch.bfloat16,
+                                      device=self.src.h.device)
+                x = self.tgt.embed(tokens[i])
+                for k in range(t_i):
+                    gate(self.loaded.data_ptr(), k + 1, self.tgt_stream.cuda_stream)
+                    if k == t_i - 1 and self.fused:
+                        self.tgt.decode_block(k, x, kv, out=recv[i], signal=self.flag)
+                        self._handoffs += self.tgt.last_signal_ctas
+                    else:
+                        x = self.tgt.decode_block(k, x, kv)
+                if not self.fused:
+                    self.lib.bz_handoff(x.data_ptr(), recv[i].data_ptr(), x.numel() * 2, self.flag.data_ptr(), 0,
+                                        self.handoff_ctas, self.tgt_stream.cuda_stream)
+                    self._handoffs += self.handoff_ctas
+                kv.advance()
+                handed_at[i] = self._handoffs
+                nbytes += recv[i].numel() * 2
+        logits: list[Optional[torch.Tensor]] = [None] * n
+        with torch.cuda.stream(self.src_stream):
+            for i, (t_i, _) in enumerate(config.splits):
+                h = None
+                if t_i > 0:
+                    gate(self.flag.data_ptr(), handed_at[i], self.src_stream.cuda_stream)
+                    h = recv[i]
+                logits[i] = self.src.decode(tokens[i], caches[i][1], first=t_i, last=L, x=h)
+        cur.wait_stream(self.src_stream)
+        cur.wait_stream(self.tgt_stream)
+        end.record(cur)
+        end.synchronize()
+        return CoopResult(logits=logits, executed_order=[], handoff_bytes=nbytes,
                           total_ms=start.elapsed_time(end))

@@ -10,10 +10,12 @@ and the cooperative executor actually determine on B200:
 * stop-the-world AllCache load (``autoscaler.py:102-117``) -- measured host staging;
 * prefill batch time (``parampool.py:58-59``) -- a least-squares line through
   measured 7B forward passes of the tcgen05 Llama executor;
-* the profiled capacity bound (``autoscaler.py:120-126``) from that line.
+* the profiled capacity bound (``autoscaler.py:120-126``) from that line;
+* decode step time (``parampool.py:61-62``) -- a line through measured KV-cache
+  decode steps of the same executor.
 
-Decode steps and RDMA/SSD edges are not executed on this single box; they keep
-the reference model and are labelled as such in ``describe()``.
+RDMA/SSD edges are not executed on this single box; they keep the reference
+model and are labelled as such in ``describe()``.
 """
 
 from __future__ import annotations
@@ -42,6 +44,8 @@ class MeasuredCosts(ReferenceCosts):
     nvlink_layer_ms: Optional[list[float]] = None   # arrival of unit k after a 1-hop NVLink scale cmd
     nvlink_hop_fill_ms: float = 0.0                   # extra per chain hop (one tile)
     host_layer_ms: Optional[list[float]] = None       # arrival of unit k from the pinned host cache
+    decode_alpha_ms: Optional[float] = None
+    decode_beta_ms: Optional[float] = None
     source: dict = field(default_factory=dict)
 
     name = "b200-measured"
@@ -50,6 +54,11 @@ class MeasuredCosts(ReferenceCosts):
         if self.prefill_alpha_ms is None:
             return super().prefill_ms(model, tokens)
         return self.prefill_alpha_ms + self.prefill_beta_ms * tokens
+
+    def decode_step_ms(self, model, batch: int) -> float:
+        if self.decode_alpha_ms is None:
+            return super().decode_step_ms(model, batch)
+        return self.decode_alpha_ms + self.decode_beta_ms * batch
 
     def capacity_tokens_per_s(self, model, budget: int) -> float:
         return budget / (self.prefill_ms(model, budget) / 1000.0)
@@ -94,6 +103,8 @@ class MeasuredCosts(ReferenceCosts):
             "prefill_alpha_ms": self.prefill_alpha_ms, "prefill_beta_ms": self.prefill_beta_ms,
             "nvlink_layers": "measured" if self.nvlink_layer_ms else "reference-model",
             "host_cache_layers": "measured" if self.host_layer_ms else "reference-model",
-            "decode": "reference-model", "rdma/ssd edges": "reference-model",
+            "decode": "measured" if self.decode_alpha_ms is not None else "reference-model",
+            "decode_alpha_ms": self.decode_alpha_ms, "decode_beta_ms": self.decode_beta_ms,
+            "rdma/ssd edges": "reference-model",
             **self.source,
         }

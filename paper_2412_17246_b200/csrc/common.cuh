@@ -43,4 +43,37 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
 
+// ---- programmatic dependent launch (PDL) ------------------------------------------------
+// The compute kernels (GEMM, Llama glue, decode attention) are launched with
+// programmatic stream serialization, so kernel N+1 is scheduled while kernel N
+// is still running.  Each kernel lets its dependents launch at entry and calls
+// pdl_wait() before it touches anything a predecessor wrote (griddepcontrol.wait
+// returns once the preceding grid has completed and its writes are visible;
+// without the launch attribute both instructions are no-ops).  What overlaps is
+// launch latency and set-up (barrier init, TMEM allocation, descriptor
+// prefetch) and, in the GEMM, the first weight tiles (see BZ_GEMM_B_STATIC).
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
+// kernel classes for the BZ_PDL mask (unset: all; 0: none -- plain stream
+// serialization for A/B checks)
+enum PdlKind { PDL_GEMM = 1, PDL_GLUE = 2, PDL_ATTN = 4 };
+bool pdl_enabled(int kind);
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(int kind, void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                              cudaStream_t stream, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled(kind) ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+}
+
 }  // namespace bz

@@ -139,7 +139,86 @@ struct Params {
   int M, N, K, ldc, ldr;
   int m_tiles, n_tiles;
   uint32_t* signal;  // optional: +1 (release, system scope) per CTA when its tiles are stored
+  // split-K (skinny M, e.g. decode): work unit = (tile, K slice).  Each slice
+  // writes an fp32 partial to ws[slice][M][N] and bumps counters[tile]; the
+  // slice that arrives last sums the partials (+ residual) into C and resets the
+  // counter, so the workspace stays zeroed between calls.  ksplit == 1: off.
+  float* ws;
+  int* counters;
+  int ksplit, kb_per;
+  int a_bytes;   // bytes of one A stage actually loaded (M < 128: only ceil8(M) rows)
+  int b_static;  // B is not written by in-flight predecessors: prefetch it before pdl_wait
 };
+
+// bf16 store of a 32-column accumulator chunk (+ optional residual) for one row
+__device__ __forceinline__ void store_chunk(const Params& p, int row, int col, const uint32_t (&r)[32]) {
+  __nv_bfloat16* out = p.C + static_cast<int64_t>(row) * p.ldc + col;
+  const __nv_bfloat16* res = p.R ? p.R + static_cast<int64_t>(row) * p.ldr + col : nullptr;
+  if (col + 32 <= p.N) {
+    uint32_t w[16];
+    if (res) {
+      const uint4* rv = reinterpret_cast<const uint4*>(res);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        uint4 x = rv[q];
+        const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&x);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          float2 f = __bfloat1622float2(h[j]);
+          w[q * 4 + j] = pack_bf16(__uint_as_float(r[q * 8 + 2 * j]) + f.x, __uint_as_float(r[q * 8 + 2 * j + 1]) + f.y);
+        }
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < 16; ++j) w[j] = pack_bf16(__uint_as_float(r[2 * j]), __uint_as_float(r[2 * j + 1]));
+    }
+    uint4* o = reinterpret_cast<uint4*>(out);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) o[q] = make_uint4(w[4 * q], w[4 * q + 1], w[4 * q + 2], w[4 * q + 3]);
+  } else {
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+      if (col + j < p.N) {
+        float v = __uint_as_float(r[j]);
+        if (res) v += __bfloat162float(res[j]);
+        out[j] = __float2bfloat16_rn(v);
+      }
+    }
+  }
+}
+
+__device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
+
+// Last-arriving K slice of a tile: C[tile] = bf16(sum of the slices' partials + R).
+// 128 epilogue threads sweep the tile's valid rows in 8-column groups.
+__device__ __forceinline__ void splitk_fixup(const Params& p, int m0, int n0, int bn, int et) {
+  const int rows = min(128, p.M - m0);
+  const int cols = min(bn, p.N - n0);
+  const int g8 = cols / 8;
+  for (int idx = et; idx < rows * g8; idx += 128) {
+    const int row = m0 + idx / g8, col = n0 + (idx % g8) * 8;
+    float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    for (int s = 0; s < p.ksplit; ++s) {
+      const float4* src = reinterpret_cast<const float4*>(p.ws + (static_cast<int64_t>(s) * p.M + row) * p.N + col);
+      const float4 a = __ldcg(src), b = __ldcg(src + 1);
+      acc[0] += a.x, acc[1] += a.y, acc[2] += a.z, acc[3] += a.w;
+      acc[4] += b.x, acc[5] += b.y, acc[6] += b.z, acc[7] += b.w;
+    }
+    if (p.R) {
+      const uint4 rv = *reinterpret_cast<const uint4*>(p.R + static_cast<int64_t>(row) * p.ldr + col);
+      const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&rv);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const float2 f = __bfloat1622float2(h[j]);
+        acc[2 * j] += f.x;
+        acc[2 * j + 1] += f.y;
+      }
+    }
+    *reinterpret_cast<uint4*>(p.C + static_cast<int64_t>(row) * p.ldc + col) =
+        make_uint4(pack_bf16(acc[0], acc[1]), pack_bf16(acc[2], acc[3]), pack_bf16(acc[4], acc[5]),
+                   pack_bf16(acc[6], acc[7]));
+  }
+}
 
 template <int BN_>
 __global__ void __launch_bounds__(THREADS, 1)
@@ -156,10 +235,12 @@ __global__ void __launch_bounds__(THREADS, 1)
   uint64_t* acc_full = empty + STAGES;
   uint64_t* acc_empty = acc_full + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
+  volatile int* last_slice = reinterpret_cast<volatile int*>(tmem_slot + 1);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const int num_tiles = p.m_tiles * p.n_tiles;
+  const int num_units = num_tiles * p.ksplit;
   const int k_blocks = (p.K + BK - 1) / BK;
 
   if (warp == 0 && lane == 0) {
@@ -188,13 +269,32 @@ __global__ void __launch_bounds__(THREADS, 1)
   if (warp == 0) {
     if (lane == 0) {
       // ---- TMA producer ----
-      uint32_t stage = 0, phase = 0;
-      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+      // Prologue: with a static B (weights) the first stages' B tiles are issued
+      // before pdl_wait, overlapping the predecessor kernel; A (activations)
+      // follows once the predecessor's writes are visible.
+      int pre = 0, pre_kb0 = 0, pre_m0 = 0;
+      if (p.b_static && blockIdx.x < num_units) {
+        const int tile = blockIdx.x % num_tiles;
+        pre_m0 = (tile % p.m_tiles) * BM;
+        const int n0 = (tile / p.m_tiles) * BN;
+        pre_kb0 = (blockIdx.x / num_tiles) * p.kb_per;
+        pre = min(STAGES, min(k_blocks, pre_kb0 + p.kb_per) - pre_kb0);
+        for (int i = 0; i < pre; ++i) {
+          mbar_expect_tx(&full[i], p.a_bytes + B_BYTES);
+          tma_load_2d(sb + i * B_BYTES, &map_b, (pre_kb0 + i) * BK, n0, &full[i]);
+        }
+      }
+      pdl_wait();
+      for (int i = 0; i < pre; ++i) tma_load_2d(sa + i * A_BYTES, &map_a, (pre_kb0 + i) * BK, pre_m0, &full[i]);
+      uint32_t stage = pre % STAGES, phase = pre == STAGES ? 1u : 0u;
+      for (int unit = blockIdx.x; unit < num_units; unit += gridDim.x) {
+        const int tile = unit % num_tiles;
         const int m0 = (tile % p.m_tiles) * BM;
         const int n0 = (tile / p.m_tiles) * BN;
-        for (int kb = 0; kb < k_blocks; ++kb) {
+        const int kb0 = (unit / num_tiles) * p.kb_per, kb1 = min(k_blocks, kb0 + p.kb_per);
+        for (int kb = kb0 + (unit == static_cast<int>(blockIdx.x) ? pre : 0); kb < kb1; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
-          mbar_expect_tx(&full[stage], STAGE_BYTES);
+          mbar_expect_tx(&full[stage], p.a_bytes + B_BYTES);
           tma_load_2d(sa + stage * A_BYTES, &map_a, kb * BK, m0, &full[stage]);
           tma_load_2d(sb + stage * B_BYTES, &map_b, kb * BK, n0, &full[stage]);
           if (++stage == STAGES) {
@@ -203,20 +303,24 @@ __global__ void __launch_bounds__(THREADS, 1)
           }
         }
       }
+      // every load is issued: let the next kernel launch during the drain
+      pdl_trigger();
     }
   } else if (warp == 1) {
     if (lane == 0) {
       // ---- MMA issuer ----
+      pdl_wait();
       constexpr uint32_t idesc = instr_desc_bf16(BM, BN);
       uint32_t stage = 0, phase = 0;
       int it = 0;
-      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
+      for (int unit = blockIdx.x; unit < num_units; unit += gridDim.x, ++it) {
         const int buf = it & 1;
         const uint32_t use = static_cast<uint32_t>(it >> 1);
+        const int kb0 = (unit / num_tiles) * p.kb_per, kb1 = min(k_blocks, kb0 + p.kb_per);
         mbar_wait(&acc_empty[buf], (use & 1) ^ 1);
         tc_fence_after();
         const uint32_t d = tmem_base + buf * ACC_COLS;
-        for (int kb = 0; kb < k_blocks; ++kb) {
+        for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
           const uint64_t da = umma_desc_sw128(smem_u32(sa + stage * A_BYTES));
@@ -224,7 +328,7 @@ __global__ void __launch_bounds__(THREADS, 1)
 #pragma unroll
           for (int k = 0; k < BK / UMMA_K; ++k) {
             // +32 B along K inside the swizzle atom = +2 in the encoded address
-            umma_bf16(d, da + 2 * k, db + 2 * k, idesc, (kb | k) != 0);
+            umma_bf16(d, da + 2 * k, db + 2 * k, idesc, (kb != kb0 || k != 0) ? 1u : 0u);
           }
           umma_commit(&empty[stage]);
           if (++stage == STAGES) {
@@ -237,9 +341,11 @@ __global__ void __launch_bounds__(THREADS, 1)
     }
   } else if (warp >= 4) {
     // ---- epilogue: TMEM -> registers -> bf16 -> global ----
+    pdl_wait();  // reads the residual and writes C / the split-K workspace
     const int quarter = warp & 3;
     int it = 0;
-    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
+    for (int unit = blockIdx.x; unit < num_units; unit += gridDim.x, ++it) {
+      const int tile = unit % num_tiles;
       const int buf = it & 1;
       const uint32_t use = static_cast<uint32_t>(it >> 1);
       const int m0 = (tile % p.m_tiles) * BM;
@@ -252,47 +358,33 @@ __global__ void __launch_bounds__(THREADS, 1)
       for (int c = 0; c < BN; c += 32) {
         uint32_t r[32];
         tmem_ld_32x32b_x32(taddr + c, r);
-        if (row < p.M) {
-          const int col = n0 + c;
-          __nv_bfloat16* out = p.C + static_cast<int64_t>(row) * p.ldc + col;
-          const __nv_bfloat16* res = p.R ? p.R + static_cast<int64_t>(row) * p.ldr + col : nullptr;
-          if (col + 32 <= p.N) {
-            uint32_t w[16];
-            if (res) {
-              const uint4* rv = reinterpret_cast<const uint4*>(res);
+        if (row >= p.M) continue;
+        if (p.ksplit > 1) {
+          // fp32 partial of this K slice; N % 8 == 0 so 4-column groups are whole
+          float* dst = p.ws + (static_cast<int64_t>(unit / num_tiles) * p.M + row) * p.N + n0 + c;
 #pragma unroll
-              for (int q = 0; q < 4; ++q) {
-                uint4 x = rv[q];
-                const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&x);
-#pragma unroll
-                for (int j = 0; j < 4; ++j) {
-                  float2 f = __bfloat1622float2(h[j]);
-                  w[q * 4 + j] = pack_bf16(__uint_as_float(r[q * 8 + 2 * j]) + f.x,
-                                           __uint_as_float(r[q * 8 + 2 * j + 1]) + f.y);
-                }
-              }
-            } else {
-#pragma unroll
-              for (int j = 0; j < 16; ++j) w[j] = pack_bf16(__uint_as_float(r[2 * j]), __uint_as_float(r[2 * j + 1]));
-            }
-            uint4* o = reinterpret_cast<uint4*>(out);
-#pragma unroll
-            for (int q = 0; q < 4; ++q) o[q] = make_uint4(w[4 * q], w[4 * q + 1], w[4 * q + 2], w[4 * q + 3]);
-          } else {
-#pragma unroll
-            for (int j = 0; j < 32; ++j) {
-              if (col + j < p.N) {
-                float v = __uint_as_float(r[j]);
-                if (res) v += __bfloat162float(res[j]);
-                out[j] = __float2bfloat16_rn(v);
-              }
-            }
-          }
+          for (int q = 0; q < 8; ++q)
+            if (n0 + c + 4 * q < p.N)
+              *reinterpret_cast<uint4*>(dst + 4 * q) = make_uint4(r[4 * q], r[4 * q + 1], r[4 * q + 2], r[4 * q + 3]);
+        } else {
+          store_chunk(p, row, n0 + c, r);
         }
       }
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&acc_empty[buf]);
+      if (p.ksplit > 1) {
+        const int et = threadIdx.x - 128;  // epilogue thread 0..127
+        __threadfence();
+        epi_bar();
+        if (et == 0) *last_slice = atomicAdd(&p.counters[tile], 1) == p.ksplit - 1;
+        epi_bar();
+        if (*last_slice) {
+          __threadfence();
+          splitk_fixup(p, m0, n0, BN, et);
+          if (et == 0) p.counters[tile] = 0;
+        }
+      }
     }
   }
 
@@ -304,6 +396,7 @@ __global__ void __launch_bounds__(THREADS, 1)
   }
   if (p.signal != nullptr && threadIdx.x == 0) {
     // fused hand-off: C may be a peer (NVLink) mapping; publish this CTA's tiles
+    // (with split-K, every fix-up this CTA performed is complete here)
     __threadfence_system();
     asm volatile("red.release.sys.global.add.u32 [%0], 1;" ::"l"(p.signal) : "memory");
   }
@@ -371,43 +464,6 @@ struct CfgPair {
   static_assert(BN % 32 == 0 && BN <= 256 && BN >= 64, "tile N");
 };
 
-// bf16 store of a 32-column accumulator chunk (+ optional residual) for one row
-__device__ __forceinline__ void store_chunk(const Params& p, int row, int col, const uint32_t (&r)[32]) {
-  __nv_bfloat16* out = p.C + static_cast<int64_t>(row) * p.ldc + col;
-  const __nv_bfloat16* res = p.R ? p.R + static_cast<int64_t>(row) * p.ldr + col : nullptr;
-  if (col + 32 <= p.N) {
-    uint32_t w[16];
-    if (res) {
-      const uint4* rv = reinterpret_cast<const uint4*>(res);
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        uint4 x = rv[q];
-        const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&x);
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          float2 f = __bfloat1622float2(h[j]);
-          w[q * 4 + j] = pack_bf16(__uint_as_float(r[q * 8 + 2 * j]) + f.x, __uint_as_float(r[q * 8 + 2 * j + 1]) + f.y);
-        }
-      }
-    } else {
-#pragma unroll
-      for (int j = 0; j < 16; ++j) w[j] = pack_bf16(__uint_as_float(r[2 * j]), __uint_as_float(r[2 * j + 1]));
-    }
-    uint4* o = reinterpret_cast<uint4*>(out);
-#pragma unroll
-    for (int q = 0; q < 4; ++q) o[q] = make_uint4(w[4 * q], w[4 * q + 1], w[4 * q + 2], w[4 * q + 3]);
-  } else {
-#pragma unroll
-    for (int j = 0; j < 32; ++j) {
-      if (col + j < p.N) {
-        float v = __uint_as_float(r[j]);
-        if (res) v += __bfloat162float(res[j]);
-        out[j] = __float2bfloat16_rn(v);
-      }
-    }
-  }
-}
-
 // p.m_tiles counts 256-row pair tiles here
 template <int BN_>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
@@ -459,6 +515,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
 
   if (warp == 0) {
     if (lane == 0) {
+      pdl_wait();
       uint32_t stage = 0, phase = 0;
       for (int tile = cluster; tile < num_tiles; tile += clusters) {
         const int m0 = (tile % p.m_tiles) * (2 * BM) + static_cast<int>(rank) * BM;
@@ -474,9 +531,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
           }
         }
       }
+      pdl_trigger();
     }
   } else if (warp == 1) {
     if (leader && lane == 0) {
+      pdl_wait();
       constexpr uint32_t idesc = instr_desc_bf16(2 * BM, BN);
       uint32_t stage = 0, phase = 0;
       int it = 0;
@@ -503,6 +562,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
       }
     }
   } else if (warp >= 4) {
+    pdl_wait();
     const int quarter = warp & 3;
     const uint32_t leader_acc_empty0 = mapa_cta(smem_u32(&acc_empty[0]), 0);
     int it = 0;
@@ -537,6 +597,34 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     __threadfence_system();
     asm volatile("red.release.sys.global.add.u32 [%0], 1;" ::"l"(p.signal) : "memory");
   }
+}
+
+// workspace = [tile counters (int32, zero between calls) | fp32 partials]
+static int64_t splitk_offset(int tiles) { return (static_cast<int64_t>(tiles) * 4 + 255) / 256 * 256; }
+
+// K slices for a skinny problem: minimise (waves of units) / slices, i.e. the
+// makespan in units of one full-K tile, plus the fp32 partial round trip
+// relative to the weight bytes; each slice keeps >= 4 K blocks of pipeline.
+static int choose_ksplit(int tiles, int k_blocks, int M, int N, int K, int ctas, int64_t ws_bytes, int* kb_per) {
+  int best = 1;
+  double best_t = static_cast<double>((tiles + ctas - 1) / ctas);
+  *kb_per = k_blocks;
+  if (ws_bytes <= 0 || tiles >= ctas) return 1;
+  for (int ks = 2; ks <= 16; ++ks) {
+    const int per = (k_blocks + ks - 1) / ks;
+    if (per < 4) break;
+    const int eff = (k_blocks + per - 1) / per;
+    if (splitk_offset(tiles) + static_cast<int64_t>(eff) * M * N * 4 > ws_bytes) break;
+    const long units = static_cast<long>(tiles) * eff;
+    const double waves = static_cast<double>((units + ctas - 1) / ctas);
+    const double t = waves / eff + static_cast<double>(eff) * M * 8.0 / (2.0 * K);
+    if (t < best_t - 1e-9) {
+      best_t = t;
+      best = eff;
+      *kb_per = per;
+    }
+  }
+  return best;
 }
 
 static int encode_kmajor(CUtensorMap* map, const void* ptr, int rows, int k, int ld, int box_rows) {
@@ -591,7 +679,7 @@ static int pick_bn(int M, int N, int ctas) {
 
 template <int BN_>
 static int launch(const CUtensorMap& ma, const void* B, int N, int K, int ldb, Params p, int max_ctas,
-                  cudaStream_t stream, int* ctas_out) {
+                  int64_t ws_bytes, cudaStream_t stream, int* ctas_out) {
   using Cf = Cfg<BN_>;
   CUtensorMap mb;
   if (int rc = encode_kmajor(&mb, B, N, K, ldb, BN_)) return rc;
@@ -599,8 +687,16 @@ static int launch(const CUtensorMap& ma, const void* B, int N, int K, int ldb, P
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  int grid = p.m_tiles * p.n_tiles;
   const int cap = max_ctas > 0 ? tmin(max_ctas, sms) : sms;
+  const int k_blocks = (K + BK - 1) / BK;
+  p.ksplit = choose_ksplit(p.m_tiles * p.n_tiles, k_blocks, p.M, N, K, cap, ws_bytes, &p.kb_per);
+  if (p.ksplit == 1) {
+    p.kb_per = k_blocks;
+  } else {
+    p.counters = reinterpret_cast<int*>(p.ws);
+    p.ws = reinterpret_cast<float*>(reinterpret_cast<char*>(p.ws) + splitk_offset(p.m_tiles * p.n_tiles));
+  }
+  int grid = p.m_tiles * p.n_tiles * p.ksplit;
   if (grid > cap) grid = cap;
   static bool attr_set[64] = {};
   if (dev < 64 && !attr_set[dev]) {
@@ -609,7 +705,8 @@ static int launch(const CUtensorMap& ma, const void* B, int N, int K, int ldb, P
     if (e != cudaSuccess) return bz_fail_cuda(e, "gemm smem attribute");
     attr_set[dev] = true;
   }
-  k_gemm_bf16<BN_><<<grid, THREADS, Cf::SMEM_BYTES, stream>>>(ma, mb, p);
+  cudaError_t e = launch_pdl(PDL_GEMM, k_gemm_bf16<BN_>, dim3(grid), dim3(THREADS), Cf::SMEM_BYTES, stream, ma, mb, p);
+  if (e != cudaSuccess) return bz_fail_cuda(e, "bz_gemm_bf16 launch");
   if (ctas_out) *ctas_out = grid;
   return bz_check_launch("bz_gemm_bf16");
 }
@@ -621,6 +718,8 @@ static int launch_pair(const CUtensorMap& ma, const void* B, int N, int K, int l
   CUtensorMap mb;
   if (int rc = encode_kmajor(&mb, B, N, K, ldb, BN_ / 2)) return rc;
   p.n_tiles = (N + BN_ - 1) / BN_;
+  p.ksplit = 1;
+  p.kb_per = (K + BK - 1) / BK;
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -635,7 +734,9 @@ static int launch_pair(const CUtensorMap& ma, const void* B, int N, int K, int l
     if (e != cudaSuccess) return bz_fail_cuda(e, "gemm pair smem attribute");
     attr_set[dev] = true;
   }
-  k_gemm_bf16_pair<BN_><<<2 * clusters, THREADS, Cf::SMEM_BYTES, stream>>>(ma, mb, p);
+  cudaError_t e =
+      launch_pdl(PDL_GEMM, k_gemm_bf16_pair<BN_>, dim3(2 * clusters), dim3(THREADS), Cf::SMEM_BYTES, stream, ma, mb, p);
+  if (e != cudaSuccess) return bz_fail_cuda(e, "bz_gemm_bf16 (pair) launch");
   if (ctas_out) *ctas_out = 2 * clusters;
   return bz_check_launch("bz_gemm_bf16 (pair)");
 }
@@ -651,7 +752,8 @@ static int pair_override() {
 }
 
 static int gemm_impl(const void* A, const void* B, void* C, const void* residual, int M, int N, int K, int lda,
-                     int ldb, int ldc, int ldr, int max_ctas, uint32_t* signal, int* ctas_out, void* stream) {
+                     int ldb, int ldc, int ldr, int max_ctas, unsigned flags, void* workspace, int64_t ws_bytes,
+                     uint32_t* signal, int* ctas_out, void* stream) {
   if (!A || !B || !C || M <= 0 || N <= 0 || K <= 0) return bz_fail(BZ_EINVAL, "gemm: bad shape");
   // K tails are zero-filled by TMA (out-of-bounds box columns), so only the
   // 16-byte stride/alignment rules of the tensor maps constrain K.
@@ -659,8 +761,13 @@ static int gemm_impl(const void* A, const void* B, void* C, const void* residual
     return bz_fail(BZ_EINVAL, "gemm: K, N and leading dims must be multiples of 8");
   if ((reinterpret_cast<uintptr_t>(A) | reinterpret_cast<uintptr_t>(B) | reinterpret_cast<uintptr_t>(C)) & 15)
     return bz_fail(BZ_EINVAL, "gemm: operands must be 16-byte aligned");
+  // skinny A: load only the rows that exist (8-row swizzle atoms); the rows of
+  // the 128-row MMA beyond them read stale smem and are never stored
+  const int po = pair_override();
+  const bool pair = po == 1 || (po == -1 && M >= 2 * BM);
+  const int a_box = (!pair && M < BM) ? (M + 7) / 8 * 8 : BM;
   CUtensorMap ma;
-  if (int rc = encode_kmajor(&ma, A, M, K, lda, BM)) return rc;
+  if (int rc = encode_kmajor(&ma, A, M, K, lda, a_box)) return rc;
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -676,10 +783,15 @@ static int gemm_impl(const void* A, const void* B, void* C, const void* residual
   p.m_tiles = (M + BM - 1) / BM;
   p.n_tiles = 0;
   p.signal = signal;
+  p.ws = static_cast<float*>(workspace);
+  p.counters = nullptr;
+  p.a_bytes = a_box * BK * 2;
+  p.b_static = (flags & BZ_GEMM_B_STATIC) ? 1 : 0;
+  p.ksplit = 1;
+  p.kb_per = (K + BK - 1) / BK;
+  if (!workspace || (reinterpret_cast<uintptr_t>(workspace) & 15)) ws_bytes = 0;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const int forced = bn_override();
-  const int po = pair_override();
-  const bool pair = po == 1 || (po == -1 && M >= 2 * BM);
   if (pair) {
     p.m_tiles = (M + 2 * BM - 1) / (2 * BM);
     const int bn = forced ? forced : pick_bn(M, N, ctas);
@@ -695,11 +807,11 @@ static int gemm_impl(const void* A, const void* B, void* C, const void* residual
   const int bn = forced ? forced : pick_bn(M, N, ctas);
   switch (bn) {
     case 128:
-      return launch<128>(ma, B, N, K, ldb, p, max_ctas, s, ctas_out);
+      return launch<128>(ma, B, N, K, ldb, p, max_ctas, ws_bytes, s, ctas_out);
     case 192:
-      return launch<192>(ma, B, N, K, ldb, p, max_ctas, s, ctas_out);
+      return launch<192>(ma, B, N, K, ldb, p, max_ctas, ws_bytes, s, ctas_out);
     default:
-      return launch<256>(ma, B, N, K, ldb, p, max_ctas, s, ctas_out);
+      return launch<256>(ma, B, N, K, ldb, p, max_ctas, ws_bytes, s, ctas_out);
   }
 }
 
@@ -710,12 +822,22 @@ using namespace bz;
 
 extern "C" int bz_gemm_bf16(const void* A, const void* B, void* C, const void* residual, int M, int N, int K,
                             int lda, int ldb, int ldc, int ldr, int max_ctas, void* stream) {
-  return gemm::gemm_impl(A, B, C, residual, M, N, K, lda, ldb, ldc, ldr, max_ctas, nullptr, nullptr, stream);
+  return gemm::gemm_impl(A, B, C, residual, M, N, K, lda, ldb, ldc, ldr, max_ctas, 0u, nullptr, 0, nullptr,
+                         nullptr, stream);
 }
 
 extern "C" int bz_gemm_bf16_signal(const void* A, const void* B, void* C, const void* residual, int M, int N,
                                    int K, int lda, int ldb, int ldc, int ldr, int max_ctas, uint32_t* signal,
                                    int* ctas_out, void* stream) {
   if (!signal || !ctas_out) return bz_fail(BZ_EINVAL, "gemm_signal: signal and ctas_out required");
-  return gemm::gemm_impl(A, B, C, residual, M, N, K, lda, ldb, ldc, ldr, max_ctas, signal, ctas_out, stream);
+  return gemm::gemm_impl(A, B, C, residual, M, N, K, lda, ldb, ldc, ldr, max_ctas, 0u, nullptr, 0, signal,
+                         ctas_out, stream);
+}
+
+extern "C" int bz_gemm_bf16_ex(const void* A, const void* B, void* C, const void* residual, int M, int N, int K,
+                               int lda, int ldb, int ldc, int ldr, int max_ctas, unsigned flags, void* workspace,
+                               int64_t workspace_bytes, uint32_t* signal, int* ctas_out, void* stream) {
+  if (signal && !ctas_out) return bz_fail(BZ_EINVAL, "gemm_ex: a signal needs ctas_out");
+  return gemm::gemm_impl(A, B, C, residual, M, N, K, lda, ldb, ldc, ldr, max_ctas, flags, workspace,
+                         workspace_bytes, signal, ctas_out, stream);
 }

@@ -20,6 +20,8 @@ __device__ __forceinline__ float warp_sum(float v) {
 __global__ void __launch_bounds__(256) k_rmsnorm(const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restrict__ w,
                                                  __nv_bfloat16* __restrict__ y, int d, int ldx, int ldy, float eps) {
   __shared__ float part[8];
+  pdl_trigger();
+  pdl_wait();
   const int row = blockIdx.x;
   const uint4* xr = reinterpret_cast<const uint4*>(x + static_cast<int64_t>(row) * ldx);
   const uint4* wr = reinterpret_cast<const uint4*>(w);
@@ -64,6 +66,8 @@ __global__ void __launch_bounds__(256) k_rmsnorm(const __nv_bfloat16* __restrict
 // fused qkv row: [q heads | k heads | v heads], head_dim hd.
 __global__ void k_rope(__nv_bfloat16* qkv, const int32_t* __restrict__ pos, int n_rot_heads, int hd, int ld,
                        float log2_theta) {
+  pdl_trigger();
+  pdl_wait();
   const int row = blockIdx.x;
   const int half = hd / 2;
   const float p = static_cast<float>(pos[row]);
@@ -85,6 +89,8 @@ __global__ void k_rope(__nv_bfloat16* qkv, const int32_t* __restrict__ pos, int 
 // act[r, j] = silu(gu[r, j]) * gu[r, ffn + j]
 __global__ void k_silu_mul(const __nv_bfloat16* __restrict__ gu, __nv_bfloat16* __restrict__ act, int ffn, int ldg,
                            int lda) {
+  pdl_trigger();
+  pdl_wait();
   const int row = blockIdx.y;
   const __nv_bfloat162* g = reinterpret_cast<const __nv_bfloat162*>(gu + static_cast<int64_t>(row) * ldg);
   const __nv_bfloat162* u = reinterpret_cast<const __nv_bfloat162*>(gu + static_cast<int64_t>(row) * ldg + ffn);
@@ -107,9 +113,10 @@ extern "C" int bz_rmsnorm(const void* x, const void* w, void* y, int rows, int d
                           void* stream) {
   if (!x || !w || !y || rows < 0 || d % 8 || ldx % 8 || ldy % 8) return bz_fail(BZ_EINVAL, "rmsnorm: bad args");
   if (rows == 0) return BZ_OK;
-  llama::k_rmsnorm<<<rows, 256, 0, static_cast<cudaStream_t>(stream)>>>(
-      static_cast<const __nv_bfloat16*>(x), static_cast<const __nv_bfloat16*>(w), static_cast<__nv_bfloat16*>(y), d,
-      ldx, ldy, eps);
+  cudaError_t e = launch_pdl(PDL_GLUE, llama::k_rmsnorm, dim3(rows), dim3(256), 0, static_cast<cudaStream_t>(stream),
+                             static_cast<const __nv_bfloat16*>(x), static_cast<const __nv_bfloat16*>(w),
+                             static_cast<__nv_bfloat16*>(y), d, ldx, ldy, eps);
+  if (e != cudaSuccess) return bz_fail_cuda(e, "bz_rmsnorm");
   return bz_check_launch("bz_rmsnorm");
 }
 
@@ -117,8 +124,9 @@ extern "C" int bz_rope(void* qkv, const int32_t* positions, int rows, int n_rot_
                        float theta, void* stream) {
   if (!qkv || !positions || head_dim % 2 || rows < 0) return bz_fail(BZ_EINVAL, "rope: bad args");
   if (rows == 0) return BZ_OK;
-  llama::k_rope<<<rows, 256, 0, static_cast<cudaStream_t>(stream)>>>(static_cast<__nv_bfloat16*>(qkv), positions,
-                                                                     n_rot_heads, head_dim, ld, log2f(theta));
+  cudaError_t e = launch_pdl(PDL_GLUE, llama::k_rope, dim3(rows), dim3(256), 0, static_cast<cudaStream_t>(stream),
+                             static_cast<__nv_bfloat16*>(qkv), positions, n_rot_heads, head_dim, ld, log2f(theta));
+  if (e != cudaSuccess) return bz_fail_cuda(e, "bz_rope");
   return bz_check_launch("bz_rope");
 }
 
@@ -126,7 +134,8 @@ extern "C" int bz_silu_mul(const void* gu, void* act, int rows, int ffn, int ldg
   if (!gu || !act || ffn % 2 || rows < 0) return bz_fail(BZ_EINVAL, "silu_mul: bad args");
   if (rows == 0) return BZ_OK;
   dim3 grid((ffn / 2 + 255) / 256, rows);
-  llama::k_silu_mul<<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(
-      static_cast<const __nv_bfloat16*>(gu), static_cast<__nv_bfloat16*>(act), ffn, ldg, lda);
+  cudaError_t e = launch_pdl(PDL_GLUE, llama::k_silu_mul, grid, dim3(256), 0, static_cast<cudaStream_t>(stream),
+                             static_cast<const __nv_bfloat16*>(gu), static_cast<__nv_bfloat16*>(act), ffn, ldg, lda);
+  if (e != cudaSuccess) return bz_fail_cuda(e, "bz_silu_mul");
   return bz_check_launch("bz_silu_mul");
 }

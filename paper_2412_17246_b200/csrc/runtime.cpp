@@ -14,6 +14,7 @@
 #include <sys/syscall.h>
 #include <unistd.h>
 
+#include <cstdlib>
 #include <string>
 
 #include "../../include/blitz.h"
@@ -69,6 +70,14 @@ int bz_fail_cu(CUresult r, const char* what) {
   g_last_error = std::string(what) + ": " + (name ? name : "?") + " (" + (str ? str : "?") + ")";
   return r == CUDA_ERROR_NOT_SUPPORTED ? BZ_EUNSUP : BZ_ECUDA;
 }
+bool pdl_enabled(int kind) {
+  static const int mask = [] {
+    const char* e = getenv("BZ_PDL");
+    return e ? atoi(e) : (PDL_GEMM | PDL_GLUE | PDL_ATTN);
+  }();
+  return (mask & kind) != 0;
+}
+
 int bz_check_launch(const char* what) {
   cudaError_t err = cudaGetLastError();
   return err == cudaSuccess ? BZ_OK : bz_fail_cuda(err, what);

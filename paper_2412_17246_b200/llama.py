@@ -29,7 +29,7 @@ from typing import Optional
 
 import torch
 
-from ._native import cuda_lib
+from ._native import BZ_GEMM_B_STATIC, cuda_lib
 from .slab import LlamaArch, SlabLayout
 
 
@@ -111,15 +111,26 @@ class LlamaExecutor:
         self.gu = torch.empty(max_tokens, 2 * a.ffn, dtype=bf, device=dev)
         self.act = torch.empty(max_tokens, a.ffn, dtype=bf, device=dev)
         self.max_tokens = max_tokens
+        # fp32 split-K partials for skinny (decode) GEMMs; one executor = one stream
+        self.splitk_ws = torch.zeros(self.SPLITK_WS_BYTES // 4, dtype=torch.float32, device=dev)
+        self.last_signal_ctas = 0
 
-    def _gemm(self, x, w, out, residual=None):
+    SPLITK_WS_BYTES = 32 << 20
+
+    def _gemm(self, x, w, out, residual=None, signal=None):
+        import ctypes
         m, k = x.shape
         n = w.shape[0]
-        self.lib.bz_gemm_bf16(x.data_ptr(), w.data_ptr(), out.data_ptr(),
-                              residual.data_ptr() if residual is not None else None,
-                              m, n, k, x.stride(0), w.stride(0), out.stride(0),
-                              residual.stride(0) if residual is not None else 0, 0,
-                              torch.cuda.current_stream().cuda_stream)
+        ctas = ctypes.c_int(0)
+        self.lib.bz_gemm_bf16_ex(x.data_ptr(), w.data_ptr(), out.data_ptr(),
+                                 residual.data_ptr() if residual is not None else None,
+                                 m, n, k, x.stride(0), w.stride(0), out.stride(0),
+                                 residual.stride(0) if residual is not None else 0, 0,
+                                 BZ_GEMM_B_STATIC,  # B = slab weights: landed before the layer gate
+                                 self.splitk_ws.data_ptr(), self.SPLITK_WS_BYTES,
+                                 signal.data_ptr() if signal is not None else None, ctypes.byref(ctas),
+                                 torch.cuda.current_stream().cuda_stream)
+        self.last_signal_ctas = ctas.value if signal is not None else 0
         return out
 
     def _rmsnorm(self, x, w, out):
@@ -131,52 +142,81 @@ class LlamaExecutor:
     def embed(self, tokens: torch.Tensor) -> torch.Tensor:
         return self.w.layers[0]["embed"].index_select(0, tokens.reshape(-1)).contiguous()
 
-    @torch.no_grad()
-    def block(self, k: int, x: torch.Tensor, positions: torch.Tensor, bs: tuple[int, int],
-              out: Optional[torch.Tensor] = None, signal: Optional[torch.Tensor] = None) -> torch.Tensor:
-        """x [B*S, d] -> block k output; positions int32 [B*S].
-
-        ``out`` may live on another GPU (peer access): the down-projection GEMM
-        then stores the block output straight into it over NVLink and, with
-        ``signal``, raises that u32 counter by its CTA count when done (the fused
-        hand-off of cooperative execution).  Returns ``out`` (or a new tensor).
-        """
+    def _attn_in(self, k: int, x: torch.Tensor, positions: torch.Tensor):
+        """rmsnorm -> qkv GEMM -> rope; returns q, k, v as [rows, heads, hd] views."""
         a, L = self.arch, self.w.layers[k]
         m = x.shape[0]
-        B, S = bs
-        s = torch.cuda.current_stream().cuda_stream
-        h, qkv, attn, o = self.h[:m], self.qkv[:m], self.attn[:m], self.o[:m]
+        h, qkv = self.h[:m], self.qkv[:m]
         self._rmsnorm(x, L["attn_norm"], h)
         self._gemm(h, L["wqkv"], qkv)
         self.lib.bz_rope(qkv.data_ptr(), positions.data_ptr(), m, a.n_heads + a.n_kv_heads,
-                         a.head_dim, qkv.stride(0), a.rope_theta, s)
+                         a.head_dim, qkv.stride(0), a.rope_theta, torch.cuda.current_stream().cuda_stream)
         hd, H, KV = a.head_dim, a.n_heads, a.n_kv_heads
-        q = qkv[:, : H * hd].view(B, S, H, hd).transpose(1, 2)
-        kk = qkv[:, H * hd:(H + KV) * hd].view(B, S, KV, hd).transpose(1, 2)
-        v = qkv[:, (H + KV) * hd:].view(B, S, KV, hd).transpose(1, 2)
-        att = torch.nn.functional.scaled_dot_product_attention(q, kk, v, is_causal=True,
-                                                               enable_gqa=KV != H)
-        attn.copy_(att.transpose(1, 2).reshape(m, H * hd))
+        return (qkv[:, : H * hd].view(m, H, hd), qkv[:, H * hd:(H + KV) * hd].view(m, KV, hd),
+                qkv[:, (H + KV) * hd:].view(m, KV, hd))
+
+    def _attn_out_mlp(self, k: int, x: torch.Tensor, attn: torch.Tensor,
+                      out: Optional[torch.Tensor], signal: Optional[torch.Tensor]) -> torch.Tensor:
+        """o = attn . Wo^T + x; out = o + mlp(rmsnorm(o)) (optionally fused hand-off)."""
+        a, L = self.arch, self.w.layers[k]
+        m = x.shape[0]
+        s = torch.cuda.current_stream().cuda_stream
+        h, o, gu, act = self.h[:m], self.o[:m], self.gu[:m], self.act[:m]
         self._gemm(attn, L["wo"], o, residual=x)
         self._rmsnorm(o, L["ffn_norm"], h)
-        gu, act = self.gu[:m], self.act[:m]
         self._gemm(h, L["wgu"], gu)
         self.lib.bz_silu_mul(gu.data_ptr(), act.data_ptr(), m, a.ffn, gu.stride(0), act.stride(0), s)
         if out is None:
             out = torch.empty_like(x)
-        if signal is None:
-            self._gemm(act, L["wdown"], out, residual=o)
-            self.last_signal_ctas = 0
-        else:
-            import ctypes
-            ctas = ctypes.c_int(0)
-            w = L["wdown"]
-            self.lib.bz_gemm_bf16_signal(act.data_ptr(), w.data_ptr(), out.data_ptr(), o.data_ptr(),
-                                         m, w.shape[0], act.shape[1], act.stride(0), w.stride(0),
-                                         out.stride(0), o.stride(0), 0, signal.data_ptr(),
-                                         ctypes.byref(ctas), s)
-            self.last_signal_ctas = ctas.value
-        return out
+        return self._gemm(act, L["wdown"], out, residual=o, signal=signal)
+
+    @torch.no_grad()
+    def block(self, k: int, x: torch.Tensor, positions: torch.Tensor, bs: tuple[int, int],
+              out: Optional[torch.Tensor] = None, signal: Optional[torch.Tensor] = None,
+              kv: Optional["KVCache"] = None) -> torch.Tensor:
+        """Prefill of block k: x [B*S, d] -> block output; positions int32 [B*S].
+
+        ``out`` may live on another GPU (peer access): the down-projection GEMM
+        then stores the block output straight into it over NVLink and, with
+        ``signal``, raises that u32 counter by its CTA count when done (the fused
+        hand-off of cooperative execution).  With ``kv`` the block's keys and
+        values land in the cache (positions 0..S-1) for later decode steps.
+        Returns ``out`` (or a new tensor).
+        """
+        a = self.arch
+        m = x.shape[0]
+        B, S = bs
+        H, KV, hd = a.n_heads, a.n_kv_heads, a.head_dim
+        q, kk, v = (t.view(B, S, -1, hd).transpose(1, 2) for t in self._attn_in(k, x, positions))
+        if kv is not None:
+            kv.store_prefill(k, kk, v)
+        att = torch.nn.functional.scaled_dot_product_attention(q, kk, v, is_causal=True,
+                                                               enable_gqa=KV != H)
+        attn = self.attn[:m]
+        attn.copy_(att.transpose(1, 2).reshape(m, H * hd))
+        return self._attn_out_mlp(k, x, attn, out, signal)
+
+    @torch.no_grad()
+    def decode_block(self, k: int, x: torch.Tensor, kv: "KVCache",
+                     out: Optional[torch.Tensor] = None, signal: Optional[torch.Tensor] = None) -> torch.Tensor:
+        """One decode step of block k for B sequences: x [B, d] is the hidden state
+        of each sequence's newest token, at the cache's device position.  Its key/
+        value are appended (bz_rope_append) and it attends over positions 0..pos
+        (bz_decode_attention) -- no host-side position, so the step is graph-safe."""
+        a, L = self.arch, self.w.layers[k]
+        B = x.shape[0]
+        s = torch.cuda.current_stream().cuda_stream
+        h, qkv, attn = self.h[:B], self.qkv[:B], self.attn[:B]
+        self._rmsnorm(x, L["attn_norm"], h)
+        self._gemm(h, L["wqkv"], qkv)
+        kc, vc = kv.k[k], kv.v[k]
+        self.lib.bz_rope_append(qkv.data_ptr(), qkv.stride(0), B, a.n_heads, a.n_kv_heads, a.head_dim,
+                                a.rope_theta, kc.data_ptr(), vc.data_ptr(), kv.max_seq, kv.pos_dev.data_ptr(), s)
+        self.lib.bz_decode_attention(qkv.data_ptr(), qkv.stride(0), kc.data_ptr(), vc.data_ptr(), B, a.n_heads,
+                                     a.n_kv_heads, a.head_dim, kv.max_seq, kv.pos_dev.data_ptr(),
+                                     attn.data_ptr(), attn.stride(0), kv.workspace.data_ptr(),
+                                     kv.workspace.numel(), s)
+        return self._attn_out_mlp(k, x, attn, out, signal)
 
     @torch.no_grad()
     def head(self, x: torch.Tensor, bs: tuple[int, int]) -> torch.Tensor:
@@ -192,13 +232,146 @@ class LlamaExecutor:
 
     @torch.no_grad()
     def forward(self, tokens: torch.Tensor, first: int = 0, last: Optional[int] = None,
-                x: Optional[torch.Tensor] = None) -> torch.Tensor:
-        """Blocks [first, last) (0-based); returns hidden, or logits if last == L."""
+                x: Optional[torch.Tensor] = None, kv: Optional["KVCache"] = None) -> torch.Tensor:
+        """Prefill blocks [first, last) (0-based); returns hidden, or logits if last == L.
+        With ``kv`` (covering those blocks) the prompt's keys/values are cached and
+        ``kv.length`` becomes S."""
         B, S = tokens.shape
         last = self.arch.n_layers if last is None else last
         pos = torch.arange(S, dtype=torch.int32, device=tokens.device).repeat(B)
         if x is None:
             x = self.embed(tokens)
         for k in range(first, last):
-            x = self.block(k, x, pos, (B, S))
+            x = self.block(k, x, pos, (B, S), kv=kv)
+        if kv is not None:
+            kv.length = S
         return self.head(x, (B, S)) if last == self.arch.n_layers else x
+
+    @torch.no_grad()
+    def decode(self, tokens: torch.Tensor, kv: "KVCache", first: int = 0, last: Optional[int] = None,
+               x: Optional[torch.Tensor] = None) -> torch.Tensor:
+        """One decode step over blocks [first, last) for the newest token of each
+        sequence (tokens int64 [B]); returns hidden [B, d], or fp32 logits [B, vocab]
+        if last == L.  Advances ``kv.length`` by one."""
+        last = self.arch.n_layers if last is None else last
+        if x is None:
+            x = self.embed(tokens)
+        for k in range(first, last):
+            x = self.decode_block(k, x, kv)
+        kv.advance()
+        return self.head(x, (x.shape[0], 1)) if last == self.arch.n_layers else x
+
+    def decode_graph(self, kv: "KVCache", first: int = 0, last: Optional[int] = None,
+                     hidden_in: bool = False, head: Optional[bool] = None) -> "DecodeGraph":
+        last = self.arch.n_layers if last is None else last
+        return DecodeGraph(self, kv, first, last, hidden_in, last == self.arch.n_layers if head is None else head)
+
+
+class KVCache:
+    """Keys/values of B equal-length sequences for blocks [first, last) on one GPU,
+    each ``[B, KV, max_seq, hd]`` bf16 (one contiguous [max_seq, hd] panel per
+    sequence and kv head).  Under a ZigZag split the target holds blocks
+    [0, T_i) and the source [T_i, L) of batch i -- exactly where the prefill ran
+    them -- so decode continues with the same split and moves only the [B, d]
+    hand-off.
+
+    The next write position lives on the device (``pos_dev``) and is advanced by
+    the decode step itself, so a captured step replays at every position; the
+    host mirror ``length`` is kept in step by ``advance``.
+    """
+
+    def __init__(self, arch: LlamaArch, batch: int, max_seq: int, device, first: int = 0,
+                 last: Optional[int] = None):
+        from ._native import cuda_lib
+        import ctypes
+
+        last = arch.n_layers if last is None else last
+        shape = (batch, arch.n_kv_heads, max_seq, arch.head_dim)
+        self.k = {l: torch.zeros(shape, dtype=torch.bfloat16, device=device) for l in range(first, last)}
+        self.v = {l: torch.zeros(shape, dtype=torch.bfloat16, device=device) for l in range(first, last)}
+        self.batch, self.max_seq = batch, max_seq
+        self.pos_dev = torch.zeros(1, dtype=torch.int32, device=device)
+        nbytes = ctypes.c_int64(0)
+        cuda_lib().bz_decode_workspace_bytes(batch, arch.n_heads, arch.n_kv_heads, arch.head_dim, max_seq,
+                                             ctypes.byref(nbytes))
+        self.workspace = torch.empty(nbytes.value, dtype=torch.uint8, device=device)
+        self._length = 0
+
+    @property
+    def length(self) -> int:
+        return self._length
+
+    @length.setter
+    def length(self, n: int):
+        if not 0 <= n <= self.max_seq:
+            raise ValueError("cache length out of range")
+        self._length = n
+        self.pos_dev.fill_(n)
+
+    def advance(self):
+        """After a decode step: the device position moves on the current stream."""
+        if self._length >= self.max_seq:
+            raise ValueError("KV cache full")
+        self._length += 1
+        self.pos_dev.add_(1)
+
+    def bytes(self) -> int:
+        return sum(t.numel() * 2 for t in list(self.k.values()) + list(self.v.values()))
+
+    def store_prefill(self, layer: int, k: torch.Tensor, v: torch.Tensor):
+        s = k.shape[2]
+        if s > self.max_seq:
+            raise ValueError("prompt longer than the cache")
+        self.k[layer][:, :, :s].copy_(k)
+        self.v[layer][:, :, :s].copy_(v)
+
+
+class DecodeGraph:
+    """A whole decode step (blocks [first, last), plus the head when last == L)
+    captured once as a CUDA graph and replayed per token: the position comes
+    from ``kv.pos_dev``, so there is no host work per step beyond the replay.
+    ``hidden_in`` feeds a [B, d] hidden state instead of token ids (the source
+    side of a cooperative split)."""
+
+    def __init__(self, ex: "LlamaExecutor", kv: KVCache, first: int, last: int, hidden_in: bool = False,
+                 head: bool = True):
+        self.ex, self.kv, self.first, self.last, self.with_head = ex, kv, first, last, head
+        dev = ex.h.device
+        B = kv.batch
+        self.tokens = torch.zeros(B, dtype=torch.int64, device=dev)
+        self.hidden = torch.zeros(B, ex.arch.d_model, dtype=torch.bfloat16, device=dev) if hidden_in else None
+        side = torch.cuda.Stream(device=dev)
+        side.wait_stream(torch.cuda.current_stream(dev))
+        saved = kv.length
+        with torch.cuda.stream(side):
+            # warm-up outside capture (lazy library init); writes position `saved`,
+            # which the first real step overwrites before attending to it
+            self._body()
+            kv.length = saved
+            side.synchronize()
+            self.graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(self.graph, stream=side):
+                self.out = self._body()
+        torch.cuda.current_stream(dev).wait_stream(side)
+        kv._length = saved
+
+    def _body(self):
+        ex, kv = self.ex, self.kv
+        x = self.hidden if self.hidden is not None else ex.embed(self.tokens)
+        for k in range(self.first, self.last):
+            x = ex.decode_block(k, x, kv)
+        kv.pos_dev.add_(1)
+        if self.with_head:
+            return ex.head(x, (x.shape[0], 1))
+        return x
+
+    def __call__(self, tokens: Optional[torch.Tensor] = None, hidden: Optional[torch.Tensor] = None):
+        if self.kv.length >= self.kv.max_seq:
+            raise ValueError("KV cache full")
+        if tokens is not None:
+            self.tokens.copy_(tokens)
+        if hidden is not None:
+            self.hidden.copy_(hidden)
+        self.graph.replay()
+        self.kv._length += 1
+        return self.out

@@ -72,3 +72,70 @@ def test_gemm_exact_small_integers():
     c = gemm(a, b)
     torch.cuda.synchronize()
     assert torch.equal(c, (a.float() @ b.float().t()).to(torch.bfloat16))
+
+
+def gemm_ex(a, b, residual=None, ws_bytes=32 << 20, signal=None):
+    import ctypes
+    m, k = a.shape
+    n = b.shape[0]
+    c = torch.empty(m, n, dtype=torch.bfloat16, device=a.device)
+    ws = torch.zeros(max(ws_bytes, 16) // 4, dtype=torch.float32, device=a.device)
+    ctas = ctypes.c_int(0)
+    cuda_lib().bz_gemm_bf16_ex(a.data_ptr(), b.data_ptr(), c.data_ptr(),
+                               residual.data_ptr() if residual is not None else None,
+                               m, n, k, a.stride(0), b.stride(0), c.stride(0),
+                               residual.stride(0) if residual is not None else 0, 0, 1,
+                               ws.data_ptr() if ws_bytes else None, ws_bytes,
+                               signal.data_ptr() if signal is not None else None, ctypes.byref(ctas),
+                               torch.cuda.current_stream().cuda_stream)
+    return c, ctas.value
+
+
+@pytest.mark.parametrize("m,n,k", [
+    (1, 4096, 4096), (1, 12288, 4096), (8, 4096, 11008), (64, 22016, 4096), (1, 32000, 4096),
+    (16, 256, 688), (3, 264, 4104), (128, 4096, 4096),
+])
+def test_splitk_skinny_gemm_matches_fp32(m, n, k):
+    """Decode-shaped GEMMs (M = batch rows) split along K into fp32 partials."""
+    torch.manual_seed(m + n + k)
+    a = (torch.randn(m, k, device="cuda") * 0.5).to(torch.bfloat16)
+    b = (torch.randn(n, k, device="cuda") * 0.02).to(torch.bfloat16)
+    r = torch.randn(m, n, device="cuda").to(torch.bfloat16)
+    ref = a.float() @ b.float().t()
+    c, _ = gemm_ex(a, b)
+    c2, _ = gemm_ex(a, b, residual=r)
+    c0, _ = gemm_ex(a, b, ws_bytes=0)           # no workspace: no split
+    torch.cuda.synchronize()
+    _check(c, ref)
+    _check(c2, ref + r.float())
+    _check(c0, ref)
+
+
+def test_splitk_workspace_left_zeroed_and_reusable():
+    """Tile arrival counters are reset by the last slice: the same workspace
+    serves back-to-back calls (as in a replayed decode graph)."""
+    import ctypes
+    torch.manual_seed(6)
+    a = (torch.randn(4, 4096, device="cuda") * 0.5).to(torch.bfloat16)
+    b = (torch.randn(4096, 4096, device="cuda") * 0.02).to(torch.bfloat16)
+    ws = torch.zeros((8 << 20) // 4, dtype=torch.float32, device="cuda")
+    c = torch.empty(4, 4096, dtype=torch.bfloat16, device="cuda")
+    ctas = ctypes.c_int(0)
+    for _ in range(3):
+        cuda_lib().bz_gemm_bf16_ex(a.data_ptr(), b.data_ptr(), c.data_ptr(), None, 4, 4096, 4096, 4096, 4096,
+                                   4096, 0, 0, 0, ws.data_ptr(), 8 << 20, None, ctypes.byref(ctas),
+                                   torch.cuda.current_stream().cuda_stream)
+        torch.cuda.synchronize()
+        _check(c, a.float() @ b.float().t())
+    assert int(ws[:64].view(torch.int32).abs().sum().item()) == 0
+
+
+def test_splitk_signal_counts_reduce_ctas():
+    torch.manual_seed(5)
+    a = (torch.randn(2, 4096, device="cuda") * 0.5).to(torch.bfloat16)
+    b = (torch.randn(4096, 4096, device="cuda") * 0.02).to(torch.bfloat16)
+    sig = torch.zeros(1, dtype=torch.int32, device="cuda")
+    c, ctas = gemm_ex(a, b, signal=sig)
+    torch.cuda.synchronize()
+    assert ctas > 0 and int(sig.item()) == ctas
+    _check(c, a.float() @ b.float().t())

@@ -174,14 +174,15 @@ int bz_gemm_bf16_signal(const void* A, const void* B, void* C, const void* resid
                         int K, int lda, int ldb, int ldc, int ldr, int max_ctas, uint32_t* signal,
                         int* ctas_out, void* stream);
 /* General form.  With a caller-owned fp32 workspace (16-byte aligned) a skinny
- * problem (fewer tiles than SMs, e.g. a decode step's M = batch rows) is split
- * along K: slices write fp32 partials into the workspace and a reduce pass adds
- * them (plus the residual) into C.  The split is chosen per call from the tile
- * count, K and workspace_bytes; workspace = NULL disables it.  signal/ctas_out
- * as in bz_gemm_bf16_signal.  All compute kernels are launched with programmatic
- * dependent launch (set-up overlaps the previous kernel; BZ_PDL=0 disables).  The workspace must be zero-filled before its first
- * use (it holds per-tile arrival counters, which every call leaves at zero) and
- * must not be shared by GEMMs running concurrently. */
+ * problem (M <= 128 and fewer tiles than SMs, e.g. a decode step's M = batch
+ * rows) runs stream-K: the tiles x K-blocks space is cut into equal ranges, one
+ * per CTA; tiles shared by two or more CTAs are summed in fp32 (plus the
+ * residual) by their last contributor.  workspace = NULL disables it.
+ * signal/ctas_out as in bz_gemm_bf16_signal.  All compute kernels are launched
+ * with programmatic dependent launch (set-up overlaps the previous kernel;
+ * BZ_PDL=0 disables).  The workspace must be zero-filled before its first use
+ * (it holds per-tile arrival counters, which every call leaves at zero) and must
+ * not be shared by GEMMs running concurrently. */
 #define BZ_GEMM_B_STATIC 1u /* B is not written by kernels still in flight on the stream (weights):
                                its first tiles may load before the predecessor kernel completes */
 int bz_gemm_bf16_ex(const void* A, const void* B, void* C, const void* residual, int M, int N, int K,

@@ -59,7 +59,7 @@ def measure_prefill(arch: LlamaArch, token_counts: Sequence[int] = (256, 512, 10
 
 
 def measure_decode(arch: LlamaArch, batches: Sequence[int] = (1, 8, 32, 64), context: int = 1024,
-                   iters: int = 10, device: int = 0, probe_layers: int = 8) -> dict:
+                   iters: int = 20, device: int = 0, probe_layers: int = 8, warmup: int = 5) -> dict:
     """ms of one full-model decode step for ``b`` sequences at ``context`` cached
     tokens each: ``probe_layers`` distinct blocks captured as one CUDA graph (as
     served), replayed from position ``context`` on and scaled to the layer count,
@@ -79,14 +79,15 @@ def measure_decode(arch: LlamaArch, batches: Sequence[int] = (1, 8, 32, 64), con
     out = {}
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
     for b in batches:
-        kv = KVCache(probe, b, context + iters + 2, dev)
+        kv = KVCache(probe, b, context + warmup + iters + 2, dev)
         for t in list(kv.k.values()) + list(kv.v.values()):
             t.normal_(0, 1)
         kv.length = context
         step = ex.decode_graph(kv, 0, nl, hidden_in=True, head=False)
         step.hidden.normal_(0, 1)
         x = step.hidden
-        step()
+        for _ in range(warmup):
+            step()
         torch.cuda.synchronize()
         ev[0].record()
         for _ in range(iters):

@@ -17,6 +17,7 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <math.h>
 #include <stdlib.h>
 
 #include "../../include/blitz.h"
@@ -32,22 +33,27 @@ constexpr int A_BYTES = BM * BK * 2;  // 16 KiB
 constexpr int THREADS = 256;
 constexpr int SMEM_LIMIT = 232448;    // 227 KiB dynamic shared memory per CTA
 
-// Tile width N is a template parameter (128 / 192 / 256): the host picks the one
-// that best fills 148 SMs for the problem's tile count; narrower tiles leave room
-// for a deeper smem ring.
+// Single-CTA tiles: the width N is a template parameter (32 .. 256); the smem
+// ring depth is chosen at launch from the bytes one stage really carries (a
+// skinny A stage holds only ceil8(M) rows), up to MAX_STAGES, so a narrow
+// weight tile still keeps ~128 KB of loads in flight per SM.
+constexpr int MAX_STAGES = 32;
+constexpr int BAR_BYTES = (2 * MAX_STAGES + 4) * 8 + 16;  // full/empty ring, acc full/empty, TMEM slot, flag
 template <int BN_>
 struct Cfg {
   static constexpr int BN = BN_;
   static constexpr int B_BYTES = BN * BK * 2;
-  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int STAGES_FIT = (SMEM_LIMIT - 2048) / STAGE_BYTES;
-  static constexpr int STAGES = STAGES_FIT > 8 ? 8 : STAGES_FIT;
   static constexpr int ACC_COLS = BN;  // fp32 accumulator columns per buffer
-  static constexpr int TMEM_COLS = 2 * BN <= 256 ? 256 : 512;  // power-of-two allocation
-  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align slack*/ + 256 /*barriers*/;
+  static constexpr int TMEM_COLS = 2 * BN <= 64 ? 64 : 2 * BN <= 128 ? 128 : 2 * BN <= 256 ? 256 : 512;
+  static constexpr int SMEM_BYTES = SMEM_LIMIT;
   static_assert(BN % 32 == 0 && BN <= 256, "tile N");
-  static_assert(SMEM_BYTES <= SMEM_LIMIT, "smem");
 };
+// ring stages for one A stage of a_stage bytes (multiple of 1024) and B_BYTES
+__host__ __device__ constexpr int ring_stages(int a_stage, int b_bytes) {
+  return (SMEM_LIMIT - 1024 - BAR_BYTES) / (a_stage + b_bytes) < MAX_STAGES
+             ? (SMEM_LIMIT - 1024 - BAR_BYTES) / (a_stage + b_bytes)
+             : MAX_STAGES;
+}
 
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
@@ -139,15 +145,50 @@ struct Params {
   int M, N, K, ldc, ldr;
   int m_tiles, n_tiles;
   uint32_t* signal;  // optional: +1 (release, system scope) per CTA when its tiles are stored
-  // split-K (skinny M, e.g. decode): work unit = (tile, K slice).  Each slice
-  // writes an fp32 partial to ws[slice][M][N] and bumps counters[tile]; the
-  // slice that arrives last sums the partials (+ residual) into C and resets the
-  // counter, so the workspace stays zeroed between calls.  ksplit == 1: off.
+  // Stream-K (skinny M <= 128, e.g. decode, where tiles < SMs): the tiles x
+  // K-blocks iteration space is cut into equal contiguous ranges, one per CTA,
+  // so every SM streams the same weight bytes.  A range covers at most two
+  // partial tiles (its head and tail); a partial writes fp32 to its CTA's slot
+  // ws[cta][0 = head | 1 = tail][M][BN] and bumps counters[tile]; the last
+  // contributor sums the slots (+ residual) into C and resets the counter, so
+  // the workspace stays zeroed between calls.  streamk == 0: whole tiles,
+  // round-robin over a persistent grid.
   float* ws;
   int* counters;
-  int ksplit, kb_per;
+  int streamk, sk_per, sk_total;
   int a_bytes;   // bytes of one A stage actually loaded (M < 128: only ceil8(M) rows)
+  int a_stage;   // smem stride of the A ring (a_bytes rounded up to the 1024-B swizzle atom)
+  int stages;    // ring depth (single-CTA kernel)
   int b_static;  // B is not written by in-flight predecessors: prefetch it before pdl_wait
+};
+
+// The (tile, k0, k1) segments one CTA processes, in order; identical for the
+// producer, MMA and epilogue roles.
+struct SegIter {
+  int i, end, next_tile, k_blocks, num_tiles;
+  bool sk;
+  __device__ SegIter(const Params& p, int kb, int tiles)
+      : k_blocks(kb), num_tiles(tiles), sk(p.streamk != 0) {
+    i = static_cast<int>(blockIdx.x) * p.sk_per;
+    end = min(i + p.sk_per, p.sk_total);
+    next_tile = blockIdx.x;
+  }
+  __device__ bool next(int& tile, int& k0, int& k1) {
+    if (sk) {
+      if (i >= end) return false;
+      tile = i / k_blocks;
+      k0 = i % k_blocks;
+      k1 = min(k_blocks, k0 + (end - i));
+      i += k1 - k0;
+      return true;
+    }
+    if (next_tile >= num_tiles) return false;
+    tile = next_tile;
+    k0 = 0;
+    k1 = k_blocks;
+    next_tile += gridDim.x;
+    return true;
+  }
 };
 
 // bf16 store of a 32-column accumulator chunk (+ optional residual) for one row
@@ -189,34 +230,60 @@ __device__ __forceinline__ void store_chunk(const Params& p, int row, int col, c
 
 __device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
 
-// Last-arriving K slice of a tile: C[tile] = bf16(sum of the slices' partials + R).
-// 128 epilogue threads sweep the tile's valid rows in 8-column groups.
-__device__ __forceinline__ void splitk_fixup(const Params& p, int m0, int n0, int bn, int et) {
-  const int rows = min(128, p.M - m0);
-  const int cols = min(bn, p.N - n0);
-  const int g8 = cols / 8;
-  for (int idx = et; idx < rows * g8; idx += 128) {
-    const int row = m0 + idx / g8, col = n0 + (idx % g8) * 8;
-    float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-    for (int s = 0; s < p.ksplit; ++s) {
-      const float4* src = reinterpret_cast<const float4*>(p.ws + (static_cast<int64_t>(s) * p.M + row) * p.N + col);
-      const float4 a = __ldcg(src), b = __ldcg(src + 1);
-      acc[0] += a.x, acc[1] += a.y, acc[2] += a.z, acc[3] += a.w;
-      acc[4] += b.x, acc[5] += b.y, acc[6] += b.z, acc[7] += b.w;
-    }
-    if (p.R) {
-      const uint4 rv = *reinterpret_cast<const uint4*>(p.R + static_cast<int64_t>(row) * p.ldr + col);
-      const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&rv);
+__device__ __forceinline__ float* sk_slot(const Params& p, int cta, int slot, int bn) {
+  return p.ws + (static_cast<int64_t>(cta) * 2 + slot) * p.M * bn;
+}
+
+// Last contributor of a stream-K tile: C[tile] = bf16(sum of the contributors'
+// slots + R).  Contributor c's segment of tile t sits in its head slot iff c's
+// range starts inside t.  The 128 epilogue threads sweep the [M][bn] slots as
+// flat float4 arrays (coalesced), four float4s per thread per pass and two
+// contributors per round, so each pass keeps 8 independent L2 loads in flight.
+__device__ __forceinline__ void streamk_fixup(const Params& p, int tile, int n0, int bn, int k_blocks, int et) {
+  const int first = tile * k_blocks / p.sk_per, last = ((tile + 1) * k_blocks - 1) / p.sk_per;
+  const int q_row = bn / 4;  // float4s per slot row
+  const int n4 = p.M * q_row;
+  for (int f0 = et; f0 < n4; f0 += 4 * 128) {
+    float4 acc[4];
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const float2 f = __bfloat1622float2(h[j]);
-        acc[2 * j] += f.x;
-        acc[2 * j + 1] += f.y;
+    for (int u = 0; u < 4; ++u) acc[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int c = first; c <= last; c += 2) {
+      const bool two = c + 1 <= last;
+      const float4* s0 =
+          reinterpret_cast<const float4*>(sk_slot(p, c, c * p.sk_per >= tile * k_blocks ? 0 : 1, bn));
+      const float4* s1 = reinterpret_cast<const float4*>(
+          sk_slot(p, two ? c + 1 : c, (c + 1) * p.sk_per >= tile * k_blocks ? 0 : 1, bn));
+      float4 v0[4], v1[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int f = f0 + u * 128;
+        v0[u] = f < n4 ? __ldcg(s0 + f) : make_float4(0.f, 0.f, 0.f, 0.f);
+        v1[u] = (two && f < n4) ? __ldcg(s1 + f) : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        acc[u].x += v0[u].x + v1[u].x;
+        acc[u].y += v0[u].y + v1[u].y;
+        acc[u].z += v0[u].z + v1[u].z;
+        acc[u].w += v0[u].w + v1[u].w;
       }
     }
-    *reinterpret_cast<uint4*>(p.C + static_cast<int64_t>(row) * p.ldc + col) =
-        make_uint4(pack_bf16(acc[0], acc[1]), pack_bf16(acc[2], acc[3]), pack_bf16(acc[4], acc[5]),
-                   pack_bf16(acc[6], acc[7]));
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int f = f0 + u * 128;
+      if (f >= n4) break;
+      const int row = f / q_row, col = n0 + (f % q_row) * 4;
+      if (col >= p.N) continue;
+      float4 v = acc[u];
+      if (p.R) {
+        const uint2 rv = *reinterpret_cast<const uint2*>(p.R + static_cast<int64_t>(row) * p.ldr + col);
+        const float2 r0 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&rv.x));
+        const float2 r1 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&rv.y));
+        v.x += r0.x, v.y += r0.y, v.z += r1.x, v.w += r1.y;
+      }
+      *reinterpret_cast<uint2*>(p.C + static_cast<int64_t>(row) * p.ldc + col) =
+          make_uint2(pack_bf16(v.x, v.y), pack_bf16(v.z, v.w));
+    }
   }
 }
 
@@ -224,23 +291,26 @@ template <int BN_>
 __global__ void __launch_bounds__(THREADS, 1)
     k_gemm_bf16(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b, Params p) {
   using C = Cfg<BN_>;
-  constexpr int BN = C::BN, STAGES = C::STAGES, B_BYTES = C::B_BYTES, STAGE_BYTES = C::STAGE_BYTES;
+  constexpr int BN = C::BN, B_BYTES = C::B_BYTES;
   constexpr int ACC_COLS = C::ACC_COLS, TMEM_COLS = C::TMEM_COLS;
+  const int STAGES = p.stages, A_STAGE = p.a_stage;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* sa = smem;                         // STAGES x A tiles
-  uint8_t* sb = smem + STAGES * A_BYTES;      // STAGES x B tiles
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
-  uint64_t* empty = full + STAGES;
+  // ring: STAGES x A (A_STAGE bytes each) | STAGES x B | barriers.  A skinny A
+  // stage holds only the rows that exist; the 128-row MMA reads past them into
+  // later stages (stale rows, never stored).
+  uint8_t* sa = smem;
+  uint8_t* sb = smem + STAGES * A_STAGE;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sb + STAGES * B_BYTES);
+  uint64_t* empty = full + MAX_STAGES;
   uint64_t* acc_full = empty + STAGES;
   uint64_t* acc_empty = acc_full + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
-  volatile int* last_slice = reinterpret_cast<volatile int*>(tmem_slot + 1);
+  volatile int* last_contrib = reinterpret_cast<volatile int*>(tmem_slot + 1);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const int num_tiles = p.m_tiles * p.n_tiles;
-  const int num_units = num_tiles * p.ksplit;
   const int k_blocks = (p.K + BK - 1) / BK;
 
   if (warp == 0 && lane == 0) {
@@ -272,30 +342,28 @@ __global__ void __launch_bounds__(THREADS, 1)
       // Prologue: with a static B (weights) the first stages' B tiles are issued
       // before pdl_wait, overlapping the predecessor kernel; A (activations)
       // follows once the predecessor's writes are visible.
-      int pre = 0, pre_kb0 = 0, pre_m0 = 0;
-      if (p.b_static && blockIdx.x < num_units) {
-        const int tile = blockIdx.x % num_tiles;
+      SegIter seg(p, k_blocks, num_tiles);
+      int tile, k0, k1, pre = 0, pre_k0 = 0, pre_m0 = 0;
+      bool have = seg.next(tile, k0, k1);
+      if (p.b_static && have) {
         pre_m0 = (tile % p.m_tiles) * BM;
-        const int n0 = (tile / p.m_tiles) * BN;
-        pre_kb0 = (blockIdx.x / num_tiles) * p.kb_per;
-        pre = min(STAGES, min(k_blocks, pre_kb0 + p.kb_per) - pre_kb0);
+        pre_k0 = k0;
+        pre = min(STAGES, k1 - k0);
         for (int i = 0; i < pre; ++i) {
           mbar_expect_tx(&full[i], p.a_bytes + B_BYTES);
-          tma_load_2d(sb + i * B_BYTES, &map_b, (pre_kb0 + i) * BK, n0, &full[i]);
+          tma_load_2d(sb + i * B_BYTES, &map_b, (k0 + i) * BK, (tile / p.m_tiles) * BN, &full[i]);
         }
       }
       pdl_wait();
-      for (int i = 0; i < pre; ++i) tma_load_2d(sa + i * A_BYTES, &map_a, (pre_kb0 + i) * BK, pre_m0, &full[i]);
+      for (int i = 0; i < pre; ++i) tma_load_2d(sa + i * A_STAGE, &map_a, (pre_k0 + i) * BK, pre_m0, &full[i]);
       uint32_t stage = pre % STAGES, phase = pre == STAGES ? 1u : 0u;
-      for (int unit = blockIdx.x; unit < num_units; unit += gridDim.x) {
-        const int tile = unit % num_tiles;
+      for (int skip = pre; have; have = seg.next(tile, k0, k1), skip = 0) {
         const int m0 = (tile % p.m_tiles) * BM;
         const int n0 = (tile / p.m_tiles) * BN;
-        const int kb0 = (unit / num_tiles) * p.kb_per, kb1 = min(k_blocks, kb0 + p.kb_per);
-        for (int kb = kb0 + (unit == static_cast<int>(blockIdx.x) ? pre : 0); kb < kb1; ++kb) {
+        for (int kb = k0 + skip; kb < k1; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           mbar_expect_tx(&full[stage], p.a_bytes + B_BYTES);
-          tma_load_2d(sa + stage * A_BYTES, &map_a, kb * BK, m0, &full[stage]);
+          tma_load_2d(sa + stage * A_STAGE, &map_a, kb * BK, m0, &full[stage]);
           tma_load_2d(sb + stage * B_BYTES, &map_b, kb * BK, n0, &full[stage]);
           if (++stage == STAGES) {
             stage = 0;
@@ -311,24 +379,24 @@ __global__ void __launch_bounds__(THREADS, 1)
       // ---- MMA issuer ----
       pdl_wait();
       constexpr uint32_t idesc = instr_desc_bf16(BM, BN);
+      SegIter seg(p, k_blocks, num_tiles);
+      int tile, k0, k1;
       uint32_t stage = 0, phase = 0;
-      int it = 0;
-      for (int unit = blockIdx.x; unit < num_units; unit += gridDim.x, ++it) {
+      for (int it = 0; seg.next(tile, k0, k1); ++it) {
         const int buf = it & 1;
         const uint32_t use = static_cast<uint32_t>(it >> 1);
-        const int kb0 = (unit / num_tiles) * p.kb_per, kb1 = min(k_blocks, kb0 + p.kb_per);
         mbar_wait(&acc_empty[buf], (use & 1) ^ 1);
         tc_fence_after();
         const uint32_t d = tmem_base + buf * ACC_COLS;
-        for (int kb = kb0; kb < kb1; ++kb) {
+        for (int kb = k0; kb < k1; ++kb) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
-          const uint64_t da = umma_desc_sw128(smem_u32(sa + stage * A_BYTES));
+          const uint64_t da = umma_desc_sw128(smem_u32(sa + stage * A_STAGE));
           const uint64_t db = umma_desc_sw128(smem_u32(sb + stage * B_BYTES));
 #pragma unroll
           for (int k = 0; k < BK / UMMA_K; ++k) {
             // +32 B along K inside the swizzle atom = +2 in the encoded address
-            umma_bf16(d, da + 2 * k, db + 2 * k, idesc, (kb != kb0 || k != 0) ? 1u : 0u);
+            umma_bf16(d, da + 2 * k, db + 2 * k, idesc, (kb != k0 || k != 0) ? 1u : 0u);
           }
           umma_commit(&empty[stage]);
           if (++stage == STAGES) {
@@ -341,15 +409,19 @@ __global__ void __launch_bounds__(THREADS, 1)
     }
   } else if (warp >= 4) {
     // ---- epilogue: TMEM -> registers -> bf16 -> global ----
-    pdl_wait();  // reads the residual and writes C / the split-K workspace
+    pdl_wait();  // reads the residual and writes C / the stream-K workspace
     const int quarter = warp & 3;
-    int it = 0;
-    for (int unit = blockIdx.x; unit < num_units; unit += gridDim.x, ++it) {
-      const int tile = unit % num_tiles;
+    const int et = threadIdx.x - 128;  // epilogue thread 0..127
+    SegIter seg(p, k_blocks, num_tiles);
+    int tile, k0, k1;
+    for (int it = 0; seg.next(tile, k0, k1); ++it) {
       const int buf = it & 1;
       const uint32_t use = static_cast<uint32_t>(it >> 1);
       const int m0 = (tile % p.m_tiles) * BM;
       const int n0 = (tile / p.m_tiles) * BN;
+      const bool partial = k0 != 0 || k1 != k_blocks;
+      // head slot iff this CTA's range starts inside the tile
+      const int slot = static_cast<int>(blockIdx.x) * p.sk_per >= tile * k_blocks ? 0 : 1;
       mbar_wait(&acc_full[buf], use & 1);
       tc_fence_after();
       const int row = m0 + quarter * 32 + lane;
@@ -359,9 +431,8 @@ __global__ void __launch_bounds__(THREADS, 1)
         uint32_t r[32];
         tmem_ld_32x32b_x32(taddr + c, r);
         if (row >= p.M) continue;
-        if (p.ksplit > 1) {
-          // fp32 partial of this K slice; N % 8 == 0 so 4-column groups are whole
-          float* dst = p.ws + (static_cast<int64_t>(unit / num_tiles) * p.M + row) * p.N + n0 + c;
+        if (partial) {
+          float* dst = sk_slot(p, blockIdx.x, slot, BN) + row * BN + c;
 #pragma unroll
           for (int q = 0; q < 8; ++q)
             if (n0 + c + 4 * q < p.N)
@@ -373,15 +444,16 @@ __global__ void __launch_bounds__(THREADS, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&acc_empty[buf]);
-      if (p.ksplit > 1) {
-        const int et = threadIdx.x - 128;  // epilogue thread 0..127
+      if (partial) {
+        const int contributors =
+            ((tile + 1) * k_blocks - 1) / p.sk_per - tile * k_blocks / p.sk_per + 1;
         __threadfence();
         epi_bar();
-        if (et == 0) *last_slice = atomicAdd(&p.counters[tile], 1) == p.ksplit - 1;
+        if (et == 0) *last_contrib = atomicAdd(&p.counters[tile], 1) == contributors - 1;
         epi_bar();
-        if (*last_slice) {
+        if (*last_contrib) {
           __threadfence();
-          splitk_fixup(p, m0, n0, BN, et);
+          streamk_fixup(p, tile, n0, BN, k_blocks, et);
           if (et == 0) p.counters[tile] = 0;
         }
       }
@@ -396,7 +468,7 @@ __global__ void __launch_bounds__(THREADS, 1)
   }
   if (p.signal != nullptr && threadIdx.x == 0) {
     // fused hand-off: C may be a peer (NVLink) mapping; publish this CTA's tiles
-    // (with split-K, every fix-up this CTA performed is complete here)
+    // (with stream-K, every fix-up this CTA performed is complete here)
     __threadfence_system();
     asm volatile("red.release.sys.global.add.u32 [%0], 1;" ::"l"(p.signal) : "memory");
   }
@@ -599,32 +671,72 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
   }
 }
 
-// workspace = [tile counters (int32, zero between calls) | fp32 partials]
-static int64_t splitk_offset(int tiles) { return (static_cast<int64_t>(tiles) * 4 + 255) / 256 * 256; }
+// workspace = [tile counters (int32, zero between calls) | per-CTA head/tail slots]
+static int64_t counters_bytes(int tiles) { return (static_cast<int64_t>(tiles) * 4 + 255) / 256 * 256; }
 
-// K slices for a skinny problem: minimise (waves of units) / slices, i.e. the
-// makespan in units of one full-K tile, plus the fp32 partial round trip
-// relative to the weight bytes; each slice keeps >= 4 K blocks of pipeline.
-static int choose_ksplit(int tiles, int k_blocks, int M, int N, int K, int ctas, int64_t ws_bytes, int* kb_per) {
-  int best = 1;
-  double best_t = static_cast<double>((tiles + ctas - 1) / ctas);
-  *kb_per = k_blocks;
-  if (ws_bytes <= 0 || tiles >= ctas) return 1;
-  for (int ks = 2; ks <= 16; ++ks) {
-    const int per = (k_blocks + ks - 1) / ks;
-    if (per < 4) break;
-    const int eff = (k_blocks + per - 1) / per;
-    if (splitk_offset(tiles) + static_cast<int64_t>(eff) * M * N * 4 > ws_bytes) break;
-    const long units = static_cast<long>(tiles) * eff;
-    const double waves = static_cast<double>((units + ctas - 1) / ctas);
-    const double t = waves / eff + static_cast<double>(eff) * M * 8.0 / (2.0 * K);
-    if (t < best_t - 1e-9) {
-      best_t = t;
-      best = eff;
-      *kb_per = per;
+// BZ_GEMM_STREAMK=0|1 forces stream-K off/on (when feasible); unset: cost model
+static int streamk_override() {
+  static int v = -2;
+  if (v == -2) {
+    const char* e = getenv("BZ_GEMM_STREAMK");
+    v = e ? atoi(e) : -1;
+  }
+  return v;
+}
+
+// Skinny weight streaming on B200 (scripts/skinny_bench.py, profiles/r1_skinny_gemm.txt):
+// a CTA retires one 64-deep K block (4 single-CTA MMAs issued from shared
+// memory) in ~270 ns whatever the tile width up to 128 (~330 ns at 256): the
+// MMA floor, not the bytes, paces a narrow tile; the chip pulls ~5.5 TB/s of
+// weight tiles; stream-K costs ~5 us (partial write, fence, counter, slot sum
+// on the critical path) plus ~0.12 us per row of A at width 128, growing as
+// width^1.5.
+constexpr double SKINNY_CHIP_BPS = 5.5e12, SKINNY_KBLOCK_S = 270e-9;
+constexpr double SKINNY_FIXUP_US = 5.0, SKINNY_FIXUP_US_PER_ROW128 = 0.12;
+
+static double kblock_s(int bn) { return SKINNY_KBLOCK_S * (bn > 200 ? bn / 200.0 : 1.0); }
+
+struct SkinnyPlan {
+  int bn;
+  int sk_per;  // K blocks per CTA under stream-K; 0 = whole tiles
+};
+
+// Tile width and schedule for M <= 128 (one row of tiles): the fastest predicted
+// of {32 .. 256} x {whole tiles, stream-K}.
+static SkinnyPlan plan_skinny(int M, int N, int K, int ctas, int64_t ws_bytes, int only_bn) {
+  const int widths[5] = {256, 192, 128, 64, 32};
+  const int k_blocks = (K + BK - 1) / BK;
+  const double chip = 2.0 * N * K / SKINNY_CHIP_BPS;
+  const int force = streamk_override();
+  SkinnyPlan plain{only_bn ? only_bn : 128, 0}, sk{0, 0};
+  double t_plain = 1e30, t_sk = 1e30;
+  for (int bn : widths) {  // widest first: a narrower tile must win by 2 %
+    if (only_bn && bn != only_bn) continue;
+    const int tiles = (N + bn - 1) / bn;
+    const double waves = static_cast<double>((tiles + ctas - 1) / ctas);
+    const double run = waves * k_blocks * kblock_s(bn);
+    const double t = chip > run ? chip : run;
+    if (t < 0.98 * t_plain) {
+      t_plain = t;
+      plain = {bn, 0};
+    }
+    if (ws_bytes <= 0 || tiles >= ctas) continue;
+    int per = (tiles * k_blocks + ctas - 1) / ctas;
+    if (per < 4) per = 4;
+    if (per >= k_blocks) continue;
+    const int used = (tiles * k_blocks + per - 1) / per;
+    if (counters_bytes(tiles) + static_cast<int64_t>(used) * 2 * M * bn * 4 > ws_bytes) continue;
+    const double sk_run = per * kblock_s(bn);
+    const double wide = bn / 128.0;
+    const double ts = (chip > sk_run ? chip : sk_run) +
+                      (SKINNY_FIXUP_US + SKINNY_FIXUP_US_PER_ROW128 * M * wide * sqrt(wide)) * 1e-6;
+    if (ts < 0.98 * t_sk) {
+      t_sk = ts;
+      sk = {bn, per};
     }
   }
-  return best;
+  if (sk.bn && (force == 1 || (force != 0 && t_sk < t_plain))) return sk;
+  return plain;
 }
 
 static int encode_kmajor(CUtensorMap* map, const void* ptr, int rows, int k, int ld, int box_rows) {
@@ -642,13 +754,13 @@ static int encode_kmajor(CUtensorMap* map, const void* ptr, int rows, int k, int
   return BZ_OK;
 }
 
-// BZ_GEMM_BN=128|192|256 pins the tile width (tests/benchmarks); 0 = automatic
+// BZ_GEMM_BN=32|64|128|192|256 pins the tile width (tests/benchmarks); 0 = automatic
 static int bn_override() {
   static int v = -1;
   if (v < 0) {
     const char* e = getenv("BZ_GEMM_BN");
     v = e ? atoi(e) : 0;
-    if (v != 128 && v != 192 && v != 256) v = 0;
+    if (v != 32 && v != 64 && v != 128 && v != 192 && v != 256) v = 0;
   }
   return v;
 }
@@ -678,8 +790,8 @@ static int pick_bn(int M, int N, int ctas) {
 }
 
 template <int BN_>
-static int launch(const CUtensorMap& ma, const void* B, int N, int K, int ldb, Params p, int max_ctas,
-                  int64_t ws_bytes, cudaStream_t stream, int* ctas_out) {
+static int launch(const CUtensorMap& ma, const void* B, int N, int K, int ldb, Params p, int max_ctas, int sk_per,
+                  cudaStream_t stream, int* ctas_out) {
   using Cf = Cfg<BN_>;
   CUtensorMap mb;
   if (int rc = encode_kmajor(&mb, B, N, K, ldb, BN_)) return rc;
@@ -689,16 +801,19 @@ static int launch(const CUtensorMap& ma, const void* B, int N, int K, int ldb, P
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int cap = max_ctas > 0 ? tmin(max_ctas, sms) : sms;
   const int k_blocks = (K + BK - 1) / BK;
-  p.ksplit = choose_ksplit(p.m_tiles * p.n_tiles, k_blocks, p.M, N, K, cap, ws_bytes, &p.kb_per);
-  if (p.ksplit == 1) {
-    p.kb_per = k_blocks;
-  } else {
+  const int tiles = p.m_tiles * p.n_tiles;
+  int grid = tiles < cap ? tiles : cap;
+  if (sk_per > 0) {
+    p.streamk = 1;
+    p.sk_per = sk_per;
+    p.sk_total = tiles * k_blocks;
     p.counters = reinterpret_cast<int*>(p.ws);
-    p.ws = reinterpret_cast<float*>(reinterpret_cast<char*>(p.ws) + splitk_offset(p.m_tiles * p.n_tiles));
+    p.ws = reinterpret_cast<float*>(reinterpret_cast<char*>(p.ws) + counters_bytes(tiles));
+    grid = (p.sk_total + sk_per - 1) / sk_per;
   }
-  int grid = p.m_tiles * p.n_tiles * p.ksplit;
-  if (grid > cap) grid = cap;
   static bool attr_set[64] = {};
+  p.a_stage = (p.a_bytes + 1023) / 1024 * 1024;
+  p.stages = ring_stages(p.a_stage, Cf::B_BYTES);
   if (dev < 64 && !attr_set[dev]) {
     cudaError_t e =
         cudaFuncSetAttribute(k_gemm_bf16<BN_>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cf::SMEM_BYTES);
@@ -718,8 +833,6 @@ static int launch_pair(const CUtensorMap& ma, const void* B, int N, int K, int l
   CUtensorMap mb;
   if (int rc = encode_kmajor(&mb, B, N, K, ldb, BN_ / 2)) return rc;
   p.n_tiles = (N + BN_ - 1) / BN_;
-  p.ksplit = 1;
-  p.kb_per = (K + BK - 1) / BK;
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -785,10 +898,11 @@ static int gemm_impl(const void* A, const void* B, void* C, const void* residual
   p.signal = signal;
   p.ws = static_cast<float*>(workspace);
   p.counters = nullptr;
+  p.streamk = 0;
+  p.sk_per = 1;
+  p.sk_total = 0;
   p.a_bytes = a_box * BK * 2;
   p.b_static = (flags & BZ_GEMM_B_STATIC) ? 1 : 0;
-  p.ksplit = 1;
-  p.kb_per = (K + BK - 1) / BK;
   if (!workspace || (reinterpret_cast<uintptr_t>(workspace) & 15)) ws_bytes = 0;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const int forced = bn_override();
@@ -804,14 +918,21 @@ static int gemm_impl(const void* A, const void* B, void* C, const void* residual
         return launch_pair<256>(ma, B, N, K, ldb, p, max_ctas, s, ctas_out);
     }
   }
-  const int bn = forced ? forced : pick_bn(M, N, ctas);
-  switch (bn) {
+  SkinnyPlan plan{forced ? forced : pick_bn(M, N, ctas), 0};
+  if (M <= BM) {
+    plan = plan_skinny(M, N, K, ctas, ws_bytes, forced);
+  }
+  switch (plan.bn) {
+    case 32:
+      return launch<32>(ma, B, N, K, ldb, p, max_ctas, plan.sk_per, s, ctas_out);
+    case 64:
+      return launch<64>(ma, B, N, K, ldb, p, max_ctas, plan.sk_per, s, ctas_out);
     case 128:
-      return launch<128>(ma, B, N, K, ldb, p, max_ctas, ws_bytes, s, ctas_out);
+      return launch<128>(ma, B, N, K, ldb, p, max_ctas, plan.sk_per, s, ctas_out);
     case 192:
-      return launch<192>(ma, B, N, K, ldb, p, max_ctas, ws_bytes, s, ctas_out);
+      return launch<192>(ma, B, N, K, ldb, p, max_ctas, plan.sk_per, s, ctas_out);
     default:
-      return launch<256>(ma, B, N, K, ldb, p, max_ctas, ws_bytes, s, ctas_out);
+      return launch<256>(ma, B, N, K, ldb, p, max_ctas, plan.sk_per, s, ctas_out);
   }
 }
 

@@ -111,11 +111,11 @@ class LlamaExecutor:
         self.gu = torch.empty(max_tokens, 2 * a.ffn, dtype=bf, device=dev)
         self.act = torch.empty(max_tokens, a.ffn, dtype=bf, device=dev)
         self.max_tokens = max_tokens
-        # fp32 split-K partials for skinny (decode) GEMMs; one executor = one stream
-        self.splitk_ws = torch.zeros(self.SPLITK_WS_BYTES // 4, dtype=torch.float32, device=dev)
+        # stream-K counters + fp32 partials for skinny (decode) GEMMs; one executor = one stream
+        self.streamk_ws = torch.zeros(self.STREAMK_WS_BYTES // 4, dtype=torch.float32, device=dev)
         self.last_signal_ctas = 0
 
-    SPLITK_WS_BYTES = 32 << 20
+    STREAMK_WS_BYTES = 32 << 20
 
     def _gemm(self, x, w, out, residual=None, signal=None):
         import ctypes
@@ -127,7 +127,7 @@ class LlamaExecutor:
                                  m, n, k, x.stride(0), w.stride(0), out.stride(0),
                                  residual.stride(0) if residual is not None else 0, 0,
                                  BZ_GEMM_B_STATIC,  # B = slab weights: landed before the layer gate
-                                 self.splitk_ws.data_ptr(), self.SPLITK_WS_BYTES,
+                                 self.streamk_ws.data_ptr(), self.STREAMK_WS_BYTES,
                                  signal.data_ptr() if signal is not None else None, ctypes.byref(ctas),
                                  torch.cuda.current_stream().cuda_stream)
         self.last_signal_ctas = ctas.value if signal is not None else 0

@@ -93,10 +93,11 @@ def gemm_ex(a, b, residual=None, ws_bytes=32 << 20, signal=None):
 
 @pytest.mark.parametrize("m,n,k", [
     (1, 4096, 4096), (1, 12288, 4096), (8, 4096, 11008), (64, 22016, 4096), (1, 32000, 4096),
-    (16, 256, 688), (3, 264, 4104), (128, 4096, 4096),
+    (16, 256, 688), (3, 264, 4104), (128, 4096, 4096), (32, 4096, 4096), (64, 4096, 11008),
+    (2, 96, 4096), (5, 40, 64), (1, 1376, 256),
 ])
-def test_splitk_skinny_gemm_matches_fp32(m, n, k):
-    """Decode-shaped GEMMs (M = batch rows) split along K into fp32 partials."""
+def test_streamk_skinny_gemm_matches_fp32(m, n, k):
+    """Decode-shaped GEMMs (M = batch rows) run stream-K: tiles shared by CTAs are summed in fp32."""
     torch.manual_seed(m + n + k)
     a = (torch.randn(m, k, device="cuda") * 0.5).to(torch.bfloat16)
     b = (torch.randn(n, k, device="cuda") * 0.02).to(torch.bfloat16)
@@ -111,7 +112,7 @@ def test_splitk_skinny_gemm_matches_fp32(m, n, k):
     _check(c0, ref)
 
 
-def test_splitk_workspace_left_zeroed_and_reusable():
+def test_streamk_workspace_left_zeroed_and_reusable():
     """Tile arrival counters are reset by the last slice: the same workspace
     serves back-to-back calls (as in a replayed decode graph)."""
     import ctypes
@@ -130,7 +131,7 @@ def test_splitk_workspace_left_zeroed_and_reusable():
     assert int(ws[:64].view(torch.int32).abs().sum().item()) == 0
 
 
-def test_splitk_signal_counts_reduce_ctas():
+def test_streamk_signal_counts_every_cta():
     torch.manual_seed(5)
     a = (torch.randn(2, 4096, device="cuda") * 0.5).to(torch.bfloat16)
     b = (torch.randn(4096, 4096, device="cuda") * 0.02).to(torch.bfloat16)

@@ -292,9 +292,34 @@ def coop_c1(device: int, n_batches: int = 8, seqs: int = 2, seq_len: int = 1000)
     cfg = ss.configure_pipeline(n_batches, arch.n_layers, time_l)
     tl = ss.zigzag_schedule(cfg)
     pair = CooperativePair(source, target, tgt.loaded)
-    ex.launch()                       # fresh transfer: layers arrive while the pair serves
-    res = pair.run(batches, cfg, tl)
+    decode_steps = 8
+    caches = pair.make_caches(batches, cfg, max_new_tokens=decode_steps)
+    ex.launch()                       # untimed warm-up pass (first-use costs of every path)
+    pair.run(batches, cfg, tl, caches=caches)
     ex.synchronize()
+    ex.launch()                       # fresh transfer: layers arrive while the pair serves
+    res = pair.run(batches, cfg, tl, caches=caches)
+    ex.synchronize()
+    # cooperative decode: same split, each side attends over its own KV blocks
+    # (first step eager, the rest one captured two-stream graph per step)
+    toks = [lg.argmax(-1) for lg in res.logits]
+    gen = [[t] for t in toks]
+    step = pair.decode(toks, cfg, caches)
+    toks = [lg.argmax(-1) for lg in step.logits]
+    for gl, t in zip(gen, toks):
+        gl.append(t)
+    graph = pair.decode_graph(toks, cfg, caches)
+    d0, d1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    d0.record()
+    for _ in range(decode_steps - 1):
+        logits = graph(toks)
+        toks = [lg.argmax(-1) for lg in logits]
+        for gl, t in zip(gen, toks):
+            gl.append(t)
+    d1.record()
+    d1.synchronize()
+    dec_ms = d0.elapsed_time(d1)
+    last_logits = [lg.clone() for lg in logits]
     tokens = n_batches * seqs * seq_len
     ref_w = weights_to_cpu_fp32(w)
     torch.set_num_threads(os.cpu_count() or 1)
@@ -308,6 +333,11 @@ def coop_c1(device: int, n_batches: int = 8, seqs: int = 2, seq_len: int = 1000)
     decisive = (top2[:, 0] - top2[:, 1]) > 2e-2 * ref0.abs().max()
     greedy = bool(torch.equal(got.argmax(-1)[decisive], ref0.argmax(-1)[decisive]))
     ties = int((~decisive).sum())
+    # last decode step of batch 0 vs a full fp32 recompute over prompt + generated tokens
+    seq0 = torch.cat([batches[0].cpu()] + [t.cpu()[:, None] for t in gen[0][:-1]], 1)
+    ref_dec = forward_fp32(arch, ref_w, seq0)
+    got_dec = last_logits[0].cpu()
+    dec_rel = float((got_dec - ref_dec).abs().max() / (ref_dec.abs().max() + 1e-6))
     out = {"workload": f"C1 tiny-4l d=256, 1->2 on one GPU, {n_batches} x {seqs * seq_len}-token prefill "
                        f"batches served while the new slab streams from the pinned host cache",
            "time_l_measured": time_l, "splits": cfg.splits, "objective": cfg.objective(),
@@ -315,6 +345,10 @@ def coop_c1(device: int, n_batches: int = 8, seqs: int = 2, seq_len: int = 1000)
            "handoff_bytes": res.handoff_bytes, "max_rel_err_vs_fp32": rel,
            "greedy_equal_where_decisive": greedy, "near_tie_rows": ties,
            "rows": int(ref0.shape[0]),
+           "decode": {"steps": decode_steps, "graph_steps_timed": decode_steps - 1, "ms": dec_ms,
+                      "tokens_per_s": n_batches * seqs * (decode_steps - 1) / (dec_ms / 1e3),
+                      "handoff_bytes_per_step": step.handoff_bytes,
+                      "max_rel_err_vs_fp32_last_step": dec_rel},
            "cpu_fp32_oracle_tokens_per_s": seqs * seq_len / cpu_s,
            "cpu_cores": os.cpu_count()}
     ex.close()
@@ -560,7 +594,8 @@ def run_blitz(args):
                                                          measure_prefill)
             log("c3: measuring prefill and decode")
             pre = measure_prefill(arch, device=fabric.device)
-            dec = measure_decode(arch, device=fabric.device)
+            dec_runs = [measure_decode(arch, device=fabric.device) for _ in range(2)]
+            dec = {b: min(r[b] for r in dec_runs) for b in dec_runs[0]}   # per-size best of two passes
             costs = build_costs(prefill=pre, nvlink_layer_ms=nv, host_layer_ms=host, decode=dec,
                                 source={"prefill_points_ms": pre, "decode_points_ms": dec,
                                         "decode_context_tokens": 1024,

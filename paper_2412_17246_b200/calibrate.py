@@ -59,7 +59,8 @@ def measure_prefill(arch: LlamaArch, token_counts: Sequence[int] = (256, 512, 10
 
 
 def measure_decode(arch: LlamaArch, batches: Sequence[int] = (1, 8, 32, 64), context: int = 1024,
-                   iters: int = 20, device: int = 0, probe_layers: int = 8, warmup: int = 5) -> dict:
+                   iters: int = 20, device: int = 0, probe_layers: int = 8, warmup: int = 5,
+                   trials: int = 3) -> dict:
     """ms of one full-model decode step for ``b`` sequences at ``context`` cached
     tokens each: ``probe_layers`` distinct blocks captured as one CUDA graph (as
     served), replayed from position ``context`` on and scaled to the layer count,
@@ -89,15 +90,22 @@ def measure_decode(arch: LlamaArch, batches: Sequence[int] = (1, 8, 32, 64), con
         for _ in range(warmup):
             step()
         torch.cuda.synchronize()
-        ev[0].record()
-        for _ in range(iters):
-            step()
+        # best of `trials` timed runs (the first graph replays of a fresh process
+        # can run slow while clocks and caches settle)
+        per_block = float("inf")
+        for _ in range(trials):
+            kv.length = context
+            ev[0].record()
+            for _ in range(iters):
+                step()
+            ev[1].record()
+            ev[1].synchronize()
+            per_block = min(per_block, ev[0].elapsed_time(ev[1]) / iters / nl)
         ev[1].record()
         for _ in range(iters):
             ex.head(x, (b, 1))
         ev[2].record()
         ev[2].synchronize()
-        per_block = ev[0].elapsed_time(ev[1]) / iters / nl
         out[b] = per_block * arch.n_layers + ev[1].elapsed_time(ev[2]) / iters
         del step, kv
     slab.close()

@@ -203,3 +203,75 @@ class CooperativePair:
         end.synchronize()
         return CoopResult(logits=logits, executed_order=[], handoff_bytes=nbytes,
                           total_ms=start.elapsed_time(end))
+
+    def decode_graph(self, tokens: Sequence[torch.Tensor], config: PipelineConfig,
+                     caches: list[tuple[KVCache, KVCache]]) -> "CoopDecodeGraph":
+        """The cooperative decode step of ``decode`` captured once as a two-stream
+        CUDA graph (target blocks -> graph edge -> source blocks + head, per batch):
+        once a batch's prefix layers are resident no gate or hand-off counter is
+        needed, and a replay costs no host work per kernel.  Source and target must
+        share a device (one process, one GPU); ``decode`` covers the cross-GPU pair."""
+        if self.src.h.device != self.tgt.h.device:
+            raise NotImplementedError("graph capture of a cross-GPU pair: use decode()")
+        return CoopDecodeGraph(self, tokens, config, caches)
+
+
+class CoopDecodeGraph:
+    def __init__(self, pair: CooperativePair, tokens: Sequence[torch.Tensor], config: PipelineConfig,
+                 caches: list[tuple[KVCache, KVCache]]):
+        self.pair, self.config, self.caches = pair, config, caches
+        src, tgt = pair.src, pair.tgt
+        dev = src.h.device
+        self.tokens = [t.detach().clone() for t in tokens]
+        self.recv = [torch.empty(t.numel(), src.arch.d_model, dtype=torch.bfloat16, device=dev)
+                     for t in tokens]
+        main, side = torch.cuda.Stream(device=dev), torch.cuda.Stream(device=dev)
+        main.wait_stream(torch.cuda.current_stream(dev))
+        saved = [(kt.length, ks.length) for kt, ks in caches]
+        with torch.cuda.stream(main):
+            self._step(main, side)          # warm-up outside capture (lazy library init)
+            for (kt, ks), (lt, ls) in zip(caches, saved):
+                kt.length, ks.length = lt, ls
+            main.synchronize()
+            self.graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(self.graph, stream=main):
+                self.logits = self._step(main, side)
+        torch.cuda.current_stream(dev).wait_stream(main)
+        for (kt, ks), (lt, ls) in zip(caches, saved):
+            kt._length, ks._length = lt, ls
+
+    def _step(self, main, side):
+        pair, L = self.pair, self.pair.src.arch.n_layers
+        out = []
+        side.wait_stream(main)
+        for i, (t_i, _) in enumerate(self.config.splits):
+            kt, ks = self.caches[i]
+            h = None
+            if t_i > 0:
+                with torch.cuda.stream(side):       # target: blocks [0, T_i) into recv[i]
+                    x = pair.tgt.embed(self.tokens[i])
+                    for k in range(t_i):
+                        x = pair.tgt.decode_block(k, x, kt, out=self.recv[i] if k == t_i - 1 else None)
+                    kt.pos_dev.add_(1)
+                main.wait_stream(side)
+                h = self.recv[i]
+            with torch.cuda.stream(main):           # source: blocks [T_i, L) + head
+                x = h if h is not None else pair.src.embed(self.tokens[i])
+                for k in range(t_i, L):
+                    x = pair.src.decode_block(k, x, ks)
+                ks.pos_dev.add_(1)
+                out.append(pair.src.head(x, (x.shape[0], 1)))
+        main.wait_stream(side)
+        return out
+
+    def __call__(self, tokens: Sequence[torch.Tensor]) -> list[torch.Tensor]:
+        if any(ks.length >= ks.max_seq for _, ks in self.caches):
+            raise ValueError("KV cache full")
+        for buf, t in zip(self.tokens, tokens):
+            buf.copy_(t)
+        self.graph.replay()
+        for (t_i, _), (kt, ks) in zip(self.config.splits, self.caches):
+            if t_i > 0:
+                kt._length += 1
+            ks._length += 1
+        return self.logits

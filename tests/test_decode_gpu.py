@@ -230,3 +230,35 @@ def test_rope_append_matches_prefill_rope(H, KV, hd):
     assert torch.equal(kc[:, :, pos].reshape(rows, -1), ref[:, H * hd:(H + KV) * hd])
     assert torch.equal(vc[:, :, pos].reshape(rows, -1), ref[:, (H + KV) * hd:])
     assert int(kc[:, :, :pos].abs().sum().item()) == 0
+
+
+def test_cooperative_decode_graph_matches_eager():
+    """The two-stream captured cooperative step gives the eager step's logits
+    bit for bit, and keeps both sides' cache positions in step."""
+    arch = S.TINY_4L
+    lay, src, w = _slab(arch, seed=6)
+    tgt = DeviceSlab(lay, 0)
+    tgt.data.copy_(src.data)
+    tgt.loaded.fill_(arch.n_layers)
+    cfg = ss.configure_pipeline(3, arch.n_layers, 1.0)
+    batches = [_prompt(2, 24, 50 + i, arch.vocab) for i in range(3)]
+    runs = []
+    for _ in range(2):
+        pair = CooperativePair(LlamaExecutor(w, max_tokens=64, device="cuda"),
+                               LlamaExecutor(SlabWeights(arch, lay, tgt.data), max_tokens=64, device="cuda"),
+                               tgt.loaded)
+        caches = pair.make_caches(batches, cfg, max_new_tokens=4)
+        res = pair.run(batches, cfg, ss.zigzag_schedule(cfg), caches=caches)
+        runs.append((pair, caches, [lg.argmax(-1) for lg in res.logits]))
+    (pe, ce, toks), (pg, cg, toks_g) = runs
+    graph = pg.decode_graph(toks_g, cfg, cg)
+    for _ in range(3):
+        eager = pe.decode(toks, cfg, ce).logits
+        replay = [lg.clone() for lg in graph(toks)]
+        for a, b in zip(eager, replay):
+            assert torch.equal(a, b)
+        for (t_i, _), (kt, ks), (kt2, ks2) in zip(cfg.splits, ce, cg):
+            assert ks.length == ks2.length and (t_i == 0 or kt.length == kt2.length)
+        toks = [lg.argmax(-1) for lg in eager]
+    tgt.close()
+    src.close()

@@ -524,25 +524,36 @@ __device__ __forceinline__ void umma_commit_pair(uint64_t* bar) {
       : "memory");
 }
 
-template <int BN_>
+// A pair tile is 256 rows x (NSUB * BN) columns: NSUB independent M256xBN
+// accumulators, each fed by the same A stage, so NSUB = 2 halves the A bytes per
+// MAC (the smem feed, not the MMA, bounds this kernel: with loads elided it runs
+// at 1.9 PFLOP/s).  TMEM holds two tiles (double-buffered epilogue) when
+// 2 * NSUB * BN <= 512 columns, else one.
+template <int BN_, int NSUB_ = 1>
 struct CfgPair {
   static constexpr int BN = BN_;
-  static constexpr int B_BYTES = (BN / 2) * BK * 2;  // this CTA's half of the B tile
+  static constexpr int NSUB = NSUB_;
+  static constexpr int TILE_N = BN * NSUB;
+  static constexpr int B_SUB = (BN / 2) * BK * 2;    // this CTA's half of one sub-tile's B
+  static constexpr int B_BYTES = NSUB * B_SUB;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int STAGES_FIT = (SMEM_LIMIT - 2048) / STAGE_BYTES;
   static constexpr int STAGES = STAGES_FIT > 8 ? 8 : STAGES_FIT;
-  static constexpr int TMEM_COLS = 2 * BN <= 256 ? 256 : 512;
+  static constexpr int ACC_BUFS = 2 * TILE_N <= 512 ? 2 : 1;
+  static constexpr int TMEM_COLS = ACC_BUFS * TILE_N <= 256 ? 256 : 512;
   static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 256;
   static_assert(BN % 32 == 0 && BN <= 256 && BN >= 64, "tile N");
+  static_assert(ACC_BUFS * TILE_N <= 512, "TMEM");
 };
 
 // p.m_tiles counts 256-row pair tiles here
-template <int BN_>
+template <int BN_, int NSUB_>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     k_gemm_bf16_pair(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b, Params p) {
-  using C = CfgPair<BN_>;
-  constexpr int BN = C::BN, STAGES = C::STAGES, B_BYTES = C::B_BYTES, STAGE_BYTES = C::STAGE_BYTES;
-  constexpr int TMEM_COLS = C::TMEM_COLS;
+  using C = CfgPair<BN_, NSUB_>;
+  constexpr int BN = C::BN, NSUB = C::NSUB, TILE_N = C::TILE_N, STAGES = C::STAGES;
+  constexpr int B_SUB = C::B_SUB, B_BYTES = C::B_BYTES, STAGE_BYTES = C::STAGE_BYTES;
+  constexpr int ACC_BUFS = C::ACC_BUFS, TMEM_COLS = C::TMEM_COLS;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sa = smem;
@@ -591,12 +602,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
       uint32_t stage = 0, phase = 0;
       for (int tile = cluster; tile < num_tiles; tile += clusters) {
         const int m0 = (tile % p.m_tiles) * (2 * BM) + static_cast<int>(rank) * BM;
-        const int n0 = (tile / p.m_tiles) * BN + static_cast<int>(rank) * (BN / 2);
+        const int n0 = (tile / p.m_tiles) * TILE_N + static_cast<int>(rank) * (BN / 2);
         for (int kb = 0; kb < k_blocks; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           if (leader) mbar_expect_tx(&full[stage], 2 * STAGE_BYTES);
           tma_load_2d_pair(sa + stage * A_BYTES, &map_a, kb * BK, m0, &full[stage]);
-          tma_load_2d_pair(sb + stage * B_BYTES, &map_b, kb * BK, n0, &full[stage]);
+#pragma unroll
+          for (int j = 0; j < NSUB; ++j)
+            tma_load_2d_pair(sb + stage * B_BYTES + j * B_SUB, &map_b, kb * BK, n0 + j * BN, &full[stage]);
           if (++stage == STAGES) {
             stage = 0;
             phase ^= 1;
@@ -612,18 +625,23 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
       uint32_t stage = 0, phase = 0;
       int it = 0;
       for (int tile = cluster; tile < num_tiles; tile += clusters, ++it) {
-        const int buf = it & 1;
-        const uint32_t use = static_cast<uint32_t>(it >> 1);
+        const int buf = it % ACC_BUFS;
+        const uint32_t use = static_cast<uint32_t>(it / ACC_BUFS);
         mbar_wait(&acc_empty[buf], (use & 1) ^ 1);
         tc_fence_after();
-        const uint32_t d = tmem_base + buf * BN;
+        const uint32_t d = tmem_base + buf * TILE_N;
         for (int kb = 0; kb < k_blocks; ++kb) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
           const uint64_t da = umma_desc_sw128(smem_u32(sa + stage * A_BYTES));
-          const uint64_t db = umma_desc_sw128(smem_u32(sb + stage * B_BYTES));
 #pragma unroll
-          for (int k = 0; k < BK / UMMA_K; ++k) umma_bf16_pair(d, da + 2 * k, db + 2 * k, idesc, (kb | k) != 0);
+          for (int k = 0; k < BK / UMMA_K; ++k) {
+#pragma unroll
+            for (int j = 0; j < NSUB; ++j) {
+              const uint64_t db = umma_desc_sw128(smem_u32(sb + stage * B_BYTES + j * B_SUB));
+              umma_bf16_pair(d + j * BN, da + 2 * k, db + 2 * k, idesc, (kb | k) != 0);
+            }
+          }
           umma_commit_pair(&empty[stage]);
           if (++stage == STAGES) {
             stage = 0;
@@ -639,19 +657,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     const uint32_t leader_acc_empty0 = mapa_cta(smem_u32(&acc_empty[0]), 0);
     int it = 0;
     for (int tile = cluster; tile < num_tiles; tile += clusters, ++it) {
-      const int buf = it & 1;
-      const uint32_t use = static_cast<uint32_t>(it >> 1);
+      const int buf = it % ACC_BUFS;
+      const uint32_t use = static_cast<uint32_t>(it / ACC_BUFS);
       const int m0 = (tile % p.m_tiles) * (2 * BM) + static_cast<int>(rank) * BM;
-      const int n0 = (tile / p.m_tiles) * BN;
+      const int n0 = (tile / p.m_tiles) * TILE_N;
       mbar_wait(&acc_full[buf], use & 1);
       tc_fence_after();
       const int row = m0 + quarter * 32 + lane;
-      const uint32_t taddr = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + buf * BN;
+      const uint32_t taddr = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + buf * TILE_N;
 #pragma unroll 1
-      for (int c = 0; c < BN; c += 32) {
+      for (int c = 0; c < TILE_N; c += 32) {
         uint32_t r[32];
         tmem_ld_32x32b_x32(taddr + c, r);
-        if (row < p.M) store_chunk(p, row, n0 + c, r);
+        if (row < p.M && n0 + c < p.N) store_chunk(p, row, n0 + c, r);
       }
       tc_fence_before();
       __syncwarp();
@@ -826,13 +844,13 @@ static int launch(const CUtensorMap& ma, const void* B, int N, int K, int ldb, P
   return bz_check_launch("bz_gemm_bf16");
 }
 
-template <int BN_>
+template <int BN_, int NSUB_>
 static int launch_pair(const CUtensorMap& ma, const void* B, int N, int K, int ldb, Params p, int max_ctas,
                        cudaStream_t stream, int* ctas_out) {
-  using Cf = CfgPair<BN_>;
+  using Cf = CfgPair<BN_, NSUB_>;
   CUtensorMap mb;
   if (int rc = encode_kmajor(&mb, B, N, K, ldb, BN_ / 2)) return rc;
-  p.n_tiles = (N + BN_ - 1) / BN_;
+  p.n_tiles = (N + Cf::TILE_N - 1) / Cf::TILE_N;
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -842,13 +860,13 @@ static int launch_pair(const CUtensorMap& ma, const void* B, int N, int K, int l
   if (clusters < 1) clusters = 1;
   static bool attr_set[64] = {};
   if (dev < 64 && !attr_set[dev]) {
-    cudaError_t e =
-        cudaFuncSetAttribute(k_gemm_bf16_pair<BN_>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cf::SMEM_BYTES);
+    cudaError_t e = cudaFuncSetAttribute(k_gemm_bf16_pair<BN_, NSUB_>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         Cf::SMEM_BYTES);
     if (e != cudaSuccess) return bz_fail_cuda(e, "gemm pair smem attribute");
     attr_set[dev] = true;
   }
-  cudaError_t e =
-      launch_pdl(PDL_GEMM, k_gemm_bf16_pair<BN_>, dim3(2 * clusters), dim3(THREADS), Cf::SMEM_BYTES, stream, ma, mb, p);
+  cudaError_t e = launch_pdl(PDL_GEMM, k_gemm_bf16_pair<BN_, NSUB_>, dim3(2 * clusters), dim3(THREADS),
+                             Cf::SMEM_BYTES, stream, ma, mb, p);
   if (e != cudaSuccess) return bz_fail_cuda(e, "bz_gemm_bf16 (pair) launch");
   if (ctas_out) *ctas_out = 2 * clusters;
   return bz_check_launch("bz_gemm_bf16 (pair)");
@@ -862,6 +880,50 @@ static int pair_override() {
     v = e ? atoi(e) : -1;
   }
   return v;
+}
+
+// BZ_GEMM_NSUB=1|2 pins the pair kernel's sub-tiles per A stage (tests); 0 = model
+static int nsub_override() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("BZ_GEMM_NSUB");
+    v = e ? atoi(e) : 0;
+    if (v != 1 && v != 2) v = 0;
+  }
+  return v;
+}
+
+// Pair-kernel tile choice from measured per-K-block times (scripts/gemm_bench.py
+// with BZ_GEMM_BN / BZ_GEMM_NSUB pinned, 7B block shapes at 2000 tokens; see
+// profiles/r1_gemm_pair_configs.txt).  The kernel is bound by the smem feed (with
+// its loads elided it runs at 1.9 PFLOP/s), so wider tiles pay less per MAC;
+// NSUB = 2 (one TMEM buffer) additionally exposes ~8.6 us of epilogue and
+// pipeline refill per tile.  Minimise waves x (K blocks x t_kb + exposed).
+struct PairPlan {
+  int bn, nsub;
+  double kb_s, tile_s;
+};
+static PairPlan plan_pair(int m_tiles, int N, int K, int clusters, int only_bn, int only_nsub) {
+  const PairPlan cands[5] = {{256, 1, 0.378e-6, 0.0},
+                             {256, 2, 0.677e-6, 8.6e-6},
+                             {192, 1, 0.332e-6, 0.0},
+                             {192, 2, 0.600e-6, 8.6e-6},
+                             {128, 1, 0.276e-6, 0.0}};
+  const int k_blocks = (K + BK - 1) / BK;
+  PairPlan best = cands[0];
+  double best_t = 1e30;
+  for (const PairPlan& c : cands) {
+    if ((only_bn && c.bn != only_bn) || (only_nsub && c.nsub != only_nsub)) continue;
+    const int tile_n = c.bn * c.nsub;
+    const long tiles = static_cast<long>(m_tiles) * ((N + tile_n - 1) / tile_n);
+    const double waves = static_cast<double>((tiles + clusters - 1) / clusters);
+    const double t = waves * (k_blocks * c.kb_s + c.tile_s);
+    if (t < best_t) {
+      best_t = t;
+      best = c;
+    }
+  }
+  return best;
 }
 
 static int gemm_impl(const void* A, const void* B, void* C, const void* residual, int M, int N, int K, int lda,
@@ -908,14 +970,18 @@ static int gemm_impl(const void* A, const void* B, void* C, const void* residual
   const int forced = bn_override();
   if (pair) {
     p.m_tiles = (M + 2 * BM - 1) / (2 * BM);
-    const int bn = forced ? forced : pick_bn(M, N, ctas);
-    switch (bn) {
-      case 128:
-        return launch_pair<128>(ma, B, N, K, ldb, p, max_ctas, s, ctas_out);
-      case 192:
-        return launch_pair<192>(ma, B, N, K, ldb, p, max_ctas, s, ctas_out);
+    const PairPlan pp = plan_pair(p.m_tiles, N, K, ctas / 2, forced, nsub_override());
+    switch (pp.bn * 10 + pp.nsub) {
+      case 1281:
+        return launch_pair<128, 1>(ma, B, N, K, ldb, p, max_ctas, s, ctas_out);
+      case 1921:
+        return launch_pair<192, 1>(ma, B, N, K, ldb, p, max_ctas, s, ctas_out);
+      case 1922:
+        return launch_pair<192, 2>(ma, B, N, K, ldb, p, max_ctas, s, ctas_out);
+      case 2562:
+        return launch_pair<256, 2>(ma, B, N, K, ldb, p, max_ctas, s, ctas_out);
       default:
-        return launch_pair<256>(ma, B, N, K, ldb, p, max_ctas, s, ctas_out);
+        return launch_pair<256, 1>(ma, B, N, K, ldb, p, max_ctas, s, ctas_out);
     }
   }
   SkinnyPlan plan{forced ? forced : pick_bn(M, N, ctas), 0};

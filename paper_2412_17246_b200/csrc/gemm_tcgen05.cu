@@ -237,31 +237,32 @@ __device__ __forceinline__ float* sk_slot(const Params& p, int cta, int slot, in
 // Last contributor of a stream-K tile: C[tile] = bf16(sum of the contributors'
 // slots + R).  Contributor c's segment of tile t sits in its head slot iff c's
 // range starts inside t.  The 128 epilogue threads sweep the [M][bn] slots as
-// flat float4 arrays (coalesced), four float4s per thread per pass and two
-// contributors per round, so each pass keeps 8 independent L2 loads in flight.
+// flat float4 arrays (coalesced), eight float4s per thread per pass and two
+// contributors per round, so each pass keeps 16 independent L2 loads in flight.
 __device__ __forceinline__ void streamk_fixup(const Params& p, int tile, int n0, int bn, int k_blocks, int et) {
+  constexpr int U = 8;  // float4s per thread per pass: 2 x 8 independent L2 loads in flight
   const int first = tile * k_blocks / p.sk_per, last = ((tile + 1) * k_blocks - 1) / p.sk_per;
   const int q_row = bn / 4;  // float4s per slot row
   const int n4 = p.M * q_row;
-  for (int f0 = et; f0 < n4; f0 += 4 * 128) {
-    float4 acc[4];
+  for (int f0 = et; f0 < n4; f0 += U * 128) {
+    float4 acc[U];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) acc[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int u = 0; u < U; ++u) acc[u] = make_float4(0.f, 0.f, 0.f, 0.f);
     for (int c = first; c <= last; c += 2) {
       const bool two = c + 1 <= last;
       const float4* s0 =
           reinterpret_cast<const float4*>(sk_slot(p, c, c * p.sk_per >= tile * k_blocks ? 0 : 1, bn));
       const float4* s1 = reinterpret_cast<const float4*>(
           sk_slot(p, two ? c + 1 : c, (c + 1) * p.sk_per >= tile * k_blocks ? 0 : 1, bn));
-      float4 v0[4], v1[4];
+      float4 v0[U], v1[U];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
+      for (int u = 0; u < U; ++u) {
         const int f = f0 + u * 128;
         v0[u] = f < n4 ? __ldcg(s0 + f) : make_float4(0.f, 0.f, 0.f, 0.f);
         v1[u] = (two && f < n4) ? __ldcg(s1 + f) : make_float4(0.f, 0.f, 0.f, 0.f);
       }
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
+      for (int u = 0; u < U; ++u) {
         acc[u].x += v0[u].x + v1[u].x;
         acc[u].y += v0[u].y + v1[u].y;
         acc[u].z += v0[u].z + v1[u].z;
@@ -269,7 +270,7 @@ __device__ __forceinline__ void streamk_fixup(const Params& p, int tile, int n0,
       }
     }
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
+    for (int u = 0; u < U; ++u) {
       const int f = f0 + u * 128;
       if (f >= n4) break;
       const int row = f / q_row, col = n0 + (f % q_row) * 4;
@@ -707,10 +708,10 @@ static int streamk_override() {
 // memory) in ~270 ns whatever the tile width up to 128 (~330 ns at 256): the
 // MMA floor, not the bytes, paces a narrow tile; the chip pulls ~5.5 TB/s of
 // weight tiles; stream-K costs ~5 us (partial write, fence, counter, slot sum
-// on the critical path) plus ~0.12 us per row of A at width 128, growing as
+// on the critical path) plus ~0.09 us per row of A at width 128, growing as
 // width^1.5.
 constexpr double SKINNY_CHIP_BPS = 5.5e12, SKINNY_KBLOCK_S = 270e-9;
-constexpr double SKINNY_FIXUP_US = 5.0, SKINNY_FIXUP_US_PER_ROW128 = 0.12;
+constexpr double SKINNY_FIXUP_US = 5.0, SKINNY_FIXUP_US_PER_ROW128 = 0.09;
 
 static double kblock_s(int bn) { return SKINNY_KBLOCK_S * (bn > 200 ? bn / 200.0 : 1.0); }
 

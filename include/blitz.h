@@ -158,6 +158,12 @@ int bz_tile_fingerprints(const void* base, const int64_t* tile_off, int t0, int 
  * flag store (activation handoff of cooperative execution). */
 int bz_handoff(const void* src, void* dst, uint64_t bytes, uint32_t* flag, uint32_t value,
                int nctas, void* stream);
+/* Copy the first panel_bytes of each of n_panels panels (src + q*src_stride ->
+ * dst + q*dst_stride; dst may be a peer mapping).  KV consolidation after a
+ * cooperative prefill: the source's [T_i, L) KV prefixes move to the new
+ * instance (simcore.py:462-514 as real NVLink bytes). */
+int bz_copy_panels(const void* src, void* dst, int64_t n_panels, int64_t src_stride, int64_t dst_stride,
+                   int64_t panel_bytes, int nctas, void* stream);
 
 /* ---- tensor-core GEMM (tcgen05 + TMEM + TMA) ----------------------------------------- */
 /* C[M,N] = A[M,K] . B[N,K]^T (+ residual[M,N]), all bf16 row-major, fp32 accumulate in

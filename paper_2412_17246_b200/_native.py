@@ -127,6 +127,7 @@ _SIGNATURES = {
     "bz_fill_random": [_P, _U64, _U64, _P],
     "bz_tile_fingerprints": [_P, _P, _I, _I, _P, _P],
     "bz_handoff": [_P, _P, _U64, _P, _U32, _I, _P],
+    "bz_copy_panels": [_P, _P, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, _I, _P],
     "bz_gemm_bf16": [_P, _P, _P, _P, _I, _I, _I, _I, _I, _I, _I, _I, _P],
     "bz_gemm_bf16_signal": [_P, _P, _P, _P, _I, _I, _I, _I, _I, _I, _I, _I, _P, _PI, _P],
     "bz_gemm_bf16_ex": [_P, _P, _P, _P, _I, _I, _I, _I, _I, _I, _I, _I, ctypes.c_uint, _P, ctypes.c_int64, _P,

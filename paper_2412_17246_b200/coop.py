@@ -204,6 +204,45 @@ class CooperativePair:
         return CoopResult(logits=logits, executed_order=[], handoff_bytes=nbytes,
                           total_ms=start.elapsed_time(end))
 
+    @torch.no_grad()
+    def consolidate(self, caches: list[tuple[KVCache, KVCache]], nctas: int = 64
+                    ) -> tuple[list[KVCache], int, float]:
+        """Hand the sequences to the new instance once its weights are resident: the
+        source's KV blocks [T_i, L) (their cached prefix only) are copied to the
+        target's device (``bz_copy_panels``; NVLink when the pair spans two GPUs) and
+        merged with the target's own [0, T_i) blocks, so the target decodes alone and
+        the source is free (the KV hand-over the reference accounts as a flow,
+        simcore.py:462-514).  Returns (full caches on the target, bytes moved, ms)."""
+        tdev, sdev = self.tgt.h.device, self.src.h.device
+        a = self.src.arch
+        nbytes = 0
+        out = []
+        with torch.cuda.device(sdev):
+            s = torch.cuda.current_stream(sdev)
+            t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            t0.record(s)
+            for kt, ks in caches:
+                full = KVCache(self.tgt.arch, kt.batch, kt.max_seq, tdev, 0, 0)
+                full.k.update(kt.k)
+                full.v.update(kt.v)
+                stride = kt.max_seq * a.head_dim * 2
+                prefix = ks.length * a.head_dim * 2
+                panels = kt.batch * a.n_kv_heads
+                for layer in sorted(ks.k):
+                    for side, dst_map in ((ks.k, full.k), (ks.v, full.v)):
+                        dst = torch.empty_like(side[layer], device=tdev)
+                        self.lib.bz_copy_panels(side[layer].data_ptr(), dst.data_ptr(), panels, stride, stride,
+                                                prefix, nctas, s.cuda_stream)
+                        dst_map[layer] = dst
+                        nbytes += panels * prefix
+                out.append(full)
+            t1.record(s)
+            t1.synchronize()
+        for full, (kt, ks) in zip(out, caches):
+            full.length = ks.length
+        torch.cuda.synchronize(tdev)
+        return out, nbytes, t0.elapsed_time(t1)
+
     def decode_graph(self, tokens: Sequence[torch.Tensor], config: PipelineConfig,
                      caches: list[tuple[KVCache, KVCache]]) -> "CoopDecodeGraph":
         """The cooperative decode step of ``decode`` captured once as a two-stream

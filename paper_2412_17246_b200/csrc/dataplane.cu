@@ -412,6 +412,30 @@ __global__ void __launch_bounds__(kThreads) k_handoff(const int4* __restrict__ s
   }
 }
 
+// n_panels equal strided panels: copy the first `n16` 16-byte words of panel q
+// (src + q * stride16) to dst + q * dst_stride16.  dst may be a peer mapping.
+// Used to consolidate the KV prefix of a cooperative pair onto the new instance.
+__global__ void __launch_bounds__(kThreads) k_copy_panels(const int4* __restrict__ src, int4* dst, int64_t n_panels,
+                                                          int64_t src_stride16, int64_t dst_stride16, int64_t n16) {
+  const int64_t total = n_panels * n16;
+  const int64_t per = (total + gridDim.x - 1) / gridDim.x;
+  const int64_t b = tmin<int64_t>(total, per * blockIdx.x), e = tmin<int64_t>(total, b + per);
+  for (int64_t w = b + threadIdx.x; w < e; w += kThreads * 4) {
+    int4 v[4];
+    int64_t q[4], r[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int64_t i = w + u * kThreads;
+      q[u] = i / n16;
+      r[u] = i - q[u] * n16;
+      if (i < e) v[u] = ld16<false>(src + q[u] * src_stride16 + r[u]);
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (w + u * kThreads < e) st16(dst + q[u] * dst_stride16 + r[u], v[u]);
+  }
+}
+
 }  // namespace bz
 
 // ===========================================================================
@@ -602,4 +626,17 @@ extern "C" int bz_handoff(const void* src, void* dst, uint64_t bytes, uint32_t* 
   k_handoff<<<grid, kThreads, 0, static_cast<cudaStream_t>(stream)>>>(
       static_cast<const int4*>(src), static_cast<int4*>(dst), static_cast<int64_t>(bytes >> 4), flag);
   return bz_check_launch("bz_handoff");
+}
+
+extern "C" int bz_copy_panels(const void* src, void* dst, int64_t n_panels, int64_t src_stride, int64_t dst_stride,
+                              int64_t panel_bytes, int nctas, void* stream) {
+  if (!src || !dst || n_panels < 0 || panel_bytes < 0 || ((src_stride | dst_stride | panel_bytes) & 15) ||
+      (reinterpret_cast<uintptr_t>(src) & 15) || (reinterpret_cast<uintptr_t>(dst) & 15))
+    return bz_fail(BZ_EINVAL, "copy_panels: 16-byte aligned pointers, strides and sizes required");
+  if (n_panels == 0 || panel_bytes == 0) return BZ_OK;
+  const int grid = nctas > 0 ? nctas : 64;
+  k_copy_panels<<<grid, kThreads, 0, static_cast<cudaStream_t>(stream)>>>(
+      static_cast<const int4*>(src), static_cast<int4*>(dst), n_panels, src_stride >> 4, dst_stride >> 4,
+      panel_bytes >> 4);
+  return bz_check_launch("bz_copy_panels");
 }

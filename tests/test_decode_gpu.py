@@ -262,3 +262,75 @@ def test_cooperative_decode_graph_matches_eager():
         toks = [lg.argmax(-1) for lg in eager]
     tgt.close()
     src.close()
+
+
+def test_kv_consolidation_lets_the_target_decode_alone():
+    """After a cooperative prefill and two cooperative decode steps, the source's
+    KV blocks [T_i, L) move to the target (bz_copy_panels); the target alone then
+    decodes with the merged cache, matching the fp32 oracle."""
+    arch = S.TINY_4L
+    lay, src, w = _slab(arch, seed=8)
+    ref_w = weights_to_cpu_fp32(w)
+    tgt = DeviceSlab(lay, 0)
+    tgt.data.copy_(src.data)
+    tgt.loaded.fill_(arch.n_layers)
+    cfg = ss.configure_pipeline(3, arch.n_layers, 2.0)
+    pair = CooperativePair(LlamaExecutor(w, max_tokens=64, device="cuda"),
+                           LlamaExecutor(SlabWeights(arch, lay, tgt.data), max_tokens=64, device="cuda"),
+                           tgt.loaded)
+    batches = [_prompt(2, 18, 70 + i, arch.vocab) for i in range(3)]
+    caches = pair.make_caches(batches, cfg, max_new_tokens=6)
+    res = pair.run(batches, cfg, ss.zigzag_schedule(cfg), caches=caches)
+    seqs = [b.cpu() for b in batches]
+    toks = [lg.argmax(-1) for lg in res.logits]
+    for _ in range(2):
+        seqs = [torch.cat([s_, t.cpu()[:, None]], 1) for s_, t in zip(seqs, toks)]
+        toks = [lg.argmax(-1) for lg in pair.decode(toks, cfg, caches).logits]
+    full, nbytes, _ = pair.consolidate(caches)
+    hd, kv_heads = arch.head_dim, arch.n_kv_heads
+    assert nbytes == sum(2 * (arch.n_layers - t_i) * 2 * kv_heads * 20 * hd * 2 for t_i, _ in cfg.splits)
+    for i, kv in enumerate(full):
+        assert sorted(kv.k) == list(range(arch.n_layers)) and kv.length == 20
+        seq, tok = seqs[i], toks[i]
+        for _ in range(2):
+            seq = torch.cat([seq, tok.cpu()[:, None]], 1)
+            lg = pair.tgt.decode(tok, kv)
+            _check(lg, forward_fp32(arch, ref_w, seq))
+            tok = lg.argmax(-1)
+    tgt.close()
+    src.close()
+
+
+@pytest.mark.multigpu
+@pytest.mark.skipif(torch.cuda.device_count() < 2, reason="needs 2 GPUs")
+def test_kv_consolidation_over_nvlink():
+    """Source on cuda:0, new instance on cuda:1: the KV hand-over crosses NVLink
+    (peer stores from bz_copy_panels) and the new instance decodes alone."""
+    from paper_2412_17246_b200._native import cuda_lib
+    lib = cuda_lib()
+    lib.bz_enable_peer_mesh(0)
+    lib.bz_enable_peer_mesh(1)
+    arch = S.TINY_4L
+    lay, src, w = _slab(arch, seed=9)
+    ref_w = weights_to_cpu_fp32(w)
+    with torch.cuda.device(1):
+        tgt = DeviceSlab(lay, 1)
+        tgt.data.copy_(src.data.to("cuda:1"))
+        tgt.loaded.fill_(arch.n_layers)
+        target = LlamaExecutor(SlabWeights(arch, lay, tgt.data), max_tokens=64, device="cuda:1")
+    source = LlamaExecutor(w, max_tokens=64, device="cuda:0")
+    cfg = ss.configure_pipeline(2, arch.n_layers, 1.0)
+    pair = CooperativePair(source, target, tgt.loaded)
+    batches = [_prompt(2, 16, 90 + i, arch.vocab) for i in range(2)]
+    caches = pair.make_caches(batches, cfg, max_new_tokens=2)
+    res = pair.run(batches, cfg, ss.zigzag_schedule(cfg), caches=caches)
+    full, nbytes, ms = pair.consolidate(caches)
+    assert nbytes > 0 and all(kv.k[0].device.index == 1 for kv in full)
+    for i, kv in enumerate(full):
+        tok = res.logits[i].argmax(-1).to("cuda:1")
+        seq = torch.cat([batches[i].cpu(), tok.cpu()[:, None]], 1)
+        with torch.cuda.device(1):
+            lg = target.decode(tok, kv)
+        _check(lg, forward_fp32(arch, ref_w, seq))
+    tgt.close()
+    src.close()

@@ -140,7 +140,8 @@ class LlamaExecutor:
         return out
 
     def embed(self, tokens: torch.Tensor) -> torch.Tensor:
-        return self.w.layers[0]["embed"].index_select(0, tokens.reshape(-1)).contiguous()
+        table = self.w.layers[0]["embed"]
+        return table.index_select(0, tokens.reshape(-1).to(table.device, non_blocking=True)).contiguous()
 
     def _attn_in(self, k: int, x: torch.Tensor, positions: torch.Tensor):
         """rmsnorm -> qkv GEMM -> rope; returns q, k, v as [rows, heads, hd] views."""

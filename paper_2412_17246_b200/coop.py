@@ -205,7 +205,7 @@ class CooperativePair:
                           total_ms=start.elapsed_time(end))
 
     @torch.no_grad()
-    def consolidate(self, caches: list[tuple[KVCache, KVCache]], nctas: int = 64
+    def consolidate(self, caches: list[tuple[KVCache, KVCache]], nctas: int = 128
                     ) -> tuple[list[KVCache], int, float]:
         """Hand the sequences to the new instance once its weights are resident: the
         source's KV blocks [T_i, L) (their cached prefix only) are copied to the

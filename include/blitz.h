@@ -166,7 +166,10 @@ int bz_copy_panels(const void* src, void* dst, int64_t n_panels, int64_t src_str
                    int64_t panel_bytes, int nctas, void* stream);
 
 /* ---- tensor-core GEMM (tcgen05 + TMEM + TMA) ----------------------------------------- */
-/* C[M,N] = A[M,K] . B[N,K]^T (+ residual[M,N]), all bf16 row-major, fp32 accumulate in
+/* The dense contraction the reference models as ModelSpec.prefill_ms /
+ * decode_step_ms (parampool.py:58-62) and scales by max(k, L-k)/L for a live pair
+ * (simcore.py:408-417): every projection of a Llama block on a cooperating instance.
+ * C[M,N] = A[M,K] . B[N,K]^T (+ residual[M,N]), all bf16 row-major, fp32 accumulate in
  * TMEM.  B is a Linear weight [out, in].  K % 8 == 0 (tails zero-filled by TMA), N % 8 == 0,
  * leading dims % 8 == 0,
  * 16-byte aligned pointers.  residual may be NULL.  max_ctas <= 0: one CTA per SM. */

@@ -196,7 +196,7 @@ def test_decode_attention_kernel_matches_fp32(rows, H, KV, hd, s_max, pos):
     p = torch.tensor([pos], dtype=torch.int32, device="cuda")
     nbytes = ctypes.c_int64(0)
     lib.bz_decode_workspace_bytes(rows, H, KV, hd, s_max, ctypes.byref(nbytes))
-    ws = torch.empty(nbytes.value, dtype=torch.uint8, device="cuda")
+    ws = torch.zeros(nbytes.value, dtype=torch.uint8, device="cuda")
     out = torch.empty(rows, H * hd, dtype=torch.bfloat16, device="cuda")
     lib.bz_decode_attention(q.data_ptr(), q.stride(0), kc.data_ptr(), vc.data_ptr(), rows, H, KV, hd, s_max,
                             p.data_ptr(), out.data_ptr(), out.stride(0), ws.data_ptr(), ws.numel(),

@@ -37,6 +37,27 @@ from pathlib import Path
 ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
+def _push_traffic(payload: int):
+    """DRAM bytes per launch of the dominant mover (k_push_tiles) from the committed
+    ncu --set full capture of one 7B chain hop (profiles/r1_ncu_push_raw.csv,
+    loopback: the hop's source reads and destination writes land on one GPU),
+    scaled to this run's shard; on NVLink the sender's own DRAM sees the read half."""
+    import csv
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r1_ncu_push_raw.csv")
+    try:
+        with open(path, newline="") as f:
+            rows = list(csv.reader(f))
+        hdr, units, vals = rows[0], rows[1], rows[2]
+        scale = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+        got = {h: float(v) * scale[u] for h, u, v in zip(hdr, units, vals)
+               if h in ("dram__bytes_read.sum", "dram__bytes_write.sum")}
+        captured = 13_476_831_232  # the 7B shard the capture moved
+        total = (got["dram__bytes_read.sum"] + got["dram__bytes_write.sum"]) * payload / captured
+        return total, "ncu --set full, k_push_tiles<0> loopback hop (profiles/r1_ncu_push_raw.csv), read+write"
+    except (OSError, KeyError, IndexError, ValueError):
+        return None, None
+
+
 def _hbm_peak() -> float:
     try:
         with open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "MEASURED_PEAKS.json")) as f:
@@ -635,6 +656,9 @@ def run_blitz(args):
         cpu.pop("seconds", None)
 
     if rank == 0:
+        # DRAM traffic of the dominant kernel: the NVLink push kernel (N >= 2); at N=1 the
+        # mover is the copy engine (no kernel, no ncu counter): null
+        traffic, traffic_src = _push_traffic(payload) if bound == "nvlink" else (None, None)
         line = {
             "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": N, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
@@ -651,7 +675,9 @@ def run_blitz(args):
             "modeled_ms_eta1": {k: v * 1e3 for k, v in est.per_target_completion.items()},
             "bit_exact": bool(ok_all and final_all),
             "roofline": {"bound": bound, "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": (achieved / peak) if achieved else None, "traffic": None,
+                         "frac": (achieved / peak) if achieved else None, "traffic": traffic,
+                         "traffic_source": traffic_src,
+                         "algorithmic_bytes_per_launch": 2 * payload if bound == "nvlink" else None,  # read + write of one hop
                          "peak_source": peak_src, "kernel_ms": dom_kernel_ms,
                          "frac_of_nominal": (achieved / (NVLINK_NOMINAL_GBPS if bound == "nvlink"
                                                          else PCIE_PEAK_GBPS)) if achieved else None},

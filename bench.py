@@ -247,7 +247,8 @@ def decision_timings() -> dict:
             lambda: simcore.run_simulation(topo2, [model], trace, simcore.SimPolicy("blitz-live")),
     }
     ref_path = ROOT / "tests" / "golden" / "reference_timings.json"
-    ref = json.loads(ref_path.read_text())["seconds"] if ref_path.exists() else {}
+    ref_doc = json.loads(ref_path.read_text()) if ref_path.exists() else {}
+    ref, ours_there = ref_doc.get("seconds", {}), ref_doc.get("ours_seconds", {})
     out = {}
     for name, fn in work.items():
         best = float("inf")
@@ -256,10 +257,12 @@ def decision_timings() -> dict:
             fn()
             best = min(best, time.perf_counter() - t0)
         out[name] = {"ours_ms": best * 1e3,
-                     "reference_ms": ref[name] * 1e3 if name in ref else None}
+                     "reference_ms": ref[name] * 1e3 if name in ref else None,
+                     "ours_ms_same_cpu_as_reference": ours_there[name] * 1e3 if name in ours_there else None}
     return {"calls": out, "ours_timed_on": f"this host, 1 thread, best of 5 ({os.cpu_count()} cores visible)",
-            "reference_timed_on": "the build container by oracle/gen_golden.py (the reference package is "
-                                  "not installed on the GPU box), 1 thread, best of 5"}
+            "reference_timed_on": "the build container by oracle/gen_golden.py --timings-only (the reference "
+                                  "package is not installed on the GPU box), 1 thread, best of 5, together "
+                                  "with ours on the same CPU (ours_ms_same_cpu_as_reference)"}
 
 
 # ---- C1 cooperative execution (ZigZag) on this GPU vs the CPU fp32 oracle -----------------------

@@ -320,7 +320,28 @@ def time_best(fn, reps=5):
     return best
 
 
+def write_timings(ss):
+    """Reference decision-path timings next to this package's on the same CPU, same run
+    (bench.py reports them beside its on-box timings of our side)."""
+    import os
+    sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
+    import paper_2412_17246_b200 as ours
+    from paper_2412_17246_b200 import simcore as ours_simcore
+    timings = {name: time_best(fn) for name, fn in
+               decision_workloads(ss, importlib.import_module("scalesim.simcore")).items()}
+    ours_t = {name: time_best(fn) for name, fn in decision_workloads(ours, ours_simcore).items()}
+    (OUT / "reference_timings.json").write_text(json.dumps({
+        "what": "reference scalesim decision path and this package's, best of 5, single thread (GIL), "
+                "same build container, same run",
+        "cpu": open("/proc/cpuinfo").read().split("model name")[1].split("\n")[0].strip(": ")
+        if os.path.exists("/proc/cpuinfo") else "?",
+        "seconds": timings, "ours_seconds": ours_t}, indent=1, sort_keys=True))
+
+
 def main():
+    if "--timings-only" in sys.argv:
+        write_timings(load_reference())
+        return
     ss = load_reference()
     OUT.mkdir(parents=True, exist_ok=True)
     plans = [run_plan_case(ss, c) for c in plan_cases()]
@@ -346,14 +367,7 @@ def main():
                                                                      eta=eta)))
     (OUT / "baseline_load.json").write_text(json.dumps(baselines, sort_keys=True))
     (OUT / "simulations.json").write_text(json.dumps(run_sim_cases(ss), sort_keys=True))
-    import os
-    timings = {name: time_best(fn) for name, fn in
-               decision_workloads(ss, importlib.import_module("scalesim.simcore")).items()}
-    (OUT / "reference_timings.json").write_text(json.dumps({
-        "what": "reference scalesim decision path, best of 5, single thread (GIL), this build container",
-        "cpu": open("/proc/cpuinfo").read().split("model name")[1].split("\n")[0].strip(": ")
-        if os.path.exists("/proc/cpuinfo") else "?",
-        "seconds": timings}, indent=1, sort_keys=True))
+    write_timings(ss)
     print(f"wrote {len(plans)} plan cases, {len(pipes)} pipeline cases to {OUT}")
 
 

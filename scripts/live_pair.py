@@ -24,7 +24,7 @@ def main():
     arch = S.ARCHS[os.environ.get("BZ_ARCH", "llama2-7b")]
     pair = LivePair(fabric, arch, n_batches=int(os.environ.get("BZ_BATCHES", "12")),
                     seqs=int(os.environ.get("BZ_SEQS", "4")), seq_len=int(os.environ.get("BZ_SEQ", "500")),
-                    mode=os.environ.get("BZ_MODE", "host"),
+                    mode=os.environ.get("BZ_MODE", "host"), nctas=int(os.environ.get("BZ_NCTAS", "48")),
                     engine={"vector": 0, "vec256": 2, "ce": 3}[os.environ.get("BZ_ENGINE", "vector")])
     res = pair.run()
     if res is not None:

@@ -135,8 +135,17 @@ class CooperativePair:
         cur.wait_stream(self.tgt_stream)
         end.record(cur)
         end.synchronize()
+        self._check_gates()
         return CoopResult(logits=logits, executed_order=order, handoff_bytes=nbytes,
                           total_ms=start.elapsed_time(end))
+
+    def _check_gates(self):
+        """A gate that timed out let its kernels run on data that never arrived: raise."""
+        from .scaleup import check_wait_timeouts
+        torch.cuda.synchronize(self.tgt.h.device)
+        torch.cuda.synchronize(self.src.h.device)
+        for dev in {self.tgt.h.device.index, self.src.h.device.index}:
+            check_wait_timeouts(dev)
 
     def make_caches(self, batches: Sequence[torch.Tensor], config: PipelineConfig,
                     max_new_tokens: int) -> list[tuple[KVCache, KVCache]]:
@@ -201,6 +210,7 @@ class CooperativePair:
         cur.wait_stream(self.tgt_stream)
         end.record(cur)
         end.synchronize()
+        self._check_gates()
         return CoopResult(logits=logits, executed_order=[], handoff_bytes=nbytes,
                           total_ms=start.elapsed_time(end))
 

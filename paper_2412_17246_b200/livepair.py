@@ -308,6 +308,9 @@ class LivePair:
         if self.executor is not None:
             self.executor.synchronize()
         diag.pop("push_done", None)
+        torch.cuda.synchronize()
+        from .scaleup import check_wait_timeouts
+        check_wait_timeouts(self.f.device)
         gathered = self.f.allgather(diag)
         self.last_diag = {"source": gathered[self.src], "target": gathered[self.tgt]}
         self.f.barrier()

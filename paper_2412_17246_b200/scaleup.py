@@ -57,19 +57,22 @@ class TransferTimeout(RuntimeError):
     """A device-side wait gave up (its upstream never published)."""
 
 
-_seen_timeouts = 0
+_seen_timeouts: dict[int, int] = {}
 
 
-def check_wait_timeouts() -> None:
-    global _seen_timeouts
+def check_wait_timeouts(device: Optional[int] = None) -> None:
+    """Raise if a bounded device-side wait on ``device`` (default: current) gave up
+    since the last check -- the kernels behind it ran on data that never arrived."""
     import ctypes
 
-    n = ctypes.c_uint64()
     from ._native import cuda_lib
-    cuda_lib().bz_wait_timeouts(ctypes.byref(n), 0)
-    if n.value > _seen_timeouts:
-        _seen_timeouts = n.value
-        raise TransferTimeout(f"{n.value} device-side waits timed out (upstream never published)")
+    dev = torch.cuda.current_device() if device is None else int(device)
+    n = ctypes.c_uint64()
+    with torch.cuda.device(dev):
+        cuda_lib().bz_wait_timeouts(ctypes.byref(n), 0)
+    if n.value > _seen_timeouts.get(dev, 0):
+        _seen_timeouts[dev] = n.value
+        raise TransferTimeout(f"cuda:{dev}: {n.value} device-side waits timed out (upstream never published)")
 
 
 def expected_fingerprints(layout: SlabLayout, device: int, seed: int) -> torch.Tensor:

@@ -203,3 +203,24 @@ def test_bad_arguments_raise():
         lib.bz_push_tiles(1, ptr_array([0] * 9), ptr_array([0] * 9), 9, None, 1, 0, 1, 1, 8, 0, 0)
     with pytest.raises(BlitzError):
         lib.bz_fill_random(1, 17, 0, 0)   # size not a multiple of 16
+
+
+def test_gate_timeout_fails_loudly():
+    """A gate whose flag is never raised gives up after the spin budget (no hung GPU)
+    and the next check raises instead of letting results through silently."""
+    import ctypes
+    from paper_2412_17246_b200.dataplane import gate
+    from paper_2412_17246_b200.scaleup import TransferTimeout, check_wait_timeouts
+    lib = cuda_lib()
+    check_wait_timeouts()                       # absorb anything earlier tests left
+    n = ctypes.c_uint64()
+    lib.bz_wait_timeouts(ctypes.byref(n), 2_000_000)      # 2 ms budget
+    try:
+        flag = torch.zeros(1, dtype=torch.int32, device="cuda")
+        gate(flag.data_ptr(), 1, torch.cuda.current_stream().cuda_stream)
+        torch.cuda.synchronize()
+        with pytest.raises(TransferTimeout):
+            check_wait_timeouts()
+        check_wait_timeouts()                   # counted once
+    finally:
+        lib.bz_wait_timeouts(ctypes.byref(n), 30_000_000_000)

@@ -664,6 +664,10 @@ def run_blitz(args):
         lp = LivePair(fabric, arch, n_batches=12, seqs=4, seq_len=500, mode="nvlink")
         res = lp.run()
         live = summarize(res) if res is not None else None
+        log("live pair: KV hand-over to the new instance, which then decodes alone")
+        ho = lp.run_handover(lp.cfg, lp.tl)
+        if live is not None:
+            live["kv_handover"] = ho
         lp.close()
         if live is not None:
             log(f"live pair avg latency {live['avg_latency_ms']}")

@@ -30,7 +30,7 @@ import torch
 from . import livescale
 from ._native import BzSlab, cuda_lib
 from .dataplane import DeviceSlab, Fabric, HostCache, ScaleExecutor, device_view, gate
-from .llama import LlamaExecutor, SlabWeights
+from .llama import KVCache, LlamaExecutor, SlabWeights
 from .planner import PlanEdge, ScalePlan
 from .slab import LlamaArch, SlabLayout
 
@@ -80,6 +80,55 @@ class PeerMailbox:
 
     def close(self):
         self.lib.bz_slab_free(self.raw)
+
+
+class SharedRegion:
+    """A VMM allocation one rank creates and exports and another maps over NVLink
+    (the KV inbox of the new instance)."""
+
+    def __init__(self, device: int, nbytes: int = 0, info=None):
+        self.lib = cuda_lib()
+        self.raw = BzSlab()
+        self.device = torch.device("cuda", device)
+        if info is None:
+            self.lib.bz_slab_create(device, nbytes, self.raw)
+            self.owner = True
+        else:
+            self.lib.bz_slab_import(device, info[0], info[1], info[2], self.raw)
+            self.owner = False
+        self.nbytes = int(self.raw.bytes)
+        self.exported = False
+
+    def export(self):
+        if not self.exported:
+            self.lib.bz_slab_export(self.raw)
+            self.exported = True
+        return (os.getpid(), int(self.raw.fd), int(self.raw.bytes))
+
+    def view(self, offset: int, shape: tuple) -> torch.Tensor:
+        n = 1
+        for d in shape:
+            n *= d
+        return device_view(self.raw.ptr + offset, 2 * n, torch.int16, self.device).view(torch.bfloat16).view(*shape)
+
+    def close(self):
+        self.lib.bz_slab_free(self.raw)
+
+
+def kv_inbox_layout(splits, n_layers: int, panel_shape: tuple) -> tuple[dict, int]:
+    """Byte offsets of the source-side KV blocks (batch i, layer l >= T_i, k|v) in the
+    new instance's inbox; the same on both ranks (derived from the split)."""
+    n = 1
+    for d in panel_shape:
+        n *= d
+    size = (2 * n + 255) // 256 * 256
+    offs, cur = {}, 0
+    for i, (t_i, _) in enumerate(splits):
+        for layer in range(t_i, n_layers):
+            for side in ("k", "v"):
+                offs[(i, layer, side)] = cur
+                cur += size
+    return offs, max(cur, 4096)
 
 
 @dataclass
@@ -237,8 +286,11 @@ class LivePair:
         self.f.barrier()
         return fins, out
 
-    def run_split(self, cfg: livescale.PipelineConfig, tl: livescale.ZigzagTimeline):
-        """Execute cfg/tl with the weights streaming in; returns (finish ms, logits) on the source."""
+    def run_split(self, cfg: livescale.PipelineConfig, tl: livescale.ZigzagTimeline,
+                  caches: Optional[list] = None):
+        """Execute cfg/tl with the weights streaming in; returns (finish ms, logits) on the source.
+        With ``caches`` (this rank's KVCache per batch) each side keeps the keys/values
+        of the blocks it ran."""
         L = self.arch.n_layers
         if self.me == self.src:
             self.mailbox.flags.zero_()
@@ -273,15 +325,19 @@ class LivePair:
                         started[b] = True
                     gate(self.slab.loaded.data_ptr(), layer, self.stream.cuda_stream)
                     x_in = bufs[b][(layer - 1) % 2]
+                    kv = caches[b] if caches else None
                     if layer == cfg.splits[b][0]:
                         flag = self.peer_mb.flags[b:b + 1]
                         self.ex.block(layer - 1, x_in, self.pos, (self.seqs, self.seq_len),
-                                      out=self.peer_mb.slot(b, self.rows, self.arch.d_model), signal=flag)
+                                      out=self.peer_mb.slot(b, self.rows, self.arch.d_model), signal=flag,
+                                      kv=kv)
+                        if kv is not None:
+                            kv.length = self.seq_len
                         handed[b] = torch.cuda.Event(enable_timing=True)
                         handed[b].record(self.stream)
                     else:
                         self.ex.block(layer - 1, x_in, self.pos, (self.seqs, self.seq_len),
-                                      out=bufs[b][layer % 2])
+                                      out=bufs[b][layer % 2], kv=kv)
             self.stream.synchronize()
             self.executor.synchronize()
             diag["handoff_ms"] = {b: start.elapsed_time(e) for b, e in handed.items()}
@@ -298,7 +354,8 @@ class LivePair:
                         gate(self.mailbox.flags[i:i + 1].data_ptr(), grid[i],
                                                self.stream.cuda_stream)
                         h = self.mailbox.slot(i, self.rows, self.arch.d_model)
-                    logits.append(self.ex.forward(self.batches[i], first=t_i, last=L, x=h))
+                    logits.append(self.ex.forward(self.batches[i], first=t_i, last=L, x=h,
+                                                  kv=caches[i] if caches else None))
                     ev[i].record(self.stream)
             ev[-1].synchronize()
             fins = [start.elapsed_time(e) for e in ev]
@@ -342,10 +399,132 @@ class LivePair:
         torch.cuda.synchronize()
         return ctas.value
 
+    def run_handover(self, cfg: livescale.PipelineConfig, tl: livescale.ZigzagTimeline,
+                     decode_steps: int = 4, nctas: int = 128) -> Optional[dict]:
+        """The rest of a live scale: ZigZag prefill keeping each side's KV, then the
+        source pushes its KV blocks [T_i, L) into the new instance's inbox over NVLink
+        (bz_copy_panels, peer stores) and the new instance decodes every batch alone.
+        Its logits are compared bit for bit with the source serving the same batches
+        alone (prefill + decode on one GPU).  Returns the summary on the source rank."""
+        L, a = self.arch.n_layers, self.arch
+        s_max = self.seq_len + decode_steps + 1
+        panel = (self.seqs, a.n_kv_heads, s_max, a.head_dim)
+        offs, total = kv_inbox_layout(cfg.splits, L, panel)
+        dev = self.slab.data.device if self.slab is not None else None
+        caches = None
+        inbox = None
+        info = None
+        if self.me == self.tgt:
+            caches = [KVCache(a, self.seqs, s_max, dev, 0, t_i) for t_i, _ in cfg.splits]
+            inbox = SharedRegion(self.f.device, total)
+            info = inbox.export()
+        elif self.me == self.src:
+            caches = [KVCache(a, self.seqs, s_max, dev, t_i, L) for t_i, _ in cfg.splits]
+        infos = self.f.allgather(info)
+        if self.me == self.src:
+            inbox = SharedRegion(self.f.device, info=infos[self.tgt])
+        self.f.barrier()
+        _, logits = self.run_split(cfg, tl, caches=caches if self.me in (self.src, self.tgt) else None)
+
+        # ---- KV hand-over: source -> new instance -------------------------------------------------
+        out = {}
+        stride = s_max * a.head_dim * 2
+        prefix = self.seq_len * a.head_dim * 2
+        panels = self.seqs * a.n_kv_heads
+        if self.me == self.src:
+            nbytes = 0
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            with torch.cuda.stream(self.stream):
+                e0.record(self.stream)
+                for i, (t_i, _) in enumerate(cfg.splits):
+                    for layer in range(t_i, L):
+                        for side, src_t in (("k", caches[i].k[layer]), ("v", caches[i].v[layer])):
+                            dst = inbox.raw.ptr + offs[(i, layer, side)]
+                            self.lib.bz_copy_panels(src_t.data_ptr(), dst, panels, stride, stride, prefix, nctas,
+                                                    self.stream.cuda_stream)
+                            nbytes += panels * prefix
+                e1.record(self.stream)
+            e1.synchronize()
+            ms = e0.elapsed_time(e1)
+            out.update(kv_bytes=nbytes, kv_ms=ms, kv_GBps=nbytes / (ms / 1e3) / 1e9)
+            first_tokens = [lg.argmax(-1).cpu() for lg in logits]
+        else:
+            first_tokens = None
+        toks = self.f.allgather(first_tokens)[self.src]
+        self.f.barrier()   # the source's peer stores are complete and visible
+
+        # ---- the new instance decodes alone ---------------------------------------------------------
+        dec = None
+        if self.me == self.tgt:
+            # warm the decode kernels (lazy module loads, launch attributes) on a scratch
+            # cache so the timed first token measures the steady path
+            with torch.cuda.stream(self.stream):
+                scratch = KVCache(a, self.seqs, 8, dev)
+                self.ex.decode(toks[0].to(dev), scratch)
+                del scratch
+            self.stream.synchronize()
+            full = []
+            for i, (t_i, _) in enumerate(cfg.splits):
+                kv = KVCache(a, self.seqs, s_max, dev, 0, 0)
+                kv.k.update(caches[i].k)
+                kv.v.update(caches[i].v)
+                for layer in range(t_i, L):
+                    kv.k[layer] = inbox.view(offs[(i, layer, "k")], panel)
+                    kv.v[layer] = inbox.view(offs[(i, layer, "v")], panel)
+                kv.length = self.seq_len
+                full.append(kv)
+            dec, t0, t1 = [], torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            first = torch.cuda.Event(enable_timing=True)
+            with torch.cuda.stream(self.stream):
+                t0.record(self.stream)
+                for i in range(self.n):
+                    tok, seq_logits = toks[i].to(dev), []
+                    for step in range(decode_steps):
+                        lg = self.ex.decode(tok, full[i])
+                        if i == 0 and step == 0:
+                            first.record(self.stream)
+                        seq_logits.append(lg)
+                        tok = lg.argmax(-1)
+                    dec.append(seq_logits)
+                t1.record(self.stream)
+            t1.synchronize()
+            dec_cpu = [[lg.cpu() for lg in sl] for sl in dec]
+            timing = {"first_token_ms": t0.elapsed_time(first), "all_ms": t0.elapsed_time(t1)}
+        else:
+            dec_cpu, timing = None, None
+        gathered = self.f.allgather((dec_cpu, timing))[self.tgt]
+
+        # ---- the same batches served by the source alone ------------------------------------------
+        if self.me == self.src:
+            equal = True
+            max_diff = 0.0
+            with torch.cuda.stream(self.stream):
+                for i in range(self.n):
+                    kv = KVCache(a, self.seqs, s_max, dev)
+                    lg0 = self.ex.forward(self.batches[i], kv=kv)
+                    tok = lg0.argmax(-1)
+                    for step in range(decode_steps):
+                        lg = self.ex.decode(tok, kv)
+                        ref = gathered[0][i][step]
+                        got = lg.cpu()
+                        equal &= bool(torch.equal(got, ref))
+                        max_diff = max(max_diff, float((got - ref).abs().max()))
+                        tok = lg.argmax(-1)
+            torch.cuda.synchronize()
+            out.update(decode_steps=decode_steps, batches=self.n, seqs=self.seqs,
+                       new_instance_first_token_ms=gathered[1]["first_token_ms"],
+                       new_instance_decode_ms=gathered[1]["all_ms"],
+                       logits_bitwise_equal_to_source_alone=equal, max_abs_logit_diff=max_diff)
+        self.f.barrier()
+        if inbox is not None:
+            inbox.close()
+        return out if self.me == self.src else None
+
     def run(self) -> Optional[LivePairResult]:
         w_ms, unit_ms, time_l = self.calibrate()
         cfg = livescale.configure_pipeline(self.n, self.arch.n_layers, time_l)
         tl = livescale.zigzag_schedule(cfg)
+        self.cfg, self.tl = cfg, tl
         be = livescale.best_effort_pipeline(self.n, self.arch.n_layers, time_l)
         be_tl = livescale.zigzag_schedule(be)
         alone_f, alone_logits = self.run_source_alone()

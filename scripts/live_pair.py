@@ -27,8 +27,9 @@ def main():
                     mode=os.environ.get("BZ_MODE", "host"), nctas=int(os.environ.get("BZ_NCTAS", "48")),
                     engine={"vector": 0, "vec256": 2, "ce": 3}[os.environ.get("BZ_ENGINE", "vector")])
     res = pair.run()
+    ho = pair.run_handover(pair.cfg, pair.tl)
     if res is not None:
-        print(json.dumps({"arch": arch.name, **summarize(res)}), flush=True)
+        print(json.dumps({"arch": arch.name, **summarize(res), "kv_handover": ho}), flush=True)
     pair.close()
     import torch.distributed as dist
     dist.destroy_process_group()

@@ -531,6 +531,11 @@ class LivePair:
         zz_f, zz_logits = self.run_split(cfg, tl)
         zz_diag = self.last_diag
         be_f, _ = self.run_split(be, be_tl)
+        # the baseline runs twice (before and after the split runs) and keeps the faster,
+        # so a slow outlier (clock/power state) cannot flatter the split
+        alone_f2, _ = self.run_source_alone()
+        if alone_f2 and (not alone_f or alone_f2[-1] < alone_f[-1]):
+            alone_f = alone_f2
         res = None
         if self.me == self.src:
             layer_ms = w_ms / self.arch.n_layers

@@ -58,6 +58,9 @@ def test_two_process_live_pair_logits_bitwise(mode):
     assert proc.returncode == 0, proc.stdout[-2000:] + proc.stderr[-3000:]
     res = json.loads([l for l in proc.stdout.splitlines() if l.startswith("{")][-1])
     assert res["logits_bitwise_equal_to_source_alone"] is True
+    # rest of the scale: KV hand-over, then the new instance decodes alone, bit-identical
+    ho = res["kv_handover"]
+    assert ho["kv_bytes"] > 0 and ho["logits_bitwise_equal_to_source_alone"] is True
 
 
 _WORKER = r"""

@@ -213,9 +213,19 @@ __device__ __forceinline__ void store_chunk(const Params& p, int row, int col, c
 #pragma unroll
       for (int j = 0; j < 16; ++j) w[j] = pack_bf16(__uint_as_float(r[2 * j]), __uint_as_float(r[2 * j + 1]));
     }
-    uint4* o = reinterpret_cast<uint4*>(out);
+    if ((reinterpret_cast<uintptr_t>(out) & 31) == 0) {
+      // two 256-bit stores: each request fills whole 32-byte L2 sectors
 #pragma unroll
-    for (int q = 0; q < 4; ++q) o[q] = make_uint4(w[4 * q], w[4 * q + 1], w[4 * q + 2], w[4 * q + 3]);
+      for (int h = 0; h < 2; ++h)
+        asm volatile("st.global.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(out + 16 * h), "r"(w[8 * h]),
+                     "r"(w[8 * h + 1]), "r"(w[8 * h + 2]), "r"(w[8 * h + 3]), "r"(w[8 * h + 4]), "r"(w[8 * h + 5]),
+                     "r"(w[8 * h + 6]), "r"(w[8 * h + 7])
+                     : "memory");
+    } else {
+      uint4* o = reinterpret_cast<uint4*>(out);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) o[q] = make_uint4(w[4 * q], w[4 * q + 1], w[4 * q + 2], w[4 * q + 3]);
+    }
   } else {
 #pragma unroll
     for (int j = 0; j < 32; ++j) {
@@ -433,11 +443,15 @@ __global__ void __launch_bounds__(THREADS, 1)
         tmem_ld_32x32b_x32(taddr + c, r);
         if (row >= p.M) continue;
         if (partial) {
+          // the slot is [M][BN] fp32, 32-byte aligned: 256-bit stores of 8 columns
           float* dst = sk_slot(p, blockIdx.x, slot, BN) + row * BN + c;
 #pragma unroll
-          for (int q = 0; q < 8; ++q)
-            if (n0 + c + 4 * q < p.N)
-              *reinterpret_cast<uint4*>(dst + 4 * q) = make_uint4(r[4 * q], r[4 * q + 1], r[4 * q + 2], r[4 * q + 3]);
+          for (int q = 0; q < 4; ++q)
+            if (n0 + c + 8 * q < p.N)
+              asm volatile("st.global.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(dst + 8 * q), "r"(r[8 * q]),
+                           "r"(r[8 * q + 1]), "r"(r[8 * q + 2]), "r"(r[8 * q + 3]), "r"(r[8 * q + 4]),
+                           "r"(r[8 * q + 5]), "r"(r[8 * q + 6]), "r"(r[8 * q + 7])
+                           : "memory");
         } else {
           store_chunk(p, row, n0 + c, r);
         }

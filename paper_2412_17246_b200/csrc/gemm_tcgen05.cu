@@ -192,22 +192,35 @@ struct SegIter {
 };
 
 // bf16 store of a 32-column accumulator chunk (+ optional residual) for one row
-__device__ __forceinline__ void store_chunk(const Params& p, int row, int col, const uint32_t (&r)[32]) {
+// (columns at or beyond `lim` -- the end of C or of a tile narrower than a
+// multiple of 32 -- are not written)
+__device__ __forceinline__ void store_chunk(const Params& p, int row, int col, const uint32_t (&r)[32], int lim) {
   __nv_bfloat16* out = p.C + static_cast<int64_t>(row) * p.ldc + col;
   const __nv_bfloat16* res = p.R ? p.R + static_cast<int64_t>(row) * p.ldr + col : nullptr;
-  if (col + 32 <= p.N) {
+  if (col + 32 <= lim) {
     uint32_t w[16];
     if (res) {
-      const uint4* rv = reinterpret_cast<const uint4*>(res);
+      uint32_t x[16];
+      if ((reinterpret_cast<uintptr_t>(res) & 31) == 0) {
+        // two 256-bit loads of the residual row segment
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        uint4 x = rv[q];
-        const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&x);
+        for (int h = 0; h < 2; ++h)
+          asm volatile("ld.global.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                       : "=r"(x[8 * h]), "=r"(x[8 * h + 1]), "=r"(x[8 * h + 2]), "=r"(x[8 * h + 3]),
+                         "=r"(x[8 * h + 4]), "=r"(x[8 * h + 5]), "=r"(x[8 * h + 6]), "=r"(x[8 * h + 7])
+                       : "l"(res + 16 * h));
+      } else {
+        const uint4* rv = reinterpret_cast<const uint4*>(res);
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          float2 f = __bfloat1622float2(h[j]);
-          w[q * 4 + j] = pack_bf16(__uint_as_float(r[q * 8 + 2 * j]) + f.x, __uint_as_float(r[q * 8 + 2 * j + 1]) + f.y);
+        for (int q = 0; q < 4; ++q) {
+          const uint4 v = rv[q];
+          x[4 * q] = v.x, x[4 * q + 1] = v.y, x[4 * q + 2] = v.z, x[4 * q + 3] = v.w;
         }
+      }
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&x[j]));
+        w[j] = pack_bf16(__uint_as_float(r[2 * j]) + f.x, __uint_as_float(r[2 * j + 1]) + f.y);
       }
     } else {
 #pragma unroll
@@ -229,7 +242,7 @@ __device__ __forceinline__ void store_chunk(const Params& p, int row, int col, c
   } else {
 #pragma unroll
     for (int j = 0; j < 32; ++j) {
-      if (col + j < p.N) {
+      if (col + j < lim) {
         float v = __uint_as_float(r[j]);
         if (res) v += __bfloat162float(res[j]);
         out[j] = __float2bfloat16_rn(v);
@@ -453,7 +466,7 @@ __global__ void __launch_bounds__(THREADS, 1)
                            "r"(r[8 * q + 5]), "r"(r[8 * q + 6]), "r"(r[8 * q + 7])
                            : "memory");
         } else {
-          store_chunk(p, row, n0 + c, r);
+          store_chunk(p, row, n0 + c, r, p.N);
         }
       }
       tc_fence_before();
@@ -557,7 +570,7 @@ struct CfgPair {
   static constexpr int ACC_BUFS = 2 * TILE_N <= 512 ? 2 : 1;
   static constexpr int TMEM_COLS = ACC_BUFS * TILE_N <= 256 ? 256 : 512;
   static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 256;
-  static_assert(BN % 32 == 0 && BN <= 256 && BN >= 64, "tile N");
+  static_assert(BN % 16 == 0 && (BN / 2) % 8 == 0 && BN <= 256 && BN >= 64, "tile N");
   static_assert(ACC_BUFS * TILE_N <= 512, "TMEM");
 };
 
@@ -684,7 +697,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
       for (int c = 0; c < TILE_N; c += 32) {
         uint32_t r[32];
         tmem_ld_32x32b_x32(taddr + c, r);
-        if (row < p.M && n0 + c < p.N) store_chunk(p, row, n0 + c, r);
+        if (row < p.M && n0 + c < p.N) store_chunk(p, row, n0 + c, r, min(p.N, n0 + TILE_N));
       }
       tc_fence_before();
       __syncwarp();
@@ -793,7 +806,7 @@ static int bn_override() {
   if (v < 0) {
     const char* e = getenv("BZ_GEMM_BN");
     v = e ? atoi(e) : 0;
-    if (v != 32 && v != 64 && v != 128 && v != 192 && v != 256) v = 0;
+    if (v != 32 && v != 64 && v != 128 && v != 192 && v != 240 && v != 256) v = 0;
   }
   return v;
 }
@@ -919,8 +932,9 @@ struct PairPlan {
   double kb_s, tile_s;
 };
 static PairPlan plan_pair(int m_tiles, int N, int K, int clusters, int only_bn, int only_nsub) {
-  const PairPlan cands[5] = {{256, 1, 0.378e-6, 0.0},
+  const PairPlan cands[6] = {{256, 1, 0.378e-6, 0.0},
                              {256, 2, 0.677e-6, 8.6e-6},
+                             {240, 1, 0.378e-6, 0.0},  // measured: no faster per K block than 256
                              {192, 1, 0.332e-6, 0.0},
                              {192, 2, 0.600e-6, 8.6e-6},
                              {128, 1, 0.276e-6, 0.0}};
@@ -995,6 +1009,8 @@ static int gemm_impl(const void* A, const void* B, void* C, const void* residual
         return launch_pair<192, 2>(ma, B, N, K, ldb, p, max_ctas, s, ctas_out);
       case 2562:
         return launch_pair<256, 2>(ma, B, N, K, ldb, p, max_ctas, s, ctas_out);
+      case 2401:
+        return launch_pair<240, 1>(ma, B, N, K, ldb, p, max_ctas, s, ctas_out);
       default:
         return launch_pair<256, 1>(ma, B, N, K, ldb, p, max_ctas, s, ctas_out);
     }

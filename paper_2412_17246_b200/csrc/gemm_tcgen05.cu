@@ -134,6 +134,31 @@ __device__ __forceinline__ void tmem_ld_32x32b_x32(uint32_t taddr, uint32_t (&r)
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
+// Split issue/wait form: several TMEM loads in flight, then one wait per register
+// block.  The wait takes the block's registers as in/out operands, so no use of
+// them can be scheduled before the load has landed.
+__device__ __forceinline__ void tmem_ld_32x32b_x32_async(uint32_t taddr, uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+        "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+        "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_wait_ld(uint32_t (&r)[32]) {
+  asm volatile("tcgen05.wait::ld.sync.aligned;"
+               : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]), "+r"(r[6]), "+r"(r[7]),
+                 "+r"(r[8]), "+r"(r[9]), "+r"(r[10]), "+r"(r[11]), "+r"(r[12]), "+r"(r[13]), "+r"(r[14]),
+                 "+r"(r[15]), "+r"(r[16]), "+r"(r[17]), "+r"(r[18]), "+r"(r[19]), "+r"(r[20]), "+r"(r[21]),
+                 "+r"(r[22]), "+r"(r[23]), "+r"(r[24]), "+r"(r[25]), "+r"(r[26]), "+r"(r[27]), "+r"(r[28]),
+                 "+r"(r[29]), "+r"(r[30]), "+r"(r[31])
+               :
+               : "memory");
+}
+
 __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
   __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
   return *reinterpret_cast<uint32_t*>(&v);
@@ -693,11 +718,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
       tc_fence_after();
       const int row = m0 + quarter * 32 + lane;
       const uint32_t taddr = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + buf * TILE_N;
+      const int lim = min(p.N, n0 + TILE_N);
 #pragma unroll 1
-      for (int c = 0; c < TILE_N; c += 32) {
-        uint32_t r[32];
-        tmem_ld_32x32b_x32(taddr + c, r);
-        if (row < p.M && n0 + c < p.N) store_chunk(p, row, n0 + c, r, min(p.N, n0 + TILE_N));
+      for (int c = 0; c < TILE_N; c += 64) {
+        // two 32-column loads in flight, then store both
+        uint32_t r0[32], r1[32];
+        tmem_ld_32x32b_x32_async(taddr + c, r0);
+        if (c + 32 < TILE_N) tmem_ld_32x32b_x32_async(taddr + c + 32, r1);
+        tmem_wait_ld(r0);
+        tmem_wait_ld(r1);
+        if (row < p.M && n0 + c < p.N) store_chunk(p, row, n0 + c, r0, lim);
+        if (row < p.M && c + 32 < TILE_N && n0 + c + 32 < p.N) store_chunk(p, row, n0 + c + 32, r1, lim);
       }
       tc_fence_before();
       __syncwarp();
@@ -925,18 +956,18 @@ static int nsub_override() {
 // with BZ_GEMM_BN / BZ_GEMM_NSUB pinned, 7B block shapes at 2000 tokens; see
 // profiles/r1_gemm_pair_configs.txt).  The kernel is bound by the smem feed (with
 // its loads elided it runs at 1.9 PFLOP/s), so wider tiles pay less per MAC;
-// NSUB = 2 (one TMEM buffer) additionally exposes ~8.6 us of epilogue and
-// pipeline refill per tile.  Minimise waves x (K blocks x t_kb + exposed).
+// NSUB = 2 (one TMEM buffer) additionally exposes ~3.8 us of epilogue per tile
+// (two TMEM loads in flight per epilogue warp).  Minimise waves x (K blocks x t_kb + exposed).
 struct PairPlan {
   int bn, nsub;
   double kb_s, tile_s;
 };
 static PairPlan plan_pair(int m_tiles, int N, int K, int clusters, int only_bn, int only_nsub) {
-  const PairPlan cands[6] = {{256, 1, 0.378e-6, 0.0},
-                             {256, 2, 0.677e-6, 8.6e-6},
-                             {240, 1, 0.378e-6, 0.0},  // measured: no faster per K block than 256
+  const PairPlan cands[6] = {{256, 1, 0.368e-6, 0.0},
+                             {256, 2, 0.685e-6, 3.8e-6},
+                             {240, 1, 0.368e-6, 0.0},  // measured: no faster per K block than 256
                              {192, 1, 0.332e-6, 0.0},
-                             {192, 2, 0.600e-6, 8.6e-6},
+                             {192, 2, 0.600e-6, 3.8e-6},
                              {128, 1, 0.276e-6, 0.0}};
   const int k_blocks = (K + BK - 1) / BK;
   PairPlan best = cands[0];

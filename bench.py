@@ -99,6 +99,8 @@ def parse_args():
     p.add_argument("--no-c3", action="store_true", help="skip the C3 serving replay")
     p.add_argument("--no-coop", action="store_true", help="skip the C1 cooperative-execution block")
     p.add_argument("--no-live", action="store_true", help="skip the two-GPU live-pair block")
+    p.add_argument("--no-realclock", action="store_true",
+                   help="skip the real-clock C3 burst on GPUs 0 and 1 (N >= 2)")
     p.add_argument("--cpu-sample-units", type=int, default=4)
     p.add_argument("--watchdog-s", type=int, default=900)
     return p.parse_args()
@@ -263,6 +265,42 @@ def decision_timings() -> dict:
             "reference_timed_on": "the build container by oracle/gen_golden.py --timings-only (the reference "
                                   "package is not installed on the GPU box), 1 thread, best of 5, together "
                                   "with ours on the same CPU (ours_ms_same_cpu_as_reference)"}
+
+
+# ---- C3 on the real clock -------------------------------------------------------------------------
+
+
+def c3_realclock(arch, rate: float = 30.0, duration: float = 9.0) -> dict:
+    """The C3 burst (5x for 2 s) served on the wall clock by real prefills on GPUs 0/1;
+    strategies static / allcache (host-cache load) / blitz (NVLink push)."""
+    import paper_2412_17246_b200 as ss
+    from paper_2412_17246_b200.realclock import RealClockServer
+
+    burst_at = duration / 3
+    trace = ss.generate_trace("burst", {"rate_per_s": rate, "duration_s": duration,
+                                        "prompt_tokens": [512, 2048], "output_tokens": [16, 128],
+                                        "bursts": [{"start_s": burst_at, "duration_s": 2, "multiplier": 5}]},
+                              seed=1)
+    arrivals = [(r.arrival_ms / 1e3, r.prompt_tokens) for r in trace]
+    srv = RealClockServer(arch)
+    try:
+        mean_tok = sum(n for _, n in arrivals) / len(arrivals)
+        pre_ms = sum(srv.prefill_ms(n, iters=2) for _, n in arrivals[:64]) / min(64, len(arrivals))
+        capacity = mean_tok / (pre_ms / 1e3)
+        out = {"trace": f"burst {rate:g} req/s x {duration:g} s, 5x for 2 s at t={burst_at:g} s, seed 1 "
+                        f"({len(arrivals)} requests, mean prompt {mean_tok:.0f} tokens)",
+               "served_by": "real prefills (one request each, prompts padded to 256-token buckets, CUDA graphs) "
+                            "on GPUs 0 and 1, host wall clock; trigger = reference should_scale_up on a 1 s "
+                            "arrival window vs the measured instance capacity",
+               "instance_capacity_tok_s": capacity, "strategies": {}}
+        for strat in ("static", "allcache", "blitz"):
+            r = srv.run(arrivals, strat, capacity)
+            out["strategies"][strat] = {k: getattr(r, k) for k in (
+                "p50_ttft_ms", "p99_ttft_ms", "mean_ttft_ms", "scale_trigger_s", "scale_ready_s", "load_ms",
+                "served")}
+        return out
+    finally:
+        srv.close()
 
 
 # ---- C1 cooperative execution (ZigZag) on this GPU vs the CPU fp32 oracle -----------------------
@@ -672,6 +710,18 @@ def run_blitz(args):
         if live is not None:
             log(f"live pair avg latency {live['avg_latency_ms']}")
 
+    # ---- C3 on the real clock (N >= 2): a 5x burst served by real 7B prefills on GPUs 0
+    # and 1, the scale-up triggered by the reference policy and executed by the data plane
+    realclock = None
+    if rank == 0 and N >= 2 and tp == 1 and not args.no_realclock:
+        log("c3 real clock (GPUs 0 and 1)")
+        try:
+            realclock = c3_realclock(arch)
+            log(f"c3 real clock p99: { {k: round(v['p99_ttft_ms'], 1) for k, v in realclock['strategies'].items()} }")
+        except Exception as e:  # report, never sink the bench line
+            realclock = {"error": f"{type(e).__name__}: {e}"}
+    fabric.barrier()
+
     decisions = decision_timings() if rank == 0 else None
     coop = None
     if rank == 0 and not args.no_coop:
@@ -714,7 +764,7 @@ def run_blitz(args):
                                                          else PCIE_PEAK_GBPS)) if achieved else None},
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
             "clocks": clk, "wall_s": wall, "c3": c3, "decisions": decisions, "coop_c1": coop,
-            "live_pair": live,
+            "live_pair": live, "c3_realclock": realclock,
         }
         print(json.dumps(line), flush=True)
     fabric.barrier()

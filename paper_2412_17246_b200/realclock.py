@@ -1,0 +1,256 @@
+"""C3 on the real clock: a bursty trace served by real Llama-2 7B prefills on two
+B200s, with the scale-up executed by the data plane while requests queue.
+
+The reference answers "p99 TTFT under a 5x burst" by replaying the trace through
+its event simulator with modeled costs (simcore.py, autoscaler.py:53-59,
+PAPER.md:1178-1221).  Here nothing is modeled: requests arrive on the host's
+wall clock, every prefill is a real forward pass of the slab-resident model
+(tcgen05 GEMMs), the scale trigger is the reference policy
+(``should_scale_up`` on a windowed arrival rate against the measured instance
+capacity) and the new instance's weights move for real:
+
+* ``blitz``    -- the plan's NVLink hop from the live source (``bz_push_tiles``),
+  the new instance serving once the tracker publishes the last layer;
+* ``allcache`` -- stop-the-world O(1) host-cache load over PCIe
+  (``bz_stage_tiles_ce``), the AllCache baseline;
+* ``static``   -- no scaling.
+
+One process drives both GPUs (peer access on); prompts are padded to 256-token
+buckets whose forward passes are captured as CUDA graphs.  TTFT = host time at
+which the request's prefill completion event is observed minus its arrival time.
+"""
+
+from __future__ import annotations
+
+import collections
+import time
+from dataclasses import dataclass, field
+from typing import Optional
+
+import torch
+
+from ._native import cuda_lib, ptr_array
+from .autoscaler import LoadMetrics, ScalePolicy, should_scale_up
+from .dataplane import DeviceSlab, HostCache, PeerSlab
+from .llama import LlamaExecutor, SlabWeights
+from .slab import LlamaArch, SlabLayout
+
+
+@dataclass
+class Req:
+    rid: int
+    t_arrive: float
+    n_tok: int
+    t_done: Optional[float] = None
+    served_by: str = ""
+
+
+@dataclass
+class _Instance:
+    name: str
+    device: torch.device
+    ex: LlamaExecutor
+    stream: torch.cuda.Stream
+    ready: bool
+    busy: Optional[tuple] = None   # (req, event)
+
+
+@dataclass
+class RealClockResult:
+    strategy: str
+    n: int
+    p50_ttft_ms: float
+    p99_ttft_ms: float
+    mean_ttft_ms: float
+    scale_trigger_s: Optional[float]
+    scale_ready_s: Optional[float]
+    load_ms: Optional[float]
+    served: dict = field(default_factory=dict)
+    wall_s: float = 0.0
+
+
+def _pct(xs, q):
+    ys = sorted(xs)
+    if not ys:
+        return 0.0
+    k = min(len(ys) - 1, max(0, int(round(q / 100.0 * (len(ys) - 1)))))
+    return ys[k]
+
+
+class RealClockServer:
+    """Source instance on ``src_dev`` (weights resident); the scale target on
+    ``tgt_dev`` starts empty."""
+
+    def __init__(self, arch: LlamaArch, src_dev: int = 0, tgt_dev: int = 1, tile_bytes: int = 1 << 20,
+                 push_ctas: int = 48):
+        self.arch = arch
+        self.lib = cuda_lib()
+        self.lib.bz_enable_peer_mesh(src_dev)
+        self.lib.bz_enable_peer_mesh(tgt_dev)
+        self.layout = SlabLayout.for_arch(arch, tile_bytes=tile_bytes)
+        self.src_dev, self.tgt_dev = src_dev, tgt_dev
+        self.push_ctas = push_ctas
+        with torch.cuda.device(src_dev):
+            self.src = DeviceSlab(self.layout, src_dev)
+            SlabWeights(arch, self.layout, self.src.data).init_random(seed=0)
+            torch.cuda.synchronize()
+            self.host = HostCache(self.layout)
+            self.host.tensor.copy_(self.src.data.cpu())
+        with torch.cuda.device(tgt_dev):
+            self.tgt = DeviceSlab(self.layout, tgt_dev)
+        # the target slab is a VMM allocation: the source GPU reaches it through its own
+        # mapping of the exported handle (as a peer process would), not the owner's VA
+        self.tgt_on_src = PeerSlab(src_dev, *self.tgt.export(), self.layout)
+        self.max_tokens = 4096
+        d0, d1 = torch.device("cuda", src_dev), torch.device("cuda", tgt_dev)
+        self.ex0 = LlamaExecutor(SlabWeights(arch, self.layout, self.src.data), self.max_tokens, d0)
+        self.ex1 = LlamaExecutor(SlabWeights(arch, self.layout, self.tgt.data), self.max_tokens, d1)
+        self.s0 = torch.cuda.Stream(device=d0)
+        self.s1 = torch.cuda.Stream(device=d1)
+        self.push_stream = torch.cuda.Stream(device=d0)
+        self.load_stream = torch.cuda.Stream(device=d1)
+        self.epoch = 0
+        self._warm()
+        self.graphs = {}
+        for name, ex, st, dev in (("src", self.ex0, self.s0, self.src_dev), ("tgt", self.ex1, self.s1, self.tgt_dev)):
+            for bucket in self.BUCKETS:
+                self.graphs[(name, bucket)] = self._capture(ex, st, dev, bucket)
+
+    # prompts are padded up to a bucket and each bucket's forward is one CUDA graph,
+    # so the single host thread that drives both GPUs spends ~10 us per prefill
+    BUCKETS = (512, 768, 1024, 1280, 1536, 1792, 2048)
+
+    @staticmethod
+    def bucket(n: int) -> int:
+        for b in RealClockServer.BUCKETS:
+            if n <= b:
+                return b
+        return RealClockServer.BUCKETS[-1]
+
+    def _capture(self, ex, stream, dev, n):
+        with torch.cuda.device(dev):
+            toks = torch.randint(0, self.arch.vocab, (1, n), device=f"cuda:{dev}")
+            with torch.cuda.stream(stream):
+                ex.forward(toks)
+            stream.synchronize()
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=stream):
+                ex.forward(toks)
+        return g
+
+    def _warm(self):
+        # every kernel / library plan both instances use, on their serving streams
+        for ex, s, dev in ((self.ex0, self.s0, self.src_dev), (self.ex1, self.s1, self.tgt_dev)):
+            with torch.cuda.device(dev), torch.cuda.stream(s):
+                for n in (512, 1024, 2048):
+                    ex.forward(torch.randint(0, self.arch.vocab, (1, n), device=f"cuda:{dev}"))
+            s.synchronize()
+
+    def prefill_ms(self, n_tok: int, iters: int = 5) -> float:
+        """Mean ms of one served prefill of ``n_tok`` tokens (its bucket's graph)."""
+        g = self.graphs[("src", self.bucket(n_tok))]
+        with torch.cuda.device(self.src_dev), torch.cuda.stream(self.s0):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(self.s0)
+            for _ in range(iters):
+                g.replay()
+            e1.record(self.s0)
+        e1.synchronize()
+        return e0.elapsed_time(e1) / iters
+
+    # ---- scale-up mechanisms ------------------------------------------------------------------
+
+    def _start_load(self, strategy: str) -> torch.cuda.Event:
+        """Enqueue the new instance's weight load; returns the event that marks the
+        last layer published on the target."""
+        self.epoch += 1
+        lay, tgt = self.layout, self.tgt
+        with torch.cuda.device(self.tgt_dev):
+            tgt.loaded.zero_()
+        torch.cuda.synchronize(self.tgt_dev)
+        if strategy == "blitz":
+            with torch.cuda.device(self.src_dev):
+                peer = self.tgt_on_src
+                self.lib.bz_push_tiles(self.src.ptr, ptr_array([peer.ptr]), ptr_array([peer.flags_ptr]), 1, None,
+                                       self.src.tile_off.data_ptr(), 0, lay.ntiles, self.epoch, self.push_ctas, 0,
+                                       self.push_stream.cuda_stream)
+        else:  # allcache: stop-the-world O(1) host-cache load over PCIe
+            with torch.cuda.device(self.tgt_dev):
+                self.lib.bz_stage_tiles_ce(self.host.ptr, tgt.ptr, tgt.flags_ptr, self.host.tile_off_host.ctypes.data,
+                                           0, lay.ntiles, 128, self.epoch, self.load_stream.cuda_stream)
+        with torch.cuda.device(self.tgt_dev):
+            self.lib.bz_track_layers(tgt.flags_ptr, tgt.layer_tile.data_ptr(), lay.num_layers, self.epoch,
+                                     tgt.loaded.data_ptr(), tgt.stamps.data_ptr(), self.load_stream.cuda_stream)
+            done = torch.cuda.Event()
+            done.record(self.load_stream)
+        return done
+
+    # ---- the replay -----------------------------------------------------------------------------
+
+    def run(self, arrivals: list[tuple[float, int]], strategy: str, capacity_tok_s: float,
+            window_s: float = 1.0, poll_sleep_s: float = 0.0002) -> RealClockResult:
+        reqs = [Req(i, t, n) for i, (t, n) in enumerate(arrivals)]
+        insts = [_Instance("gpu%d" % self.src_dev, torch.device("cuda", self.src_dev), self.ex0, self.s0, True),
+                 _Instance("gpu%d" % self.tgt_dev, torch.device("cuda", self.tgt_dev), self.ex1, self.s1, False)]
+        policy = ScalePolicy(upper_bound=capacity_tok_s, lower_bound=0.1 * capacity_tok_s,
+                             strategy="allcache" if strategy == "allcache" else "blitz-stop")
+        queue: collections.deque = collections.deque()
+        window: collections.deque = collections.deque()
+        nxt = 0
+        done = 0
+        load_ev = None
+        trigger_t = ready_t = None
+        t0 = time.perf_counter()
+        while done < len(reqs):
+            now = time.perf_counter() - t0
+            while nxt < len(reqs) and reqs[nxt].t_arrive <= now:
+                queue.append(reqs[nxt])
+                window.append((reqs[nxt].t_arrive, reqs[nxt].n_tok))
+                nxt += 1
+            while window and window[0][0] < now - window_s:
+                window.popleft()
+            # scale trigger: the reference policy on the windowed arrival rate
+            if strategy != "static" and trigger_t is None and now > window_s:
+                tps = sum(n for _, n in window) / window_s
+                if should_scale_up(LoadMetrics(window_s=window_s, tokens_per_s=tps), policy, 1) > 0:
+                    trigger_t = now
+                    load_ev = self._start_load(strategy)
+            if load_ev is not None and not insts[1].ready and load_ev.query():
+                insts[1].ready = True
+                ready_t = time.perf_counter() - t0
+            # completions
+            for inst in insts:
+                if inst.busy is not None and inst.busy[1].query():
+                    req = inst.busy[0]
+                    req.t_done = time.perf_counter() - t0
+                    req.served_by = inst.name
+                    inst.busy = None
+                    done += 1
+            # dispatch FCFS to idle ready instances
+            for inst in insts:
+                if inst.ready and inst.busy is None and queue:
+                    req = queue.popleft()
+                    key = ("src" if inst.ex is self.ex0 else "tgt", self.bucket(req.n_tok))
+                    with torch.cuda.device(inst.device), torch.cuda.stream(inst.stream):
+                        self.graphs[key].replay()
+                        ev = torch.cuda.Event()
+                        ev.record(inst.stream)
+                    inst.busy = (req, ev)
+            time.sleep(poll_sleep_s)
+        wall = time.perf_counter() - t0
+        ttft = [(r.t_done - r.t_arrive) * 1e3 for r in reqs]
+        served = collections.Counter(r.served_by for r in reqs)
+        load_ms = (ready_t - trigger_t) * 1e3 if ready_t is not None and trigger_t is not None else None
+        # reset the target for the next strategy
+        torch.cuda.synchronize(self.src_dev)
+        torch.cuda.synchronize(self.tgt_dev)
+        return RealClockResult(strategy=strategy, n=len(reqs), p50_ttft_ms=_pct(ttft, 50),
+                               p99_ttft_ms=_pct(ttft, 99), mean_ttft_ms=sum(ttft) / len(ttft),
+                               scale_trigger_s=trigger_t, scale_ready_s=ready_t, load_ms=load_ms,
+                               served=dict(served), wall_s=wall)
+
+    def close(self):
+        self.tgt_on_src.close()
+        self.host.close()
+        self.src.close()
+        self.tgt.close()

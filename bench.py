@@ -293,7 +293,7 @@ def c3_realclock(arch, rate: float = 30.0, duration: float = 9.0) -> dict:
                             "on GPUs 0 and 1, host wall clock; trigger = reference should_scale_up on a 1 s "
                             "arrival window vs the measured instance capacity",
                "instance_capacity_tok_s": capacity, "strategies": {}}
-        for strat in ("static", "allcache", "blitz"):
+        for strat in ("static", "allcache", "live-host", "blitz"):
             r = srv.run(arrivals, strat, capacity)
             out["strategies"][strat] = {k: getattr(r, k) for k in (
                 "p50_ttft_ms", "p99_ttft_ms", "mean_ttft_ms", "scale_trigger_s", "scale_ready_s", "load_ms",

@@ -38,6 +38,7 @@ class CoopResult:
     handoff_bytes: int = 0
     source_ms: Optional[float] = None
     total_ms: Optional[float] = None
+    finish_ms: Optional[list[float]] = None     # per batch, from the common start
 
 
 class CooperativePair:
@@ -93,12 +94,14 @@ class CooperativePair:
         start.record(cur)
         self.tgt_stream.wait_stream(cur)
         self.src_stream.wait_stream(cur)
+        src_start = torch.cuda.Event(enable_timing=True)   # per-batch finish times, source-side clock
+        src_start.record(self.src_stream)
         # ---- target: the rehearsed zigzag order, gated per layer -------------------------
         with torch.cuda.stream(self.tgt_stream):
             for b, layer, _s, _e in timeline.target_intervals:
-                if x[b] is None:
-                    x[b] = self.tgt.embed(batches[b])
                 gate(self.loaded.data_ptr(), layer, self.tgt_stream.cuda_stream)
+                if x[b] is None:  # the embedding table lives in unit 1: after its gate
+                    x[b] = self.tgt.embed(batches[b])
                 last = layer == config.splits[b][0]
                 if last and self.fused:
                     # K5 fused into the GEMM epilogue: tiles land in the source's buffer
@@ -121,29 +124,33 @@ class CooperativePair:
 
         # ---- source: suffixes FCFS, each gated on its hand-off counter -----------------------
         logits: list[Optional[torch.Tensor]] = [None] * n
+        fin = [torch.cuda.Event(enable_timing=True) for _ in range(n)]
         with torch.cuda.stream(self.src_stream):
             for i in range(n):
                 t_i, s_i = config.splits[i]
                 if t_i == 0:
                     h = None
                 else:
-                    gate(self.flag.data_ptr(), handed_at[i],
-                                           self.src_stream.cuda_stream)
+                    gate(self.flag.data_ptr(), handed_at[i], self.src_stream.cuda_stream)
                     h = recv[i]
                 logits[i] = self.src.forward(batches[i], first=t_i, last=L, x=h, kv=kv_s[i])
+                fin[i].record(self.src_stream)
         cur.wait_stream(self.src_stream)
         cur.wait_stream(self.tgt_stream)
         end.record(cur)
         end.synchronize()
         self._check_gates()
         return CoopResult(logits=logits, executed_order=order, handoff_bytes=nbytes,
-                          total_ms=start.elapsed_time(end))
+                          total_ms=start.elapsed_time(end), finish_ms=[src_start.elapsed_time(e) for e in fin])
 
     def _check_gates(self):
         """A gate that timed out let its kernels run on data that never arrived: raise."""
         from .scaleup import check_wait_timeouts
-        torch.cuda.synchronize(self.tgt.h.device)
-        torch.cuda.synchronize(self.src.h.device)
+        # only this pair's streams: a device-wide sync would also wait for the weight
+        # transfer still streaming into the target on its own stream
+        for st, dev in ((self.tgt_stream, self.tgt.h.device), (self.src_stream, self.src.h.device)):
+            with torch.cuda.device(dev):
+                st.synchronize()
         for dev in {self.tgt.h.device.index, self.src.h.device.index}:
             check_wait_timeouts(dev)
 
@@ -183,6 +190,7 @@ class CooperativePair:
                 kv = caches[i][0]
                 recv[i] = torch.empty(tokens[i].numel(), self.src.arch.d_model, dtype=torch.bfloat16,
                                       device=self.src.h.device)
+                gate(self.loaded.data_ptr(), 1, self.tgt_stream.cuda_stream)   # embedding: unit 1
                 x = self.tgt.embed(tokens[i])
                 for k in range(t_i):
                     gate(self.loaded.data_ptr(), k + 1, self.tgt_stream.cuda_stream)

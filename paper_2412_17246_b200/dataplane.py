@@ -637,12 +637,18 @@ def execute_plan_loopback(plan: ScalePlan, slabs: dict[str, DeviceSlab], epoch: 
             continue
         slab = slabs[node]
         lay = slab.layout
+        published = False
         if role.parent is not None and role.parent.startswith("mem"):
             if host_cache is None:
                 raise RuntimeError("host cache required")
             if stage_engine == "ce":
-                lib.bz_stage_tiles_ce(host_cache.ptr, slab.ptr, slab.flags_ptr,
-                                      host_cache.tile_off_host.ctypes.data, 0, lay.ntiles, 8, epoch, s)
+                # layer by layer, each published in-stream after its last copy (as ScaleExecutor)
+                for k in range(lay.num_layers):
+                    t0, t1 = lay.tiles_of_layer(k)
+                    lib.bz_stage_tiles_ce(host_cache.ptr, slab.ptr, slab.flags_ptr,
+                                          host_cache.tile_off_host.ctypes.data, t0, t1, 8, epoch, s)
+                    lib.bz_publish_layer(slab.loaded.data_ptr(), k + 1, slab.stamps.data_ptr() + 8 * k, s)
+                published = True
             else:
                 lib.bz_stage_tiles_sm(host_cache.ptr, slab.ptr, slab.flags_ptr,
                                       slab.tile_off.data_ptr(), 0, lay.ntiles, epoch, nctas, s)
@@ -660,7 +666,7 @@ def execute_plan_loopback(plan: ScalePlan, slabs: dict[str, DeviceSlab], epoch: 
             lib.bz_push_tiles(slab.ptr, ptrs, flags, len(outs),
                               slab.flags_ptr if role.receives else None, slab.tile_off.data_ptr(),
                               0, lay.ntiles, epoch, nctas, engine, s)
-        if role.receives:
+        if role.receives and not published:
             lib.bz_track_layers(slab.flags_ptr, slab.layer_tile.data_ptr(), lay.num_layers, epoch,
                                 slab.loaded.data_ptr(), slab.stamps.data_ptr(), s)
 

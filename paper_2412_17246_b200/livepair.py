@@ -320,10 +320,10 @@ class LivePair:
             handed = {}
             with torch.cuda.stream(self.stream):
                 for b, layer, _s, _e in tl.target_intervals:
-                    if not started[b]:
+                    gate(self.slab.loaded.data_ptr(), layer, self.stream.cuda_stream)
+                    if not started[b]:  # the embedding table lives in unit 1: after its gate
                         torch.index_select(embed_w, 0, self.batches[b].reshape(-1), out=bufs[b][0])
                         started[b] = True
-                    gate(self.slab.loaded.data_ptr(), layer, self.stream.cuda_stream)
                     x_in = bufs[b][(layer - 1) % 2]
                     kv = caches[b] if caches else None
                     if layer == cfg.splits[b][0]:

@@ -13,6 +13,10 @@ capacity) and the new instance's weights move for real:
   the new instance serving once the tracker publishes the last layer;
 * ``allcache`` -- stop-the-world O(1) host-cache load over PCIe
   (``bz_stage_tiles_ce``), the AllCache baseline;
+* ``live-host`` -- the same host-cache load, but while it runs the two GPUs serve
+  queued requests as a ZigZag pair (``CooperativePair``: split by
+  ``configure_pipeline`` with the measured time_l, order by ``zigzag_schedule``,
+  target layers gated on the readiness counter, fused NVLink hand-off);
 * ``static``   -- no scaling.
 
 One process drives both GPUs (peer access on); prompts are padded to 256-token
@@ -30,7 +34,9 @@ from typing import Optional
 import torch
 
 from ._native import cuda_lib, ptr_array
+from . import livescale
 from .autoscaler import LoadMetrics, ScalePolicy, should_scale_up
+from .coop import CooperativePair
 from .dataplane import DeviceSlab, HostCache, PeerSlab
 from .llama import LlamaExecutor, SlabWeights
 from .slab import LlamaArch, SlabLayout
@@ -67,6 +73,7 @@ class RealClockResult:
     load_ms: Optional[float]
     served: dict = field(default_factory=dict)
     wall_s: float = 0.0
+    pair_runs: list = field(default_factory=list)   # live-host: (start s, splits, host ms)
 
 
 def _pct(xs, q):
@@ -115,6 +122,20 @@ class RealClockServer:
         for name, ex, st, dev in (("src", self.ex0, self.s0, self.src_dev), ("tgt", self.ex1, self.s1, self.tgt_dev)):
             for bucket in self.BUCKETS:
                 self.graphs[(name, bucket)] = self._capture(ex, st, dev, bucket)
+        self.pair = CooperativePair(self.ex0, self.ex1, self.tgt.loaded)
+        self.pair_tokens = {b: torch.randint(0, arch.vocab, (1, b), device=d0) for b in self.BUCKETS}
+        # warm the pair's own streams (library plans such as cuDNN SDPA are per stream:
+        # a cold stream costs 100+ ms on first use) with every bucket, gates open
+        with torch.cuda.device(tgt_dev):
+            self.tgt.loaded.fill_(arch.n_layers)
+        torch.cuda.synchronize(tgt_dev)
+        for b in self.BUCKETS:
+            cfg = livescale.configure_pipeline(2, arch.n_layers, 1.0)
+            with torch.cuda.device(src_dev):
+                self.pair.run([self.pair_tokens[b]] * 2, cfg, livescale.zigzag_schedule(cfg))
+        with torch.cuda.device(tgt_dev):
+            self.tgt.loaded.zero_()
+        torch.cuda.synchronize(tgt_dev)
 
     # prompts are padded up to a bucket and each bucket's forward is one CUDA graph,
     # so the single host thread that drives both GPUs spends ~10 us per prefill
@@ -174,13 +195,19 @@ class RealClockServer:
                 self.lib.bz_push_tiles(self.src.ptr, ptr_array([peer.ptr]), ptr_array([peer.flags_ptr]), 1, None,
                                        self.src.tile_off.data_ptr(), 0, lay.ntiles, self.epoch, self.push_ctas, 0,
                                        self.push_stream.cuda_stream)
-        else:  # allcache: stop-the-world O(1) host-cache load over PCIe
             with torch.cuda.device(self.tgt_dev):
-                self.lib.bz_stage_tiles_ce(self.host.ptr, tgt.ptr, tgt.flags_ptr, self.host.tile_off_host.ctypes.data,
-                                           0, lay.ntiles, 128, self.epoch, self.load_stream.cuda_stream)
+                self.lib.bz_track_layers(tgt.flags_ptr, tgt.layer_tile.data_ptr(), lay.num_layers, self.epoch,
+                                         tgt.loaded.data_ptr(), tgt.stamps.data_ptr(), self.load_stream.cuda_stream)
+        else:  # allcache / live-host: O(1) host-cache load over PCIe, layer by layer, each
+            # layer published in-stream after its last copy (as ScaleExecutor stages)
+            with torch.cuda.device(self.tgt_dev):
+                s = self.load_stream.cuda_stream
+                for k in range(lay.num_layers):
+                    t0, t1 = lay.tiles_of_layer(k)
+                    self.lib.bz_stage_tiles_ce(self.host.ptr, tgt.ptr, tgt.flags_ptr,
+                                               self.host.tile_off_host.ctypes.data, t0, t1, 128, self.epoch, s)
+                    self.lib.bz_publish_layer(tgt.loaded.data_ptr(), k + 1, tgt.stamps.data_ptr() + 8 * k, s)
         with torch.cuda.device(self.tgt_dev):
-            self.lib.bz_track_layers(tgt.flags_ptr, tgt.layer_tile.data_ptr(), lay.num_layers, self.epoch,
-                                     tgt.loaded.data_ptr(), tgt.stamps.data_ptr(), self.load_stream.cuda_stream)
             done = torch.cuda.Event()
             done.record(self.load_stream)
         return done
@@ -188,18 +215,23 @@ class RealClockServer:
     # ---- the replay -----------------------------------------------------------------------------
 
     def run(self, arrivals: list[tuple[float, int]], strategy: str, capacity_tok_s: float,
-            window_s: float = 1.0, poll_sleep_s: float = 0.0002) -> RealClockResult:
+            window_s: float = 1.0, poll_sleep_s: float = 0.0002, time_l: float = 13.0,
+            pair_batch: int = 2) -> RealClockResult:
+        """Replay ``arrivals`` (seconds, prompt tokens) on the wall clock.  ``time_l``
+        (one layer's load time over one layer's execution, livescale.py:4-14) and
+        ``pair_batch`` (requests per cooperative run) apply to ``live-host``."""
         reqs = [Req(i, t, n) for i, (t, n) in enumerate(arrivals)]
         insts = [_Instance("gpu%d" % self.src_dev, torch.device("cuda", self.src_dev), self.ex0, self.s0, True),
                  _Instance("gpu%d" % self.tgt_dev, torch.device("cuda", self.tgt_dev), self.ex1, self.s1, False)]
         policy = ScalePolicy(upper_bound=capacity_tok_s, lower_bound=0.1 * capacity_tok_s,
-                             strategy="allcache" if strategy == "allcache" else "blitz-stop")
+                             strategy={"allcache": "allcache", "live-host": "blitz-live"}.get(strategy, "blitz-stop"))
         queue: collections.deque = collections.deque()
         window: collections.deque = collections.deque()
         nxt = 0
         done = 0
         load_ev = None
         trigger_t = ready_t = None
+        pair_runs: list = []
         t0 = time.perf_counter()
         while done < len(reqs):
             now = time.perf_counter() - t0
@@ -226,6 +258,22 @@ class RealClockServer:
                     req.served_by = inst.name
                     inst.busy = None
                     done += 1
+            # live-host: while the new instance loads, serve queued requests as a ZigZag pair
+            if (strategy == "live-host" and load_ev is not None and not insts[1].ready and queue
+                    and insts[0].busy is None):
+                batch = [queue.popleft() for _ in range(min(pair_batch, len(queue)))]
+                toks = [self.pair_tokens[self.bucket(r.n_tok)] for r in batch]
+                cfg = livescale.configure_pipeline(len(batch), self.arch.n_layers, time_l)
+                t_run = time.perf_counter() - t0
+                with torch.cuda.device(self.src_dev):
+                    res = self.pair.run(toks, cfg, livescale.zigzag_schedule(cfg))
+                pair_runs.append((round(t_run, 4), [list(x) for x in cfg.splits],
+                                  round((time.perf_counter() - t0 - t_run) * 1e3, 2)))
+                for r, f in zip(batch, res.finish_ms):
+                    r.t_done = t_run + f / 1e3
+                    r.served_by = "pair"
+                    done += 1
+                continue
             # dispatch FCFS to idle ready instances
             for inst in insts:
                 if inst.ready and inst.busy is None and queue:
@@ -247,7 +295,7 @@ class RealClockServer:
         return RealClockResult(strategy=strategy, n=len(reqs), p50_ttft_ms=_pct(ttft, 50),
                                p99_ttft_ms=_pct(ttft, 99), mean_ttft_ms=sum(ttft) / len(ttft),
                                scale_trigger_s=trigger_t, scale_ready_s=ready_t, load_ms=load_ms,
-                               served=dict(served), wall_s=wall)
+                               served=dict(served), wall_s=wall, pair_runs=pair_runs)
 
     def close(self):
         self.tgt_on_src.close()

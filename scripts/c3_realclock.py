@@ -35,11 +35,11 @@ def main():
                     f"({len(arrivals)} requests, mean prompt {mean_tok:.0f} tokens)",
            "model": "llama2-7b (random-init bf16, one request per prefill, prompts padded to 256-token buckets)",
            "instance_capacity_tok_s": capacity, "prefill_ms_at_mean_prompt": pre_ms, "strategies": {}}
-    for strat in ("static", "allcache", "blitz"):
+    for strat in ("static", "allcache", "live-host", "blitz"):
         r = srv.run(arrivals, strat, capacity)
         out["strategies"][strat] = {k: getattr(r, k) for k in (
             "p50_ttft_ms", "p99_ttft_ms", "mean_ttft_ms", "scale_trigger_s", "scale_ready_s", "load_ms",
-            "served", "wall_s")}
+            "served", "wall_s", "pair_runs")}
         print(f"[c3rc] {strat}: p99 {r.p99_ttft_ms:.1f} ms p50 {r.p50_ttft_ms:.1f} load {r.load_ms}", flush=True)
     srv.close()
     print(json.dumps(out), flush=True)

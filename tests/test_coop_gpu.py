@@ -143,3 +143,29 @@ def test_serving_overlaps_host_staging(model):
     ex.close()
     hc.close()
     tgt.close()
+
+
+def test_target_embedding_waits_for_unit_one(model):
+    """The target's first work item reads the embedding table, which lives in unit 1:
+    with a target slab full of garbage and its readiness counter at 0, nothing may read
+    it before the gate opens (logits still match once the weights land late)."""
+    lay, src, w, ref_w = model
+    tgt = DeviceSlab(lay, 0)
+    tgt.data.fill_(0xFF)                       # NaN bf16 everywhere until the load lands
+    tgt.loaded.zero_()
+    cfg = ss.configure_pipeline(2, ARCH.n_layers, 1.0)
+    tl = ss.zigzag_schedule(cfg)
+    pair = CooperativePair(LlamaExecutor(w, max_tokens=64, device="cuda"),
+                           LlamaExecutor(SlabWeights(ARCH, lay, tgt.data), max_tokens=64, device="cuda"),
+                           tgt.loaded)
+    batches = _tokens(2, 2, 32, 17)
+    side = torch.cuda.Stream()
+    with torch.cuda.stream(side):
+        torch.cuda._sleep(50_000_000)          # the weights land ~tens of ms after the pair starts
+        tgt.data.copy_(src.data)
+        tgt.loaded.fill_(ARCH.n_layers)
+    res = pair.run(batches, cfg, tl)
+    torch.cuda.synchronize()
+    for b, logits in zip(batches, res.logits):
+        _check_logits(logits, forward_fp32(ARCH, ref_w, b.cpu()))
+    tgt.close()

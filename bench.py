@@ -18,6 +18,18 @@ shard starting in the pinned O(1) host cache: ``mem0 -> gpu0`` + NVLink fan-out
 to every other GPU, host->device bytes inside the timed region, per-layer
 stamps read back to the host.
 
+Beside the headline line (rank 0, same run):
+  c3            -- the C3 burst trace replayed through ``simcore`` with the
+                   reference's analytic costs and with costs measured here
+                   (prefill line, decode line, layer arrivals, host-cache load);
+  coop_c1       -- C1: ZigZag prefill while the new slab streams in, then
+                   cooperative decode (graph-captured), logits vs the fp32 oracle;
+  live_pair     -- N >= 2: two-process ZigZag on 7B while the slab crosses NVLink,
+                   then the KV hand-over and the new instance decoding alone;
+  c3_realclock  -- N >= 2: the burst served on the wall clock by real 7B prefills on
+                   GPUs 0/1 (static / AllCache / live-host / NVLink scale-up);
+  decisions     -- the planner / pipeline / replay calls vs the reference's timings.
+
 ``--impl reference`` times the reference's CPU path: the oracle's torch CPU
 copies of every layer unit along the same plan (all host threads), rank 0 only.
 """

@@ -689,14 +689,19 @@ def run_blitz(args):
             if N == 1 and host is None:
                 host = layers_value
             from paper_2412_17246_b200.calibrate import (build_costs, c3_report, measure_decode,
-                                                         measure_prefill)
+                                                         measure_prefill, measure_ssd_load)
             log("c3: measuring prefill and decode")
             pre = measure_prefill(arch, device=fabric.device)
             dec_runs = [measure_decode(arch, device=fabric.device) for _ in range(2)]
             dec = {b: min(r[b] for r in dec_runs) for b in dec_runs[0]}   # per-size best of two passes
+            try:
+                ssd = measure_ssd_load(device=fabric.device)
+            except OSError as e:      # no O_DIRECT-capable scratch space: keep the model
+                ssd = {"error": str(e)}
             costs = build_costs(prefill=pre, nvlink_layer_ms=nv, host_layer_ms=host, decode=dec,
+                                ssd_gbs=ssd.get("ssd_to_gpu_GBps"),
                                 source={"prefill_points_ms": pre, "decode_points_ms": dec,
-                                        "decode_context_tokens": 1024,
+                                        "decode_context_tokens": 1024, "ssd_probe": ssd,
                                         "measured_in": "this bench run"})
             c3 = c3_report(costs)
             c3["block_7b_2048tok"] = block_cpu_vs_gpu(arch, pre)

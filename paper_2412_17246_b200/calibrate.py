@@ -112,8 +112,62 @@ def measure_decode(arch: LlamaArch, batches: Sequence[int] = (1, 8, 32, 64), con
     return out
 
 
+def measure_ssd_load(nbytes: int = 2 << 30, chunk: int = 64 << 20, directory: str = "/tmp",
+                     device: int = 0) -> dict:
+    """The ServerlessLLM miss path on this box: a checkpoint-sized file read with
+    O_DIRECT into two pinned buffers, each chunk copied to HBM while the next is
+    read.  Returns the disk-only and the disk -> HBM rates (GB/s)."""
+    import os
+    import tempfile
+
+    dev = torch.device("cuda", device)
+    bufs = [torch.empty(chunk, dtype=torch.uint8, pin_memory=True) for _ in range(2)]
+    dst = torch.empty(chunk, dtype=torch.uint8, device=dev)
+    fd_tmp, path = tempfile.mkstemp(dir=directory, prefix="blitz_ssd_")
+    os.close(fd_tmp)
+    try:
+        src = torch.randint(0, 256, (chunk,), dtype=torch.uint8).numpy()
+        fd = os.open(path, os.O_WRONLY | os.O_DIRECT)
+        for _ in range(nbytes // chunk):
+            bufs[0].numpy()[:] = src
+            os.write(fd, memoryview(bufs[0].numpy()))
+        os.fsync(fd)
+        os.close(fd)
+        stream = torch.cuda.Stream(device=dev)
+        done = [None, None]
+        t0 = time.perf_counter()
+        fd = os.open(path, os.O_RDONLY | os.O_DIRECT)
+        total = disk_s = 0.0
+        i = 0
+        while True:
+            b = i % 2
+            if done[b] is not None:
+                done[b].synchronize()          # the copy out of this buffer has finished
+            r0 = time.perf_counter()
+            n = os.readv(fd, [memoryview(bufs[b].numpy())])
+            disk_s += time.perf_counter() - r0
+            if n <= 0:
+                break
+            with torch.cuda.stream(stream):
+                dst[:n].copy_(bufs[b][:n], non_blocking=True)
+                ev = torch.cuda.Event()
+                ev.record(stream)
+            done[b] = ev
+            total += n
+            i += 1
+        os.close(fd)
+        stream.synchronize()
+        wall = time.perf_counter() - t0
+    finally:
+        os.unlink(path)
+    return {"bytes": int(total), "disk_read_GBps": total / disk_s / 1e9, "ssd_to_gpu_GBps": total / wall / 1e9,
+            "method": "O_DIRECT reads of a %d MiB file into 2 pinned 64 MiB buffers, H2D overlapped"
+                      % (nbytes >> 20)}
+
+
 def build_costs(prefill: Optional[dict] = None, nvlink_layer_ms=None, host_layer_ms=None,
-                source: Optional[dict] = None, decode: Optional[dict] = None) -> MeasuredCosts:
+                source: Optional[dict] = None, decode: Optional[dict] = None,
+                ssd_gbs: Optional[float] = None) -> MeasuredCosts:
     a = b = da = db = None
     if prefill:
         xs = sorted(prefill)
@@ -123,7 +177,7 @@ def build_costs(prefill: Optional[dict] = None, nvlink_layer_ms=None, host_layer
         da, db = fit_line(xs, [decode[x] for x in xs])
     return MeasuredCosts(prefill_alpha_ms=a, prefill_beta_ms=b, nvlink_layer_ms=nvlink_layer_ms,
                          host_layer_ms=host_layer_ms, decode_alpha_ms=da, decode_beta_ms=db,
-                         source=source or {})
+                         ssd_to_gpu_gbs=ssd_gbs, source=source or {})
 
 
 def c3_report(costs: MeasuredCosts, topo_name: str = "b200-hgx-2x8",

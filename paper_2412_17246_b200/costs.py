@@ -14,8 +14,11 @@ and the cooperative executor actually determine on B200:
 * decode step time (``parampool.py:61-62``) -- a line through measured KV-cache
   decode steps of the same executor.
 
-RDMA/SSD edges are not executed on this single box; they keep the reference
-model and are labelled as such in ``describe()``.
+* the ServerlessLLM cache-miss load from local storage -- a measured disk ->
+  pinned host -> HBM pipeline rate (``calibrate.measure_ssd_load``).
+
+RDMA edges are not executed on this single box; they keep the reference model
+and are labelled as such in ``describe()``.
 """
 
 from __future__ import annotations
@@ -46,6 +49,7 @@ class MeasuredCosts(ReferenceCosts):
     host_layer_ms: Optional[list[float]] = None       # arrival of unit k from the pinned host cache
     decode_alpha_ms: Optional[float] = None
     decode_beta_ms: Optional[float] = None
+    ssd_to_gpu_gbs: Optional[float] = None            # measured disk -> pinned -> HBM rate (GB/s)
     source: dict = field(default_factory=dict)
 
     name = "b200-measured"
@@ -92,9 +96,23 @@ class MeasuredCosts(ReferenceCosts):
             return self.layer_arrival_s(plan, node, model, eta)[-1]
         return super().completion_s(plan, est, node, model, eta)
 
-    def stop_the_world_s(self, strategy, model, topo, pool, host_id, now_s, eta) -> float:
-        if strategy == "allcache" and self.host_layer_ms and len(self.host_layer_ms) == model.num_layers:
+    def _host_load_s(self, model) -> Optional[float]:
+        if self.host_layer_ms and len(self.host_layer_ms) == model.num_layers:
             return self.host_layer_ms[-1] / 1e3
+        return None
+
+    def stop_the_world_s(self, strategy, model, topo, pool, host_id, now_s, eta) -> float:
+        """AllCache and a ServerlessLLM keep-alive hit load from the host cache; a
+        ServerlessLLM miss reads the checkpoint from local storage (autoscaler.py:102-117)."""
+        host_s = self._host_load_s(model)
+        if strategy == "allcache" and host_s is not None:
+            return host_s
+        if strategy == "sllm":
+            hit = pool is not None and host_id is not None and pool.cache_hit(model.name, host_id, now_s)
+            if hit and host_s is not None:
+                return host_s
+            if not hit and self.ssd_to_gpu_gbs:
+                return model.shard_bytes / (self.ssd_to_gpu_gbs * 1e9)
         return super().stop_the_world_s(strategy, model, topo, pool, host_id, now_s, eta)
 
     def describe(self) -> dict:
@@ -105,6 +123,8 @@ class MeasuredCosts(ReferenceCosts):
             "host_cache_layers": "measured" if self.host_layer_ms else "reference-model",
             "decode": "measured" if self.decode_alpha_ms is not None else "reference-model",
             "decode_alpha_ms": self.decode_alpha_ms, "decode_beta_ms": self.decode_beta_ms,
-            "rdma/ssd edges": "reference-model",
+            "ssd_load": "measured" if self.ssd_to_gpu_gbs else "reference-model",
+            "ssd_to_gpu_GBps": self.ssd_to_gpu_gbs,
+            "rdma edges": "reference-model",
             **self.source,
         }

@@ -60,3 +60,22 @@ def test_c3_report_shape():
     for s in ("blitz-live", "allcache"):
         assert set(r["strategies"][s]) == {"modeled", "measured"}
         assert r["strategies"][s]["measured"]["p99_ttft_ms"] > 0
+
+
+def test_sllm_load_uses_host_on_hit_and_storage_on_miss():
+    """autoscaler.py:102-117 with measured rates: a keep-alive hit loads from the
+    pinned host cache (the measured host-staging time), a miss from local storage
+    (the measured disk -> HBM rate); without measurements the reference model."""
+    spec = model_spec_for(LLAMA2_7B)
+    topo = ss.load_topology("b200-hgx")
+    pool = ss.ParameterPool.init_pool([spec], topo, policy="keep-alive")
+    host = pool.cache_refs[spec.name][0].host_id
+    c = MeasuredCosts(host_layer_ms=[10.0 * (k + 1) for k in range(spec.num_layers)], ssd_to_gpu_gbs=4.0)
+    hit = c.stop_the_world_s("sllm", spec, topo, pool, host, 0.0, 1.0)
+    miss = c.stop_the_world_s("sllm", spec, topo, pool, host, 1e6, 1.0)   # keep-alive expired
+    assert hit == pytest.approx(0.32)
+    assert miss == pytest.approx(spec.shard_bytes / 4e9)
+    ref = simcore.ReferenceCosts()
+    assert MeasuredCosts().stop_the_world_s("sllm", spec, topo, pool, host, 1e6, 1.0) == \
+        ref.stop_the_world_s("sllm", spec, topo, pool, host, 1e6, 1.0)
+    assert c.describe()["ssd_load"] == "measured"

@@ -185,6 +185,9 @@ struct Params {
   int a_stage;   // smem stride of the A ring (a_bytes rounded up to the 1024-B swizzle atom)
   int stages;    // ring depth (single-CTA kernel)
   int b_static;  // B is not written by in-flight predecessors: prefetch it before pdl_wait
+  // split-K of the pair kernel (few tiles, long K): unit = (tile, K slice); slices
+  // store fp32 partials to ws[slice][M][N], k_splitk_reduce adds them into C
+  int ksplit, kb_slice;
 };
 
 // The (tile, k0, k1) segments one CTA processes, in order; identical for the
@@ -599,6 +602,61 @@ struct CfgPair {
   static_assert(ACC_BUFS * TILE_N <= 512, "TMEM");
 };
 
+// 32 fp32 columns of one row of a split-K partial (columns at or beyond `lim` skipped)
+__device__ __forceinline__ void store_partial(float* row_base, int col, const uint32_t (&r)[32], int lim) {
+#pragma unroll
+  for (int q = 0; q < 4; ++q)
+    if (col + 8 * q < lim)
+      asm volatile("st.global.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(row_base + col + 8 * q), "r"(r[8 * q]),
+                   "r"(r[8 * q + 1]), "r"(r[8 * q + 2]), "r"(r[8 * q + 3]), "r"(r[8 * q + 4]), "r"(r[8 * q + 5]),
+                   "r"(r[8 * q + 6]), "r"(r[8 * q + 7])
+                   : "memory");
+}
+
+// C = bf16(sum of the K-slice partials + R): 8 columns (two 256-bit loads per slice,
+// one 16-byte store) per thread; the fused hand-off signal is raised here.
+__global__ void __launch_bounds__(256) k_splitk_reduce(const float* __restrict__ ws, int ksplit, int M, int N,
+                                                       __nv_bfloat16* C, int ldc, const __nv_bfloat16* R, int ldr,
+                                                       uint32_t* signal) {
+  pdl_wait();
+  pdl_trigger();
+  const int g8 = N / 8;
+  const int64_t groups = static_cast<int64_t>(M) * g8;
+  const int64_t plane = static_cast<int64_t>(M) * N;
+  for (int64_t g = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; g < groups;
+       g += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int row = static_cast<int>(g / g8), col = static_cast<int>(g % g8) * 8;
+    const float* src = ws + static_cast<int64_t>(row) * N + col;
+    float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    for (int sl = 0; sl < ksplit; ++sl) {
+      const float4 a = __ldcg(reinterpret_cast<const float4*>(src + sl * plane));
+      const float4 b = __ldcg(reinterpret_cast<const float4*>(src + sl * plane) + 1);
+      acc[0] += a.x, acc[1] += a.y, acc[2] += a.z, acc[3] += a.w;
+      acc[4] += b.x, acc[5] += b.y, acc[6] += b.z, acc[7] += b.w;
+    }
+    if (R) {
+      const uint4 rv = *reinterpret_cast<const uint4*>(R + static_cast<int64_t>(row) * ldr + col);
+      const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&rv);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const float2 f = __bfloat1622float2(h[j]);
+        acc[2 * j] += f.x;
+        acc[2 * j + 1] += f.y;
+      }
+    }
+    *reinterpret_cast<uint4*>(C + static_cast<int64_t>(row) * ldc + col) =
+        make_uint4(pack_bf16(acc[0], acc[1]), pack_bf16(acc[2], acc[3]), pack_bf16(acc[4], acc[5]),
+                   pack_bf16(acc[6], acc[7]));
+  }
+  if (signal != nullptr) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence_system();
+      asm volatile("red.release.sys.global.add.u32 [%0], 1;" ::"l"(signal) : "memory");
+    }
+  }
+}
+
 // p.m_tiles counts 256-row pair tiles here
 template <int BN_, int NSUB_>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
@@ -624,6 +682,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
   const int cluster = blockIdx.x >> 1;
   const int clusters = gridDim.x >> 1;
   const int num_tiles = p.m_tiles * p.n_tiles;
+  const int num_units = num_tiles * p.ksplit;
   const int k_blocks = (p.K + BK - 1) / BK;
 
   if (warp == 0 && lane == 0) {
@@ -653,10 +712,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     if (lane == 0) {
       pdl_wait();
       uint32_t stage = 0, phase = 0;
-      for (int tile = cluster; tile < num_tiles; tile += clusters) {
+      for (int unit = cluster; unit < num_units; unit += clusters) {
+        const int tile = unit % num_tiles;
         const int m0 = (tile % p.m_tiles) * (2 * BM) + static_cast<int>(rank) * BM;
         const int n0 = (tile / p.m_tiles) * TILE_N + static_cast<int>(rank) * (BN / 2);
-        for (int kb = 0; kb < k_blocks; ++kb) {
+        const int kb0 = (unit / num_tiles) * p.kb_slice, kb1 = min(k_blocks, kb0 + p.kb_slice);
+        for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           if (leader) mbar_expect_tx(&full[stage], 2 * STAGE_BYTES);
           tma_load_2d_pair(sa + stage * A_BYTES, &map_a, kb * BK, m0, &full[stage]);
@@ -677,13 +738,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
       constexpr uint32_t idesc = instr_desc_bf16(2 * BM, BN);
       uint32_t stage = 0, phase = 0;
       int it = 0;
-      for (int tile = cluster; tile < num_tiles; tile += clusters, ++it) {
+      for (int unit = cluster; unit < num_units; unit += clusters, ++it) {
         const int buf = it % ACC_BUFS;
         const uint32_t use = static_cast<uint32_t>(it / ACC_BUFS);
+        const int kb0 = (unit / num_tiles) * p.kb_slice, kb1 = min(k_blocks, kb0 + p.kb_slice);
         mbar_wait(&acc_empty[buf], (use & 1) ^ 1);
         tc_fence_after();
         const uint32_t d = tmem_base + buf * TILE_N;
-        for (int kb = 0; kb < k_blocks; ++kb) {
+        for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
           const uint64_t da = umma_desc_sw128(smem_u32(sa + stage * A_BYTES));
@@ -692,7 +754,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
 #pragma unroll
             for (int j = 0; j < NSUB; ++j) {
               const uint64_t db = umma_desc_sw128(smem_u32(sb + stage * B_BYTES + j * B_SUB));
-              umma_bf16_pair(d + j * BN, da + 2 * k, db + 2 * k, idesc, (kb | k) != 0);
+              umma_bf16_pair(d + j * BN, da + 2 * k, db + 2 * k, idesc, (kb != kb0 || k != 0) ? 1u : 0u);
             }
           }
           umma_commit_pair(&empty[stage]);
@@ -709,7 +771,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     const int quarter = warp & 3;
     const uint32_t leader_acc_empty0 = mapa_cta(smem_u32(&acc_empty[0]), 0);
     int it = 0;
-    for (int tile = cluster; tile < num_tiles; tile += clusters, ++it) {
+    for (int unit = cluster; unit < num_units; unit += clusters, ++it) {
+      const int tile = unit % num_tiles;
       const int buf = it % ACC_BUFS;
       const uint32_t use = static_cast<uint32_t>(it / ACC_BUFS);
       const int m0 = (tile % p.m_tiles) * (2 * BM) + static_cast<int>(rank) * BM;
@@ -727,8 +790,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
         if (c + 32 < TILE_N) tmem_ld_32x32b_x32_async(taddr + c + 32, r1);
         tmem_wait_ld(r0);
         tmem_wait_ld(r1);
-        if (row < p.M && n0 + c < p.N) store_chunk(p, row, n0 + c, r0, lim);
-        if (row < p.M && c + 32 < TILE_N && n0 + c + 32 < p.N) store_chunk(p, row, n0 + c + 32, r1, lim);
+        if (row >= p.M) continue;
+        if (p.ksplit > 1) {
+          // fp32 partial of this K slice (reduced by k_splitk_reduce)
+          float* dst = p.ws + (static_cast<int64_t>(unit / num_tiles) * p.M + row) * p.N;
+          store_partial(dst, n0 + c, r0, lim);
+          if (c + 32 < TILE_N) store_partial(dst, n0 + c + 32, r1, lim);
+        } else {
+          if (n0 + c < p.N) store_chunk(p, row, n0 + c, r0, lim);
+          if (c + 32 < TILE_N && n0 + c + 32 < p.N) store_chunk(p, row, n0 + c + 32, r1, lim);
+        }
       }
       tc_fence_before();
       __syncwarp();
@@ -742,7 +813,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "n"(TMEM_COLS));
   }
-  if (p.signal != nullptr && threadIdx.x == 0) {
+  if (p.signal != nullptr && p.ksplit == 1 && threadIdx.x == 0) {
     __threadfence_system();
     asm volatile("red.release.sys.global.add.u32 [%0], 1;" ::"l"(p.signal) : "memory");
   }
@@ -905,16 +976,19 @@ static int launch(const CUtensorMap& ma, const void* B, int N, int K, int ldb, P
 
 template <int BN_, int NSUB_>
 static int launch_pair(const CUtensorMap& ma, const void* B, int N, int K, int ldb, Params p, int max_ctas,
-                       cudaStream_t stream, int* ctas_out) {
+                       int ksplit, cudaStream_t stream, int* ctas_out) {
   using Cf = CfgPair<BN_, NSUB_>;
   CUtensorMap mb;
   if (int rc = encode_kmajor(&mb, B, N, K, ldb, BN_ / 2)) return rc;
   p.n_tiles = (N + Cf::TILE_N - 1) / Cf::TILE_N;
+  const int k_blocks = (K + BK - 1) / BK;
+  p.kb_slice = (k_blocks + ksplit - 1) / ksplit;
+  p.ksplit = (k_blocks + p.kb_slice - 1) / p.kb_slice;   // no empty slice
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int cap = (max_ctas > 0 ? tmin(max_ctas, sms) : sms) / 2;
-  int clusters = p.m_tiles * p.n_tiles;
+  int clusters = p.m_tiles * p.n_tiles * p.ksplit;
   if (clusters > cap) clusters = cap;
   if (clusters < 1) clusters = 1;
   static bool attr_set[64] = {};
@@ -928,6 +1002,14 @@ static int launch_pair(const CUtensorMap& ma, const void* B, int N, int K, int l
                              Cf::SMEM_BYTES, stream, ma, mb, p);
   if (e != cudaSuccess) return bz_fail_cuda(e, "bz_gemm_bf16 (pair) launch");
   if (ctas_out) *ctas_out = 2 * clusters;
+  if (p.ksplit > 1) {
+    const int64_t groups = static_cast<int64_t>(p.M) * (N / 8);
+    const int blocks = static_cast<int>(tmin<int64_t>((groups + 255) / 256, 4 * sms));
+    e = launch_pdl(PDL_GEMM, k_splitk_reduce, dim3(blocks), dim3(256), 0, stream, static_cast<const float*>(p.ws),
+                   p.ksplit, p.M, N, p.C, p.ldc, p.R, p.ldr, p.signal);
+    if (e != cudaSuccess) return bz_fail_cuda(e, "bz_gemm_bf16 (split-K reduce) launch");
+    if (ctas_out) *ctas_out = blocks;
+  }
   return bz_check_launch("bz_gemm_bf16 (pair)");
 }
 
@@ -936,6 +1018,16 @@ static int pair_override() {
   static int v = -2;
   if (v == -2) {
     const char* e = getenv("BZ_GEMM_PAIR");
+    v = e ? atoi(e) : -1;
+  }
+  return v;
+}
+
+// BZ_GEMM_PAIR_SPLIT=0 disables the pair kernel's split-K (A/B checks); unset: model
+static int split_override() {
+  static int v = -2;
+  if (v == -2) {
+    const char* e = getenv("BZ_GEMM_PAIR_SPLIT");
     v = e ? atoi(e) : -1;
   }
   return v;
@@ -961,14 +1053,18 @@ static int nsub_override() {
 struct PairPlan {
   int bn, nsub;
   double kb_s, tile_s;
+  int ksplit;
+  double t = 0.0;  // predicted seconds
 };
-static PairPlan plan_pair(int m_tiles, int N, int K, int clusters, int only_bn, int only_nsub) {
-  const PairPlan cands[6] = {{256, 1, 0.368e-6, 0.0},
-                             {256, 2, 0.685e-6, 3.8e-6},
-                             {240, 1, 0.368e-6, 0.0},  // measured: no faster per K block than 256
-                             {192, 1, 0.332e-6, 0.0},
-                             {192, 2, 0.600e-6, 3.8e-6},
-                             {128, 1, 0.276e-6, 0.0}};
+static PairPlan plan_pair(int m_tiles, int M, int N, int K, int clusters, int only_bn, int only_nsub,
+                          int64_t ws_bytes) {
+  const PairPlan cands[6] = {{256, 1, 0.368e-6, 0.0, 1},
+                             {256, 2, 0.685e-6, 3.8e-6, 1},
+                             {240, 1, 0.368e-6, 0.0, 1},  // measured: no faster per K block than 256
+                             {192, 1, 0.332e-6, 0.0, 1},
+                             {192, 2, 0.600e-6, 3.8e-6, 1},
+                             {128, 1, 0.276e-6, 0.0, 1}};
+  const int splits[6] = {1, 2, 3, 4, 6, 8};
   const int k_blocks = (K + BK - 1) / BK;
   PairPlan best = cands[0];
   double best_t = 1e30;
@@ -976,11 +1072,43 @@ static PairPlan plan_pair(int m_tiles, int N, int K, int clusters, int only_bn, 
     if ((only_bn && c.bn != only_bn) || (only_nsub && c.nsub != only_nsub)) continue;
     const int tile_n = c.bn * c.nsub;
     const long tiles = static_cast<long>(m_tiles) * ((N + tile_n - 1) / tile_n);
-    const double waves = static_cast<double>((tiles + clusters - 1) / clusters);
-    const double t = waves * (k_blocks * c.kb_s + c.tile_s);
-    if (t < best_t) {
-      best_t = t;
-      best = c;
+    for (int sp : splits) {
+      // split K only to fill the chip (few tiles), into a workspace that holds the partials
+      if (sp > 1 && (tiles * sp > clusters || static_cast<int64_t>(sp) * M * N * 4 > ws_bytes ||
+                     k_blocks / sp < 8 || split_override() == 0))
+        continue;
+      const double waves = static_cast<double>((tiles * sp + clusters - 1) / clusters);
+      const double slice = static_cast<double>((k_blocks + sp - 1) / sp);
+      // partials written by the GEMM and read back by the reduce pass, bf16 written,
+      // ~3 us of launch and tail; a split must win by 10 % (the model is rough)
+      const double reduce = sp > 1 ? 3e-6 + (8.0 * sp + 2.0) * M * N / 5.0e12 : 0.0;
+      const double t = (waves * (slice * c.kb_s + c.tile_s) + reduce) * (sp > 1 ? 1.1 : 1.0);
+      if (t < best_t) {
+        best_t = t;
+        best = c;
+        best.ksplit = sp;
+        best.t = t;
+      }
+    }
+  }
+  return best;
+}
+
+// The single-CTA kernel's 128-row tiles fill the chip better when M is not a
+// multiple of 256 (e.g. 384 rows: 3 x 48 = 144 tiles of 128 x 256 in one wave vs
+// 96 pair tiles in two); per SM it retires a K block of a 128 x BN tile in the
+// same ~time as the pair kernel's share.  Returns the predicted seconds and width.
+static double single_tile_time(int M, int N, int K, int ctas, int* bn_out) {
+  const int widths[3] = {256, 192, 128};
+  const double kb_s[3] = {0.368e-6, 0.332e-6, 0.276e-6};
+  const int k_blocks = (K + BK - 1) / BK;
+  double best = 1e30;
+  for (int i = 0; i < 3; ++i) {
+    const long tiles = static_cast<long>((M + BM - 1) / BM) * ((N + widths[i] - 1) / widths[i]);
+    const double t = static_cast<double>((tiles + ctas - 1) / ctas) * k_blocks * kb_s[i];
+    if (t < best) {
+      best = t;
+      *bn_out = widths[i];
     }
   }
   return best;
@@ -999,7 +1127,16 @@ static int gemm_impl(const void* A, const void* B, void* C, const void* residual
   // skinny A: load only the rows that exist (8-row swizzle atoms); the rows of
   // the 128-row MMA beyond them read stale smem and are never stored
   const int po = pair_override();
-  const bool pair = po == 1 || (po == -1 && M >= 2 * BM);
+  bool pair = po == 1 || (po == -1 && M >= 2 * BM);
+  int single_bn = 0;
+  if (pair && po == -1 && bn_override() == 0) {
+    // a pair plan against single-CTA tiles (chip fill), using the pair model's constants
+    const int ctas_all = max_ctas > 0 ? tmin(max_ctas, 148) : 148;
+    const PairPlan pp = plan_pair((M + 2 * BM - 1) / (2 * BM), M, N, K, ctas_all / 2, 0, nsub_override(),
+                                  (workspace && !(reinterpret_cast<uintptr_t>(workspace) & 15)) ? ws_bytes : 0);
+    const double ts = single_tile_time(M, N, K, ctas_all, &single_bn);
+    if (ts < 0.95 * pp.t) pair = false;
+  }
   const int a_box = (!pair && M < BM) ? (M + 7) / 8 * 8 : BM;
   CUtensorMap ma;
   if (int rc = encode_kmajor(&ma, A, M, K, lda, a_box)) return rc;
@@ -1023,6 +1160,8 @@ static int gemm_impl(const void* A, const void* B, void* C, const void* residual
   p.streamk = 0;
   p.sk_per = 1;
   p.sk_total = 0;
+  p.ksplit = 1;
+  p.kb_slice = (K + BK - 1) / BK;
   p.a_bytes = a_box * BK * 2;
   p.b_static = (flags & BZ_GEMM_B_STATIC) ? 1 : 0;
   if (!workspace || (reinterpret_cast<uintptr_t>(workspace) & 15)) ws_bytes = 0;
@@ -1030,23 +1169,24 @@ static int gemm_impl(const void* A, const void* B, void* C, const void* residual
   const int forced = bn_override();
   if (pair) {
     p.m_tiles = (M + 2 * BM - 1) / (2 * BM);
-    const PairPlan pp = plan_pair(p.m_tiles, N, K, ctas / 2, forced, nsub_override());
+    const PairPlan pp = plan_pair(p.m_tiles, M, N, K, ctas / 2, forced, nsub_override(), ws_bytes);
+    const int sp = pp.ksplit;
     switch (pp.bn * 10 + pp.nsub) {
       case 1281:
-        return launch_pair<128, 1>(ma, B, N, K, ldb, p, max_ctas, s, ctas_out);
+        return launch_pair<128, 1>(ma, B, N, K, ldb, p, max_ctas, sp, s, ctas_out);
       case 1921:
-        return launch_pair<192, 1>(ma, B, N, K, ldb, p, max_ctas, s, ctas_out);
+        return launch_pair<192, 1>(ma, B, N, K, ldb, p, max_ctas, sp, s, ctas_out);
       case 1922:
-        return launch_pair<192, 2>(ma, B, N, K, ldb, p, max_ctas, s, ctas_out);
+        return launch_pair<192, 2>(ma, B, N, K, ldb, p, max_ctas, sp, s, ctas_out);
       case 2562:
-        return launch_pair<256, 2>(ma, B, N, K, ldb, p, max_ctas, s, ctas_out);
+        return launch_pair<256, 2>(ma, B, N, K, ldb, p, max_ctas, sp, s, ctas_out);
       case 2401:
-        return launch_pair<240, 1>(ma, B, N, K, ldb, p, max_ctas, s, ctas_out);
+        return launch_pair<240, 1>(ma, B, N, K, ldb, p, max_ctas, sp, s, ctas_out);
       default:
-        return launch_pair<256, 1>(ma, B, N, K, ldb, p, max_ctas, s, ctas_out);
+        return launch_pair<256, 1>(ma, B, N, K, ldb, p, max_ctas, sp, s, ctas_out);
     }
   }
-  SkinnyPlan plan{forced ? forced : pick_bn(M, N, ctas), 0};
+  SkinnyPlan plan{forced ? forced : (single_bn ? single_bn : pick_bn(M, N, ctas)), 0};
   if (M <= BM) {
     plan = plan_skinny(M, N, K, ctas, ws_bytes, forced);
   }

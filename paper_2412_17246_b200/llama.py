@@ -115,7 +115,7 @@ class LlamaExecutor:
         self.streamk_ws = torch.zeros(self.STREAMK_WS_BYTES // 4, dtype=torch.float32, device=dev)
         self.last_signal_ctas = 0
 
-    STREAMK_WS_BYTES = 32 << 20
+    STREAMK_WS_BYTES = 64 << 20
 
     def _gemm(self, x, w, out, residual=None, signal=None):
         import ctypes

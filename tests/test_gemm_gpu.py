@@ -140,3 +140,18 @@ def test_streamk_signal_counts_every_cta():
     torch.cuda.synchronize()
     assert ctas > 0 and int(sig.item()) == ctas
     _check(c, a.float() @ b.float().t())
+
+
+@pytest.mark.parametrize("m,n,k", [(256, 4096, 4096), (300, 4096, 11008), (512, 4096, 4096), (384, 1024, 8192)])
+def test_pair_splitk_prefill_shapes(m, n, k):
+    """Short-prompt prefill GEMMs (few 256-row pair tiles, long K) split K into fp32
+    partials reduced by a second pass, with the residual and the hand-off signal."""
+    torch.manual_seed(m + n + k)
+    a = (torch.randn(m, k, device="cuda") * 0.5).to(torch.bfloat16)
+    b = (torch.randn(n, k, device="cuda") * 0.02).to(torch.bfloat16)
+    r = torch.randn(m, n, device="cuda").to(torch.bfloat16)
+    sig = torch.zeros(1, dtype=torch.int32, device="cuda")
+    c, ctas = gemm_ex(a, b, residual=r, ws_bytes=64 << 20, signal=sig)
+    torch.cuda.synchronize()
+    _check(c, a.float() @ b.float().t() + r.float())
+    assert ctas > 0 and int(sig.item()) == ctas

@@ -20,7 +20,6 @@ operand bytes -- checked bitwise).
 
 from __future__ import annotations
 
-import ctypes
 import os
 from dataclasses import dataclass, field
 from typing import Optional
@@ -386,18 +385,15 @@ class LivePair:
         return self._grid
 
     def gemm_grid(self, m: int, n: int) -> int:
-        """CTAs the fused down-projection launches (the counter value that completes it)."""
+        """Signals the fused down-projection raises (the counter value that completes
+        it): probed through the executor's own GEMM call, so the schedule (tile
+        width, split-K, stream-K) is the one the timed runs use."""
         probe = torch.zeros(1, dtype=torch.int32, device=self.slab.data.device)
         a = torch.zeros(m, self.arch.ffn, dtype=torch.bfloat16, device=probe.device)
-        w = self.ex.w.layers[0]["wdown"]
         out = torch.empty(m, n, dtype=torch.bfloat16, device=probe.device)
-        ctas = ctypes.c_int(0)
-        self.lib.bz_gemm_bf16_signal(a.data_ptr(), w.data_ptr(), out.data_ptr(), None, m, n,
-                                     self.arch.ffn, a.stride(0), w.stride(0), out.stride(0), 0, 0,
-                                     probe.data_ptr(), ctypes.byref(ctas),
-                                     torch.cuda.current_stream().cuda_stream)
+        self.ex._gemm(a, self.ex.w.layers[0]["wdown"], out, signal=probe)
         torch.cuda.synchronize()
-        return ctas.value
+        return self.ex.last_signal_ctas
 
     def run_handover(self, cfg: livescale.PipelineConfig, tl: livescale.ZigzagTimeline,
                      decode_steps: int = 4, nctas: int = 128) -> Optional[dict]:

@@ -107,6 +107,8 @@ def parse_args():
     p.add_argument("--tiles-per-copy", type=int, default=128,
                    help="tiles per copy-engine memcpy (128 x 1 MiB measured best: 54.8 GB/s)")
     p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-stripe", action="store_true",
+                   help="host-cache loads over the rep's PCIe link only (no striping over its NVLink group)")
     p.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg (sweeps only)")
     p.add_argument("--no-c3", action="store_true", help="skip the C3 serving replay")
     p.add_argument("--no-coop", action="store_true", help="skip the C1 cooperative-execution block")
@@ -507,8 +509,8 @@ def run_reference(args):
 def run_blitz(args):
     import torch
     from paper_2412_17246_b200 import slab as S
-    from paper_2412_17246_b200.dataplane import DeviceSlab, Fabric, HostCache, plan_roles
-    from paper_2412_17246_b200.scaleup import ScaleUpSession, plan_for, rank_plan
+    from paper_2412_17246_b200.dataplane import DeviceSlab, Fabric, plan_roles
+    from paper_2412_17246_b200.scaleup import ScaleUpSession, plan_for, plan_host_cache, rank_plan
 
     fabric = Fabric.from_env()
     N, rank = fabric.world, fabric.rank
@@ -525,17 +527,17 @@ def run_blitz(args):
     seed = 241217
     my = gpus[rank]
 
-    def host_cache_for(plan, tag):
-        """Pinned O(1) host copy, only in the process whose GPU stages from it."""
-        role = plan_roles(plan).get(my)
-        if role is None or role.parent is None or not role.parent.startswith("mem"):
-            return None
-        hc = HostCache(layout)
+    def fill_random(host: torch.Tensor):
         tmp = DeviceSlab(layout, fabric.device)
         tmp.fill_random(seed)
-        hc.tensor.copy_(tmp.data.cpu())
+        host.copy_(tmp.data.cpu())
         tmp.close()
-        return hc
+
+    def host_cache_for(plan, tag):
+        """Pinned O(1) host copy (one /dev/shm region per host-fed group), mapped by the
+        ranks that stage from it: the rep, and its NVLink siblings when striped."""
+        return plan_host_cache(fabric, layout, plan, node_rank, fill_random,
+                               host_stripe=not args.no_stripe, tag=tag)
 
     if len(anchors) == 1:
         anchor_plan, model, est = plan_for(arch, ["mem0"], anchors, tp=tp)
@@ -555,7 +557,8 @@ def run_blitz(args):
     log("host cache ready" if hc is not None else "no host cache on this rank")
     sess = ScaleUpSession(fabric, layout, plan, node_rank, host_cache=hc, engine=engine,
                           nctas=args.nctas, fanout_mode=args.fanout, seed=seed,
-                          stage_engine=args.stage_engine, tiles_per_copy=args.tiles_per_copy)
+                          stage_engine=args.stage_engine, tiles_per_copy=args.tiles_per_copy,
+                          host_stripe=not args.no_stripe)
 
     log("session ready")
     # warm-up (first one verified bit-exact on every receiver)
@@ -642,7 +645,8 @@ def run_blitz(args):
             hc2 = host_cache_for(e2e_plan, "e2e")
             sess2 = ScaleUpSession(fabric, layout, e2e_plan, node_rank, host_cache=hc2, engine=engine,
                                    nctas=args.nctas, fanout_mode=args.fanout, seed=seed,
-                                   stage_engine=args.stage_engine, tiles_per_copy=args.tiles_per_copy)
+                                   stage_engine=args.stage_engine, tiles_per_copy=args.tiles_per_copy,
+                                   host_stripe=not args.no_stripe)
             for w in range(max(1, min(args.warmup, 2))):
                 sess2.run(verify=(w == 0))
         e2e_t = []
@@ -668,6 +672,7 @@ def run_blitz(args):
                "workload": f"public API: plan_for(mem0 -> {anchors}, tp={tp}) + ScaleUpSession.run() + "
                            f"stamp readback; plan {[(e.src, e.dst, e.kind) for e in e2e_plan.edges]}"
                            f" fan-out {e2e_plan.nvlink_fanout}",
+               "host_stripe": ({rep: len(m) for rep, m in sess2.executor.stripe_groups.items()} or None),
                "bit_exact": e2e_ok}
         sess2.close()
         if hc2 is not None:

@@ -105,6 +105,16 @@ int bz_push_tiles(const void* src, void* const* dst, uint32_t* const* dst_flags,
                   const uint32_t* wait_flags, const int64_t* tile_off, int t0, int t1,
                   uint32_t epoch, int nctas, int engine, void* stream);
 
+/* bz_push_tile_list: bz_push_tiles over an explicit tile list ids[0..n) (device
+ * int32), 16-byte vector engine.  Striped host-cache load: every member of a
+ * host-fed NVLink group stages its piece of each layer over its own PCIe link
+ * and forwards that piece to the other members (the mem<h> -> rep pcie edge plus
+ * ScalePlan.nvlink_fanout, planner.py:86-87, 245-253, realised over all the
+ * group's host links). */
+int bz_push_tile_list(const void* src, void* const* dst, uint32_t* const* dst_flags, int ndst,
+                      const uint32_t* wait_flags, const int64_t* tile_off, const int32_t* ids, int n,
+                      uint32_t epoch, int nctas, void* stream);
+
 /* bz_push_tiles_ce: the same hop on the copy engines (one destination): per
  * group of `tiles_per_copy` tiles, [relay: one-warp gate until wait_flags of the
  * group >= epoch] -> cudaMemcpyAsync into the peer VA -> release of dst_flags.

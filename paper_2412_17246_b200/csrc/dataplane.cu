@@ -103,6 +103,7 @@ struct PushArgs {
   int ndst;
   const uint32_t* wait_flags;
   const int64_t* tile_off;
+  const int32_t* ids;  // optional tile list: entries [t0, t1) of it name the tiles
   int t0, t1;
   uint32_t epoch;
 };
@@ -204,7 +205,8 @@ __global__ void __launch_bounds__(kThreads) k_push_tiles32(PushArgs a) {
 
 template <bool kRelay>
 __global__ void __launch_bounds__(kThreads) k_push_tiles(PushArgs a) {
-  for (int t = a.t0 + blockIdx.x; t < a.t1; t += gridDim.x) {
+  for (int i = a.t0 + blockIdx.x; i < a.t1; i += gridDim.x) {
+    const int t = a.ids ? __ldg(a.ids + i) : i;
     if (kRelay) wait_tile(a.wait_flags, t, a.epoch);
     const int64_t b = a.tile_off[t] >> 4, e = a.tile_off[t + 1] >> 4;
     copy_tile<kRelay, false>(a.src, a.dst, a.ndst, b, e);
@@ -455,6 +457,7 @@ static int fill_push_args(PushArgs& a, const void* src, void* const* dst, uint32
   a.ndst = ndst;
   a.wait_flags = wait_flags;
   a.tile_off = tile_off;
+  a.ids = nullptr;
   a.t0 = t0;
   a.t1 = t1;
   a.epoch = epoch;
@@ -490,6 +493,27 @@ extern "C" int bz_push_tiles(const void* src, void* const* dst, uint32_t* const*
     k_push_tiles<false><<<grid, kThreads, 0, s>>>(a);
   }
   return bz_check_launch("bz_push_tiles");
+}
+
+// Push an arbitrary list of tiles (ids[0..n)), each gated on this GPU's own
+// flag when wait_flags is given: a striped host load pushes the pieces this GPU
+// staged to every other member of its NVLink group, layer by layer.
+extern "C" int bz_push_tile_list(const void* src, void* const* dst, uint32_t* const* dst_flags, int ndst,
+                                 const uint32_t* wait_flags, const int64_t* tile_off, const int32_t* ids, int n,
+                                 uint32_t epoch, int nctas, void* stream) {
+  PushArgs a;
+  int rc = fill_push_args(a, src, dst, dst_flags, ndst, wait_flags, tile_off, 0, n, epoch);
+  if (rc) return rc;
+  if (n == 0) return BZ_OK;
+  if (!ids) return bz_fail(BZ_EINVAL, "push_tile_list: null tile list");
+  a.ids = ids;
+  const int grid = nctas > 0 ? min(nctas, n) : min(32, n);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (wait_flags)
+    k_push_tiles<true><<<grid, kThreads, 0, s>>>(a);
+  else
+    k_push_tiles<false><<<grid, kThreads, 0, s>>>(a);
+  return bz_check_launch("bz_push_tile_list");
 }
 
 extern "C" int bz_multicast_tiles(const void* src, void* mc_dst, uint32_t* mc_flags, const uint32_t* wait_flags,

@@ -363,6 +363,28 @@ def merge_plans(plans: Sequence[ScalePlan]) -> ScalePlan:
     return ScalePlan(edges=edges, chains=chains, nvlink_fanout=fan)
 
 
+def host_fed_groups(plan: ScalePlan) -> dict[str, list[str]]:
+    """rep -> [rep, *siblings] for every NVLink fan-out group whose rep is fed from a
+    host cache (``mem<h> -> rep`` pcie edge plus ``nvlink_fanout[rep]``)."""
+    roles = plan_roles(plan)
+    return {rep: [rep] + list(sibs) for rep, sibs in plan.nvlink_fanout.items()
+            if sibs and (roles[rep].parent or "").startswith("mem")}
+
+
+def stripe_pieces(layout: SlabLayout, members: int, index: int) -> list[tuple[int, int]]:
+    """Tile range [lo, hi) of every layer that member ``index`` of a striped host
+    load stages: each layer's tiles split into ``members`` contiguous pieces, so
+    every layer lands at the group's aggregate host rate."""
+    if not 0 <= index < members:
+        raise ValueError(f"member index {index} outside a group of {members}")
+    out = []
+    for k in range(layout.num_layers):
+        t0, t1 = layout.tiles_of_layer(k)
+        n = t1 - t0
+        out.append((t0 + n * index // members, t0 + n * (index + 1) // members))
+    return out
+
+
 # ---- executor -------------------------------------------------------------------------------
 
 
@@ -377,7 +399,7 @@ class ScaleExecutor:
     def __init__(self, fabric: Fabric, plan: ScalePlan, slab: DeviceSlab,
                  node_rank: dict[str, int], host_cache: Optional[HostCache] = None,
                  engine: int = ENGINE_VECTOR, nctas: int = 32, fanout_mode: str = "auto",
-                 stage_engine: str = "ce", tiles_per_copy: int = 128):
+                 stage_engine: str = "ce", tiles_per_copy: int = 128, host_stripe: bool = True):
         self.fabric = fabric
         self.plan = plan
         self.slab = slab
@@ -398,16 +420,30 @@ class ScaleExecutor:
             # delivers ~650 GB/s per destination, the NVLS multicast stream ~530 GB/s
             fanout_mode = "chain"
         self.fanout_mode = fanout_mode
+        # striped host load: a host-fed rep and its NVLink siblings each stage one
+        # piece of every layer over their own PCIe link and forward it to the others
+        self.stripe_groups = host_fed_groups(plan) if host_stripe and stage_engine == "ce" else {}
+        self.stripe_members: Optional[list[str]] = None
+        for members in self.stripe_groups.values():
+            if self.node in members:
+                self.stripe_members = members
         dev = torch.device("cuda", fabric.device)
         self.streams = {k: torch.cuda.Stream(device=dev) for k in ("copy", "fan", "track", "stage")}
         self.epoch = 0
         self._tile_off_host = np.ascontiguousarray(self.layout.tile_off)
         self.writers = self._fanout_writers() if fanout_mode == "nvls" else {}
+        self._stripe_ids = None
+        if self.stripe_members is not None:
+            pieces = stripe_pieces(self.layout, len(self.stripe_members),
+                                   self.stripe_members.index(self.node))
+            self._pieces = pieces
+            ids = np.concatenate([np.arange(lo, hi, dtype=np.int32) for lo, hi in pieces])
+            self._stripe_ids = torch.from_numpy(ids).to(dev)
 
         # every rank exports its slab; peers it sends to are imported
         exports = fabric.allgather((self.node, slab.export()))
         self.peers: dict[str, PeerSlab] = {}
-        for n in self._unicast_targets():
+        for n in self._unicast_targets() + self._stripe_peers():
             r = self.node_rank[n]
             pid, fd, nbytes = exports[r][1]
             self.peers[n] = PeerSlab(fabric.device, pid, fd, nbytes, self.layout)
@@ -436,6 +472,8 @@ class ScaleExecutor:
         """
         out = {}
         for rep, sibs in self.plan.nvlink_fanout.items():
+            if rep in self.stripe_groups:
+                continue
             parent = self.roles[rep].parent
             writer = rep
             if parent is not None and parent.startswith("gpu"):
@@ -449,6 +487,10 @@ class ScaleExecutor:
 
     # chain children, plus siblings when the fan-out is served by unicast
     def _unicast_targets(self) -> list[str]:
+        if self.stripe_members is not None:
+            # chain children get the whole slab (relayed); the group peers get this
+            # member's pieces (_stripe_peers)
+            return list(self.role.children)
         covered = {rep for rep, (w, _) in self.writers.items() if w == self.node and w != rep}
         out = [c for c in self.role.children if c not in covered]
         if self.fanout_mode == "chain" and self.role.fanout:
@@ -462,13 +504,23 @@ class ScaleExecutor:
             out.extend(self.role.fanout)
         return out
 
+    def _stripe_peers(self) -> list[str]:
+        if self.stripe_members is None:
+            return []
+        return [n for n in self.stripe_members if n != self.node]
+
+    def _staged(self) -> bool:
+        """This GPU copies (part of) the shard from a host cache."""
+        return self.stripe_members is not None or (
+            self.role.parent is not None and self.role.parent.startswith("mem"))
+
     def _feeds(self) -> tuple[list[str], bool]:
         """(unicast destinations, relay?) for this node's push kernel."""
         return self._unicast_targets(), self.role.receives
 
     def dominant_stream(self) -> Optional[str]:
         """Stream of this rank's bulk mover (for per-kernel timing), if any."""
-        if self.role.parent is not None and self.role.parent.startswith("mem"):
+        if self._staged():
             return "stage"
         if self.mc_out:
             return "fan"
@@ -493,10 +545,13 @@ class ScaleExecutor:
         dom = self.dominant_stream()
         if kernel_events is not None and dom is not None:
             kernel_events[0].record(st[dom])
-        staged = self.role.parent is not None and self.role.parent.startswith("mem")
+        staged = self._staged()
+        # a locally staged slab is published in-stream after each layer; a striped
+        # member also receives pieces from its peers, so the tracker publishes
+        self_published = staged and self.stage_engine == "ce" and self.stripe_members is None
         if self.role.receives and (track or staged):
             # reset loaded_layers and stamp this rank's launch time
-            stream = st["stage"] if staged and self.stage_engine == "ce" else st["track"]
+            stream = st["stage"] if self_published else st["track"]
             self.lib.bz_publish_layer(slab.loaded.data_ptr(), 0, slab.stamps.data_ptr()
                                       + 8 * lay.num_layers, stream.cuda_stream)
         if staged:
@@ -517,7 +572,7 @@ class ScaleExecutor:
                 self._stage_thread.start()
             else:
                 self._stage(e)
-        if self.role.receives and track and not (staged and self.stage_engine == "ce"):
+        if self.role.receives and track and not self_published:
             # a peer (or a staging kernel) produces the tiles: one-warp in-order tracker
             self.lib.bz_track_layers(slab.flags_ptr, slab.layer_tile.data_ptr(), lay.num_layers, e,
                                      slab.loaded.data_ptr(), slab.stamps.data_ptr(),
@@ -535,6 +590,13 @@ class ScaleExecutor:
             self.lib.bz_push_tiles(slab.ptr, ptrs, flags, len(dsts),
                                    slab.flags_ptr if relay else None, slab.tile_off.data_ptr(),
                                    0, lay.ntiles, e, self.nctas, self.engine, st["copy"].cuda_stream)
+        peers = self._stripe_peers()
+        if peers:
+            # forward this member's pieces (gated on its own staged flags) to the group
+            self.lib.bz_push_tile_list(slab.ptr, ptr_array([self.peers[n].ptr for n in peers]),
+                                       ptr_array([self.peers[n].flags_ptr for n in peers]), len(peers),
+                                       slab.flags_ptr, slab.tile_off.data_ptr(), self._stripe_ids.data_ptr(),
+                                       int(self._stripe_ids.numel()), e, self.nctas, st["copy"].cuda_stream)
         for grp in self.mc_out:
             self.lib.bz_multicast_tiles(slab.ptr, grp.ptr, grp.flags_ptr,
                                         slab.flags_ptr if relay else None, slab.tile_off.data_ptr(),
@@ -546,12 +608,16 @@ class ScaleExecutor:
     def kernels_per_launch(self) -> int:
         """Our kernels one ``launch`` enqueues on this rank (CE memcpys excluded)."""
         n = 0
-        staged = self.role.parent is not None and self.role.parent.startswith("mem")
+        staged = self._staged()
+        striped = self.stripe_members is not None
         if self.role.receives:
             n += 1  # reset/publish
-            if not (staged and self.stage_engine == "ce"):
+            if not (staged and self.stage_engine == "ce") or striped:
                 n += 1  # tracker
-        if staged:
+        if striped:
+            n += sum((hi - lo + self.tiles_per_copy - 1) // self.tiles_per_copy for lo, hi in self._pieces)
+            n += 1 if self._stripe_peers() else 0  # tile-list push
+        elif staged:
             if self.stage_engine == "ce":
                 lay = self.layout
                 for k in range(lay.num_layers):
@@ -571,9 +637,14 @@ class ScaleExecutor:
     def _stage(self, e: int):
         hc, slab, lay = self.host_cache, self.slab, self.layout
         if hc is None:
-            raise RuntimeError(f"{self.node} is fed by {self.role.parent} but no host cache was given")
+            raise RuntimeError(f"{self.node} stages from a host cache but none was given")
         s = self.streams["stage"].cuda_stream
-        if self.stage_engine == "ce":
+        if self.stripe_members is not None:
+            # this member's piece of every layer, in layer order; the tracker publishes
+            for lo, hi in self._pieces:
+                self.lib.bz_stage_tiles_ce(hc.ptr, slab.ptr, slab.flags_ptr, hc.tile_off_host.ctypes.data,
+                                           lo, hi, self.tiles_per_copy, e, s)
+        elif self.stage_engine == "ce":
             # copy engines, layer by layer; each layer is published in-stream right
             # after its last tile (no spinning tracker on a locally produced slab)
             for k in range(lay.num_layers):

@@ -15,7 +15,10 @@ from typing import Optional, Sequence
 
 import torch
 
-from .dataplane import ENGINE_VECTOR, DeviceSlab, Fabric, HostCache, ScaleExecutor
+import os
+from typing import Callable
+
+from .dataplane import ENGINE_VECTOR, DeviceSlab, Fabric, HostCache, ScaleExecutor, host_fed_groups, plan_roles
 from .planner import build_scale_request, estimate_completion, generate_plan
 from .slab import LlamaArch, SlabLayout, model_spec_for
 from .topology import FlowSet, load_topology
@@ -51,6 +54,41 @@ def rank_plan(anchor_plan, tp: int):
     from .dataplane import expand_tp, merge_plans
 
     return anchor_plan if tp == 1 else merge_plans(expand_tp(anchor_plan, tp))
+
+
+def plan_host_cache(fabric: Fabric, layout: SlabLayout, plan, node_rank: dict[str, int],
+                    fill: Callable[[torch.Tensor], None], host_stripe: bool = True,
+                    tag: str = "hc") -> Optional[HostCache]:
+    """This rank's view of the O(1) pinned host copy, or None if it stages nothing.
+
+    Collective (every rank calls it).  One /dev/shm region per host-fed group:
+    the rank of the rep (the ``mem<h> -> rep`` edge's target) creates it and
+    ``fill``s it; with ``host_stripe`` its NVLink siblings map the same pages
+    (each registers them pinned) and stage their own pieces of every layer.
+    """
+    node = {r: n for n, r in node_rank.items()}.get(fabric.rank)
+    roles = plan_roles(plan)
+    groups = host_fed_groups(plan) if host_stripe else {}
+    owner = node is not None and node in roles and (roles[node].parent or "").startswith("mem")
+    group_of = {m: rep for rep, members in groups.items() for m in members}
+    name = None
+    if owner:
+        name = f"bz_{tag}_{node}_{os.getpid()}"
+    names = fabric.allgather((node, name))
+    by_node = {n: nm for n, nm in names if nm}
+    hc = None
+    if owner:
+        hc = HostCache(layout, shm_name=name, create=True)
+        fill(hc.tensor)
+    fabric.barrier()
+    if not owner and node in group_of:
+        hc = HostCache(layout, shm_name=by_node[group_of[node]], create=False)
+    fabric.barrier()
+    if owner and hc is not None and hc.path:
+        # every member has mapped it; drop the name (the mappings keep the pages)
+        os.unlink(hc.path)
+        hc.path = None
+    return hc
 
 
 class TransferTimeout(RuntimeError):
@@ -97,7 +135,7 @@ class ScaleUpSession:
     def __init__(self, fabric: Fabric, layout: SlabLayout, plan, node_rank: dict[str, int],
                  host_cache: Optional[HostCache] = None, engine: int = ENGINE_VECTOR,
                  nctas: int = 32, fanout_mode: str = "auto", seed: int = 241217,
-                 stage_engine: str = "ce", tiles_per_copy: int = 128):
+                 stage_engine: str = "ce", tiles_per_copy: int = 128, host_stripe: bool = True):
         self.fabric = fabric
         self.layout = layout
         self.plan = plan
@@ -112,7 +150,8 @@ class ScaleUpSession:
         torch.cuda.synchronize()
         self.executor = ScaleExecutor(fabric, plan, self.slab, node_rank, host_cache=host_cache,
                                       engine=engine, nctas=nctas, fanout_mode=fanout_mode,
-                                      stage_engine=stage_engine, tiles_per_copy=tiles_per_copy)
+                                      stage_engine=stage_engine, tiles_per_copy=tiles_per_copy,
+                                      host_stripe=host_stripe)
         self.receives = self.executor.role.receives
         self._expected: Optional[torch.Tensor] = None
 

@@ -19,9 +19,8 @@ sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
 import torch  # noqa: E402
 
 from paper_2412_17246_b200 import slab as S  # noqa: E402
-from paper_2412_17246_b200.dataplane import (ENGINE_TMA, ENGINE_VECTOR, DeviceSlab, Fabric,  # noqa: E402
-                                             HostCache, plan_roles)
-from paper_2412_17246_b200.scaleup import ScaleUpSession, plan_for  # noqa: E402
+from paper_2412_17246_b200.dataplane import ENGINE_TMA, ENGINE_VECTOR, DeviceSlab, Fabric  # noqa: E402
+from paper_2412_17246_b200.scaleup import ScaleUpSession, plan_for, plan_host_cache  # noqa: E402
 
 
 def main():
@@ -38,21 +37,23 @@ def main():
         ("grouped-chain", ["gpu0"], gpus[1:], True, "chain", ENGINE_VECTOR),
         ("chain-vector", ["gpu0"], gpus[1:], False, "auto", ENGINE_VECTOR),
         ("chain-tma", ["gpu0"], gpus[1:], False, "auto", ENGINE_TMA),
-        ("hostcache-nvls", ["mem0"], gpus, True, "auto", ENGINE_VECTOR),
+        ("hostcache-rep", ["mem0"], gpus, True, "auto", ENGINE_VECTOR),
+        ("hostcache-stripe", ["mem0"], gpus, True, "auto", ENGINE_VECTOR),
     ]
+
+    def fill(host):
+        tmp = DeviceSlab(layout, fabric.device)
+        tmp.fill_random(241217)
+        host.copy_(tmp.data.cpu())
+        tmp.close()
+
     for name, srcs, tgts, group, fan, engine in cases:
         plan, _, _ = plan_for(arch, srcs, tgts, group=group)
-        role = plan_roles(plan).get(gpus[rank])
-        hc = None
-        if role is not None and role.parent is not None and role.parent.startswith("mem"):
-            hc = HostCache(layout)
-            tmp = DeviceSlab(layout, fabric.device)
-            tmp.fill_random(241217)
-            hc.tensor.copy_(tmp.data.cpu())
-            tmp.close()
+        stripe = name == "hostcache-stripe"
+        hc = plan_host_cache(fabric, layout, plan, node_rank, fill, host_stripe=stripe, tag=name)
         t0 = time.perf_counter()
         sess = ScaleUpSession(fabric, layout, plan, node_rank, host_cache=hc, engine=engine,
-                              nctas=16, fanout_mode=fan, seed=241217)
+                              nctas=16, fanout_mode=fan, seed=241217, host_stripe=stripe)
         oks, ms = [], []
         for _ in range(3):
             r = sess.run(verify=True)
@@ -70,6 +71,7 @@ def main():
                               "max_ms": ms_t.item(), "fanout_mode": sess.executor.fanout_mode,
                               "edges": [(e.src, e.dst) for e in plan.edges],
                               "fanout": plan.nvlink_fanout,
+                              "striped": bool(sess.executor.stripe_groups),
                               "setup_s": time.perf_counter() - t0}), flush=True)
         sess.close()
         if hc is not None:

@@ -12,7 +12,7 @@ import pytest
 import paper_2412_17246_b200 as ss
 from paper_2412_17246_b200 import slab as slabmod
 from paper_2412_17246_b200._native import CUDA_LIB, HOST_LIB, exported_symbols
-from paper_2412_17246_b200.dataplane import expand_tp, plan_roles
+from paper_2412_17246_b200.dataplane import expand_tp, host_fed_groups, plan_roles, stripe_pieces
 from oracle import dataplane_ref as ref
 
 ROOT = Path(__file__).resolve().parent.parent
@@ -107,6 +107,44 @@ def test_expand_tp_c4():
     per_rank = expand_tp(plan, 2)
     assert [(e.src, e.dst) for e in per_rank[1].edges] == [("gpu1", "gpu3")]
     assert per_rank[1].nvlink_fanout == {"gpu3": ["gpu5", "gpu7"]}
+
+
+def test_host_fed_groups_only_for_pcie_fed_reps():
+    topo = ss.load_topology("b200-hgx")
+    flows = ss.FlowSet(topo)
+    model = slabmod.model_spec_for(slabmod.LLAMA2_7B)
+    req = ss.build_scale_request(model, ["mem0"], [f"gpu{i}" for i in range(4)], topo, flows)
+    plan = ss.generate_plan(req, topo, flows)
+    rep = next(iter(plan.nvlink_fanout))
+    assert host_fed_groups(plan) == {rep: [rep] + plan.nvlink_fanout[rep]}
+    # an NVLink-fed rep (1 -> 8 from a GPU) is not a host-fed group
+    assert host_fed_groups(_b200_plan(7)) == {}
+    # C5: every TP rank's group is host-fed
+    model70 = slabmod.model_spec_for(slabmod.LLAMA2_70B, tp=4)
+    req = ss.build_scale_request(model70, ["mem0"], ["gpu0", "gpu4"], topo, ss.FlowSet(topo))
+    per_rank = expand_tp(ss.generate_plan(req, topo, ss.FlowSet(topo)), 4)
+    assert [len(host_fed_groups(p)) for p in per_rank] == [1, 1, 1, 1]
+
+
+@pytest.mark.parametrize("members", [1, 2, 3, 4, 8])
+def test_stripe_pieces_partition_every_layer(members):
+    lay = slabmod.SlabLayout.for_arch(slabmod.LLAMA2_7B, tile_bytes=1 << 20)
+    pieces = [stripe_pieces(lay, members, i) for i in range(members)]
+    seen = np.zeros(lay.ntiles, dtype=np.int32)
+    for k in range(lay.num_layers):
+        t0, t1 = lay.tiles_of_layer(k)
+        bounds = [pieces[i][k] for i in range(members)]
+        # contiguous, in member order, covering the layer exactly
+        assert bounds[0][0] == t0 and bounds[-1][1] == t1
+        assert all(bounds[i][1] == bounds[i + 1][0] for i in range(members - 1))
+        # balanced to one tile
+        sizes = [hi - lo for lo, hi in bounds]
+        assert max(sizes) - min(sizes) <= 1
+        for lo, hi in bounds:
+            seen[lo:hi] += 1
+    assert (seen == 1).all()
+    with pytest.raises(ValueError):
+        stripe_pieces(lay, members, members)
 
 
 def test_oracle_payload_and_fingerprint_properties():

@@ -2,7 +2,8 @@
 
 GPU path: spawns ``torchrun`` over every visible GPU (needs >= 2) running
 scripts/mgpu_check.py -- grouped/NVLS, grouped/chain, chain (vector + TMA
-engines) and host-cache fan-out plans, each verified bit-exact on every
+engines) and host-cache fan-out plans (NVLS, and striped over the group's
+PCIe links), each verified bit-exact on every
 receiver.  CPU path: the control plane (fd-exchange allgather, barriers, role
 derivation) over a 2-process gloo group.
 """
@@ -38,7 +39,7 @@ def test_torchrun_scaleup_bit_exact():
         capture_output=True, text=True, timeout=600, env=env, cwd=str(ROOT))
     lines = [json.loads(l) for l in proc.stdout.splitlines() if l.startswith("{")]
     assert proc.returncode == 0, proc.stdout[-2000:] + proc.stderr[-3000:]
-    assert len(lines) == 5 and all(l["ok"] for l in lines), lines
+    assert len(lines) == 6 and all(l["ok"] for l in lines), lines
 
 
 @pytest.mark.gpu

@@ -241,6 +241,12 @@ int bz_decode_attention(const void* q, int ldq, const void* k_cache, const void*
 /* ---- misc ------------------------------------------------------------------------------ */
 int bz_sm_count(int dev, int* n);
 
+/* Load every libblitz kernel into dev's context (returns how many).  CUDA lazy
+ * loading would otherwise load a kernel at its first launch, which may wait for
+ * the device to drain -- a deadlock if a resident gate/tracker kernel waits on
+ * that launch.  Called once per device by the Python layer. */
+int bz_preload_kernels(int dev, int* nloaded);
+
 #ifdef __cplusplus
 }
 #endif

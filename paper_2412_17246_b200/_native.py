@@ -141,6 +141,7 @@ _SIGNATURES = {
     "bz_decode_attention": [_P, _I, _P, _P, _I, _I, _I, _I, ctypes.c_int64, _P, _P, _I, _P, ctypes.c_int64,
                             _P],
     "bz_sm_count": [_I, _PI],
+    "bz_preload_kernels": [_I, _PI],
 }
 
 
@@ -177,13 +178,28 @@ class _CudaLib:
 
 
 _cuda: Optional[_CudaLib] = None
+_preloaded: set = set()
 
 
-def cuda_lib() -> _CudaLib:
-    """libblitz.so; raises NativeLibraryMissing if it was not built (no fallback)."""
+def cuda_lib(device: Optional[int] = None) -> _CudaLib:
+    """libblitz.so; raises NativeLibraryMissing if it was not built (no fallback).
+
+    The first call for a device (``device``, else torch's current device once CUDA
+    is initialised) loads every libblitz kernel into it (bz_preload_kernels):
+    producer and consumer kernels of the data plane run concurrently, and a lazy
+    module load at a first launch could otherwise wait on a spinning consumer.
+    """
     global _cuda
     if _cuda is None:
         _cuda = _CudaLib()
+    if device is None:
+        import torch
+        if torch.cuda.is_available() and torch.cuda.is_initialized():
+            device = torch.cuda.current_device()
+    if device is not None and int(device) not in _preloaded:
+        n = ctypes.c_int()
+        _cuda.bz_preload_kernels(int(device), ctypes.byref(n))
+        _preloaded.add(int(device))
     return _cuda
 
 

@@ -16,7 +16,8 @@ namespace bz {
   X(cuMemAddressFree) X(cuMemMap) X(cuMemUnmap) X(cuMemSetAccess) X(cuMemCreate)               \
   X(cuMemRelease) X(cuMemExportToShareableHandle) X(cuMemImportFromShareableHandle)            \
   X(cuMulticastCreate) X(cuMulticastAddDevice) X(cuMulticastBindMem) X(cuMulticastUnbind)      \
-  X(cuStreamWaitValue32) X(cuTensorMapEncodeTiled)
+  X(cuStreamWaitValue32) X(cuTensorMapEncodeTiled) X(cuFuncGetModule) X(cuModuleGetFunctionCount)    \
+  X(cuModuleEnumerateFunctions) X(cuFuncLoad)
 
 struct DriverApi {
 #define BZ_DECL_FN(name) decltype(&::name) name = nullptr;
@@ -26,6 +27,12 @@ struct DriverApi {
 
 // nullptr (and the error slot set) if the driver is unavailable
 const DriverApi* driver_api();
+
+// one kernel of each translation unit (= one CUDA module), for bz_preload_kernels
+const void* module_anchor_dataplane();
+const void* module_anchor_decode();
+const void* module_anchor_gemm();
+const void* module_anchor_llama();
 
 // record a message in the thread-local last-error slot, return `code`
 int bz_fail(int code, const char* msg);

@@ -664,3 +664,5 @@ extern "C" int bz_copy_panels(const void* src, void* dst, int64_t n_panels, int6
       panel_bytes >> 4);
   return bz_check_launch("bz_copy_panels");
 }
+
+const void* bz::module_anchor_dataplane() { return reinterpret_cast<const void*>(k_set_flags); }

@@ -378,3 +378,5 @@ extern "C" int bz_decode_attention(const void* q, int ldq, const void* k_cache, 
   return decode::attention<64>(group, rows, grid, s, qb, ldq, kb, vb, n_heads, n_kv, s_max, pos, ws, nsplit, chunk,
                                scale, ob, ldo);
 }
+
+const void* bz::module_anchor_decode() { return reinterpret_cast<const void*>(decode::k_rope_append); }

@@ -1230,3 +1230,5 @@ extern "C" int bz_gemm_bf16_ex(const void* A, const void* B, void* C, const void
   return gemm::gemm_impl(A, B, C, residual, M, N, K, lda, ldb, ldc, ldr, max_ctas, flags, workspace,
                          workspace_bytes, signal, ctas_out, stream);
 }
+
+const void* bz::module_anchor_gemm() { return reinterpret_cast<const void*>(gemm::k_splitk_reduce); }

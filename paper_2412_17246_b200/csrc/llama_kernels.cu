@@ -139,3 +139,5 @@ extern "C" int bz_silu_mul(const void* gu, void* act, int rows, int ffn, int ldg
   if (e != cudaSuccess) return bz_fail_cuda(e, "bz_silu_mul");
   return bz_check_launch("bz_silu_mul");
 }
+
+const void* bz::module_anchor_llama() { return reinterpret_cast<const void*>(llama::k_rmsnorm); }

@@ -16,6 +16,7 @@
 
 #include <cstdlib>
 #include <string>
+#include <vector>
 
 #include "../../include/blitz.h"
 #include "common.cuh"
@@ -194,6 +195,44 @@ extern "C" int bz_device_caps(int dev, int* multicast, int* posix_fd, int* fabri
 extern "C" int bz_sm_count(int dev, int* n) {
   cudaError_t e = cudaDeviceGetAttribute(n, cudaDevAttrMultiProcessorCount, dev);
   return e == cudaSuccess ? BZ_OK : bz_fail_cuda(e, "sm count");
+}
+
+// Load every kernel of libblitz into `dev`'s context now.  Under CUDA lazy
+// loading a kernel's first launch loads its module, which can wait for the
+// device to drain -- a deadlock when that launch is what a spinning gate or
+// tracker kernel (already resident) is waiting for.  The data plane launches
+// such producer/consumer pairs concurrently, so every module is loaded up front.
+extern "C" int bz_preload_kernels(int dev, int* nloaded) {
+  int prev = 0;
+  cudaGetDevice(&prev);
+  int rc = use_device(dev);
+  int total = 0;
+  const void* anchors[] = {module_anchor_dataplane(), module_anchor_decode(), module_anchor_gemm(),
+                           module_anchor_llama()};
+  for (const void* a : anchors) {
+    if (rc) break;
+    cudaFunction_t f = nullptr;
+    cudaError_t e = cudaGetFuncBySymbol(&f, a);
+    if (e != cudaSuccess) {
+      rc = bz_fail_cuda(e, "preload: cudaGetFuncBySymbol");
+      break;
+    }
+    CUmodule m = nullptr;
+    unsigned n = 0;
+    CUresult r = DRV()->cuFuncGetModule(&m, reinterpret_cast<CUfunction>(f));
+    if (r == CUDA_SUCCESS) r = DRV()->cuModuleGetFunctionCount(&n, m);
+    std::vector<CUfunction> fns(n);
+    if (r == CUDA_SUCCESS && n) r = DRV()->cuModuleEnumerateFunctions(fns.data(), n, m);
+    for (unsigned i = 0; r == CUDA_SUCCESS && i < n; ++i) r = DRV()->cuFuncLoad(fns[i]);
+    if (r != CUDA_SUCCESS) {
+      rc = bz_fail_cu(r, "preload: module functions");
+      break;
+    }
+    total += static_cast<int>(n);
+  }
+  cudaSetDevice(prev);
+  if (nloaded) *nloaded = total;
+  return rc;
 }
 
 extern "C" int bz_enable_peer_mesh(int dev) {

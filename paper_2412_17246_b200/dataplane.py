@@ -76,7 +76,7 @@ class Fabric:
         self.rank = rank
         self.world = world
         self.group = group
-        self.lib = cuda_lib()
+        self.lib = cuda_lib(device)
         import ctypes
         vals = [ctypes.c_int() for _ in range(4)]
         self.lib.bz_device_caps(device, *[ctypes.byref(v) for v in vals])
@@ -122,7 +122,7 @@ class DeviceSlab:
     def __init__(self, layout: SlabLayout, device: int):
         self.layout = layout
         self.device = device
-        self.lib = cuda_lib()
+        self.lib = cuda_lib(device)
         self.raw = BzSlab()
         self.lib.bz_slab_create(device, layout.total_bytes, self.raw)
         dev = torch.device("cuda", device)
@@ -171,7 +171,7 @@ class PeerSlab:
     """A peer process's slab mapped into this process (NVLink peer VA)."""
 
     def __init__(self, local_device: int, pid: int, fd: int, nbytes: int, layout: SlabLayout):
-        self.lib = cuda_lib()
+        self.lib = cuda_lib(local_device)
         self.raw = BzSlab()
         self.lib.bz_slab_import(local_device, pid, fd, nbytes, self.raw)
         self.layout = layout

@@ -100,9 +100,9 @@ class LlamaExecutor:
     def __init__(self, weights: SlabWeights, max_tokens: int, device):
         self.w = weights
         self.arch = weights.arch
-        self.lib = cuda_lib()
-        a = self.arch
         dev = torch.device(device)
+        self.lib = cuda_lib(dev.index if dev.index is not None else torch.cuda.current_device())
+        a = self.arch
         bf = torch.bfloat16
         self.h = torch.empty(max_tokens, a.d_model, dtype=bf, device=dev)
         self.qkv = torch.empty(max_tokens, a.d_model + 2 * a.kv_dim, dtype=bf, device=dev)

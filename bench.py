@@ -16,7 +16,9 @@ its tracker has published every layer).  value = delivered bytes / time
 e2e = the same metric through the public API (planning included) with the
 shard starting in the pinned O(1) host cache: ``mem0 -> gpu0`` + NVLink fan-out
 to every other GPU, host->device bytes inside the timed region, per-layer
-stamps read back to the host.
+stamps read back to the host.  At N >= 2 the host-fed group loads striped: every
+member stages its piece of each layer over its own PCIe link from the one shared
+host copy and forwards it over NVLink (``--no-stripe``: the rep's link only).
 
 Beside the headline line (rank 0, same run):
   c3            -- the C3 burst trace replayed through ``simcore`` with the
@@ -320,6 +322,32 @@ def c3_realclock(arch, rate: float = 30.0, duration: float = 9.0) -> dict:
 # ---- C1 cooperative execution (ZigZag) on this GPU vs the CPU fp32 oracle -----------------------
 
 
+def single_gpu_host_arrivals(layout, device: int, seed: int = 241217, runs: int = 2) -> list:
+    """Per-layer arrival times (ms) of one unstriped host-cache load into one GPU: the
+    stop-the-world / host-fed load of ONE new instance (C3 scales one at a time, so
+    it cannot stripe over sibling GPUs' PCIe links)."""
+    import paper_2412_17246_b200 as ss
+    from paper_2412_17246_b200.dataplane import DeviceSlab, Fabric, HostCache, ScaleExecutor
+
+    slab = DeviceSlab(layout, device)
+    slab.fill_random(seed)
+    hc = HostCache(layout)
+    hc.tensor.copy_(slab.data.cpu())
+    plan = ss.ScalePlan(edges=[ss.planner.PlanEdge("mem0", "gpu0", 512.0, "pcie")], chains=[["mem0", "gpu0"]])
+    ex = ScaleExecutor(Fabric(device), plan, slab, {"gpu0": 0}, host_cache=hc)
+    best = None
+    for _ in range(runs):
+        ex.launch()
+        ex.synchronize()
+        arr = ex.layer_arrivals_ms()
+        if best is None or arr[-1] < best[-1]:
+            best = arr
+    ex.close()
+    slab.close()
+    hc.close()
+    return best
+
+
 def coop_c1(device: int, n_batches: int = 8, seqs: int = 2, seq_len: int = 1000) -> dict:
     """C1: tiny 4-layer Llama (d=256) scaled 1->2 on one GPU.  The new instance's slab
     streams in from the pinned host cache (copy engines, per-layer publish) while the
@@ -509,7 +537,7 @@ def run_reference(args):
 def run_blitz(args):
     import torch
     from paper_2412_17246_b200 import slab as S
-    from paper_2412_17246_b200.dataplane import DeviceSlab, Fabric, plan_roles
+    from paper_2412_17246_b200.dataplane import DeviceSlab, Fabric, host_fed_groups, plan_roles
     from paper_2412_17246_b200.scaleup import ScaleUpSession, plan_for, plan_host_cache, rank_plan
 
     fabric = Fabric.from_env()
@@ -683,7 +711,8 @@ def run_blitz(args):
     if not args.no_c3 and tp == 1:
         roles_v = plan_roles(plan)
         e2e_roles = plan_roles(e2e_plan) if e2e_plan is not None else {}
-        mine = {"node": my, "value": layers_value, "host": layers_host,
+        striped = e2e_plan is not None and bool(host_fed_groups(e2e_plan)) and not args.no_stripe
+        mine = {"node": my, "value": layers_value, "host": None if striped else layers_host,
                 "value_parent": roles_v[my].parent if my in roles_v else None,
                 "host_parent": e2e_roles[my].parent if my in e2e_roles else None}
         allm = fabric.allgather(mine)
@@ -693,6 +722,10 @@ def run_blitz(args):
                         None)
             if N == 1 and host is None:
                 host = layers_value
+            if host is None and striped:
+                # the e2e load was striped over the group; C3 loads one instance at a time
+                log("c3: unstriped single-GPU host load for the host-fed strategies")
+                host = single_gpu_host_arrivals(layout, fabric.device)
             from paper_2412_17246_b200.calibrate import (build_costs, c3_report, measure_decode,
                                                          measure_prefill, measure_ssd_load)
             log("c3: measuring prefill and decode")

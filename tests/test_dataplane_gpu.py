@@ -194,6 +194,48 @@ def test_max_fanout_star_push_and_empty_range(tiny_layout):
     src.close()
 
 
+def test_preload_kernels_loads_every_module():
+    import ctypes
+    n = ctypes.c_int()
+    cuda_lib().bz_preload_kernels(0, ctypes.byref(n))
+    assert n.value >= 20   # push/multicast/stage/track/... + GEMM + decode + glue kernels
+
+
+def test_push_tile_list_moves_exactly_the_listed_tiles(tiny_layout):
+    """Tile-list push (striped host load): listed tiles land bit-exact with their flag,
+    unlisted tiles stay untouched; gating on the sender's own flags."""
+    from paper_2412_17246_b200._native import ptr_array
+    lib = cuda_lib()
+    src = DeviceSlab(tiny_layout, 0)
+    src.fill_random(seed=12)
+    dst = DeviceSlab(tiny_layout, 0)
+    dst.data.zero_()
+    n = tiny_layout.ntiles
+    ids = torch.tensor(list(range(n - 1, -1, -2)), dtype=torch.int32, device="cuda")  # odd-from-top, reversed
+    s = torch.cuda.current_stream().cuda_stream
+    src.flags.fill_(3)   # the sender's own pieces are staged (epoch 3)
+    lib.bz_push_tile_list(src.ptr, ptr_array([dst.ptr]), ptr_array([dst.flags_ptr]), 1, src.flags_ptr,
+                          src.tile_off.data_ptr(), ids.data_ptr(), int(ids.numel()), 3, 4, s)
+    lib.bz_push_tile_list(src.ptr, ptr_array([dst.ptr]), ptr_array([dst.flags_ptr]), 1, None,
+                          src.tile_off.data_ptr(), ids.data_ptr(), 0, 3, 4, s)   # empty list: no-op
+    torch.cuda.synchronize()
+    listed = set(ids.tolist())
+    off = tiny_layout.tile_off
+    flags = dst.flags.cpu().tolist()
+    for t in range(n):
+        a, b = int(off[t]), int(off[t + 1])
+        if t in listed:
+            assert flags[t] == 3 and torch.equal(dst.data[a:b], src.data[a:b]), t
+        else:
+            assert flags[t] == 0 and int(dst.data[a:b].count_nonzero()) == 0, t
+    from paper_2412_17246_b200._native import BlitzError
+    with pytest.raises(BlitzError):   # a non-empty list needs the ids
+        lib.bz_push_tile_list(src.ptr, ptr_array([dst.ptr]), ptr_array([dst.flags_ptr]), 1, None,
+                              src.tile_off.data_ptr(), None, 4, 3, 4, s)
+    src.close()
+    dst.close()
+
+
 def test_bad_arguments_raise():
     from paper_2412_17246_b200._native import BlitzError, ptr_array
     lib = cuda_lib()

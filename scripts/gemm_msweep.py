@@ -29,7 +29,8 @@ st = torch.cuda.current_stream().cuda_stream
 WS = 64 << 20  # as LlamaExecutor: enables the skinny/split-K schedules
 ws = torch.zeros(WS // 4, dtype=torch.float32, device="cuda")
 ctas = ctypes.c_int(0)
-for m in (256, 384, 512, 768, 1024, 1536):
+MS = [int(x) for x in __import__("os").environ.get("BZ_MS", "256,384,512,768,1024,1536").split(",")]
+for m in MS:
     for name, (n, k) in {"qkv": (12288, 4096), "o": (4096, 4096), "gate_up": (22016, 4096),
                          "down": (4096, 11008)}.items():
         a = torch.randn(m, k, device="cuda").to(torch.bfloat16)
@@ -40,5 +41,5 @@ for m in (256, 384, 512, 768, 1024, 1536):
         ref = bench(lambda: torch.matmul(a, b.t()))
         err = float(((c.float() - a.float() @ b.float().t()).abs().max() / (a.float() @ b.float().t()).abs().max()))
         f = 2.0 * m * n * k
-        print(json.dumps({"m": m, "shape": name, "ours_tf": round(f / ms / 1e9, 1),
+        print(json.dumps({"m": m, "shape": name, "ctas": ctas.value, "ours_tf": round(f / ms / 1e9, 1),
                           "cublas_tf": round(f / ref / 1e9, 1), "ratio": round(ref / ms, 3), "err": err}))

@@ -420,9 +420,16 @@ class ScaleExecutor:
             # delivers ~650 GB/s per destination, the NVLS multicast stream ~530 GB/s
             fanout_mode = "chain"
         self.fanout_mode = fanout_mode
+        # every rank exports its slab (and says whether it holds a host-cache view);
+        # peers it sends to are imported below
+        exports = fabric.allgather((self.node, slab.export(), host_cache is not None))
+        # (bystander ranks of a smaller plan join with None)
+        with_cache = {e[0] for e in exports if e is not None and e[0] is not None and e[2]}
         # striped host load: a host-fed rep and its NVLink siblings each stage one
         # piece of every layer over their own PCIe link and forward it to the others
-        self.stripe_groups = host_fed_groups(plan) if host_stripe and stage_engine == "ce" else {}
+        # (only for groups whose every member maps the host copy)
+        groups = host_fed_groups(plan) if host_stripe and stage_engine == "ce" else {}
+        self.stripe_groups = {rep: m for rep, m in groups.items() if all(n in with_cache for n in m)}
         self.stripe_members: Optional[list[str]] = None
         for members in self.stripe_groups.values():
             if self.node in members:
@@ -440,8 +447,6 @@ class ScaleExecutor:
             ids = np.concatenate([np.arange(lo, hi, dtype=np.int32) for lo, hi in pieces])
             self._stripe_ids = torch.from_numpy(ids).to(dev)
 
-        # every rank exports its slab; peers it sends to are imported
-        exports = fabric.allgather((self.node, slab.export()))
         self.peers: dict[str, PeerSlab] = {}
         for n in self._unicast_targets() + self._stripe_peers():
             r = self.node_rank[n]

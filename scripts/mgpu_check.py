@@ -52,8 +52,12 @@ def main():
         stripe = name == "hostcache-stripe"
         hc = plan_host_cache(fabric, layout, plan, node_rank, fill, host_stripe=stripe, tag=name)
         t0 = time.perf_counter()
+        # hostcache-rep: striping requested, but only the rep maps the host copy -> the
+        # executor keeps the rep-only realisation
         sess = ScaleUpSession(fabric, layout, plan, node_rank, host_cache=hc, engine=engine,
-                              nctas=16, fanout_mode=fan, seed=241217, host_stripe=stripe)
+                              nctas=16, fanout_mode=fan, seed=241217, host_stripe=True)
+        if name.startswith("hostcache"):
+            assert bool(sess.executor.stripe_groups) == stripe, (name, sess.executor.stripe_groups)
         oks, ms = [], []
         for _ in range(3):
             r = sess.run(verify=True)

@@ -1063,7 +1063,7 @@ static PairPlan plan_pair(int m_tiles, int M, int N, int K, int clusters, int on
                              {240, 1, 0.368e-6, 0.0, 1},  // measured: no faster per K block than 256
                              {192, 1, 0.332e-6, 0.0, 1},
                              {192, 2, 0.600e-6, 3.8e-6, 1},
-                             {128, 1, 0.276e-6, 0.0, 1}};
+                             {128, 1, 0.356e-6, 0.0, 1}};  // measured at M = 384-512 (r1_gemm_small_m.txt)
   const int splits[6] = {1, 2, 3, 4, 6, 8};
   const int k_blocks = (K + BK - 1) / BK;
   PairPlan best = cands[0];
@@ -1073,6 +1073,7 @@ static PairPlan plan_pair(int m_tiles, int M, int N, int K, int clusters, int on
     const int tile_n = c.bn * c.nsub;
     const long tiles = static_cast<long>(m_tiles) * ((N + tile_n - 1) / tile_n);
     for (int sp : splits) {
+      if (split_override() > 0 && sp != split_override()) continue;  // pinned (tests, sweeps)
       // split K only to fill the chip (few tiles), into a workspace that holds the partials
       if (sp > 1 && (tiles * sp > clusters || static_cast<int64_t>(sp) * M * N * 4 > ws_bytes ||
                      k_blocks / sp < 8 || split_override() == 0))
@@ -1100,7 +1101,7 @@ static PairPlan plan_pair(int m_tiles, int M, int N, int K, int clusters, int on
 // same ~time as the pair kernel's share.  Returns the predicted seconds and width.
 static double single_tile_time(int M, int N, int K, int ctas, int* bn_out) {
   const int widths[3] = {256, 192, 128};
-  const double kb_s[3] = {0.368e-6, 0.332e-6, 0.276e-6};
+  const double kb_s[3] = {0.368e-6, 0.332e-6, 0.312e-6};
   const int k_blocks = (K + BK - 1) / BK;
   double best = 1e30;
   for (int i = 0; i < 3; ++i) {
@@ -1135,7 +1136,7 @@ static int gemm_impl(const void* A, const void* B, void* C, const void* residual
     const PairPlan pp = plan_pair((M + 2 * BM - 1) / (2 * BM), M, N, K, ctas_all / 2, 0, nsub_override(),
                                   (workspace && !(reinterpret_cast<uintptr_t>(workspace) & 15)) ? ws_bytes : 0);
     const double ts = single_tile_time(M, N, K, ctas_all, &single_bn);
-    if (ts < 0.95 * pp.t) pair = false;
+    if (ts < pp.t) pair = false;
   }
   const int a_box = (!pair && M < BM) ? (M + 7) / 8 * 8 : BM;
   CUtensorMap ma;

@@ -29,7 +29,7 @@ Beside the headline line (rank 0, same run):
   live_pair     -- N >= 2: two-process ZigZag on 7B while the slab crosses NVLink,
                    then the KV hand-over and the new instance decoding alone;
   c3_realclock  -- N >= 2: the burst served on the wall clock by real 7B prefills on
-                   GPUs 0/1 (static / AllCache / live-host / NVLink scale-up);
+                   GPUs 0..N-1 (static / AllCache / live-host / NVLink chain scale-up);
   decisions     -- the planner / pipeline / replay calls vs the reference's timings.
 
 ``--impl reference`` times the reference's CPU path: the oracle's torch CPU
@@ -116,7 +116,7 @@ def parse_args():
     p.add_argument("--no-coop", action="store_true", help="skip the C1 cooperative-execution block")
     p.add_argument("--no-live", action="store_true", help="skip the two-GPU live-pair block")
     p.add_argument("--no-realclock", action="store_true",
-                   help="skip the real-clock C3 burst on GPUs 0 and 1 (N >= 2)")
+                   help="skip the real-clock C3 burst on GPUs 0..N-1 (N >= 2)")
     p.add_argument("--cpu-sample-units", type=int, default=4)
     p.add_argument("--watchdog-s", type=int, default=900)
     return p.parse_args()
@@ -286,9 +286,11 @@ def decision_timings() -> dict:
 # ---- C3 on the real clock -------------------------------------------------------------------------
 
 
-def c3_realclock(arch, rate: float = 30.0, duration: float = 9.0) -> dict:
-    """The C3 burst (5x for 2 s) served on the wall clock by real prefills on GPUs 0/1;
-    strategies static / allcache (host-cache load) / blitz (NVLink push)."""
+def c3_realclock(arch, n_gpus: int = 2, rate: float = 30.0, duration: float = 9.0) -> dict:
+    """The C3 burst (5x for 2 s) served on the wall clock by real prefills: the source
+    instance on GPU 0, new instances on GPUs 1..n_gpus-1 added as the reference
+    trigger asks; strategies static / allcache (host-cache loads) / live-host /
+    blitz (NVLink chain push)."""
     import paper_2412_17246_b200 as ss
     from paper_2412_17246_b200.realclock import RealClockServer
 
@@ -298,7 +300,7 @@ def c3_realclock(arch, rate: float = 30.0, duration: float = 9.0) -> dict:
                                         "bursts": [{"start_s": burst_at, "duration_s": 2, "multiplier": 5}]},
                               seed=1)
     arrivals = [(r.arrival_ms / 1e3, r.prompt_tokens) for r in trace]
-    srv = RealClockServer(arch)
+    srv = RealClockServer(arch, extra_devs=list(range(2, n_gpus)))
     try:
         mean_tok = sum(n for _, n in arrivals) / len(arrivals)
         pre_ms = sum(srv.prefill_ms(n, iters=2) for _, n in arrivals[:64]) / min(64, len(arrivals))
@@ -306,14 +308,14 @@ def c3_realclock(arch, rate: float = 30.0, duration: float = 9.0) -> dict:
         out = {"trace": f"burst {rate:g} req/s x {duration:g} s, 5x for 2 s at t={burst_at:g} s, seed 1 "
                         f"({len(arrivals)} requests, mean prompt {mean_tok:.0f} tokens)",
                "served_by": "real prefills (one request each, prompts padded to 256-token buckets, CUDA graphs) "
-                            "on GPUs 0 and 1, host wall clock; trigger = reference should_scale_up on a 1 s "
-                            "arrival window vs the measured instance capacity",
+                            f"on GPUs 0..{n_gpus - 1} (source on GPU 0), host wall clock; trigger = reference "
+                            "should_scale_up on a 1 s arrival window vs the measured instance capacity",
                "instance_capacity_tok_s": capacity, "strategies": {}}
         for strat in ("static", "allcache", "live-host", "blitz"):
             r = srv.run(arrivals, strat, capacity)
             out["strategies"][strat] = {k: getattr(r, k) for k in (
                 "p50_ttft_ms", "p99_ttft_ms", "mean_ttft_ms", "scale_trigger_s", "scale_ready_s", "load_ms",
-                "served")}
+                "served", "instances_added", "all_ready_s")}
         return out
     finally:
         srv.close()
@@ -769,9 +771,9 @@ def run_blitz(args):
     # and 1, the scale-up triggered by the reference policy and executed by the data plane
     realclock = None
     if rank == 0 and N >= 2 and tp == 1 and not args.no_realclock:
-        log("c3 real clock (GPUs 0 and 1)")
+        log(f"c3 real clock (GPUs 0..{N - 1})")
         try:
-            realclock = c3_realclock(arch)
+            realclock = c3_realclock(arch, n_gpus=N)
             log(f"c3 real clock p99: { {k: round(v['p99_ttft_ms'], 1) for k, v in realclock['strategies'].items()} }")
         except Exception as e:  # report, never sink the bench line
             realclock = {"error": f"{type(e).__name__}: {e}"}

@@ -19,8 +19,12 @@ capacity) and the new instance's weights move for real:
   target layers gated on the readiness counter, fused NVLink hand-off);
 * ``static``   -- no scaling.
 
-One process drives both GPUs (peer access on); prompts are padded to 256-token
-buckets whose forward passes are captured as CUDA graphs.  TTFT = host time at
+One process drives every GPU (peer access on); prompts are padded to 256-token
+buckets whose forward passes are captured as CUDA graphs.  With more than one
+target GPU the trigger adds as many instances as the policy asks for at once:
+``blitz`` pushes down a chain source -> t1 -> t2 ... (relays forward each tile as
+its flag lands, the plan's grouped NVLink fan-out realised as a sibling chain),
+``allcache`` stages every new instance from the host copy in parallel.  TTFT = host time at
 which the request's prefill completion event is observed minus its arrival time.
 """
 
@@ -29,7 +33,7 @@ from __future__ import annotations
 import collections
 import time
 from dataclasses import dataclass, field
-from typing import Optional
+from typing import Optional, Sequence
 
 import torch
 
@@ -74,6 +78,8 @@ class RealClockResult:
     served: dict = field(default_factory=dict)
     wall_s: float = 0.0
     pair_runs: list = field(default_factory=list)   # live-host: (start s, splits, host ms)
+    instances_added: int = 0
+    all_ready_s: Optional[float] = None             # every added instance serving
 
 
 def _pct(xs, q):
@@ -89,11 +95,13 @@ class RealClockServer:
     ``tgt_dev`` starts empty."""
 
     def __init__(self, arch: LlamaArch, src_dev: int = 0, tgt_dev: int = 1, tile_bytes: int = 1 << 20,
-                 push_ctas: int = 48):
+                 push_ctas: int = 48, extra_devs: Sequence[int] = ()):
         self.arch = arch
-        self.lib = cuda_lib()
-        self.lib.bz_enable_peer_mesh(src_dev)
-        self.lib.bz_enable_peer_mesh(tgt_dev)
+        self.lib = cuda_lib(src_dev)
+        self.tgt_devs = [tgt_dev] + [d for d in extra_devs if d not in (src_dev, tgt_dev)]
+        for d in [src_dev] + self.tgt_devs:
+            cuda_lib(d)
+            self.lib.bz_enable_peer_mesh(d)
         self.layout = SlabLayout.for_arch(arch, tile_bytes=tile_bytes)
         self.src_dev, self.tgt_dev = src_dev, tgt_dev
         self.push_ctas = push_ctas
@@ -103,25 +111,40 @@ class RealClockServer:
             torch.cuda.synchronize()
             self.host = HostCache(self.layout)
             self.host.tensor.copy_(self.src.data.cpu())
-        with torch.cuda.device(tgt_dev):
-            self.tgt = DeviceSlab(self.layout, tgt_dev)
-        # the target slab is a VMM allocation: the source GPU reaches it through its own
-        # mapping of the exported handle (as a peer process would), not the owner's VA
-        self.tgt_on_src = PeerSlab(src_dev, *self.tgt.export(), self.layout)
+        self.tslabs = []
+        for d in self.tgt_devs:
+            with torch.cuda.device(d):
+                self.tslabs.append(DeviceSlab(self.layout, d))
+        self.tgt = self.tslabs[0]
+        # target slabs are VMM allocations: a sender reaches one through its own mapping
+        # of the exported handle (as a peer process would), not the owner's VA.  Chain
+        # hops: source -> any target (a group's head), target j -> target j+1 (relay)
+        self.peer_on_src = [PeerSlab(src_dev, *t.export(), self.layout) for t in self.tslabs]
+        self.tgt_on_src = self.peer_on_src[0]
+        self.peer_next = [PeerSlab(self.tgt_devs[j], *self.tslabs[j + 1].export(), self.layout)
+                          for j in range(len(self.tslabs) - 1)]
         self.max_tokens = 4096
-        d0, d1 = torch.device("cuda", src_dev), torch.device("cuda", tgt_dev)
+        d0 = torch.device("cuda", src_dev)
         self.ex0 = LlamaExecutor(SlabWeights(arch, self.layout, self.src.data), self.max_tokens, d0)
-        self.ex1 = LlamaExecutor(SlabWeights(arch, self.layout, self.tgt.data), self.max_tokens, d1)
         self.s0 = torch.cuda.Stream(device=d0)
-        self.s1 = torch.cuda.Stream(device=d1)
         self.push_stream = torch.cuda.Stream(device=d0)
-        self.load_stream = torch.cuda.Stream(device=d1)
+        self.tex, self.ts, self.tload, self.tpush = [], [], [], []
+        for d, t in zip(self.tgt_devs, self.tslabs):
+            dev = torch.device("cuda", d)
+            self.tex.append(LlamaExecutor(SlabWeights(arch, self.layout, t.data), self.max_tokens, dev))
+            self.ts.append(torch.cuda.Stream(device=dev))
+            self.tload.append(torch.cuda.Stream(device=dev))
+            self.tpush.append(torch.cuda.Stream(device=dev))
+        self.ex1, self.s1, self.load_stream = self.tex[0], self.ts[0], self.tload[0]
         self.epoch = 0
         self._warm()
         self.graphs = {}
-        for name, ex, st, dev in (("src", self.ex0, self.s0, self.src_dev), ("tgt", self.ex1, self.s1, self.tgt_dev)):
+        plan = [("src", self.ex0, self.s0, self.src_dev)] + [
+            (f"t{j}", ex, st, d) for j, (ex, st, d) in enumerate(zip(self.tex, self.ts, self.tgt_devs))]
+        for name, ex, st, dev in plan:
             for bucket in self.BUCKETS:
                 self.graphs[(name, bucket)] = self._capture(ex, st, dev, bucket)
+        d1 = torch.device("cuda", tgt_dev)
         self.pair = CooperativePair(self.ex0, self.ex1, self.tgt.loaded)
         self.pair_tokens = {b: torch.randint(0, arch.vocab, (1, b), device=d0) for b in self.BUCKETS}
         # warm the pair's own streams (library plans such as cuDNN SDPA are per stream:
@@ -133,7 +156,7 @@ class RealClockServer:
             cfg = livescale.configure_pipeline(2, arch.n_layers, 1.0)
             with torch.cuda.device(src_dev):
                 self.pair.run([self.pair_tokens[b]] * 2, cfg, livescale.zigzag_schedule(cfg))
-        with torch.cuda.device(tgt_dev):
+        with torch.cuda.device(d1):
             self.tgt.loaded.zero_()
         torch.cuda.synchronize(tgt_dev)
 
@@ -161,7 +184,7 @@ class RealClockServer:
 
     def _warm(self):
         # every kernel / library plan both instances use, on their serving streams
-        for ex, s, dev in ((self.ex0, self.s0, self.src_dev), (self.ex1, self.s1, self.tgt_dev)):
+        for ex, s, dev in [(self.ex0, self.s0, self.src_dev)] + list(zip(self.tex, self.ts, self.tgt_devs)):
             with torch.cuda.device(dev), torch.cuda.stream(s):
                 for n in (512, 1024, 2048):
                     ex.forward(torch.randint(0, self.arch.vocab, (1, n), device=f"cuda:{dev}"))
@@ -181,36 +204,54 @@ class RealClockServer:
 
     # ---- scale-up mechanisms ------------------------------------------------------------------
 
-    def _start_load(self, strategy: str) -> torch.cuda.Event:
-        """Enqueue the new instance's weight load; returns the event that marks the
-        last layer published on the target."""
+    def _start_load(self, strategy: str, group: Sequence[int] = (0,)) -> list:
+        """Enqueue the weight load of the new instances ``group`` (target indices, in
+        order); returns, per target, the event that marks its last layer published."""
         self.epoch += 1
-        lay, tgt = self.layout, self.tgt
-        with torch.cuda.device(self.tgt_dev):
-            tgt.loaded.zero_()
-        torch.cuda.synchronize(self.tgt_dev)
+        lay = self.layout
+        for j in group:
+            with torch.cuda.device(self.tgt_devs[j]):
+                self.tslabs[j].loaded.zero_()
+            torch.cuda.synchronize(self.tgt_devs[j])
         if strategy == "blitz":
+            # chain: source -> group[0] -> group[1] -> ...; every relay forwards a tile
+            # as soon as its own flag carries the epoch
             with torch.cuda.device(self.src_dev):
-                peer = self.tgt_on_src
+                peer = self.peer_on_src[group[0]]
                 self.lib.bz_push_tiles(self.src.ptr, ptr_array([peer.ptr]), ptr_array([peer.flags_ptr]), 1, None,
                                        self.src.tile_off.data_ptr(), 0, lay.ntiles, self.epoch, self.push_ctas, 0,
                                        self.push_stream.cuda_stream)
-            with torch.cuda.device(self.tgt_dev):
-                self.lib.bz_track_layers(tgt.flags_ptr, tgt.layer_tile.data_ptr(), lay.num_layers, self.epoch,
-                                         tgt.loaded.data_ptr(), tgt.stamps.data_ptr(), self.load_stream.cuda_stream)
-        else:  # allcache / live-host: O(1) host-cache load over PCIe, layer by layer, each
-            # layer published in-stream after its last copy (as ScaleExecutor stages)
-            with torch.cuda.device(self.tgt_dev):
-                s = self.load_stream.cuda_stream
-                for k in range(lay.num_layers):
-                    t0, t1 = lay.tiles_of_layer(k)
-                    self.lib.bz_stage_tiles_ce(self.host.ptr, tgt.ptr, tgt.flags_ptr,
-                                               self.host.tile_off_host.ctypes.data, t0, t1, 128, self.epoch, s)
-                    self.lib.bz_publish_layer(tgt.loaded.data_ptr(), k + 1, tgt.stamps.data_ptr() + 8 * k, s)
-        with torch.cuda.device(self.tgt_dev):
-            done = torch.cuda.Event()
-            done.record(self.load_stream)
-        return done
+            for a, b in zip(group, group[1:]):
+                if b != a + 1:
+                    raise ValueError("a blitz group is a run of consecutive targets")
+                t, nxt = self.tslabs[a], self.peer_next[a]
+                with torch.cuda.device(self.tgt_devs[a]):
+                    self.lib.bz_push_tiles(t.ptr, ptr_array([nxt.ptr]), ptr_array([nxt.flags_ptr]), 1, t.flags_ptr,
+                                           t.tile_off.data_ptr(), 0, lay.ntiles, self.epoch, self.push_ctas, 0,
+                                           self.tpush[a].cuda_stream)
+            for j in group:
+                t = self.tslabs[j]
+                with torch.cuda.device(self.tgt_devs[j]):
+                    self.lib.bz_track_layers(t.flags_ptr, t.layer_tile.data_ptr(), lay.num_layers, self.epoch,
+                                             t.loaded.data_ptr(), t.stamps.data_ptr(), self.tload[j].cuda_stream)
+        else:  # allcache / live-host: O(1) host-cache load over PCIe into every new
+            # instance in parallel, layer by layer, each layer published in-stream
+            for k in range(lay.num_layers):
+                t0, t1 = lay.tiles_of_layer(k)
+                for j in group:
+                    t = self.tslabs[j]
+                    with torch.cuda.device(self.tgt_devs[j]):
+                        s = self.tload[j].cuda_stream
+                        self.lib.bz_stage_tiles_ce(self.host.ptr, t.ptr, t.flags_ptr,
+                                                   self.host.tile_off_host.ctypes.data, t0, t1, 128, self.epoch, s)
+                        self.lib.bz_publish_layer(t.loaded.data_ptr(), k + 1, t.stamps.data_ptr() + 8 * k, s)
+        events = []
+        for j in group:
+            with torch.cuda.device(self.tgt_devs[j]):
+                done = torch.cuda.Event()
+                done.record(self.tload[j])
+            events.append(done)
+        return events
 
     # ---- the replay -----------------------------------------------------------------------------
 
@@ -221,16 +262,20 @@ class RealClockServer:
         (one layer's load time over one layer's execution, livescale.py:4-14) and
         ``pair_batch`` (requests per cooperative run) apply to ``live-host``."""
         reqs = [Req(i, t, n) for i, (t, n) in enumerate(arrivals)]
-        insts = [_Instance("gpu%d" % self.src_dev, torch.device("cuda", self.src_dev), self.ex0, self.s0, True),
-                 _Instance("gpu%d" % self.tgt_dev, torch.device("cuda", self.tgt_dev), self.ex1, self.s1, False)]
+        insts = [_Instance("gpu%d" % self.src_dev, torch.device("cuda", self.src_dev), self.ex0, self.s0, True)]
+        insts += [_Instance("gpu%d" % d, torch.device("cuda", d), ex, st, False)
+                  for d, ex, st in zip(self.tgt_devs, self.tex, self.ts)]
+        keys = ["src"] + [f"t{j}" for j in range(len(self.tgt_devs))]
         policy = ScalePolicy(upper_bound=capacity_tok_s, lower_bound=0.1 * capacity_tok_s,
                              strategy={"allcache": "allcache", "live-host": "blitz-live"}.get(strategy, "blitz-stop"))
         queue: collections.deque = collections.deque()
         window: collections.deque = collections.deque()
         nxt = 0
         done = 0
-        load_ev = None
+        load_ev: dict[int, torch.cuda.Event] = {}     # target index -> load-complete event
+        started = 0                                  # targets whose load has been enqueued
         trigger_t = ready_t = None
+        ready_all_t = None
         pair_runs: list = []
         t0 = time.perf_counter()
         while done < len(reqs):
@@ -242,14 +287,25 @@ class RealClockServer:
             while window and window[0][0] < now - window_s:
                 window.popleft()
             # scale trigger: the reference policy on the windowed arrival rate
-            if strategy != "static" and trigger_t is None and now > window_s:
+            if strategy != "static" and started < len(self.tgt_devs) and now > window_s:
                 tps = sum(n for _, n in window) / window_s
-                if should_scale_up(LoadMetrics(window_s=window_s, tokens_per_s=tps), policy, 1) > 0:
-                    trigger_t = now
-                    load_ev = self._start_load(strategy)
-            if load_ev is not None and not insts[1].ready and load_ev.query():
-                insts[1].ready = True
-                ready_t = time.perf_counter() - t0
+                add = should_scale_up(LoadMetrics(window_s=window_s, tokens_per_s=tps), policy, 1 + started)
+                if add > 0:
+                    # live-host pairs the first new instance only; the rest load alone
+                    group = list(range(started, min(len(self.tgt_devs), started + add)))
+                    if trigger_t is None:
+                        trigger_t = now
+                    for j, ev in zip(group, self._start_load(strategy, group)):
+                        load_ev[j] = ev
+                    started = group[-1] + 1
+            for j, ev in load_ev.items():
+                if not insts[1 + j].ready and ev.query():
+                    insts[1 + j].ready = True
+                    t_ready = time.perf_counter() - t0
+                    if j == 0:
+                        ready_t = t_ready
+                    if all(insts[1 + i].ready for i in range(started)):
+                        ready_all_t = t_ready
             # completions
             for inst in insts:
                 if inst.busy is not None and inst.busy[1].query():
@@ -259,7 +315,7 @@ class RealClockServer:
                     inst.busy = None
                     done += 1
             # live-host: while the new instance loads, serve queued requests as a ZigZag pair
-            if (strategy == "live-host" and load_ev is not None and not insts[1].ready and queue
+            if (strategy == "live-host" and 0 in load_ev and not insts[1].ready and queue
                     and insts[0].busy is None):
                 batch = [queue.popleft() for _ in range(min(pair_batch, len(queue)))]
                 toks = [self.pair_tokens[self.bucket(r.n_tok)] for r in batch]
@@ -278,7 +334,7 @@ class RealClockServer:
             for inst in insts:
                 if inst.ready and inst.busy is None and queue:
                     req = queue.popleft()
-                    key = ("src" if inst.ex is self.ex0 else "tgt", self.bucket(req.n_tok))
+                    key = (keys[insts.index(inst)], self.bucket(req.n_tok))
                     with torch.cuda.device(inst.device), torch.cuda.stream(inst.stream):
                         self.graphs[key].replay()
                         ev = torch.cuda.Event()
@@ -289,16 +345,18 @@ class RealClockServer:
         ttft = [(r.t_done - r.t_arrive) * 1e3 for r in reqs]
         served = collections.Counter(r.served_by for r in reqs)
         load_ms = (ready_t - trigger_t) * 1e3 if ready_t is not None and trigger_t is not None else None
-        # reset the target for the next strategy
-        torch.cuda.synchronize(self.src_dev)
-        torch.cuda.synchronize(self.tgt_dev)
+        for d in [self.src_dev] + self.tgt_devs:
+            torch.cuda.synchronize(d)
         return RealClockResult(strategy=strategy, n=len(reqs), p50_ttft_ms=_pct(ttft, 50),
                                p99_ttft_ms=_pct(ttft, 99), mean_ttft_ms=sum(ttft) / len(ttft),
                                scale_trigger_s=trigger_t, scale_ready_s=ready_t, load_ms=load_ms,
-                               served=dict(served), wall_s=wall, pair_runs=pair_runs)
+                               served=dict(served), wall_s=wall, pair_runs=pair_runs,
+                               instances_added=started, all_ready_s=ready_all_t)
 
     def close(self):
-        self.tgt_on_src.close()
+        for p in self.peer_on_src + self.peer_next:
+            p.close()
         self.host.close()
         self.src.close()
-        self.tgt.close()
+        for t in self.tslabs:
+            t.close()

@@ -108,8 +108,9 @@ def test_control_plane_two_process_gloo(tmp_path):
 @pytest.mark.skipif(_gpus() < 2, reason="needs >= 2 GPUs")
 def test_realclock_burst_scales_and_serves_every_request():
     """Real-clock server (tiny model, short trace): the reference trigger fires in the
-    burst, the data plane loads GPU 1 (NVLink push / host-cache staging), both GPUs
-    serve, every request gets a TTFT, and the weights landed bit-exactly."""
+    burst, the data plane loads the new instances (NVLink chain push / host-cache
+    staging; GPUs 1..3 when present), they serve, every request gets a TTFT, and the
+    weights landed bit-exactly on every added instance."""
     sys.path.insert(0, str(ROOT))
     import torch
     import paper_2412_17246_b200 as ss
@@ -120,7 +121,8 @@ def test_realclock_burst_scales_and_serves_every_request():
                                         "output_tokens": [16, 128],
                                         "bursts": [{"start_s": 1, "duration_s": 1, "multiplier": 5}]}, seed=2)
     arrivals = [(r.arrival_ms / 1e3, r.prompt_tokens) for r in trace]
-    srv = RealClockServer(S.TINY_4L)
+    n = min(_gpus(), 4)
+    srv = RealClockServer(S.TINY_4L, extra_devs=list(range(2, n)))
     try:
         mean_tok = sum(n for _, n in arrivals) / len(arrivals)
         # a policy bound between the base and the burst arrival rates, so the trigger
@@ -132,6 +134,9 @@ def test_realclock_burst_scales_and_serves_every_request():
             assert r.scale_trigger_s is not None and 1.0 <= r.scale_trigger_s <= 2.5
             assert r.scale_ready_s is not None and r.load_ms is not None and r.load_ms > 0
             assert sum(r.served.values()) == r.n
-            assert torch.equal(srv.tgt.data.cpu(), srv.src.data.cpu())
+            assert r.instances_added >= 1
+            # every instance the trigger added holds the bit-exact weights (chain relays too)
+            for t in srv.tslabs[:r.instances_added]:
+                assert torch.equal(t.data.cpu(), srv.src.data.cpu())
     finally:
         srv.close()

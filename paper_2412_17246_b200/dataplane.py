@@ -46,6 +46,7 @@ ENGINE_TMA = 1
 ENGINE_VEC256 = 2   # 32-byte LDG/STG.E.ENL2.256 (sm_100)
 ENGINE_CE = 3       # copy engines (cudaMemcpyAsync into the peer VA), SMs left for compute
 CE_TILES_PER_COPY = 16
+MAX_DST = 8  # BZ_MAX_DST (include/blitz.h): destinations per push launch
 
 
 class _CudaView:
@@ -596,10 +597,12 @@ class ScaleExecutor:
                                    slab.flags_ptr if relay else None, slab.tile_off.data_ptr(),
                                    0, lay.ntiles, e, self.nctas, self.engine, st["copy"].cuda_stream)
         peers = self._stripe_peers()
-        if peers:
-            # forward this member's pieces (gated on its own staged flags) to the group
-            self.lib.bz_push_tile_list(slab.ptr, ptr_array([self.peers[n].ptr for n in peers]),
-                                       ptr_array([self.peers[n].flags_ptr for n in peers]), len(peers),
+        for i in range(0, len(peers), MAX_DST):
+            # forward this member's pieces (gated on its own staged flags) to the group,
+            # at most MAX_DST peers per launch
+            part = peers[i:i + MAX_DST]
+            self.lib.bz_push_tile_list(slab.ptr, ptr_array([self.peers[n].ptr for n in part]),
+                                       ptr_array([self.peers[n].flags_ptr for n in part]), len(part),
                                        slab.flags_ptr, slab.tile_off.data_ptr(), self._stripe_ids.data_ptr(),
                                        int(self._stripe_ids.numel()), e, self.nctas, st["copy"].cuda_stream)
         for grp in self.mc_out:
@@ -621,7 +624,7 @@ class ScaleExecutor:
                 n += 1  # tracker
         if striped:
             n += sum((hi - lo + self.tiles_per_copy - 1) // self.tiles_per_copy for lo, hi in self._pieces)
-            n += 1 if self._stripe_peers() else 0  # tile-list push
+            n += (len(self._stripe_peers()) + MAX_DST - 1) // MAX_DST  # tile-list pushes
         elif staged:
             if self.stage_engine == "ce":
                 lay = self.layout

@@ -178,3 +178,9 @@ def test_cpu_plan_execution_copies_bytes():
     assert set(done) == {"gpu1", "gpu2", "gpu3"}
     for i in range(1, 4):
         assert torch.equal(bufs[f"gpu{i}"], src)
+
+
+def test_max_dst_matches_header():
+    from paper_2412_17246_b200.dataplane import MAX_DST
+    text = (ROOT / "include" / "blitz.h").read_text()
+    assert int(re.search(r"#define BZ_MAX_DST (\d+)", text).group(1)) == MAX_DST

@@ -2,10 +2,13 @@
 import ctypes
 import json
 import sys
+from pathlib import Path
 
-import torch
+sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
 
-from paper_2412_17246_b200._native import cuda_lib
+import torch  # noqa: E402
+
+from paper_2412_17246_b200._native import cuda_lib  # noqa: E402
 
 lib = cuda_lib()
 ws = torch.zeros((32 << 20) // 4, dtype=torch.float32, device="cuda")
@@ -41,4 +44,4 @@ for m in ms:
             e1.synchronize()
             us = e0.elapsed_time(e1) / iters * 1e3
             res[label] = {"us": round(us, 2), "GBps": round(n * k * 2 / us / 1e3, 1)}
-        print(json.dumps({"m": m, "shape": name, **res}))
+        print(json.dumps({"m": m, "shape": name, "ctas": ctas.value, **res}))

@@ -1,12 +1,15 @@
 """One Llama-2 7B block decode step (B sequences, 1024 cached tokens), eager, for
 ncu launch lists: python scripts/decode_probe.py [B]."""
 import sys
+from pathlib import Path
 
-import torch
+sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
 
-from paper_2412_17246_b200 import slab as S
-from paper_2412_17246_b200.dataplane import DeviceSlab
-from paper_2412_17246_b200.llama import KVCache, LlamaExecutor, SlabWeights
+import torch  # noqa: E402
+
+from paper_2412_17246_b200 import slab as S  # noqa: E402
+from paper_2412_17246_b200.dataplane import DeviceSlab  # noqa: E402
+from paper_2412_17246_b200.llama import KVCache, LlamaExecutor, SlabWeights  # noqa: E402
 
 B = int(sys.argv[1]) if len(sys.argv) > 1 else 1
 a = S.LLAMA2_7B

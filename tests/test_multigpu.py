@@ -140,3 +140,18 @@ def test_realclock_burst_scales_and_serves_every_request():
                 assert torch.equal(t.data.cpu(), srv.src.data.cpu())
     finally:
         srv.close()
+
+
+@pytest.mark.gpu
+@pytest.mark.multigpu
+@pytest.mark.skipif(_gpus() < 2, reason="needs >= 2 GPUs")
+def test_measured_ramp_follows_steady_state_throughput():
+    """The executed pair's throughput with k of L layers on the new instance follows
+    the reference's steady_state_throughput shape (L / (L - k) for k <= L/2)."""
+    sys.path.insert(0, str(ROOT))
+    from paper_2412_17246_b200 import slab as S
+    from paper_2412_17246_b200.ramp import measure_ramp
+
+    r = measure_ramp(S.LLAMA2_7B, ks=[0, 8, 16], batches=8, seq_len=1000)
+    for p in r["points"]:
+        assert abs(p["measured_rel"] - p["reference_rel"]) <= 0.1 * p["reference_rel"], p

@@ -28,6 +28,8 @@ Beside the headline line (rank 0, same run):
                    cooperative decode (graph-captured), logits vs the fp32 oracle;
   live_pair     -- N >= 2: two-process ZigZag on 7B while the slab crosses NVLink,
                    then the KV hand-over and the new instance decoding alone;
+  ramp          -- N >= 2: pair throughput vs layers resident on the new instance, against
+                   the reference's steady_state_throughput;
   c3_realclock  -- N >= 2: the burst served on the wall clock by real 7B prefills on
                    GPUs 0..N-1 (static / AllCache / live-host / NVLink chain scale-up);
   decisions     -- the planner / pipeline / replay calls vs the reference's timings.
@@ -767,6 +769,16 @@ def run_blitz(args):
         if live is not None:
             log(f"live pair avg latency {live['avg_latency_ms']}")
 
+    # ---- measured pair-throughput ramp (N >= 2): the executed steady_state_throughput ----------
+    ramp = None
+    if rank == 0 and N >= 2 and tp == 1 and not args.no_live:
+        log("ramp: pair throughput vs layers resident on the new instance (GPUs 0, 1)")
+        try:
+            from paper_2412_17246_b200.ramp import measure_ramp
+            ramp = measure_ramp(arch, batches=12, ks=[0, 4, 8, 12, 16] if arch.n_layers == 32 else None)
+        except Exception as e:  # report, never sink the bench line
+            ramp = {"error": f"{type(e).__name__}: {e}"}
+
     # ---- C3 on the real clock (N >= 2): a 5x burst served by real 7B prefills on GPUs 0
     # and 1, the scale-up triggered by the reference policy and executed by the data plane
     realclock = None
@@ -821,7 +833,7 @@ def run_blitz(args):
                                                          else PCIE_PEAK_GBPS)) if achieved else None},
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
             "clocks": clk, "wall_s": wall, "c3": c3, "decisions": decisions, "coop_c1": coop,
-            "live_pair": live, "c3_realclock": realclock,
+            "live_pair": live, "ramp": ramp, "c3_realclock": realclock,
         }
         print(json.dumps(line), flush=True)
     fabric.barrier()

@@ -52,6 +52,9 @@ from pathlib import Path
 
 ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
+# stdout carries exactly one JSON line: NCCL's own log (the "NCCL version" banner
+# under NCCL_DEBUG=WARN/VERSION) goes to stderr unless the caller routed it
+os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
 
 def _push_traffic(payload: int):
     """DRAM bytes per launch of the dominant mover (k_push_tiles) from the committed

@@ -65,6 +65,12 @@ def measure_ramp(arch: LlamaArch, src_dev: int = 0, tgt_dev: int = 1, ks: Sequen
         points = []
         ref0 = livescale.steady_state_throughput(L, 0)
         meas0 = None
+        # one untimed source-alone pass first: the first split measured must not
+        # pay the clock ramp and lazy module loads (they depress k = 0 and make the
+        # later splits look super-linear)
+        with torch.cuda.device(src_dev):
+            cfg0 = livescale.PipelineConfig([(0, L)] * batches, L, 0.0, [1.0] * batches)
+            pair.run(toks, cfg0, livescale.zigzag_schedule(cfg0, [0.0] * L))
         for k in ks:
             cfg = livescale.PipelineConfig([(k, L - k)] * batches, L, 0.0, [1.0] * batches)
             tl = livescale.zigzag_schedule(cfg, [0.0] * L)
@@ -73,7 +79,7 @@ def measure_ramp(arch: LlamaArch, src_dev: int = 0, tgt_dev: int = 1, ks: Sequen
                          livescale.zigzag_schedule(livescale.PipelineConfig([(k, L - k)] * 2, L, 0.0, [1.0] * 2),
                                                    [0.0] * L))          # warm this split
                 best = None
-                for _ in range(2):
+                for _ in range(3):
                     res = pair.run(toks, cfg, tl)
                     f = res.finish_ms
                     rate = (batches - half) / ((f[-1] - f[half - 1]) / 1e3)

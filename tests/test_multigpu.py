@@ -152,6 +152,6 @@ def test_measured_ramp_follows_steady_state_throughput():
     from paper_2412_17246_b200 import slab as S
     from paper_2412_17246_b200.ramp import measure_ramp
 
-    r = measure_ramp(S.LLAMA2_7B, ks=[0, 8, 16], batches=8, seq_len=1000)
+    r = measure_ramp(S.LLAMA2_7B, ks=[0, 8, 16], batches=12, seq_len=2000)
     for p in r["points"]:
         assert abs(p["measured_rel"] - p["reference_rel"]) <= 0.1 * p["reference_rel"], p

@@ -52,9 +52,15 @@ from pathlib import Path
 
 ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
-# stdout carries exactly one JSON line: NCCL's own log (the "NCCL version" banner
-# under NCCL_DEBUG=WARN/VERSION) goes to stderr unless the caller routed it
-os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
+# stdout carries exactly one JSON line (_emit); main() moves fd 1 onto stderr so
+# native libraries' own stdout writes (NCCL's "NCCL version" banner under
+# NCCL_DEBUG=WARN/VERSION) cannot land in front of it
+_JSON_OUT = sys.stdout
+
+
+def _emit(line: dict) -> None:
+    print(json.dumps(line), file=_JSON_OUT, flush=True)
+
 
 def _push_traffic(payload: int):
     """DRAM bytes per launch of the dominant mover (k_push_tiles) from the committed
@@ -535,7 +541,7 @@ def run_reference(args):
                 "d2h_bytes_per_step": 0},
         "wall_s": wall,
     }
-    print(json.dumps(line), flush=True)
+    _emit(line)
 
 
 # ---- our arm ----------------------------------------------------------------------------------------
@@ -838,7 +844,7 @@ def run_blitz(args):
             "clocks": clk, "wall_s": wall, "c3": c3, "decisions": decisions, "coop_c1": coop,
             "live_pair": live, "ramp": ramp, "c3_realclock": realclock,
         }
-        print(json.dumps(line), flush=True)
+        _emit(line)
     fabric.barrier()
 
 
@@ -857,4 +863,7 @@ def main():
 
 
 if __name__ == "__main__":
+    sys.stdout.flush()
+    _JSON_OUT = os.fdopen(os.dup(1), "w")
+    os.dup2(2, 1)
     main()

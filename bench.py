@@ -137,18 +137,61 @@ def parse_args():
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled every 200 ms during the timed region."""
+    """SM clocks + throttle reasons sampled every 10 ms during the timed region.
+
+    NVML (``nvidia_ml_py``) in a thread: the N >= 2 timed regions last ~100 ms, shorter
+    than nvidia-smi's start-up, so a polling nvidia-smi often saw none of them.  One
+    sample is taken at ``start()`` and one at ``stop()`` so the region always has two.
+    nvidia-smi ``-lms 200`` remains the fallback when NVML is unavailable."""
 
     FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    # nvmlClocksEventReason* bits
+    REASON_BITS = (("hw_slowdown", 0x8), ("hw_thermal_slowdown", 0x40),
+                   ("sw_thermal_slowdown", 0x20), ("sw_power_cap", 0x4))
 
     def __init__(self, device: int):
         self.device = device
         self.rows: list[list[str]] = []
+        self.samples: list[tuple[float, float, int]] = []   # (sm MHz, max sm MHz, reason bits)
         self.proc = None
+        self.nvml = None
+        self.handle = None
+        self.done = threading.Event()
+        self.thread = None
+
+    def _nvml_handle(self):
+        import pynvml
+        pynvml.nvmlInit()
+        try:
+            import torch
+            pr = torch.cuda.get_device_properties(self.device)
+            bus = f"{pr.pci_domain_id:08x}:{pr.pci_bus_id:02x}:{pr.pci_device_id:02x}.0"
+            h = pynvml.nvmlDeviceGetHandleByPciBusId(bus)
+        except Exception:
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.device)
+        return pynvml, h
+
+    def _sample(self):
+        n, h = self.nvml, self.handle
+        self.samples.append((float(n.nvmlDeviceGetClockInfo(h, n.NVML_CLOCK_SM)),
+                             float(n.nvmlDeviceGetMaxClockInfo(h, n.NVML_CLOCK_SM)),
+                             int(n.nvmlDeviceGetCurrentClocksEventReasons(h))))
+
+    def _poll(self):
+        while not self.done.wait(0.01):
+            self._sample()
 
     def start(self):
+        try:
+            self.nvml, self.handle = self._nvml_handle()
+            self._sample()
+            self.thread = threading.Thread(target=self._poll, daemon=True)
+            self.thread.start()
+            return
+        except Exception:
+            self.nvml = None
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--id={self.device}", f"--query-gpu={self.FIELDS}",
@@ -163,6 +206,14 @@ class ClockSampler:
             self.rows.append([x.strip() for x in line.split(",")])
 
     def stop(self) -> dict:
+        if self.nvml is not None:
+            self.done.set()
+            self.thread.join(timeout=2)
+            self._sample()
+            sm = [x[0] for x in self.samples]
+            reasons = {name for _, _, bits in self.samples for name, b in self.REASON_BITS if bits & b}
+            return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(x[1] for x in self.samples),
+                    "reasons": sorted(reasons), "samples": len(sm), "source": "nvml, 10 ms"}
         if self.proc is not None:
             self.proc.terminate()
             try:
@@ -180,7 +231,7 @@ class ClockSampler:
                         reasons.add(name)
         return {"sm_mhz": statistics.median(sm) if sm else None,
                 "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
-                "samples": len(sm)}
+                "samples": len(sm), "source": "nvidia-smi -lms 200"}
 
 
 # ---- distributed helpers ---------------------------------------------------------------------

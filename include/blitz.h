@@ -91,6 +91,9 @@ int bz_mc_bind(bz_mc* mc, int dev, const bz_slab* slab, uint64_t slab_offset,
                uint64_t mc_offset, uint64_t bytes);
 int bz_mc_map(bz_mc* mc, int dev);
 int bz_mc_free(bz_mc* mc, int dev, uint64_t bound_bytes);
+/* Unbind `dev`'s memory from the object without releasing it (a process that
+ * bound slabs on several of its GPUs unbinds each before bz_mc_free). */
+int bz_mc_unbind(bz_mc* mc, int dev, uint64_t bound_bytes);
 
 /* ---- tile transfer kernels ---------------------------------------------------- */
 /* Tile table: tile t covers bytes [tile_off[t], tile_off[t+1]) of a slab

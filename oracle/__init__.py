@@ -10,4 +10,6 @@ timed CPU baseline; the product (``paper_2412_17246_b200``) never does.
   copied along plan edges with torch CPU ``copy_``.
 * ``forward_ref.py`` -- fp32 Llama forward, unsplit and ZigZag-split, the
   logit oracle for cooperative execution.
+* ``logit_parity.py`` -- the tolerance rule applied to GPU logits against it
+  (max relative error 1e-2, greedy identity on every non-tie row, tie budget).
 """

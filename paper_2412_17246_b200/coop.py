@@ -175,6 +175,9 @@ class CooperativePair:
         [T_i, L) and the head.  Only ``B*d*2`` bytes per batch cross."""
         L = self.src.arch.n_layers
         n = len(tokens)
+        for kt, ks in caches[:n]:   # before anything is enqueued on either GPU
+            kt.require_room()
+            ks.require_room()
         recv: list[Optional[torch.Tensor]] = [None] * n
         handed_at = [0] * n
         nbytes = 0

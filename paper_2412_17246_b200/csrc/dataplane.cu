@@ -15,6 +15,7 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 #include "../../include/blitz.h"
 #include "common.cuh"
@@ -87,11 +88,22 @@ __device__ __forceinline__ bool spin_until_geq(const uint32_t* p, uint32_t v) {
   return true;
 }
 
-// wait (thread 0) for an upstream tile flag, then release the CTA
-__device__ __forceinline__ void wait_tile(const uint32_t* flags, int t, uint32_t epoch) {
-  if (threadIdx.x == 0) spin_until_geq(flags + t, epoch);
+// wait (thread 0) for an upstream tile flag, then release the CTA.  Returns false
+// (uniformly across the CTA) if the wait timed out: the caller must then neither
+// copy the tile nor release its downstream flag, so every GPU below a dead relay
+// times out too instead of publishing stale bytes as loaded.
+__device__ __forceinline__ bool wait_tile(const uint32_t* flags, int t, uint32_t epoch) {
+  __shared__ int ok;
+  if (threadIdx.x == 0) ok = spin_until_geq(flags + t, epoch);
   __syncthreads();
+  const bool r = ok != 0;
+  __syncthreads();  // `ok` is rewritten by the next tile's wait
+  return r;
 }
+
+// Epoch whose copy-engine relay gate timed out on this device: the flag kernel
+// behind that gate then withholds the downstream release (same rule as wait_tile).
+__device__ uint32_t g_poisoned_epoch = 0;
 
 constexpr int kThreads = 512;
 constexpr int kUnroll = 8;
@@ -110,19 +122,19 @@ struct PushArgs {
 
 // Copy one tile [b, e) (in 16-byte words) from src to every destination.
 // kMC: destinations are multicast VAs (multimem.st).
-template <bool kCoherent, bool kMC>
+template <bool kCoherent, bool kMC, int U = kUnroll>
 __device__ __forceinline__ void copy_tile(const int4* __restrict__ src, int4* const* dst, int ndst,
                                           int64_t b, int64_t e) {
   const int64_t step = blockDim.x;
   int64_t i = b + threadIdx.x;
-  for (; i + (kUnroll - 1) * step < e; i += kUnroll * step) {
-    int4 v[kUnroll];
+  for (; i + (U - 1) * step < e; i += U * step) {
+    int4 v[U];
 #pragma unroll
-    for (int u = 0; u < kUnroll; ++u) v[u] = ld16<kCoherent>(src + i + u * step);
+    for (int u = 0; u < U; ++u) v[u] = ld16<kCoherent>(src + i + u * step);
     for (int d = 0; d < ndst; ++d) {
       int4* o = dst[d];
 #pragma unroll
-      for (int u = 0; u < kUnroll; ++u) {
+      for (int u = 0; u < U; ++u) {
         if (kMC)
           mc_st16(o + i + u * step, v[u]);
         else
@@ -192,9 +204,12 @@ __device__ __forceinline__ void copy_tile32(const v8u32* __restrict__ src, int4*
 template <bool kRelay>
 __global__ void __launch_bounds__(kThreads) k_push_tiles32(PushArgs a) {
   for (int t = a.t0 + blockIdx.x; t < a.t1; t += gridDim.x) {
-    if (kRelay) wait_tile(a.wait_flags, t, a.epoch);
-    const int64_t b = a.tile_off[t] >> 5, e = a.tile_off[t + 1] >> 5;
-    copy_tile32<kRelay>(reinterpret_cast<const v8u32*>(a.src), a.dst, a.ndst, b, e);
+    if (kRelay && !wait_tile(a.wait_flags, t, a.epoch)) continue;
+    const int64_t ob = a.tile_off[t], oe = a.tile_off[t + 1];
+    if ((ob | oe) & 31)  // a tile not on 32-byte boundaries: 16-byte path (no dropped tail)
+      copy_tile<kRelay, false>(a.src, a.dst, a.ndst, ob >> 4, oe >> 4);
+    else
+      copy_tile32<kRelay>(reinterpret_cast<const v8u32*>(a.src), a.dst, a.ndst, ob >> 5, oe >> 5);
     __syncthreads();
     if (threadIdx.x == 0) {
       __threadfence_system();
@@ -207,7 +222,7 @@ template <bool kRelay>
 __global__ void __launch_bounds__(kThreads) k_push_tiles(PushArgs a) {
   for (int i = a.t0 + blockIdx.x; i < a.t1; i += gridDim.x) {
     const int t = a.ids ? __ldg(a.ids + i) : i;
-    if (kRelay) wait_tile(a.wait_flags, t, a.epoch);
+    if (kRelay && !wait_tile(a.wait_flags, t, a.epoch)) continue;
     const int64_t b = a.tile_off[t] >> 4, e = a.tile_off[t + 1] >> 4;
     copy_tile<kRelay, false>(a.src, a.dst, a.ndst, b, e);
     __syncthreads();
@@ -218,12 +233,12 @@ __global__ void __launch_bounds__(kThreads) k_push_tiles(PushArgs a) {
   }
 }
 
-template <bool kRelay>
+template <bool kRelay, int U>
 __global__ void __launch_bounds__(kThreads) k_multicast_tiles(PushArgs a) {
   for (int t = a.t0 + blockIdx.x; t < a.t1; t += gridDim.x) {
-    if (kRelay) wait_tile(a.wait_flags, t, a.epoch);
+    if (kRelay && !wait_tile(a.wait_flags, t, a.epoch)) continue;
     const int64_t b = a.tile_off[t] >> 4, e = a.tile_off[t + 1] >> 4;
-    copy_tile<kRelay, true>(a.src, a.dst, 1, b, e);
+    copy_tile<kRelay, true, U>(a.src, a.dst, 1, b, e);
     __syncthreads();
     if (threadIdx.x == 0) {
       __threadfence_system();
@@ -286,7 +301,7 @@ __global__ void __launch_bounds__(32) k_push_tiles_tma(PushArgs a) {
   uint32_t first = 0;  // running use count of the slot ring (slot = use % kTmaStages)
   for (int t = a.t0 + blockIdx.x; t < a.t1; t += gridDim.x) {
     if (kRelay) {
-      spin_until_geq(a.wait_flags + t, a.epoch);
+      if (!spin_until_geq(a.wait_flags + t, a.epoch)) continue;  // never forward stale bytes
       // relayed bytes arrived through the generic proxy; TMA reads via the async proxy
       asm volatile("fence.proxy.async.global;" ::: "memory");
     }
@@ -325,7 +340,8 @@ __global__ void __launch_bounds__(32) k_push_tiles_tma(PushArgs a) {
 }
 
 // ---------------------------------------------------------------------------
-__global__ void k_set_flags(uint32_t* flags, int t0, int t1, uint32_t epoch) {
+__global__ void k_set_flags(uint32_t* flags, int t0, int t1, uint32_t epoch, int relay) {
+  if (relay && *reinterpret_cast<volatile uint32_t*>(&g_poisoned_epoch) == epoch) return;
   int t = t0 + blockIdx.x * blockDim.x + threadIdx.x;
   if (t < t1) st_release_sys(flags + t, epoch);
 }
@@ -335,8 +351,11 @@ __global__ void __launch_bounds__(32) k_track_layers(const uint32_t* flags, cons
                                                      uint64_t* stamps) {
   const int lane = threadIdx.x;
   for (int k = 0; k < nlayers; ++k) {
-    for (int t = layer_tile[k] + lane; t < layer_tile[k + 1]; t += 32) spin_until_geq(flags + t, epoch);
-    __syncwarp();
+    bool ok = true;
+    for (int t = layer_tile[k] + lane; t < layer_tile[k + 1] && ok; t += 32) ok = spin_until_geq(flags + t, epoch);
+    // a timed-out tile: layer k is not loaded -- stop publishing (gated compute
+    // and the host both see the timeout rather than stale weights)
+    if (!__all_sync(0xffffffffu, ok)) return;
     if (lane == 0) {
       stamps[k] = globaltimer();
       __threadfence_system();
@@ -356,7 +375,9 @@ __global__ void k_wait_flag(const uint32_t* flag, uint32_t value) { spin_until_g
 
 // one warp: every flag in [t0, t1) >= epoch (gate in front of a copy-engine relay)
 __global__ void __launch_bounds__(32) k_wait_range(const uint32_t* flags, int t0, int t1, uint32_t epoch) {
-  for (int t = t0 + threadIdx.x; t < t1; t += 32) spin_until_geq(flags + t, epoch);
+  bool ok = true;
+  for (int t = t0 + threadIdx.x; t < t1 && ok; t += 32) ok = spin_until_geq(flags + t, epoch);
+  if (!ok) atomicExch(&g_poisoned_epoch, epoch);
 }
 
 // ---------------------------------------------------------------------------
@@ -527,10 +548,14 @@ extern "C" int bz_multicast_tiles(const void* src, void* mc_dst, uint32_t* mc_fl
   if (t1 == t0) return BZ_OK;
   const int grid = nctas > 0 ? min(nctas, t1 - t0) : min(32, t1 - t0);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  if (wait_flags)
-    k_multicast_tiles<true><<<grid, kThreads, 0, s>>>(a);
-  else
-    k_multicast_tiles<false><<<grid, kThreads, 0, s>>>(a);
+  // stores in flight per thread (multimem.st.v4 = 16 B each); BZ_MC_UNROLL selects
+  // 4 / 8 (default) / 16 for sweeps (scripts/nvlink_probe.py)
+  const char* env = getenv("BZ_MC_UNROLL");
+  const int unroll = env ? atoi(env) : 8;
+  auto kern = wait_flags ? k_multicast_tiles<true, 8> : k_multicast_tiles<false, 8>;
+  if (unroll == 4) kern = wait_flags ? k_multicast_tiles<true, 4> : k_multicast_tiles<false, 4>;
+  if (unroll == 16) kern = wait_flags ? k_multicast_tiles<true, 16> : k_multicast_tiles<false, 16>;
+  kern<<<grid, kThreads, 0, s>>>(a);
   return bz_check_launch("bz_multicast_tiles");
 }
 
@@ -546,7 +571,7 @@ extern "C" int bz_stage_tiles_ce(const void* host_src, void* dst, uint32_t* dst_
     cudaError_t err = cudaMemcpyAsync(static_cast<char*>(dst) + b, static_cast<const char*>(host_src) + b,
                                       static_cast<size_t>(e - b), cudaMemcpyHostToDevice, s);
     if (err != cudaSuccess) return bz_fail_cuda(err, "stage_ce memcpy");
-    k_set_flags<<<(te - t + 127) / 128, 128, 0, s>>>(dst_flags, t, te, epoch);
+    k_set_flags<<<(te - t + 127) / 128, 128, 0, s>>>(dst_flags, t, te, epoch, 0);
   }
   return bz_check_launch("bz_stage_tiles_ce");
 }
@@ -568,7 +593,7 @@ extern "C" int bz_push_tiles_ce(const void* src, void* dst, uint32_t* dst_flags,
     cudaError_t err = cudaMemcpyAsync(static_cast<char*>(dst) + b, static_cast<const char*>(src) + b,
                                       static_cast<size_t>(e - b), cudaMemcpyDeviceToDevice, s);
     if (err != cudaSuccess) return bz_fail_cuda(err, "push_ce memcpy");
-    k_set_flags<<<(te - t + 127) / 128, 128, 0, s>>>(dst_flags, t, te, epoch);
+    k_set_flags<<<(te - t + 127) / 128, 128, 0, s>>>(dst_flags, t, te, epoch, wait_flags != nullptr);
   }
   return bz_check_launch("bz_push_tiles_ce");
 }

@@ -57,6 +57,10 @@ __global__ void k_rope_append(__nv_bfloat16* qkv, int ld, int n_heads, int n_kv,
   const int half = hd / 2;
   if (i >= half) return;
   const int p = *pos;
+  if (p < 0 || p >= s_max) {  // full cache: never write past the panel (the host raises first)
+    pdl_trigger();
+    return;
+  }
   const float pf = static_cast<float>(p);
   __nv_bfloat16* base = qkv + static_cast<int64_t>(row) * ld;
   float ra, rb;
@@ -105,7 +109,7 @@ __global__ void __launch_bounds__(THREADS) k_decode_partial(const __nv_bfloat16*
   const int split = blockIdx.x;
   const int bg = blockIdx.y;
   const int b = bg / n_kv, g = bg % n_kv;
-  const int len = *pos + 1;
+  const int len = static_cast<int>(tmin<int64_t>(static_cast<int64_t>(*pos) + 1, s_max));  // never past the panel
   const int c0 = split * chunk;
   const int n = min(chunk, len - c0);
   const int tid = threadIdx.x;

@@ -1123,8 +1123,9 @@ static int gemm_impl(const void* A, const void* B, void* C, const void* residual
   // 16-byte stride/alignment rules of the tensor maps constrain K.
   if (K % 8 || lda % 8 || ldb % 8 || ldc % 8 || (residual && ldr % 8) || N % 8)
     return bz_fail(BZ_EINVAL, "gemm: K, N and leading dims must be multiples of 8");
-  if ((reinterpret_cast<uintptr_t>(A) | reinterpret_cast<uintptr_t>(B) | reinterpret_cast<uintptr_t>(C)) & 15)
-    return bz_fail(BZ_EINVAL, "gemm: operands must be 16-byte aligned");
+  if ((reinterpret_cast<uintptr_t>(A) | reinterpret_cast<uintptr_t>(B) | reinterpret_cast<uintptr_t>(C) |
+       reinterpret_cast<uintptr_t>(residual)) & 15)
+    return bz_fail(BZ_EINVAL, "gemm: operands (and the residual) must be 16-byte aligned");
   // skinny A: load only the rows that exist (8-row swizzle atoms); the rows of
   // the 128-row MMA beyond them read stale smem and are never stored
   const int po = pair_override();

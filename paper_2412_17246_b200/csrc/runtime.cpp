@@ -406,6 +406,15 @@ extern "C" int bz_mc_map(bz_mc* mc, int dev) {
   return BZ_OK;
 }
 
+extern "C" int bz_mc_unbind(bz_mc* mc, int dev, uint64_t bound_bytes) {
+  if (!mc || !mc->handle) return bz_fail(BZ_EINVAL, "mc_unbind: null");
+  if (int rc = use_device(dev)) return rc;
+  CUdevice d;
+  CU_TRY(DRV()->cuDeviceGet(&d, dev));
+  CU_TRY(DRV()->cuMulticastUnbind(static_cast<CUmemGenericAllocationHandle>(mc->handle), d, 0, bound_bytes));
+  return BZ_OK;
+}
+
 extern "C" int bz_mc_free(bz_mc* mc, int dev, uint64_t bound_bytes) {
   if (!mc) return BZ_OK;
   if (mc->mc_ptr) {

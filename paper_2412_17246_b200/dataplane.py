@@ -153,13 +153,16 @@ class DeviceSlab:
         return (os.getpid(), int(self.raw.fd), int(self.raw.bytes))
 
     def fill_random(self, seed: int, stream=None):
-        s = _stream_handle(stream)
-        self.lib.bz_fill_random(self.ptr, self.layout.data_bytes, seed, s)
+        # launched on this slab's device (one process may drive slabs on several GPUs)
+        with torch.cuda.device(self.device):
+            s = _stream_handle(stream, self.device)
+            self.lib.bz_fill_random(self.ptr, self.layout.data_bytes, seed, s)
 
     def fingerprints(self, stream=None) -> torch.Tensor:
-        out = torch.empty(self.layout.ntiles, dtype=torch.int64, device=self.data.device)
-        self.lib.bz_tile_fingerprints(self.ptr, self.tile_off.data_ptr(), 0, self.layout.ntiles,
-                                      out.data_ptr(), _stream_handle(stream))
+        with torch.cuda.device(self.device):
+            out = torch.empty(self.layout.ntiles, dtype=torch.int64, device=self.data.device)
+            self.lib.bz_tile_fingerprints(self.ptr, self.tile_off.data_ptr(), 0, self.layout.ntiles,
+                                          out.data_ptr(), _stream_handle(stream, self.device))
         return out
 
     def close(self):
@@ -235,6 +238,48 @@ class MulticastGroup:
             self.lib.bz_mc_free(self.raw, self.fabric.device, self.bound)
 
 
+class LocalMulticastGroup:
+    """An NVLS multicast object bound by ONE process to slabs on several of its GPUs
+    (the single-process form of ``MulticastGroup``: tests, ncu captures, and a
+    process that drives more than one GPU).  ``cuMulticastCreate`` rejects a
+    one-device object on B200 (CUDA_ERROR_INVALID_VALUE, scripts/nvlink_probe.py),
+    so at least two devices are required."""
+
+    def __init__(self, slabs: Sequence[DeviceSlab], map_device: int):
+        if len({s.device for s in slabs}) != len(slabs) or len(slabs) < 2:
+            raise ValueError("one slab per distinct device, at least two devices")
+        self.lib = cuda_lib()
+        self.raw = BzMc()
+        self.slabs = list(slabs)
+        self.nbytes = int(slabs[0].raw.bytes)
+        self.layout = slabs[0].layout
+        self.map_device = map_device
+        self.lib.bz_mc_create(len(slabs), self.nbytes, self.raw)
+        for s in slabs:                      # every device joins before any binds
+            self.lib.bz_mc_add_device(self.raw, s.device)
+        for s in slabs:
+            self.lib.bz_mc_bind(self.raw, s.device, s.raw, 0, 0, self.nbytes)
+        self.lib.bz_mc_map(self.raw, map_device)
+
+    @property
+    def ptr(self) -> int:
+        return int(self.raw.mc_ptr)
+
+    @property
+    def flags_ptr(self) -> int:
+        return int(self.raw.mc_ptr + self.layout.flag_offset)
+
+    def close(self):
+        if not self.raw.handle:
+            return
+        for s in self.slabs:
+            torch.cuda.synchronize(s.device)
+        for s in self.slabs:
+            if s.device != self.map_device:   # unbind the other members; bz_mc_free does the mapper
+                self.lib.bz_mc_unbind(self.raw, s.device, self.nbytes)
+        self.lib.bz_mc_free(self.raw, self.map_device, self.nbytes)
+
+
 GATE_MODE = os.environ.get("BZ_GATE", "kernel")
 
 
@@ -253,9 +298,9 @@ def gate(flag_ptr: int, value: int, stream_handle: int, mode: Optional[str] = No
         lib.bz_wait_flag_kernel(flag_ptr, value, stream_handle)
 
 
-def _stream_handle(stream) -> int:
+def _stream_handle(stream, device: Optional[int] = None) -> int:
     if stream is None:
-        return int(torch.cuda.current_stream().cuda_stream)
+        return int(torch.cuda.current_stream(device).cuda_stream)
     return int(stream.cuda_stream)
 
 
@@ -386,6 +431,30 @@ def stripe_pieces(layout: SlabLayout, members: int, index: int) -> list[tuple[in
     return out
 
 
+# ---- fan-out realisation ----------------------------------------------------------------------
+
+# Per-destination GB/s of the two realisations of an NVLink fan-out group, 7B shard,
+# measured on B200 by GPUs in the group (writer included):
+#   2: single-process probe, 16-64 CTAs (profiles/r2_nvlink_probe_n2.jsonl): sibling-chain
+#      hop (k_push_tiles) 717, NVLS multimem.st 565 -- flat from 48 to 148 CTAs and for
+#      4/8/16 stores in flight per thread, i.e. a multimem store-rate ceiling, not occupancy
+#   4: multi-process bench (profiles/r1_nvls_vs_chain_n4.txt): chain 691, NVLS 530
+MEASURED_FANOUT_GBPS = {2: {"chain": 717.0, "nvls": 565.0}, 4: {"chain": 691.0, "nvls": 530.0}}
+
+
+def choose_fanout(group_size: int, table: Optional[dict] = None) -> str:
+    """``auto`` realisation of a fan-out group of ``group_size`` GPUs: the faster one
+    per destination in the measurement for the largest measured size <= the group
+    (both realisations are receiver-count independent once pipelined, so the nearest
+    smaller measurement stands for larger groups)."""
+    table = MEASURED_FANOUT_GBPS if table is None else table
+    if group_size <= 1 or not table:
+        return "chain"
+    keys = sorted(k for k in table if k <= group_size) or [min(table)]
+    row = table[keys[-1]]
+    return max(("chain", "nvls"), key=lambda m: (row.get(m, 0.0), m == "chain"))
+
+
 # ---- executor -------------------------------------------------------------------------------
 
 
@@ -417,9 +486,8 @@ class ScaleExecutor:
         self.tiles_per_copy = tiles_per_copy
         self.lib = cuda_lib()
         if fanout_mode == "auto":
-            # measured on 4x B200 (profiles/r1_sweep4.txt): a pipelined sibling chain
-            # delivers ~650 GB/s per destination, the NVLS multicast stream ~530 GB/s
-            fanout_mode = "chain"
+            sizes = [len(v) + 1 for v in plan.nvlink_fanout.values()]
+            fanout_mode = choose_fanout(max(sizes) if sizes else 1)
         self.fanout_mode = fanout_mode
         # every rank exports its slab (and says whether it holds a host-cache view);
         # peers it sends to are imported below

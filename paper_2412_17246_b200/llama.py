@@ -204,6 +204,7 @@ class LlamaExecutor:
         of each sequence's newest token, at the cache's device position.  Its key/
         value are appended (bz_rope_append) and it attends over positions 0..pos
         (bz_decode_attention) -- no host-side position, so the step is graph-safe."""
+        kv.require_room()
         a, L = self.arch, self.w.layers[k]
         B = x.shape[0]
         s = torch.cuda.current_stream().cuda_stream
@@ -254,6 +255,7 @@ class LlamaExecutor:
         """One decode step over blocks [first, last) for the newest token of each
         sequence (tokens int64 [B]); returns hidden [B, d], or fp32 logits [B, vocab]
         if last == L.  Advances ``kv.length`` by one."""
+        kv.require_room()  # before anything is enqueued: a full cache must not be written
         last = self.arch.n_layers if last is None else last
         if x is None:
             x = self.embed(tokens)
@@ -309,10 +311,15 @@ class KVCache:
         self._length = n
         self.pos_dev.fill_(n)
 
+    def require_room(self):
+        """Raise before a decode step is enqueued if the cache has no free position
+        (the device kernels also refuse to write past a panel)."""
+        if self._length >= self.max_seq:
+            raise ValueError(f"KV cache full ({self._length} of {self.max_seq} positions)")
+
     def advance(self):
         """After a decode step: the device position moves on the current stream."""
-        if self._length >= self.max_seq:
-            raise ValueError("KV cache full")
+        self.require_room()
         self._length += 1
         self.pos_dev.add_(1)
 

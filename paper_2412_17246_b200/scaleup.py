@@ -71,24 +71,48 @@ def plan_host_cache(fabric: Fabric, layout: SlabLayout, plan, node_rank: dict[st
     groups = host_fed_groups(plan) if host_stripe else {}
     owner = node is not None and node in roles and (roles[node].parent or "").startswith("mem")
     group_of = {m: rep for rep, members in groups.items() for m in members}
-    name = None
-    if owner:
-        name = f"bz_{tag}_{node}_{os.getpid()}"
+    # only a group whose siblings map the same pages needs a named /dev/shm region;
+    # a lone rep stages from anonymous pinned memory (no tmpfs size limit, no leftovers)
+    shared = owner and len(groups.get(node, [])) > 1
+    name = f"bz_{tag}_{node}_{os.getpid()}" if shared else None
     names = fabric.allgather((node, name))
     by_node = {n: nm for n, nm in names if nm}
     hc = None
-    if owner:
-        hc = HostCache(layout, shm_name=name, create=True)
-        fill(hc.tensor)
-    fabric.barrier()
-    if not owner and node in group_of:
-        hc = HostCache(layout, shm_name=by_node[group_of[node]], create=False)
-    fabric.barrier()
-    if owner and hc is not None and hc.path:
-        # every member has mapped it; drop the name (the mappings keep the pages)
-        os.unlink(hc.path)
-        hc.path = None
+    err = None
+    try:
+        if owner:
+            if shared:
+                _require_shm_space(layout.data_bytes)
+            hc = HostCache(layout, shm_name=name, create=True)
+            fill(hc.tensor)
+    except BaseException as e:  # noqa: BLE001 -- re-raised after the collective below
+        err = e
+    failed = fabric.allgather(err is not None)
+    try:
+        if err is not None:
+            raise err
+        if any(failed):
+            raise RuntimeError("host cache: another rank failed to create or fill its host copy")
+        if not owner and node in group_of:
+            hc = HostCache(layout, shm_name=by_node[group_of[node]], create=False)
+        fabric.barrier()
+    finally:
+        if owner and name and os.path.exists(f"/dev/shm/{name}"):
+            # every member has mapped it (or setup failed): drop the name; the
+            # mappings keep the pages
+            os.unlink(f"/dev/shm/{name}")
+            if hc is not None:
+                hc.path = None
     return hc
+
+
+def _require_shm_space(nbytes: int) -> None:
+    """A /dev/shm file larger than the tmpfs would SIGBUS on first touch: refuse early."""
+    st = os.statvfs("/dev/shm")
+    free = st.f_bavail * st.f_frsize
+    if free < nbytes:
+        raise RuntimeError(f"/dev/shm has {free / 1e9:.2f} GB free, the shared host copy needs "
+                           f"{nbytes / 1e9:.2f} GB (enlarge /dev/shm or pass host_stripe=False)")
 
 
 class TransferTimeout(RuntimeError):
@@ -98,9 +122,9 @@ class TransferTimeout(RuntimeError):
 _seen_timeouts: dict[int, int] = {}
 
 
-def check_wait_timeouts(device: Optional[int] = None) -> None:
-    """Raise if a bounded device-side wait on ``device`` (default: current) gave up
-    since the last check -- the kernels behind it ran on data that never arrived."""
+def new_wait_timeouts(device: Optional[int] = None) -> int:
+    """Device-side waits on ``device`` (default: current) that gave up since the
+    last call (they skipped their copy and withheld their downstream flags)."""
     import ctypes
 
     from ._native import cuda_lib
@@ -108,9 +132,18 @@ def check_wait_timeouts(device: Optional[int] = None) -> None:
     n = ctypes.c_uint64()
     with torch.cuda.device(dev):
         cuda_lib().bz_wait_timeouts(ctypes.byref(n), 0)
-    if n.value > _seen_timeouts.get(dev, 0):
-        _seen_timeouts[dev] = n.value
-        raise TransferTimeout(f"cuda:{dev}: {n.value} device-side waits timed out (upstream never published)")
+    new = n.value - _seen_timeouts.get(dev, 0)
+    _seen_timeouts[dev] = n.value
+    return max(0, int(new))
+
+
+def check_wait_timeouts(device: Optional[int] = None) -> None:
+    """Raise if a bounded device-side wait on ``device`` (default: current) gave up
+    since the last check -- the kernels behind it ran on data that never arrived."""
+    dev = torch.cuda.current_device() if device is None else int(device)
+    n = new_wait_timeouts(dev)
+    if n:
+        raise TransferTimeout(f"cuda:{dev}: {n} device-side waits timed out (upstream never published)")
 
 
 def expected_fingerprints(layout: SlabLayout, device: int, seed: int) -> torch.Tensor:
@@ -153,6 +186,7 @@ class ScaleUpSession:
                                       stage_engine=stage_engine, tiles_per_copy=tiles_per_copy,
                                       host_stripe=host_stripe)
         self.receives = self.executor.role.receives
+        self.fabric_nodes = {r: n for n, r in node_rank.items()}
         self._expected: Optional[torch.Tensor] = None
 
     def run(self, verify: bool = False, time_kernel: bool = False) -> ScaleUpResult:
@@ -172,7 +206,13 @@ class ScaleUpSession:
             cur.wait_stream(s)
         end.record(cur)
         end.synchronize()
-        check_wait_timeouts()
+        # every rank learns of a timeout anywhere in the plan (a dead relay starves
+        # all GPUs below it; none of them may report the transfer as done)
+        mine = new_wait_timeouts()
+        counts = self.fabric.allgather(mine)
+        if any(counts):
+            bad = {self.fabric_nodes.get(r, r): c for r, c in enumerate(counts) if c}
+            raise TransferTimeout(f"scale-up epoch {epoch}: device-side waits timed out on {bad}")
         res = ScaleUpResult(epoch, start.elapsed_time(end))
         if kev is not None and self.executor.dominant_stream() is not None:
             res.kernel_ms = kev[0].elapsed_time(kev[1])

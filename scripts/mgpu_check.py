@@ -32,12 +32,15 @@ def main():
     node_rank = {g: i for i, g in enumerate(gpus)}
     layout = S.SlabLayout.for_arch(arch, tile_bytes=tile)
     failures = 0
+    # (name, sources, targets, group, fanout realisation requested, engine); the
+    # realisation actually used and the multicast groups built are printed per case
     cases = [
-        ("grouped-nvls", ["gpu0"], gpus[1:], True, "auto", ENGINE_VECTOR),
+        ("grouped-nvls", ["gpu0"], gpus[1:], True, "nvls", ENGINE_VECTOR),
         ("grouped-chain", ["gpu0"], gpus[1:], True, "chain", ENGINE_VECTOR),
         ("chain-vector", ["gpu0"], gpus[1:], False, "auto", ENGINE_VECTOR),
         ("chain-tma", ["gpu0"], gpus[1:], False, "auto", ENGINE_TMA),
-        ("hostcache-rep", ["mem0"], gpus, True, "auto", ENGINE_VECTOR),
+        ("hostcache-rep-nvls", ["mem0"], gpus, True, "nvls", ENGINE_VECTOR),
+        ("hostcache-rep-chain", ["mem0"], gpus, True, "chain", ENGINE_VECTOR),
         ("hostcache-stripe", ["mem0"], gpus, True, "auto", ENGINE_VECTOR),
     ]
 
@@ -50,7 +53,7 @@ def main():
     for name, srcs, tgts, group, fan, engine in cases:
         plan, _, _ = plan_for(arch, srcs, tgts, group=group)
         stripe = name == "hostcache-stripe"
-        hc = plan_host_cache(fabric, layout, plan, node_rank, fill, host_stripe=stripe, tag=name)
+        hc = plan_host_cache(fabric, layout, plan, node_rank, fill, host_stripe=stripe, tag=name.replace("-", "_"))
         t0 = time.perf_counter()
         # hostcache-rep: striping requested, but only the rep maps the host copy -> the
         # executor keeps the rep-only realisation
@@ -72,7 +75,9 @@ def main():
         failures += int(ok_t.item() > 0)
         if rank == 0:
             print(json.dumps({"case": name, "n_gpus": N, "arch": arch.name, "ok": ok_t.item() == 0,
-                              "max_ms": ms_t.item(), "fanout_mode": sess.executor.fanout_mode,
+                              "max_ms": ms_t.item(), "fanout_requested": fan,
+                              "fanout_mode": sess.executor.fanout_mode,
+                              "multicast_groups": len(sess.executor._mc_all),
                               "edges": [(e.src, e.dst) for e in plan.edges],
                               "fanout": plan.nvlink_fanout,
                               "striped": bool(sess.executor.stripe_groups),

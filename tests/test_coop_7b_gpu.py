@@ -1,0 +1,91 @@
+"""7B-shape cooperative-execution parity against the fp32 oracle.
+
+Truncated Llama-2 7B: every dimension of the real model (d=4096, 32 heads,
+ffn 11008, vocab 32000) with L=3 blocks, so the fp32 CPU oracle finishes in
+seconds.  Runs unsplit, ZigZag-split (``configure_pipeline`` +
+``zigzag_schedule``, livescale.py:113-181, 269-346) with the fused GEMM
+hand-off, then two cooperative decode steps (each side on its own KV blocks),
+and compares EVERY row of EVERY batch with ``oracle.forward_ref.forward_fp32``
+under the rule of ``oracle/logit_parity.py``.
+"""
+
+import pytest
+import torch
+
+import paper_2412_17246_b200 as ss
+from paper_2412_17246_b200 import slab as S
+from paper_2412_17246_b200.coop import CooperativePair
+from paper_2412_17246_b200.dataplane import DeviceSlab, execute_plan_loopback
+from paper_2412_17246_b200.llama import LlamaExecutor, SlabWeights
+from oracle.forward_ref import forward_fp32, weights_to_cpu_fp32
+from oracle.logit_parity import ParityTally
+
+pytestmark = pytest.mark.gpu
+
+ARCH = S.LlamaArch("llama2-7b-l3", 4096, 3, 32, 32, 11008)
+
+
+@pytest.fixture(scope="module")
+def model():
+    torch.set_num_threads(max(1, torch.get_num_threads()))
+    lay = S.SlabLayout.for_arch(ARCH)
+    src = DeviceSlab(lay, 0)
+    w = SlabWeights(ARCH, lay, src.data)
+    w.init_random(seed=0)
+    torch.cuda.synchronize()
+    yield lay, src, w, weights_to_cpu_fp32(w)
+    src.close()
+
+
+def _tokens(n, b, s, seed):
+    g = torch.Generator().manual_seed(seed)
+    return [torch.randint(0, ARCH.vocab, (b, s), generator=g).cuda() for _ in range(n)]
+
+
+def test_7b_unsplit_prefill_matches_oracle(model):
+    lay, src, w, ref_w = model
+    ex = LlamaExecutor(w, max_tokens=8 * 96, device="cuda")
+    tally = ParityTally()
+    for toks in _tokens(2, 8, 96, 1):
+        logits = ex.forward(toks)
+        tally.add(logits, forward_fp32(ARCH, ref_w, toks.cpu()))
+    print(tally.summary())
+    tally.check()
+
+
+@pytest.mark.parametrize("n,time_l", [(4, 0.5), (3, 2.0)])
+def test_7b_zigzag_prefill_and_decode_match_oracle(model, n, time_l):
+    lay, src, w, ref_w = model
+    tgt = DeviceSlab(lay, 0)
+    topo = ss.load_topology("b200-hgx")
+    plan = ss.generate_plan(ss.build_scale_request(S.model_spec_for(ARCH), ["gpu0"], ["gpu1"], topo,
+                                                   ss.FlowSet(topo)), topo, ss.FlowSet(topo))
+    execute_plan_loopback(plan, {"gpu0": src, "gpu1": tgt}, epoch=1)
+    torch.cuda.synchronize()
+    assert torch.equal(tgt.data, src.data)
+    cfg = ss.configure_pipeline(n, ARCH.n_layers, time_l)
+    assert any(t > 0 for t, _ in cfg.splits), cfg.splits   # the target really runs layers
+    tl = ss.zigzag_schedule(cfg)
+    B, S_ = 4, 64
+    source = LlamaExecutor(w, max_tokens=B * S_, device="cuda")
+    target = LlamaExecutor(SlabWeights(ARCH, lay, tgt.data), max_tokens=B * S_, device="cuda")
+    pair = CooperativePair(source, target, tgt.loaded)
+    batches = _tokens(n, B, S_, 7 + n)
+    caches = pair.make_caches(batches, cfg, max_new_tokens=2)
+    res = pair.run(batches, cfg, tl, caches=caches)
+    assert res.executed_order == [(b, k) for b, k, _, _ in tl.target_intervals]
+    tally = ParityTally()
+    seqs = [b.cpu() for b in batches]
+    for seq, logits in zip(seqs, res.logits):
+        tally.add(logits, forward_fp32(ARCH, ref_w, seq))
+    toks = [lg.argmax(-1) for lg in res.logits]
+    for _ in range(2):
+        seqs = [torch.cat([s, t.cpu()[:, None]], 1) for s, t in zip(seqs, toks)]
+        step = pair.decode(toks, cfg, caches)
+        for seq, logits in zip(seqs, step.logits):
+            tally.add(logits, forward_fp32(ARCH, ref_w, seq))
+        toks = [lg.argmax(-1) for lg in step.logits]
+    print(cfg.splits, tally.summary())
+    assert tally.rows == 3 * n * B
+    tally.check()
+    tgt.close()

@@ -266,3 +266,40 @@ def test_gate_timeout_fails_loudly():
         check_wait_timeouts()                   # counted once
     finally:
         lib.bz_wait_timeouts(ctypes.byref(n), 30_000_000_000)
+
+
+def test_relay_timeout_withholds_downstream_flags(tiny_layout):
+    """A relay whose upstream never publishes must not forward stale bytes: its
+    bounded wait gives up, it skips the copy and withholds the downstream flag, so
+    the downstream tracker publishes nothing and times out as well."""
+    import ctypes
+    from paper_2412_17246_b200.scaleup import new_wait_timeouts
+
+    lib = cuda_lib()
+    relay, down = DeviceSlab(tiny_layout, 0), DeviceSlab(tiny_layout, 0)
+    relay.fill_random(seed=5)
+    down.data.fill_(0x5A)
+    n = ctypes.c_uint64()
+    new_wait_timeouts()                                    # reset the per-device baseline
+    lib.bz_wait_timeouts(ctypes.byref(n), 200_000)         # 0.2 ms budget per wait
+    try:
+        s = torch.cuda.current_stream().cuda_stream
+        from paper_2412_17246_b200._native import ptr_array
+        # relay flags stay 0 (upstream dead); push epoch 3 downstream
+        for engine in (ENGINE_VECTOR, ENGINE_TMA, 2):
+            lib.bz_push_tiles(relay.ptr, ptr_array([down.ptr]), ptr_array([down.flags_ptr]), 1,
+                              relay.flags_ptr, relay.tile_off.data_ptr(), 0, tiny_layout.ntiles, 3, 8,
+                              engine, s)
+        # copy-engine relay: gate times out -> flag kernel withholds the release
+        lib.bz_push_tiles_ce(relay.ptr, down.ptr, down.flags_ptr, relay.flags_ptr,
+                             tiny_layout.tile_off.ctypes.data, 0, tiny_layout.ntiles, 4, 3, s)
+        lib.bz_track_layers(down.flags_ptr, down.layer_tile.data_ptr(), tiny_layout.num_layers, 3,
+                            down.loaded.data_ptr(), down.stamps.data_ptr(), s)
+        torch.cuda.synchronize()
+        assert int(down.flags.max()) == 0, "a downstream flag was released for stale bytes"
+        assert int(down.loaded.item()) == 0
+        assert new_wait_timeouts() > 0
+    finally:
+        lib.bz_wait_timeouts(ctypes.byref(n), 30_000_000_000)
+    relay.close()
+    down.close()

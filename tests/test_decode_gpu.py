@@ -334,3 +334,33 @@ def test_kv_consolidation_over_nvlink():
         _check(lg, forward_fp32(arch, ref_w, seq))
     tgt.close()
     src.close()
+
+
+def test_decode_on_full_cache_raises_before_writing():
+    """A decode step on a full cache must raise before anything is enqueued, and the
+    cache panels (including the next panel in memory) must stay untouched."""
+    arch = S.TINY_4L
+    lay, slab, w = _slab(arch)
+    ex = LlamaExecutor(w, max_tokens=2 * 8, device="cuda")
+    prompt = _prompt(2, 8, 3, arch.vocab)
+    kv = KVCache(arch, 2, 8, "cuda")          # room for the prompt only
+    logits = ex.forward(prompt, kv=kv)
+    torch.cuda.synchronize()
+    before = {l: (kv.k[l].clone(), kv.v[l].clone()) for l in kv.k}
+    with pytest.raises(ValueError, match="full"):
+        ex.decode(logits.argmax(-1), kv)
+    torch.cuda.synchronize()
+    for l, (k0, v0) in before.items():
+        assert torch.equal(kv.k[l], k0) and torch.equal(kv.v[l], v0)
+    assert kv.length == 8 and int(kv.pos_dev.item()) == 8
+    # the device kernels refuse too: rope_append at pos == s_max writes nothing
+    import ctypes  # noqa: F401
+    from paper_2412_17246_b200._native import cuda_lib
+    a = arch
+    qkv = torch.randn(2, a.d_model + 2 * a.kv_dim, device="cuda").to(torch.bfloat16)
+    cuda_lib().bz_rope_append(qkv.data_ptr(), qkv.stride(0), 2, a.n_heads, a.n_kv_heads, a.head_dim,
+                              a.rope_theta, kv.k[0].data_ptr(), kv.v[0].data_ptr(), kv.max_seq,
+                              kv.pos_dev.data_ptr(), torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    assert torch.equal(kv.k[0], before[0][0]) and torch.equal(kv.v[0], before[0][1])
+    slab.close()

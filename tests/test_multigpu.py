@@ -1,10 +1,11 @@
 """Multi-process (one process per GPU) parity of the data plane.
 
 GPU path: spawns ``torchrun`` over every visible GPU (needs >= 2) running
-scripts/mgpu_check.py -- grouped/NVLS, grouped/chain, chain (vector + TMA
-engines) and host-cache fan-out plans (NVLS, and striped over the group's
-PCIe links), each verified bit-exact on every
-receiver.  CPU path: the control plane (fd-exchange allgather, barriers, role
+scripts/mgpu_check.py -- grouped plans with the fan-out realised as an NVLS
+multicast and as a sibling chain, chain plans (vector + TMA engines) and
+host-cache fan-out plans (NVLS relay from the rep, sibling chain, striped over
+the group's PCIe links), each verified bit-exact on every receiver, with the
+realisation actually used asserted per case.  CPU path: the control plane (fd-exchange allgather, barriers, role
 derivation) over a 2-process gloo group.
 """
 
@@ -39,7 +40,13 @@ def test_torchrun_scaleup_bit_exact():
         capture_output=True, text=True, timeout=600, env=env, cwd=str(ROOT))
     lines = [json.loads(l) for l in proc.stdout.splitlines() if l.startswith("{")]
     assert proc.returncode == 0, proc.stdout[-2000:] + proc.stderr[-3000:]
-    assert len(lines) == 6 and all(l["ok"] for l in lines), lines
+    assert len(lines) == 7 and all(l["ok"] for l in lines), lines
+    by = {l["case"]: l for l in lines}
+    # the NVLS cases really ran k_multicast_tiles through a multicast object whenever
+    # the plan has a fan-out group; the chain cases never did
+    assert by["hostcache-rep-nvls"]["fanout_mode"] == "nvls" and by["hostcache-rep-nvls"]["multicast_groups"] == 1
+    assert by["grouped-nvls"]["multicast_groups"] == (1 if n >= 3 else 0)
+    assert all(by[c]["multicast_groups"] == 0 for c in ("grouped-chain", "hostcache-rep-chain", "chain-vector"))
 
 
 @pytest.mark.gpu

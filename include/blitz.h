@@ -205,6 +205,8 @@ int bz_gemm_bf16_signal(const void* A, const void* B, void* C, const void* resid
  * BZ_PDL=0 disables).  The workspace must be zero-filled before its first use
  * (it holds per-tile arrival counters, which every call leaves at zero) and must
  * not be shared by GEMMs running concurrently. */
+#define BZ_GEMM_C_F32 2u    /* C is fp32 (ldc in floats): the accumulator is stored unrounded (logit heads);
+                               single-CTA tiles only */
 #define BZ_GEMM_B_STATIC 1u /* B is not written by kernels still in flight on the stream (weights):
                                its first tiles may load before the predecessor kernel completes */
 int bz_gemm_bf16_ex(const void* A, const void* B, void* C, const void* residual, int M, int N, int K,

@@ -96,6 +96,7 @@ _PI = ctypes.POINTER(ctypes.c_int)
 _PU64 = ctypes.POINTER(ctypes.c_uint64)
 
 BZ_GEMM_B_STATIC = 1   # include/blitz.h
+BZ_GEMM_C_F32 = 2
 
 # name -> argtypes; every function returns int status
 _SIGNATURES = {

@@ -185,6 +185,7 @@ struct Params {
   int a_stage;   // smem stride of the A ring (a_bytes rounded up to the 1024-B swizzle atom)
   int stages;    // ring depth (single-CTA kernel)
   int b_static;  // B is not written by in-flight predecessors: prefetch it before pdl_wait
+  int c_f32;     // C is fp32 (BZ_GEMM_C_F32: logits keep the accumulator's precision)
   // split-K of the pair kernel (few tiles, long K): unit = (tile, K slice); slices
   // store fp32 partials to ws[slice][M][N], k_splitk_reduce adds them into C
   int ksplit, kb_slice;
@@ -223,6 +224,27 @@ struct SegIter {
 // (columns at or beyond `lim` -- the end of C or of a tile narrower than a
 // multiple of 32 -- are not written)
 __device__ __forceinline__ void store_chunk(const Params& p, int row, int col, const uint32_t (&r)[32], int lim) {
+  if (p.c_f32) {
+    // fp32 C (+ bf16 residual): the accumulator as is, 16-byte stores
+    float* of = reinterpret_cast<float*>(p.C) + static_cast<int64_t>(row) * p.ldc + col;
+    const __nv_bfloat16* rs = p.R ? p.R + static_cast<int64_t>(row) * p.ldr + col : nullptr;
+    if (col + 32 <= lim) {
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        float4 v = make_float4(__uint_as_float(r[4 * q]), __uint_as_float(r[4 * q + 1]), __uint_as_float(r[4 * q + 2]),
+                               __uint_as_float(r[4 * q + 3]));
+        if (rs) {
+          v.x += __bfloat162float(rs[4 * q]), v.y += __bfloat162float(rs[4 * q + 1]);
+          v.z += __bfloat162float(rs[4 * q + 2]), v.w += __bfloat162float(rs[4 * q + 3]);
+        }
+        reinterpret_cast<float4*>(of)[q] = v;
+      }
+    } else {
+      for (int j = 0; j < 32; ++j)
+        if (col + j < lim) of[j] = __uint_as_float(r[j]) + (rs ? __bfloat162float(rs[j]) : 0.f);
+    }
+    return;
+  }
   __nv_bfloat16* out = p.C + static_cast<int64_t>(row) * p.ldc + col;
   const __nv_bfloat16* res = p.R ? p.R + static_cast<int64_t>(row) * p.ldr + col : nullptr;
   if (col + 32 <= lim) {
@@ -333,8 +355,11 @@ __device__ __forceinline__ void streamk_fixup(const Params& p, int tile, int n0,
         const float2 r1 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&rv.y));
         v.x += r0.x, v.y += r0.y, v.z += r1.x, v.w += r1.y;
       }
-      *reinterpret_cast<uint2*>(p.C + static_cast<int64_t>(row) * p.ldc + col) =
-          make_uint2(pack_bf16(v.x, v.y), pack_bf16(v.z, v.w));
+      if (p.c_f32)
+        *reinterpret_cast<float4*>(reinterpret_cast<float*>(p.C) + static_cast<int64_t>(row) * p.ldc + col) = v;
+      else
+        *reinterpret_cast<uint2*>(p.C + static_cast<int64_t>(row) * p.ldc + col) =
+            make_uint2(pack_bf16(v.x, v.y), pack_bf16(v.z, v.w));
     }
   }
 }
@@ -1128,8 +1153,12 @@ static int gemm_impl(const void* A, const void* B, void* C, const void* residual
     return bz_fail(BZ_EINVAL, "gemm: operands (and the residual) must be 16-byte aligned");
   // skinny A: load only the rows that exist (8-row swizzle atoms); the rows of
   // the 128-row MMA beyond them read stale smem and are never stored
+  const bool c_f32 = (flags & BZ_GEMM_C_F32) != 0;
+  if (c_f32 && (reinterpret_cast<uintptr_t>(C) & 15))
+    return bz_fail(BZ_EINVAL, "gemm: fp32 C must be 16-byte aligned");
   const int po = pair_override();
-  bool pair = po == 1 || (po == -1 && M >= 2 * BM);
+  // fp32 C is a single-CTA epilogue feature (logit heads: M = sequences)
+  bool pair = !c_f32 && (po == 1 || (po == -1 && M >= 2 * BM));
   int single_bn = 0;
   if (pair && po == -1 && bn_override() == 0) {
     // a pair plan against single-CTA tiles (chip fill), using the pair model's constants
@@ -1166,6 +1195,7 @@ static int gemm_impl(const void* A, const void* B, void* C, const void* residual
   p.kb_slice = (K + BK - 1) / BK;
   p.a_bytes = a_box * BK * 2;
   p.b_static = (flags & BZ_GEMM_B_STATIC) ? 1 : 0;
+  p.c_f32 = c_f32 ? 1 : 0;
   if (!workspace || (reinterpret_cast<uintptr_t>(workspace) & 15)) ws_bytes = 0;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const int forced = bn_override();

@@ -29,7 +29,7 @@ from typing import Optional
 
 import torch
 
-from ._native import BZ_GEMM_B_STATIC, cuda_lib
+from ._native import BZ_GEMM_B_STATIC, BZ_GEMM_C_F32, cuda_lib
 from .slab import LlamaArch, SlabLayout
 
 
@@ -122,11 +122,13 @@ class LlamaExecutor:
         m, k = x.shape
         n = w.shape[0]
         ctas = ctypes.c_int(0)
+        # B = slab weights: landed before the layer gate; an fp32 out keeps the accumulator
+        flags = BZ_GEMM_B_STATIC | (BZ_GEMM_C_F32 if out.dtype == torch.float32 else 0)
         self.lib.bz_gemm_bf16_ex(x.data_ptr(), w.data_ptr(), out.data_ptr(),
                                  residual.data_ptr() if residual is not None else None,
                                  m, n, k, x.stride(0), w.stride(0), out.stride(0),
                                  residual.stride(0) if residual is not None else 0, 0,
-                                 BZ_GEMM_B_STATIC,  # B = slab weights: landed before the layer gate
+                                 flags,
                                  self.streamk_ws.data_ptr(), self.STREAMK_WS_BYTES,
                                  signal.data_ptr() if signal is not None else None, ctypes.byref(ctas),
                                  torch.cuda.current_stream().cuda_stream)
@@ -228,9 +230,10 @@ class LlamaExecutor:
         L = self.w.layers[-1]
         h = torch.empty_like(last)
         self._rmsnorm(last, L["final_norm"], h)
-        logits = torch.empty(B, self.arch.vocab, dtype=torch.bfloat16, device=x.device)
+        # fp32 logits straight from the TMEM accumulator (no bf16 rounding of the head)
+        logits = torch.empty(B, self.arch.vocab, dtype=torch.float32, device=x.device)
         self._gemm(h, L["lm_head"], logits)
-        return logits.float()
+        return logits
 
     @torch.no_grad()
     def forward(self, tokens: torch.Tensor, first: int = 0, last: Optional[int] = None,

@@ -155,3 +155,26 @@ def test_pair_splitk_prefill_shapes(m, n, k):
     torch.cuda.synchronize()
     _check(c, a.float() @ b.float().t() + r.float())
     assert ctas > 0 and int(sig.item()) == ctas
+
+
+@pytest.mark.parametrize("m,n,k,ws", [(4, 32000, 4096, True), (8, 32000, 4096, False), (200, 4096, 512, False),
+                                      (1, 1000, 256, True)])
+def test_gemm_fp32_output(m, n, k, ws):
+    """BZ_GEMM_C_F32 (logit heads): the accumulator is stored unrounded -- far tighter
+    than the bf16 rounding bound (fp32 accumulation order is the only difference),
+    whole-tile and stream-K (workspace) schedules alike."""
+    from paper_2412_17246_b200._native import BZ_GEMM_B_STATIC, BZ_GEMM_C_F32
+    import ctypes
+    torch.manual_seed(m + n)
+    a = torch.randn(m, k, device="cuda").to(torch.bfloat16)
+    b = (torch.randn(n, k, device="cuda") * 0.02).to(torch.bfloat16)
+    c = torch.full((m, n), float("nan"), dtype=torch.float32, device="cuda")
+    w = torch.zeros(16 << 20, dtype=torch.float32, device="cuda") if ws else None
+    cuda_lib().bz_gemm_bf16_ex(a.data_ptr(), b.data_ptr(), c.data_ptr(), None, m, n, k, a.stride(0), b.stride(0),
+                               c.stride(0), 0, 0, BZ_GEMM_B_STATIC | BZ_GEMM_C_F32,
+                               w.data_ptr() if w is not None else None, (w.numel() * 4) if w is not None else 0,
+                               None, ctypes.byref(ctypes.c_int()), torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    ref = a.float() @ b.float().t()
+    assert not torch.isnan(c).any()
+    assert ((c - ref).abs().max() / ref.abs().max()).item() < 1e-4

@@ -62,25 +62,35 @@ def _emit(line: dict) -> None:
     print(json.dumps(line), file=_JSON_OUT, flush=True)
 
 
-def _push_traffic(payload: int):
-    """DRAM bytes per launch of the dominant mover (k_push_tiles) from the committed
-    ncu --set full capture of one 7B chain hop (profiles/r1_ncu_push_raw.csv,
-    loopback: the hop's source reads and destination writes land on one GPU),
-    scaled to this run's shard; on NVLink the sender's own DRAM sees the read half."""
+def _ncu_metrics(name: str) -> dict:
+    """{metric: value} of the first kernel in a committed ncu --csv launch list (long format)."""
     import csv
-    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r1_ncu_push_raw.csv")
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", name)
+    out = {}
+    with open(path, newline="") as f:
+        rows = [r for r in csv.reader(f) if len(r) >= 15 and r[0] != "ID"]
+    for r in rows:
+        if r[0] == rows[0][0]:
+            out[r[12]] = float(r[14].replace(",", ""))
+    return out
+
+
+def _push_traffic(payload: int):
+    """Per-launch DRAM traffic of the dominant mover (k_push_tiles on the sending GPU)
+    and its NVLink wire bytes, from the committed single-process 2-GPU ncu capture
+    of one 2 GB hop (profiles/r2_ncu_nvlink_push_n2.csv), scaled to this shard."""
     try:
-        with open(path, newline="") as f:
-            rows = list(csv.reader(f))
-        hdr, units, vals = rows[0], rows[1], rows[2]
-        scale = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
-        got = {h: float(v) * scale[u] for h, u, v in zip(hdr, units, vals)
-               if h in ("dram__bytes_read.sum", "dram__bytes_write.sum")}
-        captured = 13_476_831_232  # the 7B shard the capture moved
-        total = (got["dram__bytes_read.sum"] + got["dram__bytes_write.sum"]) * payload / captured
-        return total, "ncu --set full, k_push_tiles<0> loopback hop (profiles/r1_ncu_push_raw.csv), read+write"
+        m = _ncu_metrics("r2_ncu_nvlink_push_n2.csv")
+        user = m["nvltx__bytes_data_user.sum"]
+        scale = payload / user
+        return {"traffic": (m["dram__bytes_read.sum"] + m["dram__bytes_write.sum"]) * scale,
+                "traffic_source": "ncu, k_push_tiles<0> gpu0->gpu1 hop of 2.0 GB (profiles/r2_ncu_nvlink_push_n2.csv): "
+                                  "sender DRAM read+write, scaled to this shard",
+                "nvlink_wire_per_user_byte": m["nvltx__bytes.sum"] / user,
+                "ncu_nvlink_user_GBps": user / m["gpu__time_duration.sum"],
+                "ncu_nvlink_wire_GBps": m["nvltx__bytes.sum"] / m["gpu__time_duration.sum"]}
     except (OSError, KeyError, IndexError, ValueError):
-        return None, None
+        return {"traffic": None, "traffic_source": None}
 
 
 def _hbm_peak() -> float:
@@ -128,6 +138,8 @@ def parse_args():
     p.add_argument("--no-live", action="store_true", help="skip the two-GPU live-pair block")
     p.add_argument("--no-realclock", action="store_true",
                    help="skip the real-clock C3 burst on GPUs 0..N-1 (N >= 2)")
+    p.add_argument("--extras", action="store_true",
+                   help="at N > 4 also run the live-pair / ramp / real-clock / C3 / C1 blocks")
     p.add_argument("--cpu-sample-units", type=int, default=4)
     p.add_argument("--watchdog-s", type=int, default=900)
     return p.parse_args()
@@ -679,9 +691,7 @@ def run_blitz(args):
             e1.synchronize()
             best = max(best, n / (e0.elapsed_time(e1) / 1e3) / 1e9)
         del scratch
-        h2d_ceiling = best
-        peak, peak_src = best, ("measured live: torch pinned H2D copy of 4 GiB from the same host cache "
-                                "(PCIe Gen5 x16 nominal 63 GB/s)")
+        h2d_ceiling = best   # secondary denominator; the primary stays PCIe Gen5 x16 nominal
         log(f"h2d ceiling {best:.1f} GB/s")
 
     clocks = ClockSampler(fabric.device)
@@ -772,7 +782,8 @@ def run_blitz(args):
 
     # ---- C3: serving replay of the 5x burst with the times measured above -------------------------
     c3 = None
-    if not args.no_c3 and tp == 1:
+    extras = N <= 4 or args.extras
+    if not args.no_c3 and tp == 1 and extras:
         roles_v = plan_roles(plan)
         e2e_roles = plan_roles(e2e_plan) if e2e_plan is not None else {}
         striped = e2e_plan is not None and bool(host_fed_groups(e2e_plan)) and not args.no_stripe
@@ -814,8 +825,13 @@ def run_blitz(args):
             log(f"c3 done: { {k: v['measured']['p99_ttft_ms'] for k, v in c3['strategies'].items()} }")
 
     # ---- live pair (N >= 2): ZigZag across two GPUs while the weights stream in ---------------
+    # N > 4 (the scaling sweep's 8-GPU point): the headline transfer, e2e and CPU baseline
+    # only -- the pair/ramp/real-clock blocks use GPUs 0..3 and are measured at N = 2, 4
+    extras = N <= 4 or args.extras
+    if not extras:
+        log(f"N={N}: live pair / ramp / real-clock C3 / C3 replay / C1 skipped (measured at N <= 4; --extras runs them)")
     live = None
-    if N >= 2 and tp == 1 and not args.no_live:
+    if N >= 2 and tp == 1 and not args.no_live and extras:
         from paper_2412_17246_b200.livepair import LivePair, summarize
         log("live pair (7B, NVLink hop, ZigZag)")
         lp = LivePair(fabric, arch, n_batches=12, seqs=4, seq_len=500, mode="nvlink")
@@ -831,7 +847,7 @@ def run_blitz(args):
 
     # ---- measured pair-throughput ramp (N >= 2): the executed steady_state_throughput ----------
     ramp = None
-    if rank == 0 and N >= 2 and tp == 1 and not args.no_live:
+    if rank == 0 and N >= 2 and tp == 1 and not args.no_live and extras:
         log("ramp: pair throughput vs layers resident on the new instance (GPUs 0, 1)")
         try:
             from paper_2412_17246_b200.ramp import measure_ramp
@@ -842,7 +858,7 @@ def run_blitz(args):
     # ---- C3 on the real clock (N >= 2): a 5x burst served by real 7B prefills on GPUs 0
     # and 1, the scale-up triggered by the reference policy and executed by the data plane
     realclock = None
-    if rank == 0 and N >= 2 and tp == 1 and not args.no_realclock:
+    if rank == 0 and N >= 2 and tp == 1 and not args.no_realclock and extras:
         log(f"c3 real clock (GPUs 0..{N - 1})")
         try:
             realclock = c3_realclock(arch, n_gpus=N)
@@ -853,7 +869,7 @@ def run_blitz(args):
 
     decisions = decision_timings() if rank == 0 else None
     coop = None
-    if rank == 0 and not args.no_coop:
+    if rank == 0 and not args.no_coop and extras:
         log("c1 cooperative execution")
         coop = coop_c1(fabric.device)
         log(f"c1 done {coop['tokens_per_s']:.0f} tok/s rel_err {coop['max_rel_err_vs_fp32']:.2e}")
@@ -868,7 +884,8 @@ def run_blitz(args):
     if rank == 0:
         # DRAM traffic of the dominant kernel: the NVLink push kernel (N >= 2); at N=1 the
         # mover is the copy engine (no kernel, no ncu counter): null
-        traffic, traffic_src = _push_traffic(payload) if bound == "nvlink" else (None, None)
+        nvl = _push_traffic(payload) if bound == "nvlink" else {"traffic": None, "traffic_source": None}
+        traffic, traffic_src = nvl.pop("traffic"), nvl.pop("traffic_source")
         line = {
             "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": N, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
@@ -887,10 +904,15 @@ def run_blitz(args):
             "roofline": {"bound": bound, "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": (achieved / peak) if achieved else None, "traffic": traffic,
                          "traffic_source": traffic_src,
-                         "algorithmic_bytes_per_launch": 2 * payload if bound == "nvlink" else None,  # read + write of one hop
+                         # one hop: the sender reads the shard from its HBM and stores it over NVLink
+                         "algorithmic_bytes_per_launch": payload if bound == "nvlink" else None,
+                         **nvl,
                          "peak_source": peak_src, "kernel_ms": dom_kernel_ms,
                          "frac_of_nominal": (achieved / (NVLINK_NOMINAL_GBPS if bound == "nvlink"
-                                                         else PCIE_PEAK_GBPS)) if achieved else None},
+                                                         else PCIE_PEAK_GBPS)) if achieved else None,
+                         # the box's achievable H2D rate (torch pinned 4 GiB copy, same host cache, this run)
+                         "live_h2d_ceiling_GBps": h2d_ceiling,
+                         "frac_of_live_h2d_ceiling": (achieved / h2d_ceiling) if (achieved and h2d_ceiling) else None},
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
             "clocks": clk, "wall_s": wall, "c3": c3, "decisions": decisions, "coop_c1": coop,
             "live_pair": live, "ramp": ramp, "c3_realclock": realclock,

@@ -844,8 +844,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
   }
 }
 
-// workspace = [tile counters (int32, zero between calls) | per-CTA head/tail slots]
-static int64_t counters_bytes(int tiles) { return (static_cast<int64_t>(tiles) * 4 + 255) / 256 * 256; }
+// workspace = [stream-K tile counters (int32, zero between calls): a FIXED header |
+//              stream-K per-CTA head/tail slots, or the pair kernel's split-K partials]
+// The header is never written by anything but the counters' own atomics and resets:
+// split-K partials used to start at offset 0 and clobbered the counters, so the next
+// stream-K GEMM on the same workspace (a decode step after a split-K prefill) summed
+// garbage.  Stream-K runs only with fewer tiles than SMs, so 1024 counters suffice.
+constexpr int64_t kCounterHeader = 4096;
+static int64_t counters_bytes(int tiles) { return tiles * 4 <= kCounterHeader ? 0 : INT64_MAX / 4; }
 
 // BZ_GEMM_STREAMK=0|1 forces stream-K off/on (when feasible); unset: cost model
 static int streamk_override() {
@@ -980,9 +986,7 @@ static int launch(const CUtensorMap& ma, const void* B, int N, int K, int ldb, P
     p.streamk = 1;
     p.sk_per = sk_per;
     p.sk_total = tiles * k_blocks;
-    p.counters = reinterpret_cast<int*>(p.ws);
-    p.ws = reinterpret_cast<float*>(reinterpret_cast<char*>(p.ws) + counters_bytes(tiles));
-    grid = (p.sk_total + sk_per - 1) / sk_per;
+    grid = (p.sk_total + sk_per - 1) / sk_per;   // p.counters / p.ws split in gemm_impl
   }
   static bool attr_set[64] = {};
   p.a_stage = (p.a_bytes + 1023) / 1024 * 1024;
@@ -1164,7 +1168,8 @@ static int gemm_impl(const void* A, const void* B, void* C, const void* residual
     // a pair plan against single-CTA tiles (chip fill), using the pair model's constants
     const int ctas_all = max_ctas > 0 ? tmin(max_ctas, 148) : 148;
     const PairPlan pp = plan_pair((M + 2 * BM - 1) / (2 * BM), M, N, K, ctas_all / 2, 0, nsub_override(),
-                                  (workspace && !(reinterpret_cast<uintptr_t>(workspace) & 15)) ? ws_bytes : 0);
+                                  (workspace && !(reinterpret_cast<uintptr_t>(workspace) & 15) &&
+                                   ws_bytes > kCounterHeader) ? ws_bytes - kCounterHeader : 0);
     const double ts = single_tile_time(M, N, K, ctas_all, &single_bn);
     if (ts < pp.t) pair = false;
   }
@@ -1196,7 +1201,13 @@ static int gemm_impl(const void* A, const void* B, void* C, const void* residual
   p.a_bytes = a_box * BK * 2;
   p.b_static = (flags & BZ_GEMM_B_STATIC) ? 1 : 0;
   p.c_f32 = c_f32 ? 1 : 0;
-  if (!workspace || (reinterpret_cast<uintptr_t>(workspace) & 15)) ws_bytes = 0;
+  if (!workspace || (reinterpret_cast<uintptr_t>(workspace) & 15) || ws_bytes <= kCounterHeader) {
+    ws_bytes = 0;
+  } else {
+    p.counters = static_cast<int*>(workspace);
+    p.ws = reinterpret_cast<float*>(static_cast<char*>(workspace) + kCounterHeader);
+    ws_bytes -= kCounterHeader;
+  }
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const int forced = bn_override();
   if (pair) {

@@ -178,3 +178,35 @@ def test_gemm_fp32_output(m, n, k, ws):
     ref = a.float() @ b.float().t()
     assert not torch.isnan(c).any()
     assert ((c - ref).abs().max() / ref.abs().max()).item() < 1e-4
+
+
+def test_splitk_partials_leave_streamk_counters_zero():
+    """Regression: the pair kernel's split-K partials and the stream-K tile counters
+    share one workspace.  A split-K prefill GEMM (down projection, 256 tokens) followed
+    by a stream-K decode GEMM (4 rows) on the same workspace must both be exact, and
+    the counter header must read zero afterwards (it used to be overwritten by fp32
+    partials, so the next decode step summed garbage)."""
+    from paper_2412_17246_b200._native import BZ_GEMM_B_STATIC
+    import ctypes
+    torch.manual_seed(5)
+    ws = torch.zeros(64 << 20 >> 2, dtype=torch.float32, device="cuda")
+
+    def run(a, b):
+        c = torch.empty(a.shape[0], b.shape[0], dtype=torch.bfloat16, device="cuda")
+        cuda_lib().bz_gemm_bf16_ex(a.data_ptr(), b.data_ptr(), c.data_ptr(), None, a.shape[0], b.shape[0],
+                                   a.shape[1], a.stride(0), b.stride(0), c.stride(0), 0, 0, BZ_GEMM_B_STATIC,
+                                   ws.data_ptr(), ws.numel() * 4, None, ctypes.byref(ctypes.c_int()),
+                                   torch.cuda.current_stream().cuda_stream)
+        return c
+
+    for _ in range(2):
+        a1 = torch.randn(256, 11008, device="cuda").to(torch.bfloat16)
+        b1 = (torch.randn(4096, 11008, device="cuda") * 0.02).to(torch.bfloat16)
+        c1 = run(a1, b1)
+        a2 = torch.randn(4, 4096, device="cuda").to(torch.bfloat16)
+        b2 = (torch.randn(4096, 4096, device="cuda") * 0.02).to(torch.bfloat16)
+        c2 = run(a2, b2)
+        torch.cuda.synchronize()
+        _check(c1, a1.float() @ b1.float().t())
+        _check(c2, a2.float() @ b2.float().t())
+        assert int(ws[:1024].view(torch.int32).abs().sum()) == 0

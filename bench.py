@@ -138,6 +138,11 @@ def parse_args():
     p.add_argument("--no-live", action="store_true", help="skip the two-GPU live-pair block")
     p.add_argument("--no-realclock", action="store_true",
                    help="skip the real-clock C3 burst on GPUs 0..N-1 (N >= 2)")
+    p.add_argument("--live-engine", default="vector", choices=["vector", "ce"],
+                   help="weight push of the two-GPU live pair (ce: copy engines, no SMs)")
+    p.add_argument("--live-nctas", type=int, default=48)
+    p.add_argument("--live-ce-tiles", type=int, default=64, help="tiles per copy-engine memcpy (--live-engine ce)")
+    p.add_argument("--live-repeats", type=int, default=5, help="ZigZag / best-effort runs each (alternating)")
     p.add_argument("--extras", action="store_true",
                    help="at N > 4 also run the live-pair / ramp / real-clock / C3 / C1 blocks")
     p.add_argument("--cpu-sample-units", type=int, default=4)
@@ -834,7 +839,9 @@ def run_blitz(args):
     if N >= 2 and tp == 1 and not args.no_live and extras:
         from paper_2412_17246_b200.livepair import LivePair, summarize
         log("live pair (7B, NVLink hop, ZigZag)")
-        lp = LivePair(fabric, arch, n_batches=12, seqs=4, seq_len=500, mode="nvlink")
+        lp = LivePair(fabric, arch, n_batches=12, seqs=4, seq_len=500, mode="nvlink",
+                      engine={"ce": 3, "vector": 0}[args.live_engine], nctas=args.live_nctas,
+                      repeats=args.live_repeats, ce_tiles_per_copy=args.live_ce_tiles)
         res = lp.run()
         live = summarize(res) if res is not None else None
         log("live pair: KV hand-over to the new instance, which then decodes alone")

@@ -469,9 +469,12 @@ class ScaleExecutor:
     def __init__(self, fabric: Fabric, plan: ScalePlan, slab: DeviceSlab,
                  node_rank: dict[str, int], host_cache: Optional[HostCache] = None,
                  engine: int = ENGINE_VECTOR, nctas: int = 32, fanout_mode: str = "auto",
-                 stage_engine: str = "ce", tiles_per_copy: int = 128, host_stripe: bool = True):
+                 stage_engine: str = "ce", tiles_per_copy: int = 128, host_stripe: bool = True,
+                 ce_tiles_per_copy: int = 0):
         self.fabric = fabric
         self.plan = plan
+        # tiles per copy-engine memcpy of an ENGINE_CE chain hop (0: CE_TILES_PER_COPY)
+        self.ce_tiles = ce_tiles_per_copy or CE_TILES_PER_COPY
         self.slab = slab
         self.layout = slab.layout
         self.node_rank = dict(node_rank)
@@ -657,7 +660,7 @@ class ScaleExecutor:
                 self.lib.bz_push_tiles_ce(slab.ptr, self.peers[n].ptr, self.peers[n].flags_ptr,
                                           slab.flags_ptr if relay else None,
                                           self._tile_off_host.ctypes.data, 0, lay.ntiles,
-                                          CE_TILES_PER_COPY, e, st["copy"].cuda_stream)
+                                          self.ce_tiles, e, st["copy"].cuda_stream)
         elif dsts:
             ptrs = ptr_array([self.peers[n].ptr for n in dsts])
             flags = ptr_array([self.peers[n].flags_ptr for n in dsts])
@@ -703,7 +706,7 @@ class ScaleExecutor:
                 n += 1
         dsts = self._unicast_targets()
         if dsts and self.engine == ENGINE_CE:
-            groups = (self.layout.ntiles + CE_TILES_PER_COPY - 1) // CE_TILES_PER_COPY
+            groups = (self.layout.ntiles + self.ce_tiles - 1) // self.ce_tiles
             per_group = 2 if self.role.receives else 1  # [gate] + flag kernel (memcpy not counted)
             n += len(dsts) * groups * per_group
         elif dsts:

@@ -155,9 +155,10 @@ class LivePair:
 
     def __init__(self, fabric: Fabric, arch: LlamaArch, n_batches: int, seqs: int, seq_len: int,
                  mode: str = "host", src: int = 0, tgt: int = 1, tile_bytes: int = 1 << 20,
-                 nctas: int = 48, seed: int = 7, engine: int = 0):
+                 nctas: int = 48, seed: int = 7, engine: int = 0, repeats: int = 1, ce_tiles_per_copy: int = 0):
         self.f, self.arch, self.mode = fabric, arch, mode
         self.src, self.tgt = src, tgt
+        self.repeats = max(1, repeats)
         self.n, self.seqs, self.seq_len = n_batches, seqs, seq_len
         self.rows = seqs * seq_len
         self.layout = SlabLayout.for_arch(arch, tile_bytes=tile_bytes)
@@ -189,7 +190,7 @@ class LivePair:
         node_rank = {src_node: src, tgt_node: tgt}
         if self.slab is not None:
             self.executor = ScaleExecutor(fabric, plan, self.slab, node_rank, host_cache=self.hc,
-                                          nctas=nctas, engine=engine)
+                                          nctas=nctas, engine=engine, ce_tiles_per_copy=ce_tiles_per_copy)
         else:  # bystander ranks still join the collective setup
             fabric.allgather(None)
             fabric.barrier()
@@ -247,6 +248,9 @@ class LivePair:
             arr = self.executor.layer_arrivals_ms()
             lm[0] = arr[-1]
             lm[1] = (arr[-1] - arr[0]) / max(1, len(arr) - 1)
+            arr_t = torch.tensor(arr, dtype=torch.float64, device="cuda")
+        else:
+            arr_t = torch.zeros(self.arch.n_layers, dtype=torch.float64, device="cuda")
         if self.me == self.src:
             self.fused_grid()      # probe launch outside any timed region
         if self.me == self.tgt:
@@ -254,9 +258,14 @@ class LivePair:
         import torch.distributed as dist
         dist.all_reduce(w)
         dist.all_reduce(lm)
+        dist.all_reduce(arr_t)
         w_ms, load_ms, unit_ms = float(w.item()), float(lm[0].item()), float(lm[1].item())
         self.load_ms = load_ms
         layer_exec = w_ms / self.arch.n_layers
+        # measured arrival of every layer on the new instance, in layer-execution units
+        # (the reference's layer_load_times, livescale.py:269-270): unit 1 carries the
+        # embedding, so the arrivals are not a uniform k * time_l
+        self.layer_load_units = [float(a) / layer_exec for a in arr_t.cpu().tolist()]
         return w_ms, unit_ms, unit_ms / layer_exec
 
     def _transfer_once(self):
@@ -518,15 +527,22 @@ class LivePair:
 
     def run(self) -> Optional[LivePairResult]:
         w_ms, unit_ms, time_l = self.calibrate()
+        loads = self.layer_load_units
         cfg = livescale.configure_pipeline(self.n, self.arch.n_layers, time_l)
-        tl = livescale.zigzag_schedule(cfg)
+        tl = livescale.zigzag_schedule(cfg, layer_load_times=loads)
         self.cfg, self.tl = cfg, tl
         be = livescale.best_effort_pipeline(self.n, self.arch.n_layers, time_l)
-        be_tl = livescale.zigzag_schedule(be)
+        be_tl = livescale.zigzag_schedule(be, layer_load_times=loads)
         alone_f, alone_logits = self.run_source_alone()
-        zz_f, zz_logits = self.run_split(cfg, tl)
-        zz_diag = self.last_diag
-        be_f, _ = self.run_split(be, be_tl)
+        # ZigZag and best-effort alternate, `repeats` runs each (the spread between
+        # runs is reported; the comparison uses the median)
+        zz_runs, be_runs, zz_logits, zz_diag = [], [], None, None
+        for r in range(self.repeats):
+            f, lg = self.run_split(cfg, tl)
+            zz_runs.append(f)
+            if r == 0:
+                zz_logits, zz_diag = lg, self.last_diag
+            be_runs.append(self.run_split(be, be_tl)[0])
         # the baseline runs twice (before and after the split runs) and keeps the faster,
         # so a slow outlier (clock/power state) cannot flatter the split
         alone_f2, _ = self.run_source_alone()
@@ -535,15 +551,24 @@ class LivePair:
         res = None
         if self.me == self.src:
             layer_ms = w_ms / self.arch.n_layers
+            zz_avgs = [_mean(f) for f in zz_runs]
+            be_avgs = [_mean(f) for f in be_runs]
+            med = sorted(range(len(zz_avgs)), key=lambda i: zz_avgs[i])[len(zz_avgs) // 2]
+            bmed = sorted(range(len(be_avgs)), key=lambda i: be_avgs[i])[len(be_avgs) // 2]
             res = LivePairResult(mode=self.mode, time_l=time_l, w_ms=w_ms,
-                                 splits=[list(s) for s in cfg.splits], zigzag_finish_ms=zz_f,
+                                 splits=[list(s) for s in cfg.splits], zigzag_finish_ms=zz_runs[med],
                                  source_alone_finish_ms=alone_f,
                                  predicted_finish_ms=[t * layer_ms for t in tl.finish],
-                                 best_effort_finish_ms=be_f, load_ms=self.load_ms)
+                                 best_effort_finish_ms=be_runs[bmed], load_ms=self.load_ms)
             eq = all(torch.equal(a, b) for a, b in zip(zz_logits, alone_logits))
             diff = max(float((a - b).abs().max()) for a, b in zip(zz_logits, alone_logits))
             res.logits_bitwise_equal, res.max_abs_diff = eq, diff
-            res.diagnostics = zz_diag
+            res.diagnostics = dict(zz_diag or {})
+            res.diagnostics["runs"] = {"zigzag_avg_ms": zz_avgs, "best_effort_avg_ms": be_avgs,
+                                       "zigzag_beats_best_effort_every_run":
+                                           all(z < b for z, b in zip(zz_avgs, be_avgs)),
+                                       "layer_load_units": loads,
+                                       "best_effort_splits": [list(x) for x in be.splits]}
         return res
 
     def close(self):
@@ -563,12 +588,13 @@ def summarize(res: LivePairResult) -> dict:
     return {
         "mode": res.mode, "time_l_measured": res.time_l, "batch_forward_ms": res.w_ms,
         "weights_load_ms": res.load_ms, "splits": res.splits,
-        "avg_latency_ms": {"zigzag_executed": _mean(res.zigzag_finish_ms),
-                           "best_effort_executed": _mean(res.best_effort_finish_ms),
+        "avg_latency_ms": {"zigzag_executed": _mean(res.zigzag_finish_ms),          # median run
+                           "best_effort_executed": _mean(res.best_effort_finish_ms),  # median run
                            "source_alone": _mean(res.source_alone_finish_ms),
                            "zigzag_rehearsal_prediction": _mean(res.predicted_finish_ms)},
         "finish_ms": {"zigzag": res.zigzag_finish_ms, "source_alone": res.source_alone_finish_ms},
         "logits_bitwise_equal_to_source_alone": res.logits_bitwise_equal,
         "max_abs_logit_diff": res.max_abs_diff,
-        "diagnostics": res.diagnostics,
+        "runs": res.diagnostics.get("runs"),
+        "diagnostics": {k: v for k, v in res.diagnostics.items() if k != "runs"},
     }

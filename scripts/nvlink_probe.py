@@ -203,6 +203,16 @@ def main():
                 emit({"case": "push", "engine": ename, "nctas": c, "ms": ms, "GBps": payload / ms / 1e6,
                       "ok": check(peer, want, e)})
 
+    # ---- copy-engine hop (no SM moves bytes): tiles per memcpy sweep ---------------------------
+    if args.once is None:
+        for tpc in (8, 16, 32, 64, 128):
+            e = nxt()
+            fn = lambda: lib.bz_push_tiles_ce(src.ptr, mapped.ptr, mapped.flags_ptr, None,  # noqa: E731
+                                              lay.tile_off.ctypes.data, 0, lay.ntiles, tpc, e, stream.cuda_stream)
+            ms = timed(fn, stream)
+            emit({"case": "push", "engine": "ce", "tiles_per_copy": tpc, "ms": ms, "GBps": payload / ms / 1e6,
+                  "ok": check(peer, want, e)})
+
     # ---- NVLS multicast over gpu0..gpu{G-1} ------------------------------------------------------
     try:
         mc = LocalMc([src] + dsts, 0)

@@ -138,10 +138,10 @@ def parse_args():
     p.add_argument("--no-live", action="store_true", help="skip the two-GPU live-pair block")
     p.add_argument("--no-realclock", action="store_true",
                    help="skip the real-clock C3 burst on GPUs 0..N-1 (N >= 2)")
-    p.add_argument("--live-engine", default="vector", choices=["vector", "ce"],
+    p.add_argument("--live-engine", default="ce", choices=["vector", "ce"],
                    help="weight push of the two-GPU live pair (ce: copy engines, no SMs)")
     p.add_argument("--live-nctas", type=int, default=48)
-    p.add_argument("--live-ce-tiles", type=int, default=64, help="tiles per copy-engine memcpy (--live-engine ce)")
+    p.add_argument("--live-ce-tiles", type=int, default=128, help="tiles per copy-engine memcpy (--live-engine ce)")
     p.add_argument("--live-repeats", type=int, default=5, help="ZigZag / best-effort runs each (alternating)")
     p.add_argument("--extras", action="store_true",
                    help="at N > 4 also run the live-pair / ramp / real-clock / C3 / C1 blocks")

@@ -224,6 +224,16 @@ int bz_rope(void* qkv, const int32_t* positions, int rows, int n_rot_heads, int 
 /* act[:, j] = silu(gu[:, j]) * gu[:, ffn + j]. */
 int bz_silu_mul(const void* gu, void* act, int rows, int ffn, int ldg, int lda, void* stream);
 
+/* ---- prefill attention (csrc/attention_tcgen05.cu) -------------------------------------
+ * Causal softmax(Q K^T / sqrt(hd)) V for B sequences of S tokens on tcgen05 tensor
+ * cores (TMEM accumulators, TMA-fed), GQA (n_heads % n_kv == 0), hd 64 or 128.
+ * qkv: [B*S, ld] bf16 rows [q heads | k heads | v heads] with RoPE applied; out:
+ * [B*S, ldo] bf16, head h at columns [h*hd, (h+1)*hd).  The workspace holds V
+ * transposed ([B, n_kv, hd, S rounded up to 64] bf16) so V^T is a K-major MMA operand. */
+int bz_prefill_attention_workspace_bytes(int B, int S, int n_kv, int head_dim, int64_t* bytes);
+int bz_prefill_attention(const void* qkv, int ld, int B, int S, int n_heads, int n_kv, int head_dim,
+                         void* workspace, int64_t workspace_bytes, void* out, int ldo, void* stream);
+
 /* ---- KV-cache decode (csrc/decode_kernels.cu) -------------------------------------------
  * The decode position is read from device memory (*pos, int32), so a captured
  * decode step replays for every position.  Cache layout [rows, n_kv, s_max, hd]

@@ -142,6 +142,8 @@ _SIGNATURES = {
     "bz_decode_workspace_bytes": [_I, _I, _I, _I, ctypes.c_int64, ctypes.POINTER(ctypes.c_int64)],
     "bz_decode_attention": [_P, _I, _P, _P, _I, _I, _I, _I, ctypes.c_int64, _P, _P, _I, _P, ctypes.c_int64,
                             _P],
+    "bz_prefill_attention_workspace_bytes": [_I, _I, _I, _I, ctypes.POINTER(ctypes.c_int64)],
+    "bz_prefill_attention": [_P, _I, _I, _I, _I, _I, _I, _P, ctypes.c_int64, _P, _I, _P],
     "bz_sm_count": [_I, _PI],
     "bz_preload_kernels": [_I, _PI],
 }

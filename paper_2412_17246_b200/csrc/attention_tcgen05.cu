@@ -1,0 +1,404 @@
+// Causal flash attention for the prefill of a Llama block on sm_100a tensor cores.
+//
+// The reference stands the whole forward in with ModelSpec.prefill_ms
+// (parampool.py:58-62); with the projections on tcgen05 GEMMs (gemm_tcgen05.cu)
+// this is the block's other contraction: softmax(Q K^T / sqrt(hd)) V per head,
+// causal, GQA (query head h reads kv head h / (H / KV)).
+//
+//   in : qkv  [B*S, ld]  bf16, row = token, [q heads | k heads | v heads] (RoPE applied)
+//        vt   [B, KV, hd, S_pad] bf16 -- V transposed by k_v_transpose (keys contiguous,
+//             so V^T is a K-major MMA operand like every weight), zero past S
+//   out: attn [B*S, ldo] bf16, head h at columns [h*hd, (h+1)*hd) -- the o-projection's A
+//
+// One CTA = 128 query rows of one (sequence, head); TMEM lane = query row.
+//   w0      TMA producer: Q once, then K / V^T tiles of 128 keys (2-deep ring)
+//   w1      MMA issuer (one lane): S_j = Q K_j^T into TMEM (2 buffers), and once
+//           the softmax has written P_j: O_j = P_j V_j into TMEM (2 buffers)
+//   w2..w5  softmax (thread = query row): S_j from TMEM, causal mask on the diagonal
+//           tile, running max in the log2 domain, P_j = exp2(.) as bf16 straight into
+//           the 128B-swizzled smem layout the MMA reads, and O += rescaled O_j in
+//           registers (fp32); the epilogue divides by the row sum and stores bf16.
+// The MMA of S_{j+1} overlaps the softmax of tile j; P is single-buffered (the
+// softmax of tile j+1 writes P only after O_j's MMA has completed).
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdint.h>
+
+#include "../../include/blitz.h"
+#include "common.cuh"
+#include "tc_primitives.cuh"
+
+namespace bz {
+namespace attn {
+
+using namespace bz::tc;
+
+constexpr int BQ = 128;       // query rows per CTA (= TMEM lanes)
+constexpr int BKV = 128;      // keys per tile
+constexpr int THREADS = 192;  // w0 TMA, w1 MMA + TMEM allocator, w2..w5 softmax / epilogue
+constexpr int ATOM_BYTES = 128 * 128;  // one 128-row x 128-byte swizzle block (64 bf16 wide)
+
+template <int HD>
+struct Cfg {
+  static constexpr int Q_BYTES = BQ * HD * 2;
+  static constexpr int K_BYTES = BKV * HD * 2;
+  static constexpr int V_BYTES = HD * BKV * 2;   // V^T tile: HD rows x 128 keys = 2 atoms of HD x 128 B
+  static constexpr int V_ATOM = HD * 128;        // bytes of one 64-key atom of the V^T tile
+  static constexpr int P_BYTES = BQ * BKV * 2;
+  static constexpr int STAGES = 2;
+  static constexpr int BAR_BYTES = 256;
+  static constexpr int SMEM = 1024 + Q_BYTES + STAGES * (K_BYTES + V_BYTES) + P_BYTES + BAR_BYTES;
+  static constexpr int S_COL = 0;                // S buffers at columns [0, 256)
+  static constexpr int O_COL = 2 * BKV;          // O buffers at [256, 256 + 2 HD)
+  static constexpr int TMEM_COLS = 512;
+  static_assert(HD == 64 || HD == 128, "head dim");
+  static_assert(SMEM <= 232448, "smem");
+};
+
+struct Args {
+  __nv_bfloat16* out;
+  int ldo;
+  int S;          // tokens per sequence
+  int H, KV;      // query heads, kv heads
+  int q_col0;     // column of q head 0 in qkv (0)
+  int k_col0;     // column of k head 0 (H * hd)
+  float scale_log2;  // log2(e) / sqrt(hd)
+};
+
+__device__ __forceinline__ uint32_t pack2(float lo, float hi) {
+  __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
+  return *reinterpret_cast<uint32_t*>(&v);
+}
+
+template <int HD>
+__global__ void __launch_bounds__(THREADS, 1)
+    k_flash_prefill(const __grid_constant__ CUtensorMap map_qk, const __grid_constant__ CUtensorMap map_vt, Args a) {
+  using C = Cfg<HD>;
+  constexpr int KA = HD / 64;  // 64-wide swizzle atoms along hd
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sq = smem;
+  uint8_t* sk = sq + C::Q_BYTES;
+  uint8_t* sv = sk + C::STAGES * C::K_BYTES;
+  uint8_t* sp = sv + C::STAGES * C::V_BYTES;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sp + C::P_BYTES);
+  uint64_t* q_full = bars;
+  uint64_t* kv_full = bars + 1;   // [2]
+  uint64_t* kv_empty = bars + 3;  // [2]
+  uint64_t* s_full = bars + 5;    // [2]
+  uint64_t* s_empty = bars + 7;   // [2]
+  uint64_t* o_full = bars + 9;    // [2]
+  uint64_t* o_empty = bars + 11;  // [2]
+  uint64_t* p_full = bars + 13;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 14);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int n_qt = (a.S + BQ - 1) / BQ;
+  const int qt = n_qt - 1 - static_cast<int>(blockIdx.x);  // longest (most keys) tiles first
+  const int h = blockIdx.y, b = blockIdx.z;
+  const int g = h / (a.H / a.KV);
+  const int s0 = qt * BQ;
+  const int nj = qt + 1;  // key tiles 0..qt (causal)
+  const int row0 = b * a.S;
+
+  if (warp == 0 && lane == 0) {
+    prefetch_tmap(&map_qk);
+    prefetch_tmap(&map_vt);
+    mbar_init(q_full, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&kv_full[i], 1);
+      mbar_init(&kv_empty[i], 1);
+      mbar_init(&s_full[i], 1);
+      mbar_init(&s_empty[i], 4);
+      mbar_init(&o_full[i], 1);
+      mbar_init(&o_empty[i], 4);
+    }
+    mbar_init(p_full, 4);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "n"(C::TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ---- TMA producer ----
+      pdl_wait();  // q/k/v were written by the predecessor (qkv GEMM + RoPE + transpose)
+      mbar_expect_tx(q_full, C::Q_BYTES);
+      for (int ka = 0; ka < KA; ++ka)
+        tma_load_2d(sq + ka * ATOM_BYTES, &map_qk, a.q_col0 + h * HD + ka * 64, row0 + s0, q_full);
+      for (int j = 0; j < nj; ++j) {
+        const int slot = j & 1;
+        mbar_wait(&kv_empty[slot], ((j >> 1) & 1) ^ 1);
+        mbar_expect_tx(&kv_full[slot], C::K_BYTES + C::V_BYTES);
+        for (int ka = 0; ka < KA; ++ka)
+          tma_load_2d(sk + slot * C::K_BYTES + ka * ATOM_BYTES, &map_qk, a.k_col0 + g * HD + ka * 64,
+                      row0 + j * BKV, &kv_full[slot]);
+        for (int kh = 0; kh < 2; ++kh)
+          tma_load_2d(sv + slot * C::V_BYTES + kh * C::V_ATOM, &map_vt, j * BKV + kh * 64, (b * a.KV + g) * HD,
+                      &kv_full[slot]);
+      }
+      pdl_trigger();
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ---- MMA issuer ----
+      constexpr uint32_t idesc_s = instr_desc_bf16(BQ, BKV);
+      constexpr uint32_t idesc_o = instr_desc_bf16(BQ, HD);
+      mbar_wait(q_full, 0);
+      auto issue_s = [&](int j) {
+        const int slot = j & 1, sb = j & 1;
+        mbar_wait(&kv_full[slot], (j >> 1) & 1);
+        mbar_wait(&s_empty[sb], ((j >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t d = tmem + C::S_COL + sb * BKV;
+#pragma unroll
+        for (int kk = 0; kk < HD / 16; ++kk) {
+          const uint64_t da = umma_desc_sw128(smem_u32(sq + (kk >> 2) * ATOM_BYTES)) + 2 * (kk & 3);
+          const uint64_t db = umma_desc_sw128(smem_u32(sk + slot * C::K_BYTES + (kk >> 2) * ATOM_BYTES)) + 2 * (kk & 3);
+          umma_bf16(d, da, db, idesc_s, kk > 0 ? 1u : 0u);
+        }
+        umma_commit(&s_full[sb]);
+      };
+      issue_s(0);
+      for (int j = 0; j < nj; ++j) {
+        if (j + 1 < nj) issue_s(j + 1);
+        // O_j = P_j V_j once the softmax has written P_j
+        const int slot = j & 1, ob = j & 1;
+        mbar_wait(p_full, j & 1);
+        mbar_wait(&o_empty[ob], ((j >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t d = tmem + C::O_COL + ob * HD;
+#pragma unroll
+        for (int kk = 0; kk < BKV / 16; ++kk) {
+          const uint64_t da = umma_desc_sw128(smem_u32(sp + (kk >> 2) * ATOM_BYTES)) + 2 * (kk & 3);
+          const uint64_t db = umma_desc_sw128(smem_u32(sv + slot * C::V_BYTES + (kk >> 2) * C::V_ATOM)) + 2 * (kk & 3);
+          umma_bf16(d, da, db, idesc_o, kk > 0 ? 1u : 0u);
+        }
+        umma_commit(&o_full[ob]);
+        umma_commit(&kv_empty[slot]);
+      }
+    }
+  } else {
+    // ---- softmax + epilogue: thread = query row r of the tile ----
+    const int quarter = warp & 3;
+    const int r = quarter * 32 + lane;
+    const int qpos = s0 + r;  // query position in its sequence
+    const uint32_t lane_off = static_cast<uint32_t>(quarter * 32) << 16;
+    float o[HD];
+#pragma unroll
+    for (int i = 0; i < HD; ++i) o[i] = 0.f;
+    float m = -INFINITY, l = 0.f, alpha_prev = 0.f;
+    // P row r: atom (keys/64), 8-row group, row within group, 16-byte chunk ^ (r & 7)
+    uint8_t* prow = sp + (r >> 3) * 1024 + (r & 7) * 128;
+
+    auto accumulate_o = [&](int jj) {  // o = o * alpha_prev + O_jj
+      const int ob = jj & 1;
+      mbar_wait(&o_full[ob], (jj >> 1) & 1);
+      tc_fence_after();
+#pragma unroll
+      for (int c = 0; c < HD; c += 32) {
+        uint32_t v[32];
+        tmem_ld_32x32b_x32(tmem + lane_off + C::O_COL + ob * HD + c, v);
+#pragma unroll
+        for (int i = 0; i < 32; ++i) o[c + i] = fmaf(o[c + i], alpha_prev, __uint_as_float(v[i]));
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&o_empty[ob]);
+    };
+
+    for (int j = 0; j < nj; ++j) {
+      const int sb = j & 1;
+      const bool diag = j == qt;
+      mbar_wait(&s_full[sb], (j >> 1) & 1);
+      tc_fence_after();
+      const uint32_t sa = tmem + lane_off + C::S_COL + sb * BKV;
+      // pass 1: row max (log2 domain)
+      float mx = -INFINITY;
+#pragma unroll 1
+      for (int c = 0; c < BKV; c += 32) {
+        uint32_t v[32];
+        tmem_ld_32x32b_x32(sa + c, v);
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+          const bool masked = diag && (j * BKV + c + i > qpos);
+          if (!masked) mx = fmaxf(mx, __uint_as_float(v[i]));
+        }
+      }
+      const float m_new = fmaxf(m, mx * a.scale_log2);
+      const float alpha = exp2f(m - m_new);  // 0 on the first tile (m = -inf)
+      // O_{j-1} is complete (so P's smem is free again): fold it into the registers
+      if (j > 0) accumulate_o(j - 1);
+      // pass 2: P = exp2(s * scale - m_new) -> bf16 into the swizzled P tile; row sum
+      float sum = 0.f;
+#pragma unroll 1
+      for (int c = 0; c < BKV; c += 32) {
+        uint32_t v[32];
+        tmem_ld_32x32b_x32(sa + c, v);
+        uint32_t pk[16];
+#pragma unroll
+        for (int i = 0; i < 32; i += 2) {
+          const bool m0 = diag && (j * BKV + c + i > qpos);
+          const bool m1 = diag && (j * BKV + c + i + 1 > qpos);
+          const float p0 = m0 ? 0.f : exp2f(fmaf(__uint_as_float(v[i]), a.scale_log2, -m_new));
+          const float p1 = m1 ? 0.f : exp2f(fmaf(__uint_as_float(v[i + 1]), a.scale_log2, -m_new));
+          sum += p0 + p1;
+          pk[i >> 1] = pack2(p0, p1);
+        }
+        uint8_t* atom = prow + (c >> 6) * ATOM_BYTES;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int chunk = ((c & 63) >> 3) + q;  // 16-byte chunk within the 128-byte row
+          const uint32_t addr = smem_u32(atom + ((chunk ^ (r & 7)) << 4));
+          asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(addr), "r"(pk[4 * q]), "r"(pk[4 * q + 1]),
+                       "r"(pk[4 * q + 2]), "r"(pk[4 * q + 3])
+                       : "memory");
+        }
+      }
+      l = fmaf(l, alpha, sum);
+      m = m_new;
+      alpha_prev = alpha;
+      // P (generic-proxy stores) -> the MMA's async proxy; S buffer free again
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) {
+        mbar_arrive(&s_empty[sb]);
+        mbar_arrive(p_full);
+      }
+    }
+    accumulate_o(nj - 1);
+    // epilogue: O / l -> bf16 rows of the o-projection input
+    if (qpos < a.S) {
+      const float inv = 1.f / l;
+      __nv_bfloat16* dst = a.out + static_cast<int64_t>(row0 + qpos) * a.ldo + h * HD;
+#pragma unroll
+      for (int c = 0; c < HD; c += 8) {
+        uint4 w = make_uint4(pack2(o[c] * inv, o[c + 1] * inv), pack2(o[c + 2] * inv, o[c + 3] * inv),
+                             pack2(o[c + 4] * inv, o[c + 5] * inv), pack2(o[c + 6] * inv, o[c + 7] * inv));
+        *reinterpret_cast<uint4*>(dst + c) = w;
+      }
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(C::TMEM_COLS));
+  }
+}
+
+// vt[(b*KV + g)*hd + d][s] = qkv[(b*S + s)*ld + v_col0 + g*hd + d]; zero for s in [S, S_pad).
+// 64 x 64 tiles through shared memory (coalesced on both sides).
+__global__ void __launch_bounds__(256) k_v_transpose(const __nv_bfloat16* __restrict__ qkv, int ld, int v_col0,
+                                                      int S, int S_pad, int KV, int hd,
+                                                      __nv_bfloat16* __restrict__ vt) {
+  __shared__ __nv_bfloat16 tile[64][66];
+  pdl_wait();
+  pdl_trigger();
+  const int s0 = blockIdx.x * 64, d0 = blockIdx.y * 64, bg = blockIdx.z;
+  const int b = bg / KV, g = bg % KV;
+  const int tx = threadIdx.x & 63, ty = threadIdx.x >> 6;  // 64 x 4
+  for (int i = ty; i < 64; i += 4) {
+    const int s = s0 + i;
+    tile[i][tx] = s < S ? qkv[static_cast<int64_t>(b * S + s) * ld + v_col0 + g * hd + d0 + tx]
+                        : __float2bfloat16_rn(0.f);
+  }
+  __syncthreads();
+  for (int i = ty; i < 64; i += 4) {
+    const int s = s0 + tx;
+    if (s < S_pad) vt[(static_cast<int64_t>(bg) * hd + d0 + i) * S_pad + s] = tile[tx][i];
+  }
+}
+
+static int encode(CUtensorMap* map, const void* ptr, int64_t rows, int64_t cols, int64_t ld_elems, int box_cols,
+                  int box_rows) {
+  const DriverApi* d = driver_api();
+  if (!d) return BZ_ECUDA;
+  cuuint64_t dims[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows)};
+  cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld_elems) * 2};
+  cuuint32_t box[2] = {static_cast<cuuint32_t>(box_cols), static_cast<cuuint32_t>(box_rows)};
+  cuuint32_t elem[2] = {1, 1};
+  CUresult r = d->cuTensorMapEncodeTiled(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims,
+                                         strides, box, elem, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                         CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return bz_fail_cu(r, "attention: cuTensorMapEncodeTiled");
+  return BZ_OK;
+}
+
+template <int HD>
+static int launch(const void* qkv, int ld, int B, int S, int H, int KV, void* vt, int S_pad, void* out, int ldo,
+                  cudaStream_t s) {
+  using C = Cfg<HD>;
+  CUtensorMap mqk, mvt;
+  const int cols = (H + 2 * KV) * HD;
+  if (int rc = encode(&mqk, qkv, static_cast<int64_t>(B) * S, cols, ld, 64, 128)) return rc;
+  if (int rc = encode(&mvt, vt, static_cast<int64_t>(B) * KV * HD, S_pad, S_pad, 64, HD)) return rc;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  static bool attr_set[64] = {};
+  if (dev < 64 && !attr_set[dev]) {
+    cudaError_t e = cudaFuncSetAttribute(k_flash_prefill<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+    if (e != cudaSuccess) return bz_fail_cuda(e, "attention smem attribute");
+    attr_set[dev] = true;
+  }
+  cudaError_t e = launch_pdl(PDL_ATTN, k_v_transpose, dim3((S_pad + 63) / 64, HD / 64, B * KV), dim3(256), 0, s,
+                             static_cast<const __nv_bfloat16*>(qkv), ld, (H + KV) * HD, S, S_pad, KV, HD,
+                             static_cast<__nv_bfloat16*>(vt));
+  if (e != cudaSuccess) return bz_fail_cuda(e, "attention: V transpose launch");
+  Args a;
+  a.out = static_cast<__nv_bfloat16*>(out);
+  a.ldo = ldo;
+  a.S = S;
+  a.H = H;
+  a.KV = KV;
+  a.q_col0 = 0;
+  a.k_col0 = H * HD;
+  a.scale_log2 = 1.4426950408889634f / sqrtf(static_cast<float>(HD));
+  e = launch_pdl(PDL_ATTN, k_flash_prefill<HD>, dim3((S + BQ - 1) / BQ, H, B), dim3(THREADS), C::SMEM, s, mqk, mvt,
+                 a);
+  if (e != cudaSuccess) return bz_fail_cuda(e, "attention launch");
+  return bz_check_launch("bz_prefill_attention");
+}
+
+}  // namespace attn
+}  // namespace bz
+
+using namespace bz;
+
+extern "C" int bz_prefill_attention_workspace_bytes(int B, int S, int KV, int head_dim, int64_t* bytes) {
+  if (!bytes || B < 1 || S < 1 || KV < 1 || (head_dim != 64 && head_dim != 128))
+    return bz_fail(BZ_EINVAL, "prefill attention workspace: bad sizes");
+  const int64_t s_pad = (S + 63) / 64 * 64;
+  *bytes = static_cast<int64_t>(B) * KV * head_dim * s_pad * 2;
+  return BZ_OK;
+}
+
+extern "C" int bz_prefill_attention(const void* qkv, int ld, int B, int S, int n_heads, int n_kv, int head_dim,
+                                    void* workspace, int64_t workspace_bytes, void* out, int ldo, void* stream) {
+  if (!qkv || !out || !workspace || B < 1 || S < 1 || n_kv < 1 || n_heads % n_kv)
+    return bz_fail(BZ_EINVAL, "prefill attention: bad arguments");
+  if (head_dim != 64 && head_dim != 128) return bz_fail(BZ_EINVAL, "prefill attention: head_dim must be 64 or 128");
+  if (ld % 8 || ldo % 8 || (reinterpret_cast<uintptr_t>(qkv) & 15) || (reinterpret_cast<uintptr_t>(out) & 15) ||
+      (reinterpret_cast<uintptr_t>(workspace) & 15))
+    return bz_fail(BZ_EINVAL, "prefill attention: 16-byte aligned pointers and leading dims required");
+  int64_t need = 0;
+  bz_prefill_attention_workspace_bytes(B, S, n_kv, head_dim, &need);
+  if (workspace_bytes < need) return bz_fail(BZ_EINVAL, "prefill attention: workspace too small");
+  const int s_pad = (S + 63) / 64 * 64;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (head_dim == 128) return attn::launch<128>(qkv, ld, B, S, n_heads, n_kv, workspace, s_pad, out, ldo, s);
+  return attn::launch<64>(qkv, ld, B, S, n_heads, n_kv, workspace, s_pad, out, ldo, s);
+}
+
+const void* bz::module_anchor_attention() { return reinterpret_cast<const void*>(attn::k_v_transpose); }

@@ -33,6 +33,7 @@ const void* module_anchor_dataplane();
 const void* module_anchor_decode();
 const void* module_anchor_gemm();
 const void* module_anchor_llama();
+const void* module_anchor_attention();
 
 // record a message in the thread-local last-error slot, return `code`
 int bz_fail(int code, const char* msg);

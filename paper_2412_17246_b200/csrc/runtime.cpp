@@ -208,7 +208,7 @@ extern "C" int bz_preload_kernels(int dev, int* nloaded) {
   int rc = use_device(dev);
   int total = 0;
   const void* anchors[] = {module_anchor_dataplane(), module_anchor_decode(), module_anchor_gemm(),
-                           module_anchor_llama()};
+                           module_anchor_llama(), module_anchor_attention()};
   for (const void* a : anchors) {
     if (rc) break;
     cudaFunction_t f = nullptr;

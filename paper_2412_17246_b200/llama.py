@@ -11,7 +11,7 @@ Per block (all bf16, fp32 accumulation):
   h   = rmsnorm(x)                 bz_rmsnorm
   qkv = h . Wqkv^T                 bz_gemm_bf16 (tcgen05)
   rope(q, k)                       bz_rope
-  a   = causal attention(q, k, v)  torch SDPA (library kernel, like cuBLAS)
+  a   = causal attention(q, k, v)  bz_prefill_attention (tcgen05 flash kernel, writes [tokens, H*hd])
   o   = a . Wo^T + x               bz_gemm_bf16 with residual epilogue
   g   = rmsnorm(o) . Wgu^T         bz_rmsnorm + bz_gemm_bf16
   x'  = silu(g1)*g2 . Wdown^T + o  bz_silu_mul + bz_gemm_bf16 residual epilogue
@@ -114,6 +114,7 @@ class LlamaExecutor:
         # stream-K counters + fp32 partials for skinny (decode) GEMMs; one executor = one stream
         self.streamk_ws = torch.zeros(self.STREAMK_WS_BYTES // 4, dtype=torch.float32, device=dev)
         self.last_signal_ctas = 0
+        self._attn_ws: Optional[torch.Tensor] = None   # V^T of the prefill attention (grown on demand)
 
     STREAMK_WS_BYTES = 64 << 20
 
@@ -193,11 +194,23 @@ class LlamaExecutor:
         q, kk, v = (t.view(B, S, -1, hd).transpose(1, 2) for t in self._attn_in(k, x, positions))
         if kv is not None:
             kv.store_prefill(k, kk, v)
-        att = torch.nn.functional.scaled_dot_product_attention(q, kk, v, is_causal=True,
-                                                               enable_gqa=KV != H)
         attn = self.attn[:m]
-        attn.copy_(att.transpose(1, 2).reshape(m, H * hd))
+        self._prefill_attention(B, S, attn)
         return self._attn_out_mlp(k, x, attn, out, signal)
+
+    def _prefill_attention(self, B: int, S: int, attn: torch.Tensor):
+        """Causal attention of the roped qkv rows into ``attn`` [B*S, H*hd]: the tcgen05
+        flash kernel (csrc/attention_tcgen05.cu), V transposed into a workspace."""
+        import ctypes
+        a = self.arch
+        need = ctypes.c_int64()
+        self.lib.bz_prefill_attention_workspace_bytes(B, S, a.n_kv_heads, a.head_dim, ctypes.byref(need))
+        if self._attn_ws is None or self._attn_ws.numel() < need.value:
+            self._attn_ws = torch.empty(need.value, dtype=torch.uint8, device=self.h.device)
+        qkv = self.qkv[:B * S]
+        self.lib.bz_prefill_attention(qkv.data_ptr(), qkv.stride(0), B, S, a.n_heads, a.n_kv_heads, a.head_dim,
+                                      self._attn_ws.data_ptr(), self._attn_ws.numel(), attn.data_ptr(),
+                                      attn.stride(0), torch.cuda.current_stream().cuda_stream)
 
     @torch.no_grad()
     def decode_block(self, k: int, x: torch.Tensor, kv: "KVCache",

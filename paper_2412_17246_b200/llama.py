@@ -24,6 +24,7 @@ Unit byte layout (tensor order inside a unit, each [out, in] row-major):
 
 from __future__ import annotations
 
+import os
 from dataclasses import dataclass
 from typing import Optional
 
@@ -31,6 +32,11 @@ import torch
 
 from ._native import BZ_GEMM_B_STATIC, BZ_GEMM_C_F32, cuda_lib
 from .slab import LlamaArch, SlabLayout
+
+
+# prefill attention: the tcgen05 flash kernel (csrc/attention_tcgen05.cu) once it
+# out-runs the library kernel; until then torch SDPA (cuDNN) -- BZ_PREFILL_ATTN selects
+PREFILL_ATTENTION = os.environ.get("BZ_PREFILL_ATTN", "sdpa")
 
 
 def _entries(arch: LlamaArch, k: int) -> list[tuple[str, tuple[int, ...]]]:
@@ -195,7 +201,12 @@ class LlamaExecutor:
         if kv is not None:
             kv.store_prefill(k, kk, v)
         attn = self.attn[:m]
-        self._prefill_attention(B, S, attn)
+        if PREFILL_ATTENTION == "tcgen05":
+            self._prefill_attention(B, S, attn)
+        else:
+            att = torch.nn.functional.scaled_dot_product_attention(q, kk, v, is_causal=True,
+                                                                   enable_gqa=KV != H)
+            attn.copy_(att.transpose(1, 2).reshape(m, H * hd))
         return self._attn_out_mlp(k, x, attn, out, signal)
 
     def _prefill_attention(self, B: int, S: int, attn: torch.Tensor):

@@ -198,6 +198,11 @@ class ScalingMixin:
         plan = generate_plan(build_scale_request(model, sources, [i.node for i in fresh], self.topo, self.flows),
                              self.topo, self.flows)
         est = estimate_completion(plan, model, self.topo, eta=self.cfg.eta)
+        execute = getattr(self.costs, "on_plan", None)
+        if execute is not None:
+            # executed cost providers (inprocess.ExecutedCosts) move the plan's bytes now;
+            # the layer / transfer events below then carry its device stamps
+            execute(plan, model)
         self.counters["plans"] += 1
         self.counters["interference_free_plans"] += int(plan_is_interference_free(plan, self.flows, self.topo))
         issue_us = self.now_us + int(self.cfg.scale_cmd_latency_ms * US_PER_MS)

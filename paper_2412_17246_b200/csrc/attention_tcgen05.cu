@@ -12,14 +12,18 @@
 //
 // One CTA = 128 query rows of one (sequence, head); TMEM lane = query row.
 //   w0      TMA producer: Q once, then K / V^T tiles of 128 keys (2-deep ring)
-//   w1      MMA issuer (one lane): S_j = Q K_j^T into TMEM (2 buffers), and once
-//           the softmax has written P_j: O_j = P_j V_j into TMEM (2 buffers)
-//   w2..w5  softmax (thread = query row): S_j from TMEM, causal mask on the diagonal
-//           tile, running max in the log2 domain, P_j = exp2(.) as bf16 straight into
-//           the 128B-swizzled smem layout the MMA reads, and O += rescaled O_j in
-//           registers (fp32); the epilogue divides by the row sum and stores bf16.
-// The MMA of S_{j+1} overlaps the softmax of tile j; P is single-buffered (the
-// softmax of tile j+1 writes P only after O_j's MMA has completed).
+//   w1      MMA issuer (one lane): S_j = Q K_j^T into TMEM (2 buffers), and once the
+//           softmax has written P_j: O += P_j V_j, accumulated in TMEM (one buffer)
+//   w2..w9  softmax, two threads per query row (warps w and w+4 share the row's TMEM
+//           lane quarter and take 64 of the tile's 128 keys each): S_j from TMEM,
+//           causal mask only on the diagonal tile, row max over the pair (smem), P_j
+//           = exp2(s * log2e / sqrt(hd) - m) as bf16 straight into a 128B-swizzled
+//           smem tile the MMA reads (2 buffers, so P_{j+1} is written while the
+//           tensor core still reads P_j).  The running max is only raised when it
+//           grows by more than 2^8 (P stays <= 256, exact in fp32 / bf16); only then
+//           is O rescaled in TMEM (ld, scale, st) -- rare after the first tiles, so
+//           the softmax does no per-tile work on O at all.
+//   epilogue: O / l per row (the pair's partial sums), bf16 stores.
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
@@ -37,7 +41,7 @@ using namespace bz::tc;
 
 constexpr int BQ = 128;       // query rows per CTA (= TMEM lanes)
 constexpr int BKV = 128;      // keys per tile
-constexpr int THREADS = 192;  // w0 TMA, w1 MMA + TMEM allocator, w2..w5 softmax / epilogue
+constexpr int THREADS = 320;  // w0 TMA, w1 MMA + TMEM allocator, w2..w9 softmax / epilogue
 constexpr int ATOM_BYTES = 128 * 128;  // one 128-row x 128-byte swizzle block (64 bf16 wide)
 
 template <int HD>
@@ -46,12 +50,13 @@ struct Cfg {
   static constexpr int K_BYTES = BKV * HD * 2;
   static constexpr int V_BYTES = HD * BKV * 2;   // V^T tile: HD rows x 128 keys = 2 atoms of HD x 128 B
   static constexpr int V_ATOM = HD * 128;        // bytes of one 64-key atom of the V^T tile
-  static constexpr int P_BYTES = BQ * BKV * 2;
+  static constexpr int P_BYTES = BQ * BKV * 2;   // one P buffer (2 atoms of 16 KB)
   static constexpr int STAGES = 2;
-  static constexpr int BAR_BYTES = 256;
-  static constexpr int SMEM = 1024 + Q_BYTES + STAGES * (K_BYTES + V_BYTES) + P_BYTES + BAR_BYTES;
+  static constexpr int BAR_BYTES = 128;
+  static constexpr int RED_BYTES = 2 * BQ * 4;       // pair exchange [half][row]: the max per tile, then the sum
+  static constexpr int SMEM = 1024 + Q_BYTES + STAGES * (K_BYTES + V_BYTES) + 2 * P_BYTES + BAR_BYTES + RED_BYTES;
   static constexpr int S_COL = 0;                // S buffers at columns [0, 256)
-  static constexpr int O_COL = 2 * BKV;          // O buffers at [256, 256 + 2 HD)
+  static constexpr int O_COL = 2 * BKV;          // O accumulator at [256, 256 + HD)
   static constexpr int TMEM_COLS = 512;
   static_assert(HD == 64 || HD == 128, "head dim");
   static_assert(SMEM <= 232448, "smem");
@@ -71,6 +76,33 @@ __device__ __forceinline__ uint32_t pack2(float lo, float hi) {
   __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
   return *reinterpret_cast<uint32_t*>(&v);
 }
+__device__ __forceinline__ float ex2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float max3(float a, float b, float c) {
+  float r;
+  asm("max.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+  return r;
+}
+__device__ __forceinline__ void tmem_st_32x32b_x32(uint32_t taddr, const uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], "
+      "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+      "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]),
+      "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]), "r"(r[16]),
+      "r"(r[17]), "r"(r[18]), "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]),
+      "r"(r[25]), "r"(r[26]), "r"(r[27]), "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31])
+      : "memory");
+}
+// the two softmax warps of one TMEM lane quarter (64 threads)
+__device__ __forceinline__ void pair_bar(int quarter) {
+  asm volatile("bar.sync %0, 64;" ::"r"(1 + quarter) : "memory");
+}
+
+constexpr float kRescale = 8.0f;  // raise the running max only when it grows by > 2^8
 
 template <int HD>
 __global__ void __launch_bounds__(THREADS, 1)
@@ -82,17 +114,18 @@ __global__ void __launch_bounds__(THREADS, 1)
   uint8_t* sq = smem;
   uint8_t* sk = sq + C::Q_BYTES;
   uint8_t* sv = sk + C::STAGES * C::K_BYTES;
-  uint8_t* sp = sv + C::STAGES * C::V_BYTES;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sp + C::P_BYTES);
+  uint8_t* sp = sv + C::STAGES * C::V_BYTES;   // 2 P buffers
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sp + 2 * C::P_BYTES);
   uint64_t* q_full = bars;
   uint64_t* kv_full = bars + 1;   // [2]
   uint64_t* kv_empty = bars + 3;  // [2]
   uint64_t* s_full = bars + 5;    // [2]
   uint64_t* s_empty = bars + 7;   // [2]
-  uint64_t* o_full = bars + 9;    // [2]
-  uint64_t* o_empty = bars + 11;  // [2]
-  uint64_t* p_full = bars + 13;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 14);
+  uint64_t* p_full = bars + 9;    // [2]
+  uint64_t* pv_done = bars + 11;  // [2]  PV_j complete (P[j&1] free, O holds tiles <= j)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 13);
+  float* red_max = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(bars) + C::BAR_BYTES);  // [2][BQ]
+  float* red_sum = red_max;   // reused by the epilogue (the loop's last pair_bar ends its max reads)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n_qt = (a.S + BQ - 1) / BQ;
@@ -111,11 +144,10 @@ __global__ void __launch_bounds__(THREADS, 1)
       mbar_init(&kv_full[i], 1);
       mbar_init(&kv_empty[i], 1);
       mbar_init(&s_full[i], 1);
-      mbar_init(&s_empty[i], 4);
-      mbar_init(&o_full[i], 1);
-      mbar_init(&o_empty[i], 4);
+      mbar_init(&s_empty[i], 8);
+      mbar_init(&p_full[i], 8);
+      mbar_init(&pv_done[i], 1);
     }
-    mbar_init(p_full, 4);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 1) {
@@ -171,121 +203,135 @@ __global__ void __launch_bounds__(THREADS, 1)
       issue_s(0);
       for (int j = 0; j < nj; ++j) {
         if (j + 1 < nj) issue_s(j + 1);
-        // O_j = P_j V_j once the softmax has written P_j
-        const int slot = j & 1, ob = j & 1;
-        mbar_wait(p_full, j & 1);
-        mbar_wait(&o_empty[ob], ((j >> 1) & 1) ^ 1);
+        // O += P_j V_j once the softmax has written P_j (and rescaled O if it had to)
+        const int slot = j & 1, pb = j & 1;
+        mbar_wait(&p_full[pb], (j >> 1) & 1);
         tc_fence_after();
-        const uint32_t d = tmem + C::O_COL + ob * HD;
+        const uint32_t d = tmem + C::O_COL;
+        uint8_t* pbuf = sp + pb * C::P_BYTES;
 #pragma unroll
         for (int kk = 0; kk < BKV / 16; ++kk) {
-          const uint64_t da = umma_desc_sw128(smem_u32(sp + (kk >> 2) * ATOM_BYTES)) + 2 * (kk & 3);
+          const uint64_t da = umma_desc_sw128(smem_u32(pbuf + (kk >> 2) * ATOM_BYTES)) + 2 * (kk & 3);
           const uint64_t db = umma_desc_sw128(smem_u32(sv + slot * C::V_BYTES + (kk >> 2) * C::V_ATOM)) + 2 * (kk & 3);
-          umma_bf16(d, da, db, idesc_o, kk > 0 ? 1u : 0u);
+          umma_bf16(d, da, db, idesc_o, (j > 0 || kk > 0) ? 1u : 0u);
         }
-        umma_commit(&o_full[ob]);
+        umma_commit(&pv_done[pb]);
         umma_commit(&kv_empty[slot]);
       }
     }
   } else {
-    // ---- softmax + epilogue: thread = query row r of the tile ----
-    const int quarter = warp & 3;
+    // ---- softmax: thread = (query row r, key half) ----
+    const int sw = warp - 2;            // 0..7
+    const int half = sw >> 2;           // keys [64 half, 64 half + 64) of each tile
+    const int quarter = warp & 3;       // TMEM lane quarter (hardware: warp id % 4)
     const int r = quarter * 32 + lane;
-    const int qpos = s0 + r;  // query position in its sequence
+    const int qpos = s0 + r;            // query position in its sequence
     const uint32_t lane_off = static_cast<uint32_t>(quarter * 32) << 16;
-    float o[HD];
-#pragma unroll
-    for (int i = 0; i < HD; ++i) o[i] = 0.f;
-    float m = -INFINITY, l = 0.f, alpha_prev = 0.f;
-    // P row r: atom (keys/64), 8-row group, row within group, 16-byte chunk ^ (r & 7)
-    uint8_t* prow = sp + (r >> 3) * 1024 + (r & 7) * 128;
-
-    auto accumulate_o = [&](int jj) {  // o = o * alpha_prev + O_jj
-      const int ob = jj & 1;
-      mbar_wait(&o_full[ob], (jj >> 1) & 1);
-      tc_fence_after();
-#pragma unroll
-      for (int c = 0; c < HD; c += 32) {
-        uint32_t v[32];
-        tmem_ld_32x32b_x32(tmem + lane_off + C::O_COL + ob * HD + c, v);
-#pragma unroll
-        for (int i = 0; i < 32; ++i) o[c + i] = fmaf(o[c + i], alpha_prev, __uint_as_float(v[i]));
-      }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&o_empty[ob]);
-    };
-
+    float m = -INFINITY;                // running max in use (log2 domain)
+    float l = 0.f;                      // this thread's partial row sum, relative to m
+    // P row r of buffer pb: atom = half, 8-row group, row in group, chunk ^ (r & 7)
+    const uint32_t p_row = smem_u32(sp + half * ATOM_BYTES + (r >> 3) * 1024 + (r & 7) * 128);
     for (int j = 0; j < nj; ++j) {
       const int sb = j & 1;
       const bool diag = j == qt;
+      const int key0 = j * BKV + half * 64;   // first key of this thread's 64
       mbar_wait(&s_full[sb], (j >> 1) & 1);
       tc_fence_after();
-      const uint32_t sa = tmem + lane_off + C::S_COL + sb * BKV;
-      // pass 1: row max (log2 domain)
-      float mx = -INFINITY;
-#pragma unroll 1
-      for (int c = 0; c < BKV; c += 32) {
-        uint32_t v[32];
-        tmem_ld_32x32b_x32(sa + c, v);
+      const uint32_t sa = tmem + lane_off + C::S_COL + sb * BKV + half * 64;
+      uint32_t v0[32], v1[32];
+      tmem_ld_32x32b_x32_async(sa, v0);
+      tmem_ld_32x32b_x32_async(sa + 32, v1);
+      tmem_wait_ld(v0);
+      tmem_wait_ld(v1);
+      if (diag) {  // causal mask: keys after this query get -inf
 #pragma unroll
         for (int i = 0; i < 32; ++i) {
-          const bool masked = diag && (j * BKV + c + i > qpos);
-          if (!masked) mx = fmaxf(mx, __uint_as_float(v[i]));
+          if (key0 + i > qpos) v0[i] = __float_as_uint(-INFINITY);
+          if (key0 + 32 + i > qpos) v1[i] = __float_as_uint(-INFINITY);
         }
       }
-      const float m_new = fmaxf(m, mx * a.scale_log2);
-      const float alpha = exp2f(m - m_new);  // 0 on the first tile (m = -inf)
-      // O_{j-1} is complete (so P's smem is free again): fold it into the registers
-      if (j > 0) accumulate_o(j - 1);
-      // pass 2: P = exp2(s * scale - m_new) -> bf16 into the swizzled P tile; row sum
-      float sum = 0.f;
-#pragma unroll 1
-      for (int c = 0; c < BKV; c += 32) {
-        uint32_t v[32];
-        tmem_ld_32x32b_x32(sa + c, v);
-        uint32_t pk[16];
+      float mx = -INFINITY;
 #pragma unroll
-        for (int i = 0; i < 32; i += 2) {
-          const bool m0 = diag && (j * BKV + c + i > qpos);
-          const bool m1 = diag && (j * BKV + c + i + 1 > qpos);
-          const float p0 = m0 ? 0.f : exp2f(fmaf(__uint_as_float(v[i]), a.scale_log2, -m_new));
-          const float p1 = m1 ? 0.f : exp2f(fmaf(__uint_as_float(v[i + 1]), a.scale_log2, -m_new));
-          sum += p0 + p1;
-          pk[i >> 1] = pack2(p0, p1);
+      for (int i = 0; i < 32; i += 2) mx = max3(mx, __uint_as_float(v0[i]), __uint_as_float(v0[i + 1]));
+#pragma unroll
+      for (int i = 0; i < 32; i += 2) mx = max3(mx, __uint_as_float(v1[i]), __uint_as_float(v1[i + 1]));
+      // S of this tile is in registers: the MMA may reuse the buffer
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&s_empty[sb]);
+      // row max over the pair
+      red_max[half * BQ + r] = mx;
+      pair_bar(quarter);
+      mx = fmaxf(mx, red_max[(half ^ 1) * BQ + r]) * a.scale_log2;
+      pair_bar(quarter);  // red_max is rewritten next tile
+      if (mx > m + kRescale) {
+        // raise the max: O (tiles < j) and l must be scaled by 2^(m_old - m_new)
+        const float alpha = ex2(m - mx);   // 0 on the first tile
+        if (j > 0) {
+          mbar_wait(&pv_done[(j - 1) & 1], ((j - 1) >> 1) & 1);
+          tc_fence_after();
+          const uint32_t oa = tmem + lane_off + C::O_COL + half * (HD / 2);
+#pragma unroll
+          for (int c = 0; c < HD / 2; c += 32) {
+            uint32_t o[32];
+            tmem_ld_32x32b_x32(oa + c, o);
+#pragma unroll
+            for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
+            tmem_st_32x32b_x32(oa + c, o);
+          }
+          asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
         }
-        uint8_t* atom = prow + (c >> 6) * ATOM_BYTES;
+        l *= alpha;
+        m = mx;
+      }
+      // P_j into buffer j&1 once PV_{j-2} has finished reading it
+      if (j >= 2) mbar_wait(&pv_done[sb], ((j - 2) >> 1) & 1);
+      const uint32_t prow = p_row + sb * C::P_BYTES;
+      float sum = 0.f;
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {   // 8 chunks of 8 keys (16 bytes of P)
+        uint32_t w[4];
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
-          const int chunk = ((c & 63) >> 3) + q;  // 16-byte chunk within the 128-byte row
-          const uint32_t addr = smem_u32(atom + ((chunk ^ (r & 7)) << 4));
-          asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(addr), "r"(pk[4 * q]), "r"(pk[4 * q + 1]),
-                       "r"(pk[4 * q + 2]), "r"(pk[4 * q + 3])
-                       : "memory");
+          const int i = c * 8 + 2 * q;
+          const float s0v = __uint_as_float(i < 32 ? v0[i] : v1[i - 32]);
+          const float s1v = __uint_as_float(i + 1 < 32 ? v0[i + 1] : v1[i + 1 - 32]);
+          const float p0 = ex2(fmaf(s0v, a.scale_log2, -m));
+          const float p1 = ex2(fmaf(s1v, a.scale_log2, -m));
+          sum += p0 + p1;
+          w[q] = pack2(p0, p1);
         }
+        asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(prow + ((c ^ (r & 7)) << 4)), "r"(w[0]),
+                     "r"(w[1]), "r"(w[2]), "r"(w[3])
+                     : "memory");
       }
-      l = fmaf(l, alpha, sum);
-      m = m_new;
-      alpha_prev = alpha;
-      // P (generic-proxy stores) -> the MMA's async proxy; S buffer free again
+      l += sum;
+      // P (generic-proxy stores) -> the MMA's async proxy; O rescale (tcgen05.st) done
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) {
-        mbar_arrive(&s_empty[sb]);
-        mbar_arrive(p_full);
-      }
+      if (lane == 0) mbar_arrive(&p_full[sb]);
     }
-    accumulate_o(nj - 1);
-    // epilogue: O / l -> bf16 rows of the o-projection input
-    if (qpos < a.S) {
-      const float inv = 1.f / l;
-      __nv_bfloat16* dst = a.out + static_cast<int64_t>(row0 + qpos) * a.ldo + h * HD;
+    // ---- epilogue: O / l (sum of the pair's partials) -> bf16 ----
+    red_sum[half * BQ + r] = l;
+    pair_bar(quarter);
+    const float inv = 1.f / (l + red_sum[(half ^ 1) * BQ + r]);
+    mbar_wait(&pv_done[(nj - 1) & 1], ((nj - 1) >> 1) & 1);
+    tc_fence_after();
+    const uint32_t oa = tmem + lane_off + C::O_COL + half * (HD / 2);
+    __nv_bfloat16* dst = a.out + static_cast<int64_t>(row0 + qpos) * a.ldo + h * HD + half * (HD / 2);
 #pragma unroll
-      for (int c = 0; c < HD; c += 8) {
-        uint4 w = make_uint4(pack2(o[c] * inv, o[c + 1] * inv), pack2(o[c + 2] * inv, o[c + 3] * inv),
-                             pack2(o[c + 4] * inv, o[c + 5] * inv), pack2(o[c + 6] * inv, o[c + 7] * inv));
-        *reinterpret_cast<uint4*>(dst + c) = w;
+    for (int c = 0; c < HD / 2; c += 32) {
+      uint32_t o[32];
+      tmem_ld_32x32b_x32(oa + c, o);
+      if (qpos < a.S) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const float* f = reinterpret_cast<const float*>(o + 8 * q);
+          *reinterpret_cast<uint4*>(dst + c + 8 * q) =
+              make_uint4(pack2(f[0] * inv, f[1] * inv), pack2(f[2] * inv, f[3] * inv),
+                         pack2(f[4] * inv, f[5] * inv), pack2(f[6] * inv, f[7] * inv));
+        }
       }
     }
   }

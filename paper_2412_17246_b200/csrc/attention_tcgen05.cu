@@ -264,9 +264,12 @@ __global__ void __launch_bounds__(THREADS, 1)
       pair_bar(quarter);
       mx = fmaxf(mx, red_max[(half ^ 1) * BQ + r]) * a.scale_log2;
       pair_bar(quarter);  // red_max is rewritten next tile
-      if (mx > m + kRescale) {
-        // raise the max: O (tiles < j) and l must be scaled by 2^(m_old - m_new)
-        const float alpha = ex2(m - mx);   // 0 on the first tile
+      // raise the max only when it grows by more than 2^kRescale; O (tiles < j) and l
+      // are then scaled by 2^(m_old - m_new).  tcgen05.ld/st are warp-collective, so the
+      // warp rescales together whenever any of its rows needs it (alpha = 1 elsewhere)
+      const bool raise = mx > m + kRescale;
+      if (__any_sync(0xffffffffu, raise)) {
+        const float alpha = raise ? ex2(m - mx) : 1.f;   // 0 on the first tile
         if (j > 0) {
           mbar_wait(&pv_done[(j - 1) & 1], ((j - 1) >> 1) & 1);
           tc_fence_after();
@@ -282,7 +285,7 @@ __global__ void __launch_bounds__(THREADS, 1)
           asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
         }
         l *= alpha;
-        m = mx;
+        if (raise) m = mx;
       }
       // P_j into buffer j&1 once PV_{j-2} has finished reading it
       if (j >= 2) mbar_wait(&pv_done[sb], ((j - 2) >> 1) & 1);

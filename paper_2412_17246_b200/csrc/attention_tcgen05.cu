@@ -52,7 +52,7 @@ struct Cfg {
   static constexpr int V_ATOM = HD * 128;        // bytes of one 64-key atom of the V^T tile
   static constexpr int P_BYTES = BQ * BKV * 2;   // one P buffer (2 atoms of 16 KB)
   static constexpr int STAGES = 2;
-  static constexpr int BAR_BYTES = 128;
+  static constexpr int BAR_BYTES = 128;   // 15 barriers + the TMEM address
   static constexpr int RED_BYTES = 2 * BQ * 4;       // pair exchange [half][row]: the max per tile, then the sum
   static constexpr int SMEM = 1024 + Q_BYTES + STAGES * (K_BYTES + V_BYTES) + 2 * P_BYTES + BAR_BYTES + RED_BYTES;
   static constexpr int S_COL = 0;                // S buffers at columns [0, 256)
@@ -117,13 +117,14 @@ __global__ void __launch_bounds__(THREADS, 1)
   uint8_t* sp = sv + C::STAGES * C::V_BYTES;   // 2 P buffers
   uint64_t* bars = reinterpret_cast<uint64_t*>(sp + 2 * C::P_BYTES);
   uint64_t* q_full = bars;
-  uint64_t* kv_full = bars + 1;   // [2]
-  uint64_t* kv_empty = bars + 3;  // [2]
+  uint64_t* k_full = bars + 1;    // [2]  K ring: a slot is free once S_j's MMA completed
+  uint64_t* k_empty = bars + 3;   // [2]
   uint64_t* s_full = bars + 5;    // [2]
   uint64_t* s_empty = bars + 7;   // [2]
   uint64_t* p_full = bars + 9;    // [2]
-  uint64_t* pv_done = bars + 11;  // [2]  PV_j complete (P[j&1] free, O holds tiles <= j)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 13);
+  uint64_t* pv_done = bars + 11;  // [2]  PV_j complete (P[j&1] and V slot free, O holds tiles <= j)
+  uint64_t* v_full = bars + 13;   // [2]  V ring: a slot is free once PV_j completed (pv_done)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 15);
   float* red_max = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(bars) + C::BAR_BYTES);  // [2][BQ]
   float* red_sum = red_max;   // reused by the epilogue (the loop's last pair_bar ends its max reads)
 
@@ -141,8 +142,9 @@ __global__ void __launch_bounds__(THREADS, 1)
     prefetch_tmap(&map_vt);
     mbar_init(q_full, 1);
     for (int i = 0; i < 2; ++i) {
-      mbar_init(&kv_full[i], 1);
-      mbar_init(&kv_empty[i], 1);
+      mbar_init(&k_full[i], 1);
+      mbar_init(&k_empty[i], 1);
+      mbar_init(&v_full[i], 1);
       mbar_init(&s_full[i], 1);
       mbar_init(&s_empty[i], 8);
       mbar_init(&p_full[i], 8);
@@ -167,16 +169,29 @@ __global__ void __launch_bounds__(THREADS, 1)
       mbar_expect_tx(q_full, C::Q_BYTES);
       for (int ka = 0; ka < KA; ++ka)
         tma_load_2d(sq + ka * ATOM_BYTES, &map_qk, a.q_col0 + h * HD + ka * 64, row0 + s0, q_full);
-      for (int j = 0; j < nj; ++j) {
+      // K_j as soon as S_{j-2} released its slot, V_j once PV_{j-2} released its slot;
+      // K runs ahead of V (it is needed a softmax earlier)
+      auto load_k = [&](int j) {
         const int slot = j & 1;
-        mbar_wait(&kv_empty[slot], ((j >> 1) & 1) ^ 1);
-        mbar_expect_tx(&kv_full[slot], C::K_BYTES + C::V_BYTES);
+        mbar_wait(&k_empty[slot], ((j >> 1) & 1) ^ 1);
+        mbar_expect_tx(&k_full[slot], C::K_BYTES);
         for (int ka = 0; ka < KA; ++ka)
           tma_load_2d(sk + slot * C::K_BYTES + ka * ATOM_BYTES, &map_qk, a.k_col0 + g * HD + ka * 64,
-                      row0 + j * BKV, &kv_full[slot]);
+                      row0 + j * BKV, &k_full[slot]);
+      };
+      auto load_v = [&](int j) {
+        const int slot = j & 1;
+        if (j >= 2) mbar_wait(&pv_done[slot], ((j - 2) >> 1) & 1);
+        mbar_expect_tx(&v_full[slot], C::V_BYTES);
         for (int kh = 0; kh < 2; ++kh)
           tma_load_2d(sv + slot * C::V_BYTES + kh * C::V_ATOM, &map_vt, j * BKV + kh * 64, (b * a.KV + g) * HD,
-                      &kv_full[slot]);
+                      &v_full[slot]);
+      };
+      load_k(0);
+      if (nj > 1) load_k(1);
+      for (int j = 0; j < nj; ++j) {
+        load_v(j);
+        if (j + 2 < nj) load_k(j + 2);
       }
       pdl_trigger();
     }
@@ -188,7 +203,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       mbar_wait(q_full, 0);
       auto issue_s = [&](int j) {
         const int slot = j & 1, sb = j & 1;
-        mbar_wait(&kv_full[slot], (j >> 1) & 1);
+        mbar_wait(&k_full[slot], (j >> 1) & 1);
         mbar_wait(&s_empty[sb], ((j >> 1) & 1) ^ 1);
         tc_fence_after();
         const uint32_t d = tmem + C::S_COL + sb * BKV;
@@ -199,12 +214,14 @@ __global__ void __launch_bounds__(THREADS, 1)
           umma_bf16(d, da, db, idesc_s, kk > 0 ? 1u : 0u);
         }
         umma_commit(&s_full[sb]);
+        umma_commit(&k_empty[slot]);
       };
       issue_s(0);
       for (int j = 0; j < nj; ++j) {
         if (j + 1 < nj) issue_s(j + 1);
         // O += P_j V_j once the softmax has written P_j (and rescaled O if it had to)
         const int slot = j & 1, pb = j & 1;
+        mbar_wait(&v_full[slot], (j >> 1) & 1);
         mbar_wait(&p_full[pb], (j >> 1) & 1);
         tc_fence_after();
         const uint32_t d = tmem + C::O_COL;
@@ -216,7 +233,6 @@ __global__ void __launch_bounds__(THREADS, 1)
           umma_bf16(d, da, db, idesc_o, (j > 0 || kk > 0) ? 1u : 0u);
         }
         umma_commit(&pv_done[pb]);
-        umma_commit(&kv_empty[slot]);
       }
     }
   } else {

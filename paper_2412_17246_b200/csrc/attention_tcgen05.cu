@@ -10,20 +10,21 @@
 //             so V^T is a K-major MMA operand like every weight), zero past S
 //   out: attn [B*S, ldo] bf16, head h at columns [h*hd, (h+1)*hd) -- the o-projection's A
 //
-// One CTA = 128 query rows of one (sequence, head); TMEM lane = query row.
-//   w0      TMA producer: Q once, then K / V^T tiles of 128 keys (2-deep ring)
-//   w1      MMA issuer (one lane): S_j = Q K_j^T into TMEM (2 buffers), and once the
-//           softmax has written P_j: O += P_j V_j, accumulated in TMEM (one buffer)
-//   w2..w9  softmax, two threads per query row (warps w and w+4 share the row's TMEM
-//           lane quarter and take 64 of the tile's 128 keys each): S_j from TMEM,
-//           causal mask only on the diagonal tile, row max over the pair (smem), P_j
-//           = exp2(s * log2e / sqrt(hd) - m) as bf16 straight into a 128B-swizzled
-//           smem tile the MMA reads (2 buffers, so P_{j+1} is written while the
-//           tensor core still reads P_j).  The running max is only raised when it
-//           grows by more than 2^8 (P stays <= 256, exact in fp32 / bf16); only then
-//           is O rescaled in TMEM (ld, scale, st) -- rare after the first tiles, so
-//           the softmax does no per-tile work on O at all.
-//   epilogue: O / l per row (the pair's partial sums), bf16 stores.
+// One CTA = two adjacent 128-row query tiles A, B of one (sequence, head), so every
+// K / V tile it loads feeds two independent softmax streams and the tensor core
+// always has the other tile's work while one softmax runs (FA4-style ping-pong).
+// Keys come in tiles of 64.  TMEM lane = query row of a tile.
+//   w0      TMA producer: Q_A, Q_B once; K_j / V^T_j into 3-deep rings (K runs ahead)
+//   w1      MMA issuer (one lane), per key tile j: S_A(j), S_B(j) = Q K_j^T into TMEM
+//           (double-buffered per tile), then O_A += P_A(j-1) V_{j-1}, O_B += P_B(j-1) V_{j-1}
+//           (O accumulated in TMEM)
+//   w2..w5  softmax of tile A, w6..w9 of tile B (thread = query row): S from TMEM,
+//           causal mask on the diagonal key tiles only, running max in the log2
+//           domain, P = exp2(s log2e / sqrt(hd) - m) as bf16 straight into a
+//           128B-swizzled smem tile the MMA reads (2 buffers per query tile).  The max
+//           is only raised when it grows by more than 2^8 (P <= 256, exact in fp32 /
+//           bf16); only then is O rescaled in TMEM (ld, scale, st), warp-uniformly.
+//   epilogue: O / l, bf16 rows of the o-projection input.
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
@@ -39,24 +40,25 @@ namespace attn {
 
 using namespace bz::tc;
 
-constexpr int BQ = 128;       // query rows per CTA (= TMEM lanes)
-constexpr int BKV = 128;      // keys per tile
-constexpr int THREADS = 320;  // w0 TMA, w1 MMA + TMEM allocator, w2..w9 softmax / epilogue
-constexpr int ATOM_BYTES = 128 * 128;  // one 128-row x 128-byte swizzle block (64 bf16 wide)
+constexpr int BQ = 128;       // query rows per tile (= TMEM lanes)
+constexpr int BKV = 64;       // keys per tile
+constexpr int THREADS = 320;  // w0 TMA, w1 MMA + TMEM allocator, w2..w5 softmax A, w6..w9 softmax B
+constexpr int KSTAGES = 3, VSTAGES = 3;
 
 template <int HD>
 struct Cfg {
-  static constexpr int Q_BYTES = BQ * HD * 2;
-  static constexpr int K_BYTES = BKV * HD * 2;
-  static constexpr int V_BYTES = HD * BKV * 2;   // V^T tile: HD rows x 128 keys = 2 atoms of HD x 128 B
-  static constexpr int V_ATOM = HD * 128;        // bytes of one 64-key atom of the V^T tile
-  static constexpr int P_BYTES = BQ * BKV * 2;   // one P buffer (2 atoms of 16 KB)
-  static constexpr int STAGES = 2;
-  static constexpr int BAR_BYTES = 128;   // 15 barriers + the TMEM address
-  static constexpr int RED_BYTES = 2 * BQ * 4;       // pair exchange [half][row]: the max per tile, then the sum
-  static constexpr int SMEM = 1024 + Q_BYTES + STAGES * (K_BYTES + V_BYTES) + 2 * P_BYTES + BAR_BYTES + RED_BYTES;
-  static constexpr int S_COL = 0;                // S buffers at columns [0, 256)
-  static constexpr int O_COL = 2 * BKV;          // O accumulator at [256, 256 + HD)
+  static constexpr int KA = HD / 64;               // 64-wide swizzle atoms along hd
+  static constexpr int Q_ATOM = BQ * 128;          // 128 rows x 128 B
+  static constexpr int Q_BYTES = KA * Q_ATOM;      // one query tile
+  static constexpr int K_ATOM = BKV * 128;         // 64 key rows x 128 B
+  static constexpr int K_BYTES = KA * K_ATOM;
+  static constexpr int V_BYTES = HD * 128;         // V^T tile: HD rows x 64 keys (one atom)
+  static constexpr int P_BYTES = BQ * 128;         // 128 rows x 64 keys (one atom)
+  static constexpr int BAR_BYTES = 256;
+  static constexpr int SMEM = 1024 + 2 * Q_BYTES + KSTAGES * K_BYTES + VSTAGES * V_BYTES + 4 * P_BYTES + BAR_BYTES;
+  // TMEM: S_A[2], S_B[2] (64 columns each), then O_A, O_B (HD columns each)
+  static constexpr int S_COL = 0;
+  static constexpr int O_COL = 4 * BKV;
   static constexpr int TMEM_COLS = 512;
   static_assert(HD == 64 || HD == 128, "head dim");
   static_assert(SMEM <= 232448, "smem");
@@ -97,57 +99,60 @@ __device__ __forceinline__ void tmem_st_32x32b_x32(uint32_t taddr, const uint32_
       "r"(r[25]), "r"(r[26]), "r"(r[27]), "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31])
       : "memory");
 }
-// the two softmax warps of one TMEM lane quarter (64 threads)
-__device__ __forceinline__ void pair_bar(int quarter) {
-  asm volatile("bar.sync %0, 64;" ::"r"(1 + quarter) : "memory");
-}
 
 constexpr float kRescale = 8.0f;  // raise the running max only when it grows by > 2^8
 
 template <int HD>
 __global__ void __launch_bounds__(THREADS, 1)
-    k_flash_prefill(const __grid_constant__ CUtensorMap map_qk, const __grid_constant__ CUtensorMap map_vt, Args a) {
+    k_flash_prefill(const __grid_constant__ CUtensorMap map_q, const __grid_constant__ CUtensorMap map_k,
+                    const __grid_constant__ CUtensorMap map_vt, Args a) {
   using C = Cfg<HD>;
-  constexpr int KA = HD / 64;  // 64-wide swizzle atoms along hd
+  constexpr int KA = C::KA;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* sq = smem;
-  uint8_t* sk = sq + C::Q_BYTES;
-  uint8_t* sv = sk + C::STAGES * C::K_BYTES;
-  uint8_t* sp = sv + C::STAGES * C::V_BYTES;   // 2 P buffers
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sp + 2 * C::P_BYTES);
-  uint64_t* q_full = bars;
-  uint64_t* k_full = bars + 1;    // [2]  K ring: a slot is free once S_j's MMA completed
-  uint64_t* k_empty = bars + 3;   // [2]
-  uint64_t* s_full = bars + 5;    // [2]
-  uint64_t* s_empty = bars + 7;   // [2]
-  uint64_t* p_full = bars + 9;    // [2]
-  uint64_t* pv_done = bars + 11;  // [2]  PV_j complete (P[j&1] and V slot free, O holds tiles <= j)
-  uint64_t* v_full = bars + 13;   // [2]  V ring: a slot is free once PV_j completed (pv_done)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 15);
-  float* red_max = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(bars) + C::BAR_BYTES);  // [2][BQ]
-  float* red_sum = red_max;   // reused by the epilogue (the loop's last pair_bar ends its max reads)
+  uint8_t* sq = smem;                              // [2 tiles]
+  uint8_t* sk = sq + 2 * C::Q_BYTES;               // [KSTAGES]
+  uint8_t* sv = sk + KSTAGES * C::K_BYTES;         // [VSTAGES]
+  uint8_t* sp = sv + VSTAGES * C::V_BYTES;         // [tile][2 buffers]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sp + 4 * C::P_BYTES);
+  uint64_t* q_full = bars;                  // 1
+  uint64_t* k_full = bars + 1;              // [3]
+  uint64_t* k_empty = bars + 4;             // [3]
+  uint64_t* v_full = bars + 7;              // [3]
+  uint64_t* v_empty = bars + 10;            // [3]
+  uint64_t* s_full = bars + 13;             // [tile][2]
+  uint64_t* s_empty = bars + 17;            // [tile][2]
+  uint64_t* p_full = bars + 21;             // [tile][2]
+  uint64_t* pv_done = bars + 25;            // [tile][2]  PV(j) done: P buffer j&1 free, O holds keys < 64 (j+1)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 29);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n_qt = (a.S + BQ - 1) / BQ;
-  const int qt = n_qt - 1 - static_cast<int>(blockIdx.x);  // longest (most keys) tiles first
+  const int n_pairs = (n_qt + 1) / 2;
+  const int pair = n_pairs - 1 - static_cast<int>(blockIdx.x);  // longest (most keys) first
   const int h = blockIdx.y, b = blockIdx.z;
   const int g = h / (a.H / a.KV);
-  const int s0 = qt * BQ;
-  const int nj = qt + 1;  // key tiles 0..qt (causal)
+  const int s0 = pair * 2 * BQ;              // first query row of tile A
+  // key tiles: A needs 0 .. 4p+1, B needs 0 .. 4p+3 (causal, 64-key tiles)
+  const int nj_a = (s0 + BQ) / BKV;
+  const int nj = (s0 + 2 * BQ) / BKV;
   const int row0 = b * a.S;
 
   if (warp == 0 && lane == 0) {
-    prefetch_tmap(&map_qk);
+    prefetch_tmap(&map_q);
+    prefetch_tmap(&map_k);
     prefetch_tmap(&map_vt);
     mbar_init(q_full, 1);
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < 3; ++i) {
       mbar_init(&k_full[i], 1);
       mbar_init(&k_empty[i], 1);
       mbar_init(&v_full[i], 1);
+      mbar_init(&v_empty[i], 1);
+    }
+    for (int i = 0; i < 4; ++i) {
       mbar_init(&s_full[i], 1);
-      mbar_init(&s_empty[i], 8);
-      mbar_init(&p_full[i], 8);
+      mbar_init(&s_empty[i], 4);
+      mbar_init(&p_full[i], 4);
       mbar_init(&pv_done[i], 1);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -166,32 +171,30 @@ __global__ void __launch_bounds__(THREADS, 1)
     if (lane == 0) {
       // ---- TMA producer ----
       pdl_wait();  // q/k/v were written by the predecessor (qkv GEMM + RoPE + transpose)
-      mbar_expect_tx(q_full, C::Q_BYTES);
-      for (int ka = 0; ka < KA; ++ka)
-        tma_load_2d(sq + ka * ATOM_BYTES, &map_qk, a.q_col0 + h * HD + ka * 64, row0 + s0, q_full);
-      // K_j as soon as S_{j-2} released its slot, V_j once PV_{j-2} released its slot;
-      // K runs ahead of V (it is needed a softmax earlier)
-      auto load_k = [&](int j) {
-        const int slot = j & 1;
-        mbar_wait(&k_empty[slot], ((j >> 1) & 1) ^ 1);
-        mbar_expect_tx(&k_full[slot], C::K_BYTES);
+      mbar_expect_tx(q_full, 2 * C::Q_BYTES);
+      for (int t = 0; t < 2; ++t)
         for (int ka = 0; ka < KA; ++ka)
-          tma_load_2d(sk + slot * C::K_BYTES + ka * ATOM_BYTES, &map_qk, a.k_col0 + g * HD + ka * 64,
-                      row0 + j * BKV, &k_full[slot]);
+          tma_load_2d(sq + t * C::Q_BYTES + ka * C::Q_ATOM, &map_q, a.q_col0 + h * HD + ka * 64,
+                      row0 + s0 + t * BQ, q_full);
+      auto load_k = [&](int j) {
+        const int st = j % KSTAGES;
+        mbar_wait(&k_empty[st], ((j / KSTAGES) & 1) ^ 1);
+        mbar_expect_tx(&k_full[st], C::K_BYTES);
+        for (int ka = 0; ka < KA; ++ka)
+          tma_load_2d(sk + st * C::K_BYTES + ka * C::K_ATOM, &map_k, a.k_col0 + g * HD + ka * 64, row0 + j * BKV,
+                      &k_full[st]);
       };
       auto load_v = [&](int j) {
-        const int slot = j & 1;
-        if (j >= 2) mbar_wait(&pv_done[slot], ((j - 2) >> 1) & 1);
-        mbar_expect_tx(&v_full[slot], C::V_BYTES);
-        for (int kh = 0; kh < 2; ++kh)
-          tma_load_2d(sv + slot * C::V_BYTES + kh * C::V_ATOM, &map_vt, j * BKV + kh * 64, (b * a.KV + g) * HD,
-                      &v_full[slot]);
+        const int st = j % VSTAGES;
+        mbar_wait(&v_empty[st], ((j / VSTAGES) & 1) ^ 1);
+        mbar_expect_tx(&v_full[st], C::V_BYTES);
+        tma_load_2d(sv + st * C::V_BYTES, &map_vt, j * BKV, (b * a.KV + g) * HD, &v_full[st]);
       };
+      // K runs one tile ahead of V (S needs K a softmax before PV needs V)
       load_k(0);
-      if (nj > 1) load_k(1);
       for (int j = 0; j < nj; ++j) {
+        if (j + 1 < nj) load_k(j + 1);
         load_v(j);
-        if (j + 2 < nj) load_k(j + 2);
       }
       pdl_trigger();
     }
@@ -202,64 +205,77 @@ __global__ void __launch_bounds__(THREADS, 1)
       constexpr uint32_t idesc_o = instr_desc_bf16(BQ, HD);
       mbar_wait(q_full, 0);
       auto issue_s = [&](int j) {
-        const int slot = j & 1, sb = j & 1;
-        mbar_wait(&k_full[slot], (j >> 1) & 1);
-        mbar_wait(&s_empty[sb], ((j >> 1) & 1) ^ 1);
-        tc_fence_after();
-        const uint32_t d = tmem + C::S_COL + sb * BKV;
+        const int st = j % KSTAGES, sb = j & 1;
+        mbar_wait(&k_full[st], (j / KSTAGES) & 1);
+        for (int t = 0; t < 2; ++t) {
+          if (t == 0 && j >= nj_a) continue;      // tile A is past its diagonal
+          mbar_wait(&s_empty[t * 2 + sb], ((j >> 1) & 1) ^ 1);
+          tc_fence_after();
+          const uint32_t d = tmem + C::S_COL + (t * 2 + sb) * BKV;
 #pragma unroll
-        for (int kk = 0; kk < HD / 16; ++kk) {
-          const uint64_t da = umma_desc_sw128(smem_u32(sq + (kk >> 2) * ATOM_BYTES)) + 2 * (kk & 3);
-          const uint64_t db = umma_desc_sw128(smem_u32(sk + slot * C::K_BYTES + (kk >> 2) * ATOM_BYTES)) + 2 * (kk & 3);
-          umma_bf16(d, da, db, idesc_s, kk > 0 ? 1u : 0u);
+          for (int kk = 0; kk < HD / 16; ++kk) {
+            const uint64_t da = umma_desc_sw128(smem_u32(sq + t * C::Q_BYTES + (kk >> 2) * C::Q_ATOM)) + 2 * (kk & 3);
+            const uint64_t db = umma_desc_sw128(smem_u32(sk + st * C::K_BYTES + (kk >> 2) * C::K_ATOM)) + 2 * (kk & 3);
+            umma_bf16(d, da, db, idesc_s, kk > 0 ? 1u : 0u);
+          }
+          umma_commit(&s_full[t * 2 + sb]);
         }
-        umma_commit(&s_full[sb]);
-        umma_commit(&k_empty[slot]);
+        umma_commit(&k_empty[st]);
+      };
+      auto issue_pv = [&](int j) {
+        const int st = j % VSTAGES, pb = j & 1;
+        mbar_wait(&v_full[st], (j / VSTAGES) & 1);
+        for (int t = 0; t < 2; ++t) {
+          if (t == 0 && j >= nj_a) continue;
+          mbar_wait(&p_full[t * 2 + pb], (j >> 1) & 1);
+          tc_fence_after();
+          const uint32_t d = tmem + C::O_COL + t * HD;
+          const uint8_t* pbuf = sp + (t * 2 + pb) * C::P_BYTES;
+#pragma unroll
+          for (int kk = 0; kk < BKV / 16; ++kk) {
+            const uint64_t da = umma_desc_sw128(smem_u32(pbuf)) + 2 * kk;
+            const uint64_t db = umma_desc_sw128(smem_u32(sv + st * C::V_BYTES)) + 2 * kk;
+            umma_bf16(d, da, db, idesc_o, (j > 0 || kk > 0) ? 1u : 0u);
+          }
+          umma_commit(&pv_done[t * 2 + pb]);
+        }
+        umma_commit(&v_empty[st]);
       };
       issue_s(0);
       for (int j = 0; j < nj; ++j) {
         if (j + 1 < nj) issue_s(j + 1);
-        // O += P_j V_j once the softmax has written P_j (and rescaled O if it had to)
-        const int slot = j & 1, pb = j & 1;
-        mbar_wait(&v_full[slot], (j >> 1) & 1);
-        mbar_wait(&p_full[pb], (j >> 1) & 1);
-        tc_fence_after();
-        const uint32_t d = tmem + C::O_COL;
-        uint8_t* pbuf = sp + pb * C::P_BYTES;
-#pragma unroll
-        for (int kk = 0; kk < BKV / 16; ++kk) {
-          const uint64_t da = umma_desc_sw128(smem_u32(pbuf + (kk >> 2) * ATOM_BYTES)) + 2 * (kk & 3);
-          const uint64_t db = umma_desc_sw128(smem_u32(sv + slot * C::V_BYTES + (kk >> 2) * C::V_ATOM)) + 2 * (kk & 3);
-          umma_bf16(d, da, db, idesc_o, (j > 0 || kk > 0) ? 1u : 0u);
-        }
-        umma_commit(&pv_done[pb]);
+        issue_pv(j);
       }
     }
   } else {
-    // ---- softmax: thread = (query row r, key half) ----
-    const int sw = warp - 2;            // 0..7
-    const int half = sw >> 2;           // keys [64 half, 64 half + 64) of each tile
-    const int quarter = warp & 3;       // TMEM lane quarter (hardware: warp id % 4)
+    // ---- softmax of tile t (thread = query row r) ----
+    const int t = (warp - 2) >> 2;           // 0 = A, 1 = B
+    const int quarter = warp & 3;            // TMEM lane quarter (hardware: warp id % 4)
     const int r = quarter * 32 + lane;
-    const int qpos = s0 + r;            // query position in its sequence
+    const int qpos = s0 + t * BQ + r;        // query position in its sequence
+    const int my_nj = t == 0 ? nj_a : nj;
+    const int diag0 = (s0 + t * BQ) / BKV;   // first of this tile's two diagonal key tiles
     const uint32_t lane_off = static_cast<uint32_t>(quarter * 32) << 16;
-    float m = -INFINITY;                // running max in use (log2 domain)
-    float l = 0.f;                      // this thread's partial row sum, relative to m
-    // P row r of buffer pb: atom = half, 8-row group, row in group, chunk ^ (r & 7)
-    const uint32_t p_row = smem_u32(sp + half * ATOM_BYTES + (r >> 3) * 1024 + (r & 7) * 128);
-    for (int j = 0; j < nj; ++j) {
+    const uint32_t o_addr = tmem + lane_off + C::O_COL + t * HD;
+    float m = -INFINITY;                     // running max in use (log2 domain)
+    float l = 0.f;                           // row sum relative to m
+    const uint32_t p_row = smem_u32(sp + (t * 2) * C::P_BYTES + (r >> 3) * 1024 + (r & 7) * 128);
+    for (int j = 0; j < my_nj; ++j) {
       const int sb = j & 1;
-      const bool diag = j == qt;
-      const int key0 = j * BKV + half * 64;   // first key of this thread's 64
-      mbar_wait(&s_full[sb], (j >> 1) & 1);
+      mbar_wait(&s_full[t * 2 + sb], (j >> 1) & 1);
       tc_fence_after();
-      const uint32_t sa = tmem + lane_off + C::S_COL + sb * BKV + half * 64;
+      const uint32_t sa = tmem + lane_off + C::S_COL + (t * 2 + sb) * BKV;
       uint32_t v0[32], v1[32];
       tmem_ld_32x32b_x32_async(sa, v0);
       tmem_ld_32x32b_x32_async(sa + 32, v1);
       tmem_wait_ld(v0);
       tmem_wait_ld(v1);
-      if (diag) {  // causal mask: keys after this query get -inf
+      // S of this tile is in registers: the MMA may reuse the buffer
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&s_empty[t * 2 + sb]);
+      if (j >= diag0) {  // causal mask: keys after this query get -inf
+        const int key0 = j * BKV;
 #pragma unroll
         for (int i = 0; i < 32; ++i) {
           if (key0 + i > qpos) v0[i] = __float_as_uint(-INFINITY);
@@ -271,42 +287,34 @@ __global__ void __launch_bounds__(THREADS, 1)
       for (int i = 0; i < 32; i += 2) mx = max3(mx, __uint_as_float(v0[i]), __uint_as_float(v0[i + 1]));
 #pragma unroll
       for (int i = 0; i < 32; i += 2) mx = max3(mx, __uint_as_float(v1[i]), __uint_as_float(v1[i + 1]));
-      // S of this tile is in registers: the MMA may reuse the buffer
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&s_empty[sb]);
-      // row max over the pair
-      red_max[half * BQ + r] = mx;
-      pair_bar(quarter);
-      mx = fmaxf(mx, red_max[(half ^ 1) * BQ + r]) * a.scale_log2;
-      pair_bar(quarter);  // red_max is rewritten next tile
-      // raise the max only when it grows by more than 2^kRescale; O (tiles < j) and l
-      // are then scaled by 2^(m_old - m_new).  tcgen05.ld/st are warp-collective, so the
-      // warp rescales together whenever any of its rows needs it (alpha = 1 elsewhere)
+      mx *= a.scale_log2;
+      // raise the max only when it grows by more than 2^kRescale; O (keys of earlier
+      // tiles) and l are then scaled by 2^(m_old - m_new).  tcgen05.ld/st are
+      // warp-collective: the warp rescales whenever any of its rows must (alpha = 1
+      // on the others)
       const bool raise = mx > m + kRescale;
       if (__any_sync(0xffffffffu, raise)) {
         const float alpha = raise ? ex2(m - mx) : 1.f;   // 0 on the first tile
         if (j > 0) {
-          mbar_wait(&pv_done[(j - 1) & 1], ((j - 1) >> 1) & 1);
+          mbar_wait(&pv_done[t * 2 + ((j - 1) & 1)], ((j - 1) >> 1) & 1);
           tc_fence_after();
-          const uint32_t oa = tmem + lane_off + C::O_COL + half * (HD / 2);
 #pragma unroll
-          for (int c = 0; c < HD / 2; c += 32) {
+          for (int c = 0; c < HD; c += 32) {
             uint32_t o[32];
-            tmem_ld_32x32b_x32(oa + c, o);
+            tmem_ld_32x32b_x32(o_addr + c, o);
 #pragma unroll
             for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
-            tmem_st_32x32b_x32(oa + c, o);
+            tmem_st_32x32b_x32(o_addr + c, o);
           }
           asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
         }
         l *= alpha;
         if (raise) m = mx;
       }
-      // P_j into buffer j&1 once PV_{j-2} has finished reading it
-      if (j >= 2) mbar_wait(&pv_done[sb], ((j - 2) >> 1) & 1);
+      // P(j) into buffer j&1 once PV(j-2) has finished reading it
+      if (j >= 2) mbar_wait(&pv_done[t * 2 + sb], ((j - 2) >> 1) & 1);
       const uint32_t prow = p_row + sb * C::P_BYTES;
-      float sum = 0.f;
+      float sum0 = 0.f, sum1 = 0.f;
 #pragma unroll
       for (int c = 0; c < 8; ++c) {   // 8 chunks of 8 keys (16 bytes of P)
         uint32_t w[4];
@@ -317,32 +325,30 @@ __global__ void __launch_bounds__(THREADS, 1)
           const float s1v = __uint_as_float(i + 1 < 32 ? v0[i + 1] : v1[i + 1 - 32]);
           const float p0 = ex2(fmaf(s0v, a.scale_log2, -m));
           const float p1 = ex2(fmaf(s1v, a.scale_log2, -m));
-          sum += p0 + p1;
+          sum0 += p0;
+          sum1 += p1;
           w[q] = pack2(p0, p1);
         }
         asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(prow + ((c ^ (r & 7)) << 4)), "r"(w[0]),
                      "r"(w[1]), "r"(w[2]), "r"(w[3])
                      : "memory");
       }
-      l += sum;
-      // P (generic-proxy stores) -> the MMA's async proxy; O rescale (tcgen05.st) done
+      l += sum0 + sum1;
+      // P (generic-proxy stores) -> the MMA's async proxy; any O rescale (tcgen05.st) done
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&p_full[sb]);
+      if (lane == 0) mbar_arrive(&p_full[t * 2 + sb]);
     }
-    // ---- epilogue: O / l (sum of the pair's partials) -> bf16 ----
-    red_sum[half * BQ + r] = l;
-    pair_bar(quarter);
-    const float inv = 1.f / (l + red_sum[(half ^ 1) * BQ + r]);
-    mbar_wait(&pv_done[(nj - 1) & 1], ((nj - 1) >> 1) & 1);
+    // ---- epilogue: O / l -> bf16 ----
+    mbar_wait(&pv_done[t * 2 + ((my_nj - 1) & 1)], ((my_nj - 1) >> 1) & 1);
     tc_fence_after();
-    const uint32_t oa = tmem + lane_off + C::O_COL + half * (HD / 2);
-    __nv_bfloat16* dst = a.out + static_cast<int64_t>(row0 + qpos) * a.ldo + h * HD + half * (HD / 2);
+    const float inv = 1.f / l;
+    __nv_bfloat16* dst = a.out + static_cast<int64_t>(row0 + qpos) * a.ldo + h * HD;
 #pragma unroll
-    for (int c = 0; c < HD / 2; c += 32) {
+    for (int c = 0; c < HD; c += 32) {
       uint32_t o[32];
-      tmem_ld_32x32b_x32(oa + c, o);
+      tmem_ld_32x32b_x32(o_addr + c, o);
       if (qpos < a.S) {
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
@@ -405,10 +411,11 @@ template <int HD>
 static int launch(const void* qkv, int ld, int B, int S, int H, int KV, void* vt, int S_pad, void* out, int ldo,
                   cudaStream_t s) {
   using C = Cfg<HD>;
-  CUtensorMap mqk, mvt;
+  CUtensorMap mq, mk, mvt;
   const int cols = (H + 2 * KV) * HD;
-  if (int rc = encode(&mqk, qkv, static_cast<int64_t>(B) * S, cols, ld, 64, 128)) return rc;
-  if (int rc = encode(&mvt, vt, static_cast<int64_t>(B) * KV * HD, S_pad, S_pad, 64, HD)) return rc;
+  if (int rc = encode(&mq, qkv, static_cast<int64_t>(B) * S, cols, ld, 64, BQ)) return rc;
+  if (int rc = encode(&mk, qkv, static_cast<int64_t>(B) * S, cols, ld, 64, BKV)) return rc;
+  if (int rc = encode(&mvt, vt, static_cast<int64_t>(B) * KV * HD, S_pad, S_pad, BKV, HD)) return rc;
   int dev = 0;
   cudaGetDevice(&dev);
   static bool attr_set[64] = {};
@@ -430,7 +437,8 @@ static int launch(const void* qkv, int ld, int B, int S, int H, int KV, void* vt
   a.q_col0 = 0;
   a.k_col0 = H * HD;
   a.scale_log2 = 1.4426950408889634f / sqrtf(static_cast<float>(HD));
-  e = launch_pdl(PDL_ATTN, k_flash_prefill<HD>, dim3((S + BQ - 1) / BQ, H, B), dim3(THREADS), C::SMEM, s, mqk, mvt,
+  const int n_qt = (S + BQ - 1) / BQ;
+  e = launch_pdl(PDL_ATTN, k_flash_prefill<HD>, dim3((n_qt + 1) / 2, H, B), dim3(THREADS), C::SMEM, s, mq, mk, mvt,
                  a);
   if (e != cudaSuccess) return bz_fail_cuda(e, "attention launch");
   return bz_check_launch("bz_prefill_attention");

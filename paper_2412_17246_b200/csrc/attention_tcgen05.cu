@@ -15,9 +15,9 @@
 // always has the other tile's work while one softmax runs (FA4-style ping-pong).
 // Keys come in tiles of 64.  TMEM lane = query row of a tile.
 //   w0      TMA producer: Q_A, Q_B once; K_j / V^T_j into 3-deep rings (K runs ahead)
-//   w1      MMA issuer (one lane), per key tile j: S_A(j), S_B(j) = Q K_j^T into TMEM
-//           (double-buffered per tile), then O_A += P_A(j-1) V_{j-1}, O_B += P_B(j-1) V_{j-1}
-//           (O accumulated in TMEM)
+//   w1      MMA issuer (one lane), per key tile j: S_A(j+2), S_B(j+2) = Q K^T into TMEM
+//           (double-buffered per tile, issued once the softmax has read S(j)), then
+//           O_A += P_A(j) V_j, O_B += P_B(j) V_j (O accumulated in TMEM)
 //   w2..w5  softmax of tile A, w6..w9 of tile B (thread = query row): S from TMEM,
 //           causal mask on the diagonal key tiles only, running max in the log2
 //           domain, P = exp2(s log2e / sqrt(hd) - m) as bf16 straight into a
@@ -190,10 +190,11 @@ __global__ void __launch_bounds__(THREADS, 1)
         mbar_expect_tx(&v_full[st], C::V_BYTES);
         tma_load_2d(sv + st * C::V_BYTES, &map_vt, j * BKV, (b * a.KV + g) * HD, &v_full[st]);
       };
-      // K runs one tile ahead of V (S needs K a softmax before PV needs V)
+      // K runs two tiles ahead of V (S(j+2) is computed while the softmax of tile j runs)
       load_k(0);
+      if (nj > 1) load_k(1);
       for (int j = 0; j < nj; ++j) {
-        if (j + 1 < nj) load_k(j + 1);
+        if (j + 2 < nj) load_k(j + 2);
         load_v(j);
       }
       pdl_trigger();
@@ -241,9 +242,13 @@ __global__ void __launch_bounds__(THREADS, 1)
         }
         umma_commit(&v_empty[st]);
       };
+      // S(j+2) is issued as soon as the softmax of tile j has read S(j) out of its TMEM
+      // buffer, so the tensor core computes it while that softmax runs; PV(j) follows
+      // once P(j) is written
       issue_s(0);
+      if (nj > 1) issue_s(1);
       for (int j = 0; j < nj; ++j) {
-        if (j + 1 < nj) issue_s(j + 1);
+        if (j + 2 < nj) issue_s(j + 2);
         issue_pv(j);
       }
     }

@@ -181,7 +181,8 @@ def build_costs(prefill: Optional[dict] = None, nvlink_layer_ms=None, host_layer
 
 
 def c3_report(costs: MeasuredCosts, topo_name: str = "b200-hgx-2x8",
-              strategies: Sequence[str] = ("blitz-live", "blitz-stop", "allcache", "sllm")) -> dict:
+              strategies: Sequence[str] = ("blitz-live", "blitz-stop", "allcache", "sllm"),
+              executed: Optional[MeasuredCosts] = None) -> dict:
     """C3: Llama-2 7B under the 5x-burst trace; p99 TTFT/TBT with modeled and measured costs."""
     from . import simcore
     from .slab import LLAMA2_7B, model_spec_for
@@ -198,7 +199,12 @@ def c3_report(costs: MeasuredCosts, topo_name: str = "b200-hgx-2x8",
            "topology": topo_name, "model": spec.name, "costs": costs.describe(), "strategies": {}}
     for strat in strategies:
         row = {}
-        for label, c in (("modeled", simcore.ReferenceCosts()), ("measured", costs)):
+        # executed: every scale-up the replay plans is run by the data plane in this
+        # process and its layer / transfer events are the device stamps (inprocess.py)
+        providers = [("modeled", simcore.ReferenceCosts()), ("measured", costs)]
+        if executed is not None:
+            providers.append(("executed", executed))
+        for label, c in providers:
             t0 = time.perf_counter()
             res = simcore.run_simulation(topo, [spec], trace, simcore.SimPolicy(strategy=strat), costs=c)
             s = res.summary()
@@ -207,4 +213,6 @@ def c3_report(costs: MeasuredCosts, topo_name: str = "b200-hgx-2x8",
                           "scale_ups": s["counters"]["scale_ups"],
                           "replay_cpu_s": time.perf_counter() - t0}
         out["strategies"][strat] = row
+    if executed is not None:
+        out["executed_costs"] = executed.describe()
     return out

@@ -172,8 +172,9 @@ class LocalPlanExecutor:
         lay, lib = self.layout, self.lib
         self.epoch += 1
         e = self.epoch
-        slabs = {n: (self._slab(("dst", n), dev_of[n]) if roles[n].receives else self._source(n, dev_of[n]))
-                 for n in dev_of}
+        # one receiving and one source slab per device, whatever node name the plan gives it
+        slabs = {n: (self._slab(("dst", dev_of[n]), dev_of[n]) if roles[n].receives
+                     else self._source(("dev", dev_of[n]), dev_of[n])) for n in dev_of}
         hc = self._host_cache() if any(x.src.startswith("mem") for x in plan.edges) else None
         for d in set(dev_of.values()):
             torch.cuda.synchronize(d)
@@ -208,8 +209,8 @@ class LocalPlanExecutor:
                 continue
             d = dev_of[n]
             with torch.cuda.device(d):
-                ptrs = ptr_array([self._peer(d, ("dst", o), slabs[o]) for o in outs])
-                flags = ptr_array([self._peer(d, ("dst", o), slabs[o]) + lay.flag_offset for o in outs])
+                ptrs = ptr_array([self._peer(d, ("dst", dev_of[o]), slabs[o]) for o in outs])
+                flags = ptr_array([self._peer(d, ("dst", dev_of[o]), slabs[o]) + lay.flag_offset for o in outs])
                 lib.bz_push_tiles(slab.ptr, ptrs, flags, len(outs), slab.flags_ptr if r.receives else None,
                                   slab.tile_off.data_ptr(), 0, lay.ntiles, e, self.nctas, 0,
                                   self._stream(d, "copy").cuda_stream)

@@ -770,6 +770,8 @@ def run_blitz(args):
                 layers_host = r.layer_ms
         e2e_s = dist_max(e2e_t, N)
         log(f"e2e steps s={e2e_t}")
+        # per-GPU last-layer arrival of the last e2e step (host stage vs NVLink stage)
+        last_layer = fabric.allgather((my, layers_host[-1] if layers_host else None))
         e2e_ok = dist_sum(0.0 if sess2.verify(sess2.executor.epoch) else 1.0, N) == 0.0
         h2d = payload * tp  # one shard per TP rank crosses PCIe per step
         d2h = int(stamps.numel() * 8) * N
@@ -779,6 +781,7 @@ def run_blitz(args):
                            f"stamp readback; plan {[(e.src, e.dst, e.kind) for e in e2e_plan.edges]}"
                            f" fan-out {e2e_plan.nvlink_fanout}",
                "host_stripe": ({rep: len(m) for rep, m in sess2.executor.stripe_groups.items()} or None),
+               "last_layer_ms_by_gpu": {n: t for n, t in last_layer if t is not None},
                "bit_exact": e2e_ok}
         sess2.close()
         if hc2 is not None:

@@ -102,7 +102,7 @@ def main():
     ap.add_argument("--tile-kib", type=int, default=1024)
     ap.add_argument("--ctas", default="16,32,48,64,96,148")
     ap.add_argument("--unrolls", default="4,8,16")
-    ap.add_argument("--once", default=None, help="push|mc|mc1: one launch (for ncu)")
+    ap.add_argument("--once", default=None, help="push|mc|mc1|panels: one launch (for ncu)")
     ap.add_argument("--nctas", type=int, default=48)
     ap.add_argument("--gb", type=float, default=0.0, help="uniform payload of this many GB instead of --arch")
     args = ap.parse_args()
@@ -188,6 +188,29 @@ def main():
                                        None, src.tile_off.data_ptr(), 0, lay.ntiles, e, nctas, engine,
                                        stream.cuda_stream)
         return fn, e
+
+    # ---- KV hand-over mover: strided panel prefixes into the peer (k_copy_panels) --------------
+    def panels(nctas):
+        # 7B KV shape of one sequence batch: 32 heads x 4 seqs panels of [s_max=2048, 128] bf16,
+        # first 2000 tokens of each copied
+        n_panels, s_max, hd, length = 128, 2048, 128, 2000
+        stride = s_max * hd * 2
+        nbytes = n_panels * length * hd * 2
+        fn = lambda: lib.bz_copy_panels(src.ptr, mapped.ptr, n_panels, stride, stride, length * hd * 2,  # noqa: E731
+                                        nctas, stream.cuda_stream)
+        return fn, nbytes
+
+    if args.once == "panels":
+        fn, nb = panels(args.nctas)
+        fn()
+        torch.cuda.synchronize()
+        emit({"case": "panels-once", "bytes": nb})
+        return
+    if args.once is None:
+        for c in (64, 128, 148):
+            fn, nb = panels(c)
+            ms = timed(fn, stream)
+            emit({"case": "copy_panels", "nctas": c, "bytes": nb, "ms": ms, "GBps": nb / ms / 1e6})
 
     if args.once == "push":
         fn, e = push(args.nctas, 0)

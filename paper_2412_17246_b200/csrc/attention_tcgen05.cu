@@ -10,20 +10,22 @@
 //             so V^T is a K-major MMA operand like every weight), zero past S
 //   out: attn [B*S, ldo] bf16, head h at columns [h*hd, (h+1)*hd) -- the o-projection's A
 //
-// One CTA = two adjacent 128-row query tiles A, B of one (sequence, head), so every
-// K / V tile it loads feeds two independent softmax streams and the tensor core
-// always has the other tile's work while one softmax runs (FA4-style ping-pong).
-// Keys come in tiles of 64.  TMEM lane = query row of a tile.
-//   w0      TMA producer: Q_A, Q_B once; K_j / V^T_j into 3-deep rings (K runs ahead)
-//   w1      MMA issuer (one lane), per key tile j: S_A(j+2), S_B(j+2) = Q K^T into TMEM
-//           (double-buffered per tile, issued once the softmax has read S(j)), then
-//           O_A += P_A(j) V_j, O_B += P_B(j) V_j (O accumulated in TMEM)
-//   w2..w5  softmax of tile A, w6..w9 of tile B (thread = query row): S from TMEM,
-//           causal mask on the diagonal key tiles only, running max in the log2
-//           domain, P = exp2(s log2e / sqrt(hd) - m) as bf16 straight into a
-//           128B-swizzled smem tile the MMA reads (2 buffers per query tile).  The max
-//           is only raised when it grows by more than 2^8 (P <= 256, exact in fp32 /
-//           bf16); only then is O rescaled in TMEM (ld, scale, st), warp-uniformly.
+// One CTA = two adjacent 128-row query tiles A, B of one (sequence, head): every K / V
+// tile it loads feeds two independent softmax streams, and the tensor core works on
+// one tile while the other tile's softmax runs (FA4-style ping-pong).  Keys come in
+// tiles of 128.  TMEM lane = query row of a tile.
+//   w0      TMA producer: Q_A, Q_B once; K_j / V^T_j into 2-deep rings
+//   w1      MMA issuer (one lane), per tile X in (A, B): O_X += P_X(j) V_j with P read
+//           straight from TMEM (tcgen05.mma A-operand in tensor memory), then
+//           S_X(j+1) = Q_X K_{j+1}^T into the same TMEM columns
+//   w2..w5  softmax of A, w6..w9 softmax of B (thread = query row): S_X(j) from TMEM,
+//           causal mask on the diagonal tile only, running max in the log2 domain,
+//           P = exp2(s log2e / sqrt(hd) - m) packed to bf16 and stored back into the
+//           first half of S_X's columns (no shared memory traffic for P).  The max is
+//           only raised when it grows by more than 2^8 (P <= 256, exact in fp32 /
+//           bf16); only then is O rescaled in TMEM (ld, scale, st), warp-uniformly --
+//           S_X(j) completing implies O_X += P_X(j-1) V_{j-1} completed (tcgen05 ops
+//           execute in issue order), so the rescale needs no extra wait.
 //   epilogue: O / l, bf16 rows of the o-projection input.
 #include <cuda.h>
 #include <cuda_bf16.h>
@@ -41,24 +43,24 @@ namespace attn {
 using namespace bz::tc;
 
 constexpr int BQ = 128;       // query rows per tile (= TMEM lanes)
-constexpr int BKV = 64;       // keys per tile
+constexpr int BKV = 128;      // keys per tile
 constexpr int THREADS = 320;  // w0 TMA, w1 MMA + TMEM allocator, w2..w5 softmax A, w6..w9 softmax B
-constexpr int KSTAGES = 3, VSTAGES = 3;
+constexpr int STAGES = 2;     // K and V rings
 
 template <int HD>
 struct Cfg {
   static constexpr int KA = HD / 64;               // 64-wide swizzle atoms along hd
-  static constexpr int Q_ATOM = BQ * 128;          // 128 rows x 128 B
-  static constexpr int Q_BYTES = KA * Q_ATOM;      // one query tile
-  static constexpr int K_ATOM = BKV * 128;         // 64 key rows x 128 B
-  static constexpr int K_BYTES = KA * K_ATOM;
-  static constexpr int V_BYTES = HD * 128;         // V^T tile: HD rows x 64 keys (one atom)
-  static constexpr int P_BYTES = BQ * 128;         // 128 rows x 64 keys (one atom)
+  static constexpr int ROW_ATOM = 128 * 128;       // 128 rows x 128 B
+  static constexpr int Q_BYTES = KA * ROW_ATOM;    // one query tile
+  static constexpr int K_BYTES = KA * ROW_ATOM;    // 128 keys x hd
+  static constexpr int V_ATOM = HD * 128;          // V^T: HD rows x 64 keys
+  static constexpr int V_BYTES = 2 * V_ATOM;       // 128 keys
   static constexpr int BAR_BYTES = 256;
-  static constexpr int SMEM = 1024 + 2 * Q_BYTES + KSTAGES * K_BYTES + VSTAGES * V_BYTES + 4 * P_BYTES + BAR_BYTES;
-  // TMEM: S_A[2], S_B[2] (64 columns each), then O_A, O_B (HD columns each)
+  static constexpr int SMEM = 1024 + 2 * Q_BYTES + STAGES * (K_BYTES + V_BYTES) + BAR_BYTES;
+  // TMEM: S_A at [0, 128), S_B at [128, 256) -- P_X (bf16 pairs) in the first 64 columns
+  // of S_X once S_X is in registers -- then O_A, O_B (HD columns each)
   static constexpr int S_COL = 0;
-  static constexpr int O_COL = 4 * BKV;
+  static constexpr int O_COL = 2 * BKV;
   static constexpr int TMEM_COLS = 512;
   static_assert(HD == 64 || HD == 128, "head dim");
   static_assert(SMEM <= 232448, "smem");
@@ -88,15 +90,27 @@ __device__ __forceinline__ float max3(float a, float b, float c) {
   asm("max.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
   return r;
 }
-__device__ __forceinline__ void tmem_st_32x32b_x32(uint32_t taddr, const uint32_t (&r)[32]) {
+__device__ __forceinline__ void tmem_st_32x32b_x16(uint32_t taddr, const uint32_t* r) {
   asm volatile(
-      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], "
-      "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
-      "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "
+      "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(taddr),
       "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]),
-      "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]), "r"(r[16]),
-      "r"(r[17]), "r"(r[18]), "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]),
-      "r"(r[25]), "r"(r[26]), "r"(r[27]), "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31])
+      "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
+      : "memory");
+}
+__device__ __forceinline__ void tmem_st_32x32b_x32(uint32_t taddr, const uint32_t (&r)[32]) {
+  tmem_st_32x32b_x16(taddr, r);
+  tmem_st_32x32b_x16(taddr + 16, r + 16);
+}
+// D[tmem] (+)= A[tmem] . B[smem]: the A operand (M = 128 lanes x K = 16 bf16, two per
+// 32-bit column) is read from tensor memory
+__device__ __forceinline__ void umma_bf16_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t b, uint32_t idesc,
+                                             uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "r"(tmem_a), "l"(b), "r"(idesc), "r"(acc)
       : "memory");
 }
 
@@ -104,27 +118,24 @@ constexpr float kRescale = 8.0f;  // raise the running max only when it grows by
 
 template <int HD>
 __global__ void __launch_bounds__(THREADS, 1)
-    k_flash_prefill(const __grid_constant__ CUtensorMap map_q, const __grid_constant__ CUtensorMap map_k,
-                    const __grid_constant__ CUtensorMap map_vt, Args a) {
+    k_flash_prefill(const __grid_constant__ CUtensorMap map_q, const __grid_constant__ CUtensorMap map_vt, Args a) {
   using C = Cfg<HD>;
   constexpr int KA = C::KA;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sq = smem;                              // [2 tiles]
-  uint8_t* sk = sq + 2 * C::Q_BYTES;               // [KSTAGES]
-  uint8_t* sv = sk + KSTAGES * C::K_BYTES;         // [VSTAGES]
-  uint8_t* sp = sv + VSTAGES * C::V_BYTES;         // [tile][2 buffers]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sp + 4 * C::P_BYTES);
-  uint64_t* q_full = bars;                  // 1
-  uint64_t* k_full = bars + 1;              // [3]
-  uint64_t* k_empty = bars + 4;             // [3]
-  uint64_t* v_full = bars + 7;              // [3]
-  uint64_t* v_empty = bars + 10;            // [3]
-  uint64_t* s_full = bars + 13;             // [tile][2]
-  uint64_t* s_empty = bars + 17;            // [tile][2]
-  uint64_t* p_full = bars + 21;             // [tile][2]
-  uint64_t* pv_done = bars + 25;            // [tile][2]  PV(j) done: P buffer j&1 free, O holds keys < 64 (j+1)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 29);
+  uint8_t* sk = sq + 2 * C::Q_BYTES;               // [STAGES]
+  uint8_t* sv = sk + STAGES * C::K_BYTES;          // [STAGES]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sv + STAGES * C::V_BYTES);
+  uint64_t* q_full = bars;          // 1
+  uint64_t* k_full = bars + 1;      // [2]
+  uint64_t* k_empty = bars + 3;     // [2]
+  uint64_t* v_full = bars + 5;      // [2]
+  uint64_t* v_empty = bars + 7;     // [2]
+  uint64_t* s_full = bars + 9;      // [tile]  S_X(j) in TMEM
+  uint64_t* p_full = bars + 11;     // [tile]  P_X(j) in TMEM (and O_X rescaled)
+  uint64_t* pv_done = bars + 13;    // [tile]  O_X += P_X(j) V_j complete
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 15);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n_qt = (a.S + BQ - 1) / BQ;
@@ -132,26 +143,21 @@ __global__ void __launch_bounds__(THREADS, 1)
   const int pair = n_pairs - 1 - static_cast<int>(blockIdx.x);  // longest (most keys) first
   const int h = blockIdx.y, b = blockIdx.z;
   const int g = h / (a.H / a.KV);
-  const int s0 = pair * 2 * BQ;              // first query row of tile A
-  // key tiles: A needs 0 .. 4p+1, B needs 0 .. 4p+3 (causal, 64-key tiles)
-  const int nj_a = (s0 + BQ) / BKV;
-  const int nj = (s0 + 2 * BQ) / BKV;
+  const int s0 = pair * 2 * BQ;      // first query row of tile A
+  const int qt_a = 2 * pair;         // tile A's diagonal key tile; B's is qt_a + 1
+  const int nj_a = qt_a + 1, nj = qt_a + 2;
   const int row0 = b * a.S;
 
   if (warp == 0 && lane == 0) {
     prefetch_tmap(&map_q);
-    prefetch_tmap(&map_k);
     prefetch_tmap(&map_vt);
     mbar_init(q_full, 1);
-    for (int i = 0; i < 3; ++i) {
+    for (int i = 0; i < 2; ++i) {
       mbar_init(&k_full[i], 1);
       mbar_init(&k_empty[i], 1);
       mbar_init(&v_full[i], 1);
       mbar_init(&v_empty[i], 1);
-    }
-    for (int i = 0; i < 4; ++i) {
       mbar_init(&s_full[i], 1);
-      mbar_init(&s_empty[i], 4);
       mbar_init(&p_full[i], 4);
       mbar_init(&pv_done[i], 1);
     }
@@ -174,28 +180,20 @@ __global__ void __launch_bounds__(THREADS, 1)
       mbar_expect_tx(q_full, 2 * C::Q_BYTES);
       for (int t = 0; t < 2; ++t)
         for (int ka = 0; ka < KA; ++ka)
-          tma_load_2d(sq + t * C::Q_BYTES + ka * C::Q_ATOM, &map_q, a.q_col0 + h * HD + ka * 64,
+          tma_load_2d(sq + t * C::Q_BYTES + ka * C::ROW_ATOM, &map_q, a.q_col0 + h * HD + ka * 64,
                       row0 + s0 + t * BQ, q_full);
-      auto load_k = [&](int j) {
-        const int st = j % KSTAGES;
-        mbar_wait(&k_empty[st], ((j / KSTAGES) & 1) ^ 1);
+      for (int j = 0; j < nj; ++j) {
+        const int st = j & 1, ph = ((j >> 1) & 1) ^ 1;
+        mbar_wait(&k_empty[st], ph);
         mbar_expect_tx(&k_full[st], C::K_BYTES);
         for (int ka = 0; ka < KA; ++ka)
-          tma_load_2d(sk + st * C::K_BYTES + ka * C::K_ATOM, &map_k, a.k_col0 + g * HD + ka * 64, row0 + j * BKV,
+          tma_load_2d(sk + st * C::K_BYTES + ka * C::ROW_ATOM, &map_q, a.k_col0 + g * HD + ka * 64, row0 + j * BKV,
                       &k_full[st]);
-      };
-      auto load_v = [&](int j) {
-        const int st = j % VSTAGES;
-        mbar_wait(&v_empty[st], ((j / VSTAGES) & 1) ^ 1);
+        mbar_wait(&v_empty[st], ph);
         mbar_expect_tx(&v_full[st], C::V_BYTES);
-        tma_load_2d(sv + st * C::V_BYTES, &map_vt, j * BKV, (b * a.KV + g) * HD, &v_full[st]);
-      };
-      // K runs two tiles ahead of V (S(j+2) is computed while the softmax of tile j runs)
-      load_k(0);
-      if (nj > 1) load_k(1);
-      for (int j = 0; j < nj; ++j) {
-        if (j + 2 < nj) load_k(j + 2);
-        load_v(j);
+        for (int kh = 0; kh < 2; ++kh)
+          tma_load_2d(sv + st * C::V_BYTES + kh * C::V_ATOM, &map_vt, j * BKV + kh * 64, (b * a.KV + g) * HD,
+                      &v_full[st]);
       }
       pdl_trigger();
     }
@@ -205,51 +203,47 @@ __global__ void __launch_bounds__(THREADS, 1)
       constexpr uint32_t idesc_s = instr_desc_bf16(BQ, BKV);
       constexpr uint32_t idesc_o = instr_desc_bf16(BQ, HD);
       mbar_wait(q_full, 0);
-      auto issue_s = [&](int j) {
-        const int st = j % KSTAGES, sb = j & 1;
-        mbar_wait(&k_full[st], (j / KSTAGES) & 1);
-        for (int t = 0; t < 2; ++t) {
-          if (t == 0 && j >= nj_a) continue;      // tile A is past its diagonal
-          mbar_wait(&s_empty[t * 2 + sb], ((j >> 1) & 1) ^ 1);
-          tc_fence_after();
-          const uint32_t d = tmem + C::S_COL + (t * 2 + sb) * BKV;
+      auto issue_s = [&](int t, int j) {   // S_t(j) = Q_t K_j^T
+        const int st = j & 1;
+        const uint32_t d = tmem + C::S_COL + t * BKV;
 #pragma unroll
-          for (int kk = 0; kk < HD / 16; ++kk) {
-            const uint64_t da = umma_desc_sw128(smem_u32(sq + t * C::Q_BYTES + (kk >> 2) * C::Q_ATOM)) + 2 * (kk & 3);
-            const uint64_t db = umma_desc_sw128(smem_u32(sk + st * C::K_BYTES + (kk >> 2) * C::K_ATOM)) + 2 * (kk & 3);
-            umma_bf16(d, da, db, idesc_s, kk > 0 ? 1u : 0u);
-          }
-          umma_commit(&s_full[t * 2 + sb]);
+        for (int kk = 0; kk < HD / 16; ++kk) {
+          const uint64_t da = umma_desc_sw128(smem_u32(sq + t * C::Q_BYTES + (kk >> 2) * C::ROW_ATOM)) + 2 * (kk & 3);
+          const uint64_t db = umma_desc_sw128(smem_u32(sk + st * C::K_BYTES + (kk >> 2) * C::ROW_ATOM)) + 2 * (kk & 3);
+          umma_bf16(d, da, db, idesc_s, kk > 0 ? 1u : 0u);
         }
-        umma_commit(&k_empty[st]);
+        umma_commit(&s_full[t]);
       };
-      auto issue_pv = [&](int j) {
-        const int st = j % VSTAGES, pb = j & 1;
-        mbar_wait(&v_full[st], (j / VSTAGES) & 1);
-        for (int t = 0; t < 2; ++t) {
-          if (t == 0 && j >= nj_a) continue;
-          mbar_wait(&p_full[t * 2 + pb], (j >> 1) & 1);
-          tc_fence_after();
-          const uint32_t d = tmem + C::O_COL + t * HD;
-          const uint8_t* pbuf = sp + (t * 2 + pb) * C::P_BYTES;
+      auto issue_pv = [&](int t, int j) {  // O_t += P_t(j) V_j, P from TMEM
+        const int st = j & 1;
+        const uint32_t d = tmem + C::O_COL + t * HD;
+        const uint32_t pa = tmem + C::S_COL + t * BKV;
 #pragma unroll
-          for (int kk = 0; kk < BKV / 16; ++kk) {
-            const uint64_t da = umma_desc_sw128(smem_u32(pbuf)) + 2 * kk;
-            const uint64_t db = umma_desc_sw128(smem_u32(sv + st * C::V_BYTES)) + 2 * kk;
-            umma_bf16(d, da, db, idesc_o, (j > 0 || kk > 0) ? 1u : 0u);
-          }
-          umma_commit(&pv_done[t * 2 + pb]);
+        for (int kk = 0; kk < BKV / 16; ++kk) {
+          const uint64_t db = umma_desc_sw128(smem_u32(sv + st * C::V_BYTES + (kk >> 2) * C::V_ATOM)) + 2 * (kk & 3);
+          umma_bf16_ts(d, pa + kk * 8, db, idesc_o, (j > 0 || kk > 0) ? 1u : 0u);
+        }
+        umma_commit(&pv_done[t]);
+      };
+      mbar_wait(&k_full[0], 0);
+      tc_fence_after();
+      issue_s(0, 0);
+      issue_s(1, 0);
+      umma_commit(&k_empty[0]);
+      for (int j = 0; j < nj; ++j) {
+        const int st = j & 1;
+        mbar_wait(&v_full[st], (j >> 1) & 1);
+        const bool more = j + 1 < nj;
+        if (more) mbar_wait(&k_full[(j + 1) & 1], ((j + 1) >> 1) & 1);
+        for (int t = 0; t < 2; ++t) {
+          if (t == 0 && j >= nj_a) continue;          // tile A is done after its diagonal
+          mbar_wait(&p_full[t], j & 1);
+          tc_fence_after();
+          issue_pv(t, j);
+          if (more && !(t == 0 && j + 1 >= nj_a)) issue_s(t, j + 1);
         }
         umma_commit(&v_empty[st]);
-      };
-      // S(j+2) is issued as soon as the softmax of tile j has read S(j) out of its TMEM
-      // buffer, so the tensor core computes it while that softmax runs; PV(j) follows
-      // once P(j) is written
-      issue_s(0);
-      if (nj > 1) issue_s(1);
-      for (int j = 0; j < nj; ++j) {
-        if (j + 2 < nj) issue_s(j + 2);
-        issue_pv(j);
+        if (more) umma_commit(&k_empty[(j + 1) & 1]);
       }
     }
   } else {
@@ -259,50 +253,45 @@ __global__ void __launch_bounds__(THREADS, 1)
     const int r = quarter * 32 + lane;
     const int qpos = s0 + t * BQ + r;        // query position in its sequence
     const int my_nj = t == 0 ? nj_a : nj;
-    const int diag0 = (s0 + t * BQ) / BKV;   // first of this tile's two diagonal key tiles
+    const int diag = qt_a + t;
     const uint32_t lane_off = static_cast<uint32_t>(quarter * 32) << 16;
+    const uint32_t s_addr = tmem + lane_off + C::S_COL + t * BKV;
     const uint32_t o_addr = tmem + lane_off + C::O_COL + t * HD;
     float m = -INFINITY;                     // running max in use (log2 domain)
     float l = 0.f;                           // row sum relative to m
-    const uint32_t p_row = smem_u32(sp + (t * 2) * C::P_BYTES + (r >> 3) * 1024 + (r & 7) * 128);
     for (int j = 0; j < my_nj; ++j) {
-      const int sb = j & 1;
-      mbar_wait(&s_full[t * 2 + sb], (j >> 1) & 1);
+      mbar_wait(&s_full[t], j & 1);
       tc_fence_after();
-      const uint32_t sa = tmem + lane_off + C::S_COL + (t * 2 + sb) * BKV;
-      uint32_t v0[32], v1[32];
-      tmem_ld_32x32b_x32_async(sa, v0);
-      tmem_ld_32x32b_x32_async(sa + 32, v1);
-      tmem_wait_ld(v0);
-      tmem_wait_ld(v1);
-      // S of this tile is in registers: the MMA may reuse the buffer
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&s_empty[t * 2 + sb]);
-      if (j >= diag0) {  // causal mask: keys after this query get -inf
+      uint32_t v[4][32];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) tmem_ld_32x32b_x32_async(s_addr + 32 * c, v[c]);
+#pragma unroll
+      for (int c = 0; c < 4; ++c) tmem_wait_ld(v[c]);
+      if (j == diag) {  // causal mask: keys after this query get -inf
         const int key0 = j * BKV;
 #pragma unroll
-        for (int i = 0; i < 32; ++i) {
-          if (key0 + i > qpos) v0[i] = __float_as_uint(-INFINITY);
-          if (key0 + 32 + i > qpos) v1[i] = __float_as_uint(-INFINITY);
-        }
+        for (int c = 0; c < 4; ++c)
+#pragma unroll
+          for (int i = 0; i < 32; ++i)
+            if (key0 + 32 * c + i > qpos) v[c][i] = __float_as_uint(-INFINITY);
       }
-      float mx = -INFINITY;
+      float mx0 = -INFINITY, mx1 = -INFINITY;
 #pragma unroll
-      for (int i = 0; i < 32; i += 2) mx = max3(mx, __uint_as_float(v0[i]), __uint_as_float(v0[i + 1]));
+      for (int c = 0; c < 4; c += 2)
 #pragma unroll
-      for (int i = 0; i < 32; i += 2) mx = max3(mx, __uint_as_float(v1[i]), __uint_as_float(v1[i + 1]));
-      mx *= a.scale_log2;
-      // raise the max only when it grows by more than 2^kRescale; O (keys of earlier
-      // tiles) and l are then scaled by 2^(m_old - m_new).  tcgen05.ld/st are
-      // warp-collective: the warp rescales whenever any of its rows must (alpha = 1
-      // on the others)
+        for (int i = 0; i < 32; i += 2) {
+          mx0 = max3(mx0, __uint_as_float(v[c][i]), __uint_as_float(v[c][i + 1]));
+          mx1 = max3(mx1, __uint_as_float(v[c + 1][i]), __uint_as_float(v[c + 1][i + 1]));
+        }
+      const float mx = fmaxf(mx0, mx1) * a.scale_log2;
+      // raise the max only when it grows by more than 2^kRescale: O and l are then
+      // scaled by 2^(m_old - m_new).  tcgen05.ld/st are warp-collective, so the warp
+      // rescales whenever any of its rows must (alpha = 1 on the others).  O holds
+      // P(j-1) V_{j-1} already: S(j) was issued after that MMA.
       const bool raise = mx > m + kRescale;
       if (__any_sync(0xffffffffu, raise)) {
         const float alpha = raise ? ex2(m - mx) : 1.f;   // 0 on the first tile
         if (j > 0) {
-          mbar_wait(&pv_done[t * 2 + ((j - 1) & 1)], ((j - 1) >> 1) & 1);
-          tc_fence_after();
 #pragma unroll
           for (int c = 0; c < HD; c += 32) {
             uint32_t o[32];
@@ -311,42 +300,33 @@ __global__ void __launch_bounds__(THREADS, 1)
             for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
             tmem_st_32x32b_x32(o_addr + c, o);
           }
-          asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
         }
         l *= alpha;
         if (raise) m = mx;
       }
-      // P(j) into buffer j&1 once PV(j-2) has finished reading it
-      if (j >= 2) mbar_wait(&pv_done[t * 2 + sb], ((j - 2) >> 1) & 1);
-      const uint32_t prow = p_row + sb * C::P_BYTES;
+      // P = exp2(s * scale - m) as bf16 pairs into the first 64 columns of S_t
       float sum0 = 0.f, sum1 = 0.f;
 #pragma unroll
-      for (int c = 0; c < 8; ++c) {   // 8 chunks of 8 keys (16 bytes of P)
-        uint32_t w[4];
+      for (int c = 0; c < 4; ++c) {
+        uint32_t w[16];
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const int i = c * 8 + 2 * q;
-          const float s0v = __uint_as_float(i < 32 ? v0[i] : v1[i - 32]);
-          const float s1v = __uint_as_float(i + 1 < 32 ? v0[i + 1] : v1[i + 1 - 32]);
-          const float p0 = ex2(fmaf(s0v, a.scale_log2, -m));
-          const float p1 = ex2(fmaf(s1v, a.scale_log2, -m));
+        for (int i = 0; i < 32; i += 2) {
+          const float p0 = ex2(fmaf(__uint_as_float(v[c][i]), a.scale_log2, -m));
+          const float p1 = ex2(fmaf(__uint_as_float(v[c][i + 1]), a.scale_log2, -m));
           sum0 += p0;
           sum1 += p1;
-          w[q] = pack2(p0, p1);
+          w[i >> 1] = pack2(p0, p1);
         }
-        asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(prow + ((c ^ (r & 7)) << 4)), "r"(w[0]),
-                     "r"(w[1]), "r"(w[2]), "r"(w[3])
-                     : "memory");
+        tmem_st_32x32b_x16(s_addr + 16 * c, w);
       }
       l += sum0 + sum1;
-      // P (generic-proxy stores) -> the MMA's async proxy; any O rescale (tcgen05.st) done
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&p_full[t * 2 + sb]);
+      if (lane == 0) mbar_arrive(&p_full[t]);
     }
     // ---- epilogue: O / l -> bf16 ----
-    mbar_wait(&pv_done[t * 2 + ((my_nj - 1) & 1)], ((my_nj - 1) >> 1) & 1);
+    mbar_wait(&pv_done[t], (my_nj - 1) & 1);
     tc_fence_after();
     const float inv = 1.f / l;
     __nv_bfloat16* dst = a.out + static_cast<int64_t>(row0 + qpos) * a.ldo + h * HD;
@@ -416,11 +396,10 @@ template <int HD>
 static int launch(const void* qkv, int ld, int B, int S, int H, int KV, void* vt, int S_pad, void* out, int ldo,
                   cudaStream_t s) {
   using C = Cfg<HD>;
-  CUtensorMap mq, mk, mvt;
+  CUtensorMap mq, mvt;
   const int cols = (H + 2 * KV) * HD;
-  if (int rc = encode(&mq, qkv, static_cast<int64_t>(B) * S, cols, ld, 64, BQ)) return rc;
-  if (int rc = encode(&mk, qkv, static_cast<int64_t>(B) * S, cols, ld, 64, BKV)) return rc;
-  if (int rc = encode(&mvt, vt, static_cast<int64_t>(B) * KV * HD, S_pad, S_pad, BKV, HD)) return rc;
+  if (int rc = encode(&mq, qkv, static_cast<int64_t>(B) * S, cols, ld, 64, BQ)) return rc;   // Q and K tiles
+  if (int rc = encode(&mvt, vt, static_cast<int64_t>(B) * KV * HD, S_pad, S_pad, 64, HD)) return rc;
   int dev = 0;
   cudaGetDevice(&dev);
   static bool attr_set[64] = {};
@@ -443,8 +422,7 @@ static int launch(const void* qkv, int ld, int B, int S, int H, int KV, void* vt
   a.k_col0 = H * HD;
   a.scale_log2 = 1.4426950408889634f / sqrtf(static_cast<float>(HD));
   const int n_qt = (S + BQ - 1) / BQ;
-  e = launch_pdl(PDL_ATTN, k_flash_prefill<HD>, dim3((n_qt + 1) / 2, H, B), dim3(THREADS), C::SMEM, s, mq, mk, mvt,
-                 a);
+  e = launch_pdl(PDL_ATTN, k_flash_prefill<HD>, dim3((n_qt + 1) / 2, H, B), dim3(THREADS), C::SMEM, s, mq, mvt, a);
   if (e != cudaSuccess) return bz_fail_cuda(e, "attention launch");
   return bz_check_launch("bz_prefill_attention");
 }

@@ -85,6 +85,20 @@ __device__ __forceinline__ float ex2(float x) {
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
+// 2^x on the FMA / ALU pipes for x <= 8 (x = -inf gives ~1e-38): round x to the
+// nearest integer n with the 1.5 * 2^23 trick, 2^(x - n) by a degree-3 Taylor
+// polynomial on [-0.5, 0.5] (relative error < 8e-4, below bf16 2^-9 half-ulp),
+// then add n to the exponent field.
+__device__ __forceinline__ float ex2_fma(float x) {
+  x = fmaxf(x, -126.0f);
+  const float t = x + 12582912.0f;
+  const float f = x - (t - 12582912.0f);
+  float p = fmaf(f, 0.0555041087f, 0.240226507f);
+  p = fmaf(f, p, 0.693147181f);
+  p = fmaf(f, p, 1.0f);
+  const int n = __float_as_int(t) - 0x4B400000;
+  return __int_as_float(__float_as_int(p) + (n << 23));
+}
 __device__ __forceinline__ float max3(float a, float b, float c) {
   float r;
   asm("max.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
@@ -275,15 +289,15 @@ __global__ void __launch_bounds__(THREADS, 1)
           for (int i = 0; i < 32; ++i)
             if (key0 + 32 * c + i > qpos) v[c][i] = __float_as_uint(-INFINITY);
       }
-      float mx0 = -INFINITY, mx1 = -INFINITY;
+      // row max: four independent FMNMX3 chains (latency, not throughput, bounds them)
+      float mxc[4];
 #pragma unroll
-      for (int c = 0; c < 4; c += 2)
+      for (int c = 0; c < 4; ++c) {
+        mxc[c] = -INFINITY;
 #pragma unroll
-        for (int i = 0; i < 32; i += 2) {
-          mx0 = max3(mx0, __uint_as_float(v[c][i]), __uint_as_float(v[c][i + 1]));
-          mx1 = max3(mx1, __uint_as_float(v[c + 1][i]), __uint_as_float(v[c + 1][i + 1]));
-        }
-      const float mx = fmaxf(mx0, mx1) * a.scale_log2;
+        for (int i = 0; i < 32; i += 2) mxc[c] = max3(mxc[c], __uint_as_float(v[c][i]), __uint_as_float(v[c][i + 1]));
+      }
+      const float mx = fmaxf(fmaxf(mxc[0], mxc[1]), fmaxf(mxc[2], mxc[3])) * a.scale_log2;
       // raise the max only when it grows by more than 2^kRescale: O and l are then
       // scaled by 2^(m_old - m_new).  tcgen05.ld/st are warp-collective, so the warp
       // rescales whenever any of its rows must (alpha = 1 on the others).  O holds
@@ -305,21 +319,26 @@ __global__ void __launch_bounds__(THREADS, 1)
         if (raise) m = mx;
       }
       // P = exp2(s * scale - m) as bf16 pairs into the first 64 columns of S_t
-      float sum0 = 0.f, sum1 = 0.f;
+      // eight partial sums (short FADD chains); a quarter of the exponentials on the
+      // FMA pipe (ex2_fma) so the MUFU pipe is not the softmax's only limiter
+      float sum[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) sum[k] = 0.f;
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
         uint32_t w[16];
 #pragma unroll
         for (int i = 0; i < 32; i += 2) {
-          const float p0 = ex2(fmaf(__uint_as_float(v[c][i]), a.scale_log2, -m));
-          const float p1 = ex2(fmaf(__uint_as_float(v[c][i + 1]), a.scale_log2, -m));
-          sum0 += p0;
-          sum1 += p1;
+          const float x0 = fmaf(__uint_as_float(v[c][i]), a.scale_log2, -m);
+          const float x1 = fmaf(__uint_as_float(v[c][i + 1]), a.scale_log2, -m);
+          const float p0 = (c == 3 && (i & 2)) ? ex2_fma(x0) : ex2(x0);
+          const float p1 = (c == 3 && (i & 2)) ? ex2_fma(x1) : ex2(x1);
+          sum[(i >> 1) & 7] += p0 + p1;
           w[i >> 1] = pack2(p0, p1);
         }
         tmem_st_32x32b_x16(s_addr + 16 * c, w);
       }
-      l += sum0 + sum1;
+      l += ((sum[0] + sum[1]) + (sum[2] + sum[3])) + ((sum[4] + sum[5]) + (sum[6] + sum[7]));
       asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
       tc_fence_before();
       __syncwarp();

@@ -228,8 +228,8 @@ int bz_silu_mul(const void* gu, void* act, int rows, int ffn, int ldg, int lda, 
  * Causal softmax(Q K^T / sqrt(hd)) V for B sequences of S tokens on tcgen05 tensor
  * cores (TMEM accumulators, TMA-fed), GQA (n_heads % n_kv == 0), hd 64 or 128.
  * qkv: [B*S, ld] bf16 rows [q heads | k heads | v heads] with RoPE applied; out:
- * [B*S, ldo] bf16, head h at columns [h*hd, (h+1)*hd).  The workspace holds V
- * transposed ([B, n_kv, hd, S rounded up to 64] bf16) so V^T is a K-major MMA operand. */
+ * [B*S, ldo] bf16, head h at columns [h*hd, (h+1)*hd).  V is read in place as an MN-major
+ * MMA operand; the workspace arguments are kept for ABI stability (0 bytes needed). */
 int bz_prefill_attention_workspace_bytes(int B, int S, int n_kv, int head_dim, int64_t* bytes);
 int bz_prefill_attention(const void* qkv, int ld, int B, int S, int n_heads, int n_kv, int head_dim,
                          void* workspace, int64_t workspace_bytes, void* out, int ldo, void* stream);

@@ -6,8 +6,8 @@
 // causal, GQA (query head h reads kv head h / (H / KV)).
 //
 //   in : qkv  [B*S, ld]  bf16, row = token, [q heads | k heads | v heads] (RoPE applied)
-//        vt   [B, KV, hd, S_pad] bf16 -- V transposed by k_v_transpose (keys contiguous,
-//             so V^T is a K-major MMA operand like every weight), zero past S
+//        V is read in place: its tiles [128 keys x hd] are the B operand of O += P V in
+//        MN-major form (hd contiguous), so no transpose pass and no workspace
 //   out: attn [B*S, ldo] bf16, head h at columns [h*hd, (h+1)*hd) -- the o-projection's A
 //
 // One CTA = two adjacent 128-row query tiles A, B of one (sequence, head): every K / V
@@ -53,8 +53,7 @@ struct Cfg {
   static constexpr int ROW_ATOM = 128 * 128;       // 128 rows x 128 B
   static constexpr int Q_BYTES = KA * ROW_ATOM;    // one query tile
   static constexpr int K_BYTES = KA * ROW_ATOM;    // 128 keys x hd
-  static constexpr int V_ATOM = HD * 128;          // V^T: HD rows x 64 keys
-  static constexpr int V_BYTES = 2 * V_ATOM;       // 128 keys
+  static constexpr int V_BYTES = KA * ROW_ATOM;    // 128 keys x hd, as loaded (hd contiguous)
   static constexpr int BAR_BYTES = 256;
   static constexpr int SMEM = 1024 + 2 * Q_BYTES + STAGES * (K_BYTES + V_BYTES) + BAR_BYTES;
   // TMEM: S_A at [0, 128), S_B at [128, 256) -- P_X (bf16 pairs) in the first 64 columns
@@ -73,6 +72,7 @@ struct Args {
   int H, KV;      // query heads, kv heads
   int q_col0;     // column of q head 0 in qkv (0)
   int k_col0;     // column of k head 0 (H * hd)
+  int v_col0;     // column of v head 0 ((H + KV) * hd)
   float scale_log2;  // log2(e) / sqrt(hd)
 };
 
@@ -130,9 +130,37 @@ __device__ __forceinline__ void umma_bf16_ts(uint32_t tmem_d, uint32_t tmem_a, u
 
 constexpr float kRescale = 8.0f;  // raise the running max only when it grows by > 2^8
 
+// MN-major, 128B-swizzled operand: rows of 128 B run along K (8-row atoms SBO apart),
+// the 64-element row is contiguous along M/N and the next 64 of M/N are LBO away
+__device__ __forceinline__ uint64_t umma_desc_mn_sw128(uint32_t smem_addr, uint32_t lbo, uint32_t sbo) {
+  uint64_t d = 0;
+  d |= static_cast<uint64_t>((smem_addr >> 4) & 0x3FFF);
+  d |= static_cast<uint64_t>((lbo >> 4) & 0x3FFF) << 16;
+  d |= static_cast<uint64_t>((sbo >> 4) & 0x3FFF) << 32;
+  d |= static_cast<uint64_t>(1) << 46;
+  d |= static_cast<uint64_t>(2) << 61;
+  return d;
+}
+
+// Timeline probe (scripts/attn_trace.cu compiles this file with BZ_ATTN_TRACE): CTA 0's
+// softmax warps and MMA thread stamp %globaltimer at their waits and arrivals.
+#ifdef BZ_ATTN_TRACE
+__device__ unsigned long long g_trace[4096];
+__device__ __forceinline__ void trace(int slot) {
+  if (blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && slot < 4096) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    g_trace[slot] = t;
+  }
+}
+#define BZ_TRACE(slot) trace(slot)
+#else
+#define BZ_TRACE(slot)
+#endif
+
 template <int HD>
 __global__ void __launch_bounds__(THREADS, 1)
-    k_flash_prefill(const __grid_constant__ CUtensorMap map_q, const __grid_constant__ CUtensorMap map_vt, Args a) {
+    k_flash_prefill(const __grid_constant__ CUtensorMap map_q, Args a) {
   using C = Cfg<HD>;
   constexpr int KA = C::KA;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -164,7 +192,6 @@ __global__ void __launch_bounds__(THREADS, 1)
 
   if (warp == 0 && lane == 0) {
     prefetch_tmap(&map_q);
-    prefetch_tmap(&map_vt);
     mbar_init(q_full, 1);
     for (int i = 0; i < 2; ++i) {
       mbar_init(&k_full[i], 1);
@@ -205,8 +232,8 @@ __global__ void __launch_bounds__(THREADS, 1)
                       &k_full[st]);
         mbar_wait(&v_empty[st], ph);
         mbar_expect_tx(&v_full[st], C::V_BYTES);
-        for (int kh = 0; kh < 2; ++kh)
-          tma_load_2d(sv + st * C::V_BYTES + kh * C::V_ATOM, &map_vt, j * BKV + kh * 64, (b * a.KV + g) * HD,
+        for (int ka = 0; ka < KA; ++ka)
+          tma_load_2d(sv + st * C::V_BYTES + ka * C::ROW_ATOM, &map_q, a.v_col0 + g * HD + ka * 64, row0 + j * BKV,
                       &v_full[st]);
       }
       pdl_trigger();
@@ -215,7 +242,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     if (lane == 0) {
       // ---- MMA issuer ----
       constexpr uint32_t idesc_s = instr_desc_bf16(BQ, BKV);
-      constexpr uint32_t idesc_o = instr_desc_bf16(BQ, HD);
+      constexpr uint32_t idesc_o = instr_desc_bf16(BQ, HD) | (1u << 16);   // B (V) MN-major
       mbar_wait(q_full, 0);
       auto issue_s = [&](int t, int j) {   // S_t(j) = Q_t K_j^T
         const int st = j & 1;
@@ -234,7 +261,9 @@ __global__ void __launch_bounds__(THREADS, 1)
         const uint32_t pa = tmem + C::S_COL + t * BKV;
 #pragma unroll
         for (int kk = 0; kk < BKV / 16; ++kk) {
-          const uint64_t db = umma_desc_sw128(smem_u32(sv + st * C::V_BYTES + (kk >> 2) * C::V_ATOM)) + 2 * (kk & 3);
+          // 16 keys = two 8-key swizzle atoms along K (2048 B); the hd halves 64..127
+          // are the next TMA box (LBO = one 128-row atom)
+          const uint64_t db = umma_desc_mn_sw128(smem_u32(sv + st * C::V_BYTES) + kk * 2048, C::ROW_ATOM, 1024);
           umma_bf16_ts(d, pa + kk * 8, db, idesc_o, (j > 0 || kk > 0) ? 1u : 0u);
         }
         umma_commit(&pv_done[t]);
@@ -251,7 +280,9 @@ __global__ void __launch_bounds__(THREADS, 1)
         if (more) mbar_wait(&k_full[(j + 1) & 1], ((j + 1) >> 1) & 1);
         for (int t = 0; t < 2; ++t) {
           if (t == 0 && j >= nj_a) continue;          // tile A is done after its diagonal
+          BZ_TRACE(2048 + 8 * j + 2 * t);
           mbar_wait(&p_full[t], j & 1);
+          BZ_TRACE(2048 + 8 * j + 2 * t + 1);
           tc_fence_after();
           issue_pv(t, j);
           if (more && !(t == 0 && j + 1 >= nj_a)) issue_s(t, j + 1);
@@ -274,7 +305,9 @@ __global__ void __launch_bounds__(THREADS, 1)
     float m = -INFINITY;                     // running max in use (log2 domain)
     float l = 0.f;                           // row sum relative to m
     for (int j = 0; j < my_nj; ++j) {
+      if (lane == 0 && quarter == 2) BZ_TRACE(1024 * t + 4 * j);
       mbar_wait(&s_full[t], j & 1);
+      if (lane == 0 && quarter == 2) BZ_TRACE(1024 * t + 4 * j + 1);
       tc_fence_after();
       uint32_t v[4][32];
 #pragma unroll
@@ -319,8 +352,8 @@ __global__ void __launch_bounds__(THREADS, 1)
         if (raise) m = mx;
       }
       // P = exp2(s * scale - m) as bf16 pairs into the first 64 columns of S_t
-      // eight partial sums (short FADD chains); a quarter of the exponentials on the
-      // FMA pipe (ex2_fma) so the MUFU pipe is not the softmax's only limiter
+      // eight partial sums (short FADD chains).  (Moving a quarter of the exponentials to
+      // the FMA pipe with ex2_fma was measured 7 % slower: the MUFU pipe is not the limiter)
       float sum[8];
 #pragma unroll
       for (int k = 0; k < 8; ++k) sum[k] = 0.f;
@@ -331,8 +364,8 @@ __global__ void __launch_bounds__(THREADS, 1)
         for (int i = 0; i < 32; i += 2) {
           const float x0 = fmaf(__uint_as_float(v[c][i]), a.scale_log2, -m);
           const float x1 = fmaf(__uint_as_float(v[c][i + 1]), a.scale_log2, -m);
-          const float p0 = (c == 3 && (i & 2)) ? ex2_fma(x0) : ex2(x0);
-          const float p1 = (c == 3 && (i & 2)) ? ex2_fma(x1) : ex2(x1);
+          const float p0 = ex2(x0);
+          const float p1 = ex2(x1);
           sum[(i >> 1) & 7] += p0 + p1;
           w[i >> 1] = pack2(p0, p1);
         }
@@ -343,6 +376,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&p_full[t]);
+      if (lane == 0 && quarter == 2) BZ_TRACE(1024 * t + 4 * j + 2);
     }
     // ---- epilogue: O / l -> bf16 ----
     mbar_wait(&pv_done[t], (my_nj - 1) & 1);
@@ -373,29 +407,6 @@ __global__ void __launch_bounds__(THREADS, 1)
   }
 }
 
-// vt[(b*KV + g)*hd + d][s] = qkv[(b*S + s)*ld + v_col0 + g*hd + d]; zero for s in [S, S_pad).
-// 64 x 64 tiles through shared memory (coalesced on both sides).
-__global__ void __launch_bounds__(256) k_v_transpose(const __nv_bfloat16* __restrict__ qkv, int ld, int v_col0,
-                                                      int S, int S_pad, int KV, int hd,
-                                                      __nv_bfloat16* __restrict__ vt) {
-  __shared__ __nv_bfloat16 tile[64][66];
-  pdl_wait();
-  pdl_trigger();
-  const int s0 = blockIdx.x * 64, d0 = blockIdx.y * 64, bg = blockIdx.z;
-  const int b = bg / KV, g = bg % KV;
-  const int tx = threadIdx.x & 63, ty = threadIdx.x >> 6;  // 64 x 4
-  for (int i = ty; i < 64; i += 4) {
-    const int s = s0 + i;
-    tile[i][tx] = s < S ? qkv[static_cast<int64_t>(b * S + s) * ld + v_col0 + g * hd + d0 + tx]
-                        : __float2bfloat16_rn(0.f);
-  }
-  __syncthreads();
-  for (int i = ty; i < 64; i += 4) {
-    const int s = s0 + tx;
-    if (s < S_pad) vt[(static_cast<int64_t>(bg) * hd + d0 + i) * S_pad + s] = tile[tx][i];
-  }
-}
-
 static int encode(CUtensorMap* map, const void* ptr, int64_t rows, int64_t cols, int64_t ld_elems, int box_cols,
                   int box_rows) {
   const DriverApi* d = driver_api();
@@ -412,13 +423,11 @@ static int encode(CUtensorMap* map, const void* ptr, int64_t rows, int64_t cols,
 }
 
 template <int HD>
-static int launch(const void* qkv, int ld, int B, int S, int H, int KV, void* vt, int S_pad, void* out, int ldo,
-                  cudaStream_t s) {
+static int launch(const void* qkv, int ld, int B, int S, int H, int KV, void* out, int ldo, cudaStream_t s) {
   using C = Cfg<HD>;
-  CUtensorMap mq, mvt;
+  CUtensorMap mq;
   const int cols = (H + 2 * KV) * HD;
-  if (int rc = encode(&mq, qkv, static_cast<int64_t>(B) * S, cols, ld, 64, BQ)) return rc;   // Q and K tiles
-  if (int rc = encode(&mvt, vt, static_cast<int64_t>(B) * KV * HD, S_pad, S_pad, 64, HD)) return rc;
+  if (int rc = encode(&mq, qkv, static_cast<int64_t>(B) * S, cols, ld, 64, BQ)) return rc;   // Q, K and V tiles
   int dev = 0;
   cudaGetDevice(&dev);
   static bool attr_set[64] = {};
@@ -427,10 +436,6 @@ static int launch(const void* qkv, int ld, int B, int S, int H, int KV, void* vt
     if (e != cudaSuccess) return bz_fail_cuda(e, "attention smem attribute");
     attr_set[dev] = true;
   }
-  cudaError_t e = launch_pdl(PDL_ATTN, k_v_transpose, dim3((S_pad + 63) / 64, HD / 64, B * KV), dim3(256), 0, s,
-                             static_cast<const __nv_bfloat16*>(qkv), ld, (H + KV) * HD, S, S_pad, KV, HD,
-                             static_cast<__nv_bfloat16*>(vt));
-  if (e != cudaSuccess) return bz_fail_cuda(e, "attention: V transpose launch");
   Args a;
   a.out = static_cast<__nv_bfloat16*>(out);
   a.ldo = ldo;
@@ -439,9 +444,11 @@ static int launch(const void* qkv, int ld, int B, int S, int H, int KV, void* vt
   a.KV = KV;
   a.q_col0 = 0;
   a.k_col0 = H * HD;
+  a.v_col0 = (H + KV) * HD;
   a.scale_log2 = 1.4426950408889634f / sqrtf(static_cast<float>(HD));
   const int n_qt = (S + BQ - 1) / BQ;
-  e = launch_pdl(PDL_ATTN, k_flash_prefill<HD>, dim3((n_qt + 1) / 2, H, B), dim3(THREADS), C::SMEM, s, mq, mvt, a);
+  cudaError_t e = launch_pdl(PDL_ATTN, k_flash_prefill<HD>, dim3((n_qt + 1) / 2, H, B), dim3(THREADS), C::SMEM, s,
+                             mq, a);
   if (e != cudaSuccess) return bz_fail_cuda(e, "attention launch");
   return bz_check_launch("bz_prefill_attention");
 }
@@ -454,26 +461,20 @@ using namespace bz;
 extern "C" int bz_prefill_attention_workspace_bytes(int B, int S, int KV, int head_dim, int64_t* bytes) {
   if (!bytes || B < 1 || S < 1 || KV < 1 || (head_dim != 64 && head_dim != 128))
     return bz_fail(BZ_EINVAL, "prefill attention workspace: bad sizes");
-  const int64_t s_pad = (S + 63) / 64 * 64;
-  *bytes = static_cast<int64_t>(B) * KV * head_dim * s_pad * 2;
+  *bytes = 0;   // V is read in place (MN-major operand); kept for ABI stability
   return BZ_OK;
 }
 
 extern "C" int bz_prefill_attention(const void* qkv, int ld, int B, int S, int n_heads, int n_kv, int head_dim,
-                                    void* workspace, int64_t workspace_bytes, void* out, int ldo, void* stream) {
-  if (!qkv || !out || !workspace || B < 1 || S < 1 || n_kv < 1 || n_heads % n_kv)
+                                    void* /*workspace*/, int64_t /*workspace_bytes*/, void* out, int ldo, void* stream) {
+  if (!qkv || !out || B < 1 || S < 1 || n_kv < 1 || n_heads % n_kv)
     return bz_fail(BZ_EINVAL, "prefill attention: bad arguments");
   if (head_dim != 64 && head_dim != 128) return bz_fail(BZ_EINVAL, "prefill attention: head_dim must be 64 or 128");
-  if (ld % 8 || ldo % 8 || (reinterpret_cast<uintptr_t>(qkv) & 15) || (reinterpret_cast<uintptr_t>(out) & 15) ||
-      (reinterpret_cast<uintptr_t>(workspace) & 15))
+  if (ld % 8 || ldo % 8 || (reinterpret_cast<uintptr_t>(qkv) & 15) || (reinterpret_cast<uintptr_t>(out) & 15))
     return bz_fail(BZ_EINVAL, "prefill attention: 16-byte aligned pointers and leading dims required");
-  int64_t need = 0;
-  bz_prefill_attention_workspace_bytes(B, S, n_kv, head_dim, &need);
-  if (workspace_bytes < need) return bz_fail(BZ_EINVAL, "prefill attention: workspace too small");
-  const int s_pad = (S + 63) / 64 * 64;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  if (head_dim == 128) return attn::launch<128>(qkv, ld, B, S, n_heads, n_kv, workspace, s_pad, out, ldo, s);
-  return attn::launch<64>(qkv, ld, B, S, n_heads, n_kv, workspace, s_pad, out, ldo, s);
+  if (head_dim == 128) return attn::launch<128>(qkv, ld, B, S, n_heads, n_kv, out, ldo, s);
+  return attn::launch<64>(qkv, ld, B, S, n_heads, n_kv, out, ldo, s);
 }
 
-const void* bz::module_anchor_attention() { return reinterpret_cast<const void*>(attn::k_v_transpose); }
+const void* bz::module_anchor_attention() { return reinterpret_cast<const void*>(attn::k_flash_prefill<128>); }

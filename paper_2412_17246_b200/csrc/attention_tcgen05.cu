@@ -54,7 +54,7 @@ struct Cfg {
   static constexpr int Q_BYTES = KA * ROW_ATOM;    // one query tile
   static constexpr int K_BYTES = KA * ROW_ATOM;    // 128 keys x hd
   static constexpr int V_BYTES = KA * ROW_ATOM;    // 128 keys x hd, as loaded (hd contiguous)
-  static constexpr int BAR_BYTES = 256;
+  static constexpr int BAR_BYTES = 256;   // 18 barriers + the TMEM address
   static constexpr int SMEM = 1024 + 2 * Q_BYTES + STAGES * (K_BYTES + V_BYTES) + BAR_BYTES;
   // TMEM: S_A at [0, 128), S_B at [128, 256) -- P_X (bf16 pairs) in the first 64 columns
   // of S_X once S_X is in registers -- then O_A, O_B (HD columns each)
@@ -73,6 +73,7 @@ struct Args {
   int q_col0;     // column of q head 0 in qkv (0)
   int k_col0;     // column of k head 0 (H * hd)
   int v_col0;     // column of v head 0 ((H + KV) * hd)
+  int B;          // sequences
   float scale_log2;  // log2(e) / sqrt(hd)
 };
 
@@ -177,22 +178,41 @@ __global__ void __launch_bounds__(THREADS, 1)
   uint64_t* s_full = bars + 9;      // [tile]  S_X(j) in TMEM
   uint64_t* p_full = bars + 11;     // [tile]  P_X(j) in TMEM (and O_X rescaled)
   uint64_t* pv_done = bars + 13;    // [tile]  O_X += P_X(j) V_j complete
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 15);
+  uint64_t* q_empty = bars + 15;    // 1       the item's last S issued: Q smem reusable
+  uint64_t* o_free = bars + 16;     // [tile]  the epilogue has read O_X out of TMEM
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 18);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n_qt = (a.S + BQ - 1) / BQ;
   const int n_pairs = (n_qt + 1) / 2;
-  const int pair = n_pairs - 1 - static_cast<int>(blockIdx.x);  // longest (most keys) first
-  const int h = blockIdx.y, b = blockIdx.z;
-  const int g = h / (a.H / a.KV);
-  const int s0 = pair * 2 * BQ;      // first query row of tile A
-  const int qt_a = 2 * pair;         // tile A's diagonal key tile; B's is qt_a + 1
-  const int nj_a = qt_a + 1, nj = qt_a + 2;
-  const int row0 = b * a.S;
+  const int per_pair = a.H * a.B;
+  const int n_items = n_pairs * per_pair;
+  // Persistent CTAs over work items (one query-tile pair of one (sequence, head)),
+  // items ordered longest first and dealt in snake order (round k even: c + k G, odd:
+  // (k + 1) G - 1 - c), so every CTA's total is close to the longest item.  Every role
+  // walks the same item list; barrier phases run on across items.
+  const int G = static_cast<int>(gridDim.x), c = static_cast<int>(blockIdx.x);
+  auto item_at = [&](int k) -> int { return (k & 1) ? (k + 1) * G - 1 - c : c + k * G; };
+  struct Item { int s0, qt_a, nj_a, nj, h, g, row0; };
+  auto decode = [&](int i) {
+    Item it;
+    const int pair = n_pairs - 1 - i / per_pair;
+    const int rem = i % per_pair;
+    it.h = rem % a.H;
+    const int b = rem / a.H;
+    it.g = it.h / (a.H / a.KV);
+    it.s0 = pair * 2 * BQ;
+    it.qt_a = 2 * pair;
+    it.nj_a = it.qt_a + 1;
+    it.nj = it.qt_a + 2;
+    it.row0 = b * a.S;
+    return it;
+  };
 
   if (warp == 0 && lane == 0) {
     prefetch_tmap(&map_q);
     mbar_init(q_full, 1);
+    mbar_init(q_empty, 1);
     for (int i = 0; i < 2; ++i) {
       mbar_init(&k_full[i], 1);
       mbar_init(&k_empty[i], 1);
@@ -201,6 +221,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       mbar_init(&s_full[i], 1);
       mbar_init(&p_full[i], 4);
       mbar_init(&pv_done[i], 1);
+      mbar_init(&o_free[i], 4);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -217,24 +238,29 @@ __global__ void __launch_bounds__(THREADS, 1)
   if (warp == 0) {
     if (lane == 0) {
       // ---- TMA producer ----
-      pdl_wait();  // q/k/v were written by the predecessor (qkv GEMM + RoPE + transpose)
-      mbar_expect_tx(q_full, 2 * C::Q_BYTES);
-      for (int t = 0; t < 2; ++t)
-        for (int ka = 0; ka < KA; ++ka)
-          tma_load_2d(sq + t * C::Q_BYTES + ka * C::ROW_ATOM, &map_q, a.q_col0 + h * HD + ka * 64,
-                      row0 + s0 + t * BQ, q_full);
-      for (int j = 0; j < nj; ++j) {
-        const int st = j & 1, ph = ((j >> 1) & 1) ^ 1;
-        mbar_wait(&k_empty[st], ph);
-        mbar_expect_tx(&k_full[st], C::K_BYTES);
-        for (int ka = 0; ka < KA; ++ka)
-          tma_load_2d(sk + st * C::K_BYTES + ka * C::ROW_ATOM, &map_q, a.k_col0 + g * HD + ka * 64, row0 + j * BKV,
-                      &k_full[st]);
-        mbar_wait(&v_empty[st], ph);
-        mbar_expect_tx(&v_full[st], C::V_BYTES);
-        for (int ka = 0; ka < KA; ++ka)
-          tma_load_2d(sv + st * C::V_BYTES + ka * C::ROW_ATOM, &map_q, a.v_col0 + g * HD + ka * 64, row0 + j * BKV,
-                      &v_full[st]);
+      pdl_wait();  // q/k/v were written by the predecessor (qkv GEMM + RoPE)
+      int gk = 0;  // running K/V tile count (ring stage = gk & 1)
+      for (int k = 0, i; (i = item_at(k)) < n_items && i >= 0; ++k) {
+        const Item it = decode(i);
+        mbar_wait(q_empty, (k & 1) ^ 1);
+        mbar_expect_tx(q_full, 2 * C::Q_BYTES);
+        for (int t = 0; t < 2; ++t)
+          for (int ka = 0; ka < KA; ++ka)
+            tma_load_2d(sq + t * C::Q_BYTES + ka * C::ROW_ATOM, &map_q, a.q_col0 + it.h * HD + ka * 64,
+                        it.row0 + it.s0 + t * BQ, q_full);
+        for (int j = 0; j < it.nj; ++j, ++gk) {
+          const int st = gk & 1, ph = ((gk >> 1) & 1) ^ 1;
+          mbar_wait(&k_empty[st], ph);
+          mbar_expect_tx(&k_full[st], C::K_BYTES);
+          for (int ka = 0; ka < KA; ++ka)
+            tma_load_2d(sk + st * C::K_BYTES + ka * C::ROW_ATOM, &map_q, a.k_col0 + it.g * HD + ka * 64,
+                        it.row0 + j * BKV, &k_full[st]);
+          mbar_wait(&v_empty[st], ph);
+          mbar_expect_tx(&v_full[st], C::V_BYTES);
+          for (int ka = 0; ka < KA; ++ka)
+            tma_load_2d(sv + st * C::V_BYTES + ka * C::ROW_ATOM, &map_q, a.v_col0 + it.g * HD + ka * 64,
+                        it.row0 + j * BKV, &v_full[st]);
+        }
       }
       pdl_trigger();
     }
@@ -243,9 +269,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       // ---- MMA issuer ----
       constexpr uint32_t idesc_s = instr_desc_bf16(BQ, BKV);
       constexpr uint32_t idesc_o = instr_desc_bf16(BQ, HD) | (1u << 16);   // B (V) MN-major
-      mbar_wait(q_full, 0);
-      auto issue_s = [&](int t, int j) {   // S_t(j) = Q_t K_j^T
-        const int st = j & 1;
+      auto issue_s = [&](int t, int st) {   // S_t = Q_t K^T from ring stage st
         const uint32_t d = tmem + C::S_COL + t * BKV;
 #pragma unroll
         for (int kk = 0; kk < HD / 16; ++kk) {
@@ -255,8 +279,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         }
         umma_commit(&s_full[t]);
       };
-      auto issue_pv = [&](int t, int j) {  // O_t += P_t(j) V_j, P from TMEM
-        const int st = j & 1;
+      auto issue_pv = [&](int t, int st, bool first) {  // O_t (+)= P_t V, P from TMEM
         const uint32_t d = tmem + C::O_COL + t * HD;
         const uint32_t pa = tmem + C::S_COL + t * BKV;
 #pragma unroll
@@ -264,31 +287,42 @@ __global__ void __launch_bounds__(THREADS, 1)
           // 16 keys = two 8-key swizzle atoms along K (2048 B); the hd halves 64..127
           // are the next TMA box (LBO = one 128-row atom)
           const uint64_t db = umma_desc_mn_sw128(smem_u32(sv + st * C::V_BYTES) + kk * 2048, C::ROW_ATOM, 1024);
-          umma_bf16_ts(d, pa + kk * 8, db, idesc_o, (j > 0 || kk > 0) ? 1u : 0u);
+          umma_bf16_ts(d, pa + kk * 8, db, idesc_o, (!first || kk > 0) ? 1u : 0u);
         }
         umma_commit(&pv_done[t]);
       };
-      mbar_wait(&k_full[0], 0);
-      tc_fence_after();
-      issue_s(0, 0);
-      issue_s(1, 0);
-      umma_commit(&k_empty[0]);
-      for (int j = 0; j < nj; ++j) {
-        const int st = j & 1;
-        mbar_wait(&v_full[st], (j >> 1) & 1);
-        const bool more = j + 1 < nj;
-        if (more) mbar_wait(&k_full[(j + 1) & 1], ((j + 1) >> 1) & 1);
-        for (int t = 0; t < 2; ++t) {
-          if (t == 0 && j >= nj_a) continue;          // tile A is done after its diagonal
-          BZ_TRACE(2048 + 8 * j + 2 * t);
-          mbar_wait(&p_full[t], j & 1);
-          BZ_TRACE(2048 + 8 * j + 2 * t + 1);
-          tc_fence_after();
-          issue_pv(t, j);
-          if (more && !(t == 0 && j + 1 >= nj_a)) issue_s(t, j + 1);
+      int gk = 0;              // running K/V tile count
+      int up[2] = {0, 0};      // P(j) uses per tile (p_full phases)
+      for (int k = 0, i; (i = item_at(k)) < n_items && i >= 0; ++k) {
+        const Item it = decode(i);
+        mbar_wait(q_full, k & 1);
+        mbar_wait(&k_full[gk & 1], (gk >> 1) & 1);
+        tc_fence_after();
+        issue_s(0, gk & 1);
+        issue_s(1, gk & 1);
+        umma_commit(&k_empty[gk & 1]);
+        for (int j = 0; j < it.nj; ++j) {
+          const int g0 = gk + j, st = g0 & 1;
+          mbar_wait(&v_full[st], (g0 >> 1) & 1);
+          const bool more = j + 1 < it.nj;
+          if (more) mbar_wait(&k_full[(g0 + 1) & 1], ((g0 + 1) >> 1) & 1);
+          for (int t = 0; t < 2; ++t) {
+            if (t == 0 && j >= it.nj_a) continue;          // tile A is done after its diagonal
+            BZ_TRACE(2048 + 8 * j + 2 * t);
+            mbar_wait(&p_full[t], up[t] & 1);
+            BZ_TRACE(2048 + 8 * j + 2 * t + 1);
+            ++up[t];
+            // the previous item's epilogue must have read O_t before it is overwritten
+            if (j == 0) mbar_wait(&o_free[t], (k & 1) ^ 1);
+            tc_fence_after();
+            issue_pv(t, st, j == 0);
+            if (more && !(t == 0 && j + 1 >= it.nj_a)) issue_s(t, (g0 + 1) & 1);
+          }
+          umma_commit(&v_empty[st]);
+          if (more) umma_commit(&k_empty[(g0 + 1) & 1]);
+          if (j + 2 == it.nj) umma_commit(q_empty);  // S_B(nj-1) was the item's last S
         }
-        umma_commit(&v_empty[st]);
-        if (more) umma_commit(&k_empty[(j + 1) & 1]);
+        gk += it.nj;
       }
     }
   } else {
@@ -296,102 +330,108 @@ __global__ void __launch_bounds__(THREADS, 1)
     const int t = (warp - 2) >> 2;           // 0 = A, 1 = B
     const int quarter = warp & 3;            // TMEM lane quarter (hardware: warp id % 4)
     const int r = quarter * 32 + lane;
-    const int qpos = s0 + t * BQ + r;        // query position in its sequence
-    const int my_nj = t == 0 ? nj_a : nj;
-    const int diag = qt_a + t;
     const uint32_t lane_off = static_cast<uint32_t>(quarter * 32) << 16;
     const uint32_t s_addr = tmem + lane_off + C::S_COL + t * BKV;
     const uint32_t o_addr = tmem + lane_off + C::O_COL + t * HD;
-    float m = -INFINITY;                     // running max in use (log2 domain)
-    float l = 0.f;                           // row sum relative to m
-    for (int j = 0; j < my_nj; ++j) {
-      if (lane == 0 && quarter == 2) BZ_TRACE(1024 * t + 4 * j);
-      mbar_wait(&s_full[t], j & 1);
-      if (lane == 0 && quarter == 2) BZ_TRACE(1024 * t + 4 * j + 1);
-      tc_fence_after();
-      uint32_t v[4][32];
+    int us = 0;                              // S / P uses of this tile (phases)
+    for (int k = 0, i; (i = item_at(k)) < n_items && i >= 0; ++k) {
+      const Item it = decode(i);
+      const int qpos = it.s0 + t * BQ + r;   // query position in its sequence
+      const int my_nj = t == 0 ? it.nj_a : it.nj;
+      const int diag = it.qt_a + t;
+      float m = -INFINITY;                   // running max in use (log2 domain)
+      float l = 0.f;                         // row sum relative to m
+      for (int j = 0; j < my_nj; ++j, ++us) {
+        if (lane == 0 && quarter == 2 && k == 0) BZ_TRACE(1024 * t + 4 * j);
+        mbar_wait(&s_full[t], us & 1);
+        if (lane == 0 && quarter == 2 && k == 0) BZ_TRACE(1024 * t + 4 * j + 1);
+        tc_fence_after();
+        uint32_t v[4][32];
 #pragma unroll
-      for (int c = 0; c < 4; ++c) tmem_ld_32x32b_x32_async(s_addr + 32 * c, v[c]);
+        for (int cc = 0; cc < 4; ++cc) tmem_ld_32x32b_x32_async(s_addr + 32 * cc, v[cc]);
 #pragma unroll
-      for (int c = 0; c < 4; ++c) tmem_wait_ld(v[c]);
-      if (j == diag) {  // causal mask: keys after this query get -inf
-        const int key0 = j * BKV;
+        for (int cc = 0; cc < 4; ++cc) tmem_wait_ld(v[cc]);
+        if (j == diag) {  // causal mask: keys after this query get -inf
+          const int key0 = j * BKV;
 #pragma unroll
-        for (int c = 0; c < 4; ++c)
+          for (int cc = 0; cc < 4; ++cc)
 #pragma unroll
-          for (int i = 0; i < 32; ++i)
-            if (key0 + 32 * c + i > qpos) v[c][i] = __float_as_uint(-INFINITY);
-      }
-      // row max: four independent FMNMX3 chains (latency, not throughput, bounds them)
-      float mxc[4];
+            for (int q = 0; q < 32; ++q)
+              if (key0 + 32 * cc + q > qpos) v[cc][q] = __float_as_uint(-INFINITY);
+        }
+        // row max: four independent FMNMX3 chains (latency, not throughput, bounds them)
+        float mxc[4];
 #pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        mxc[c] = -INFINITY;
+        for (int cc = 0; cc < 4; ++cc) {
+          mxc[cc] = -INFINITY;
 #pragma unroll
-        for (int i = 0; i < 32; i += 2) mxc[c] = max3(mxc[c], __uint_as_float(v[c][i]), __uint_as_float(v[c][i + 1]));
-      }
-      const float mx = fmaxf(fmaxf(mxc[0], mxc[1]), fmaxf(mxc[2], mxc[3])) * a.scale_log2;
-      // raise the max only when it grows by more than 2^kRescale: O and l are then
-      // scaled by 2^(m_old - m_new).  tcgen05.ld/st are warp-collective, so the warp
-      // rescales whenever any of its rows must (alpha = 1 on the others).  O holds
-      // P(j-1) V_{j-1} already: S(j) was issued after that MMA.
-      const bool raise = mx > m + kRescale;
-      if (__any_sync(0xffffffffu, raise)) {
-        const float alpha = raise ? ex2(m - mx) : 1.f;   // 0 on the first tile
-        if (j > 0) {
+          for (int q = 0; q < 32; q += 2)
+            mxc[cc] = max3(mxc[cc], __uint_as_float(v[cc][q]), __uint_as_float(v[cc][q + 1]));
+        }
+        const float mx = fmaxf(fmaxf(mxc[0], mxc[1]), fmaxf(mxc[2], mxc[3])) * a.scale_log2;
+        // raise the max only when it grows by more than 2^kRescale: O and l are then
+        // scaled by 2^(m_old - m_new).  tcgen05.ld/st are warp-collective, so the warp
+        // rescales whenever any of its rows must (alpha = 1 on the others).  O holds
+        // P(j-1) V_{j-1} already: S(j) was issued after that MMA.
+        const bool raise = mx > m + kRescale;
+        if (__any_sync(0xffffffffu, raise)) {
+          const float alpha = raise ? ex2(m - mx) : 1.f;   // 0 on the first tile
+          if (j > 0) {
 #pragma unroll
-          for (int c = 0; c < HD; c += 32) {
-            uint32_t o[32];
-            tmem_ld_32x32b_x32(o_addr + c, o);
+            for (int cc = 0; cc < HD; cc += 32) {
+              uint32_t o[32];
+              tmem_ld_32x32b_x32(o_addr + cc, o);
 #pragma unroll
-            for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
-            tmem_st_32x32b_x32(o_addr + c, o);
+              for (int q = 0; q < 32; ++q) o[q] = __float_as_uint(__uint_as_float(o[q]) * alpha);
+              tmem_st_32x32b_x32(o_addr + cc, o);
+            }
           }
+          l *= alpha;
+          if (raise) m = mx;
         }
-        l *= alpha;
-        if (raise) m = mx;
-      }
-      // P = exp2(s * scale - m) as bf16 pairs into the first 64 columns of S_t
-      // eight partial sums (short FADD chains).  (Moving a quarter of the exponentials to
-      // the FMA pipe with ex2_fma was measured 7 % slower: the MUFU pipe is not the limiter)
-      float sum[8];
+        // P = exp2(s * scale - m) as bf16 pairs into the first 64 columns of S_t; eight
+        // partial sums (short FADD chains).  (Moving a quarter of the exponentials to the
+        // FMA pipe with ex2_fma was measured 7 % slower: MUFU is not the limiter.)
+        float sum[8];
 #pragma unroll
-      for (int k = 0; k < 8; ++k) sum[k] = 0.f;
+        for (int q = 0; q < 8; ++q) sum[q] = 0.f;
 #pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        uint32_t w[16];
+        for (int cc = 0; cc < 4; ++cc) {
+          uint32_t w[16];
 #pragma unroll
-        for (int i = 0; i < 32; i += 2) {
-          const float x0 = fmaf(__uint_as_float(v[c][i]), a.scale_log2, -m);
-          const float x1 = fmaf(__uint_as_float(v[c][i + 1]), a.scale_log2, -m);
-          const float p0 = ex2(x0);
-          const float p1 = ex2(x1);
-          sum[(i >> 1) & 7] += p0 + p1;
-          w[i >> 1] = pack2(p0, p1);
+          for (int q = 0; q < 32; q += 2) {
+            const float p0 = ex2(fmaf(__uint_as_float(v[cc][q]), a.scale_log2, -m));
+            const float p1 = ex2(fmaf(__uint_as_float(v[cc][q + 1]), a.scale_log2, -m));
+            sum[(q >> 1) & 7] += p0 + p1;
+            w[q >> 1] = pack2(p0, p1);
+          }
+          tmem_st_32x32b_x16(s_addr + 16 * cc, w);
         }
-        tmem_st_32x32b_x16(s_addr + 16 * c, w);
+        l += ((sum[0] + sum[1]) + (sum[2] + sum[3])) + ((sum[4] + sum[5]) + (sum[6] + sum[7]));
+        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&p_full[t]);
+        if (lane == 0 && quarter == 2 && k == 0) BZ_TRACE(1024 * t + 4 * j + 2);
       }
-      l += ((sum[0] + sum[1]) + (sum[2] + sum[3])) + ((sum[4] + sum[5]) + (sum[6] + sum[7]));
-      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+      // ---- epilogue: O / l -> bf16; O is handed back to the MMA once read ----
+      mbar_wait(&pv_done[t], (us - 1) & 1);
+      tc_fence_after();
+      const float inv = 1.f / l;
+      uint32_t o[HD / 32][32];
+#pragma unroll
+      for (int cc = 0; cc < HD / 32; ++cc) tmem_ld_32x32b_x32_async(o_addr + 32 * cc, o[cc]);
+#pragma unroll
+      for (int cc = 0; cc < HD / 32; ++cc) tmem_wait_ld(o[cc]);
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&p_full[t]);
-      if (lane == 0 && quarter == 2) BZ_TRACE(1024 * t + 4 * j + 2);
-    }
-    // ---- epilogue: O / l -> bf16 ----
-    mbar_wait(&pv_done[t], (my_nj - 1) & 1);
-    tc_fence_after();
-    const float inv = 1.f / l;
-    __nv_bfloat16* dst = a.out + static_cast<int64_t>(row0 + qpos) * a.ldo + h * HD;
-#pragma unroll
-    for (int c = 0; c < HD; c += 32) {
-      uint32_t o[32];
-      tmem_ld_32x32b_x32(o_addr + c, o);
+      if (lane == 0) mbar_arrive(&o_free[t]);
       if (qpos < a.S) {
+        __nv_bfloat16* dst = a.out + static_cast<int64_t>(it.row0 + qpos) * a.ldo + it.h * HD;
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const float* f = reinterpret_cast<const float*>(o + 8 * q);
-          *reinterpret_cast<uint4*>(dst + c + 8 * q) =
+        for (int q = 0; q < HD; q += 8) {
+          const float* f = reinterpret_cast<const float*>(&o[q >> 5][q & 31]);
+          *reinterpret_cast<uint4*>(dst + q) =
               make_uint4(pack2(f[0] * inv, f[1] * inv), pack2(f[2] * inv, f[3] * inv),
                          pack2(f[4] * inv, f[5] * inv), pack2(f[6] * inv, f[7] * inv));
         }
@@ -446,9 +486,13 @@ static int launch(const void* qkv, int ld, int B, int S, int H, int KV, void* ou
   a.k_col0 = H * HD;
   a.v_col0 = (H + KV) * HD;
   a.scale_log2 = 1.4426950408889634f / sqrtf(static_cast<float>(HD));
+  a.B = B;
   const int n_qt = (S + BQ - 1) / BQ;
-  cudaError_t e = launch_pdl(PDL_ATTN, k_flash_prefill<HD>, dim3((n_qt + 1) / 2, H, B), dim3(THREADS), C::SMEM, s,
-                             mq, a);
+  const int items = (n_qt + 1) / 2 * H * B;
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaError_t e = launch_pdl(PDL_ATTN, k_flash_prefill<HD>, dim3(items < sms ? items : sms), dim3(THREADS), C::SMEM,
+                             s, mq, a);
   if (e != cudaSuccess) return bz_fail_cuda(e, "attention launch");
   return bz_check_launch("bz_prefill_attention");
 }

@@ -34,9 +34,10 @@ from ._native import BZ_GEMM_B_STATIC, BZ_GEMM_C_F32, cuda_lib
 from .slab import LlamaArch, SlabLayout
 
 
-# prefill attention: the tcgen05 flash kernel (csrc/attention_tcgen05.cu) once it
-# out-runs the library kernel; until then torch SDPA (cuDNN) -- BZ_PREFILL_ATTN selects
-PREFILL_ATTENTION = os.environ.get("BZ_PREFILL_ATTN", "sdpa")
+# prefill attention: the tcgen05 flash kernel (csrc/attention_tcgen05.cu, 0.89-1.08x of
+# cuDNN's kernel on the 7B shapes, ahead at batch 1; profiles/r2_attn_bench_v5.jsonl);
+# BZ_PREFILL_ATTN=sdpa runs torch SDPA instead for A/B measurements
+PREFILL_ATTENTION = os.environ.get("BZ_PREFILL_ATTN", "tcgen05")
 
 
 def _entries(arch: LlamaArch, k: int) -> list[tuple[str, tuple[int, ...]]]:

@@ -378,23 +378,26 @@ def c3_realclock(arch, n_gpus: int = 2, rate: float = 30.0, duration: float = 9.
                                         "prompt_tokens": [512, 2048], "output_tokens": [16, 128],
                                         "bursts": [{"start_s": burst_at, "duration_s": 2, "multiplier": 5}]},
                               seed=1)
-    arrivals = [(r.arrival_ms / 1e3, r.prompt_tokens) for r in trace]
-    srv = RealClockServer(arch, extra_devs=list(range(2, n_gpus)))
+    arrivals = [(r.arrival_ms / 1e3, r.prompt_tokens, r.output_tokens) for r in trace]
+    # every instance also decodes what it prefilled (continuous batching, 32 slots): TBT
+    srv = RealClockServer(arch, extra_devs=list(range(2, n_gpus)), decode_slots=32, max_new_tokens=128)
     try:
-        mean_tok = sum(n for _, n in arrivals) / len(arrivals)
-        pre_ms = sum(srv.prefill_ms(n, iters=2) for _, n in arrivals[:64]) / min(64, len(arrivals))
+        mean_tok = sum(a[1] for a in arrivals) / len(arrivals)
+        pre_ms = sum(srv.prefill_ms(a[1], iters=2) for a in arrivals[:64]) / min(64, len(arrivals))
         capacity = mean_tok / (pre_ms / 1e3)
         out = {"trace": f"burst {rate:g} req/s x {duration:g} s, 5x for 2 s at t={burst_at:g} s, seed 1 "
                         f"({len(arrivals)} requests, mean prompt {mean_tok:.0f} tokens)",
                "served_by": "real prefills (one request each, prompts padded to 256-token buckets, CUDA graphs) "
-                            f"on GPUs 0..{n_gpus - 1} (source on GPU 0), host wall clock; trigger = reference "
-                            "should_scale_up on a 1 s arrival window vs the measured instance capacity",
+                            f"on GPUs 0..{n_gpus - 1} (source on GPU 0), each instance then decoding its requests' "
+                            "output tokens in a 32-slot continuous batch (captured steps, alternating with "
+                            "prefills), host wall clock; trigger = reference should_scale_up on a 1 s arrival "
+                            "window vs the measured instance capacity",
                "instance_capacity_tok_s": capacity, "strategies": {}}
         for strat in ("static", "allcache", "live-host", "blitz"):
             r = srv.run(arrivals, strat, capacity)
             out["strategies"][strat] = {k: getattr(r, k) for k in (
-                "p50_ttft_ms", "p99_ttft_ms", "mean_ttft_ms", "scale_trigger_s", "scale_ready_s", "load_ms",
-                "served", "instances_added", "all_ready_s")}
+                "p50_ttft_ms", "p99_ttft_ms", "mean_ttft_ms", "p50_tbt_ms", "p99_tbt_ms", "decode_steps",
+                "scale_trigger_s", "scale_ready_s", "load_ms", "served", "instances_added", "all_ready_s")}
         return out
     finally:
         srv.close()

@@ -244,6 +244,10 @@ int bz_prefill_attention(const void* qkv, int ld, int B, int S, int n_heads, int
  * position *pos, and write k, v into the caches at that position. */
 int bz_rope_append(void* qkv, int ld, int rows, int n_heads, int n_kv, int head_dim, float theta,
                    void* k_cache, void* v_cache, int64_t s_max, const int32_t* pos, void* stream);
+/* Continuous batching: the same with one position per row, pos[rows] (each sequence
+ * of the batch at its own length; a row at or past s_max is skipped). */
+int bz_rope_append_rows(void* qkv, int ld, int rows, int n_heads, int n_kv, int head_dim, float theta,
+                        void* k_cache, void* v_cache, int64_t s_max, const int32_t* pos, void* stream);
 /* Bytes of workspace bz_decode_attention needs for these sizes. */
 int bz_decode_workspace_bytes(int rows, int n_heads, int n_kv, int head_dim, int64_t s_max, int64_t* bytes);
 /* out[r, h*hd:(h+1)*hd] = softmax(q_h K[0..*pos]^T / sqrt(hd)) V over each row's
@@ -252,6 +256,10 @@ int bz_decode_workspace_bytes(int rows, int n_heads, int n_kv, int head_dim, int
 int bz_decode_attention(const void* q, int ldq, const void* k_cache, const void* v_cache, int rows, int n_heads,
                         int n_kv, int head_dim, int64_t s_max, const int32_t* pos, void* out, int ldo,
                         void* workspace, int64_t workspace_bytes, void* stream);
+/* ... with one position per row, pos[rows] (attended prefix pos[r] + 1 tokens). */
+int bz_decode_attention_rows(const void* q, int ldq, const void* k_cache, const void* v_cache, int rows,
+                             int n_heads, int n_kv, int head_dim, int64_t s_max, const int32_t* pos, void* out,
+                             int ldo, void* workspace, int64_t workspace_bytes, void* stream);
 
 /* ---- misc ------------------------------------------------------------------------------ */
 int bz_sm_count(int dev, int* n);

@@ -139,9 +139,12 @@ _SIGNATURES = {
     "bz_rope": [_P, _P, _I, _I, _I, _I, ctypes.c_float, _P],
     "bz_silu_mul": [_P, _P, _I, _I, _I, _I, _P],
     "bz_rope_append": [_P, _I, _I, _I, _I, _I, ctypes.c_float, _P, _P, ctypes.c_int64, _P, _P],
+    "bz_rope_append_rows": [_P, _I, _I, _I, _I, _I, ctypes.c_float, _P, _P, ctypes.c_int64, _P, _P],
     "bz_decode_workspace_bytes": [_I, _I, _I, _I, ctypes.c_int64, ctypes.POINTER(ctypes.c_int64)],
     "bz_decode_attention": [_P, _I, _P, _P, _I, _I, _I, _I, ctypes.c_int64, _P, _P, _I, _P, ctypes.c_int64,
                             _P],
+    "bz_decode_attention_rows": [_P, _I, _P, _P, _I, _I, _I, _I, ctypes.c_int64, _P, _P, _I, _P, ctypes.c_int64,
+                                 _P],
     "bz_prefill_attention_workspace_bytes": [_I, _I, _I, _I, ctypes.POINTER(ctypes.c_int64)],
     "bz_prefill_attention": [_P, _I, _I, _I, _I, _I, _I, _P, ctypes.c_int64, _P, _I, _P],
     "bz_sm_count": [_I, _PI],

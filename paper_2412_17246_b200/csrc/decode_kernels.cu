@@ -51,12 +51,13 @@ __device__ __forceinline__ void rotate_pair(float a, float b, float p, int i, in
 // head h in place; block (r, n_heads + g) rotates k head g into the cache and
 // copies v head g.
 __global__ void k_rope_append(__nv_bfloat16* qkv, int ld, int n_heads, int n_kv, int hd, float log2_theta,
-                              __nv_bfloat16* kc, __nv_bfloat16* vc, int64_t s_max, const int32_t* __restrict__ pos) {
+                              __nv_bfloat16* kc, __nv_bfloat16* vc, int64_t s_max, const int32_t* __restrict__ pos,
+                              int pos_stride) {
   pdl_wait();
   const int row = blockIdx.x, head = blockIdx.y, i = threadIdx.x;
   const int half = hd / 2;
   if (i >= half) return;
-  const int p = *pos;
+  const int p = pos[row * pos_stride];   // one position for the batch (stride 0) or one per row
   if (p < 0 || p >= s_max) {  // full cache: never write past the panel (the host raises first)
     pdl_trigger();
     return;
@@ -94,8 +95,8 @@ __global__ void __launch_bounds__(THREADS) k_decode_partial(const __nv_bfloat16*
                                                             const __nv_bfloat16* __restrict__ kc,
                                                             const __nv_bfloat16* __restrict__ vc, int n_heads,
                                                             int n_kv, int64_t s_max, const int32_t* __restrict__ pos,
-                                                            float* __restrict__ ws, int nsplit, int chunk,
-                                                            float scale) {
+                                                            int pos_stride, float* __restrict__ ws, int nsplit,
+                                                            int chunk, float scale) {
   constexpr int VEC = HD / 8;            // uint4 per row
   constexpr int LANES = THREADS / VEC;   // rows per PV sweep
   constexpr int KCH = G >= 4 ? 4 : VEC;  // K-row uint4s held at once (register budget)
@@ -109,7 +110,8 @@ __global__ void __launch_bounds__(THREADS) k_decode_partial(const __nv_bfloat16*
   const int split = blockIdx.x;
   const int bg = blockIdx.y;
   const int b = bg / n_kv, g = bg % n_kv;
-  const int len = static_cast<int>(tmin<int64_t>(static_cast<int64_t>(*pos) + 1, s_max));  // never past the panel
+  // attended prefix of this sequence: one position for the batch or one per row; never past the panel
+  const int len = static_cast<int>(tmin<int64_t>(static_cast<int64_t>(pos[b * pos_stride]) + 1, s_max));
   const int c0 = split * chunk;
   const int n = min(chunk, len - c0);
   const int tid = threadIdx.x;
@@ -276,29 +278,34 @@ __global__ void k_decode_combine(const float* __restrict__ ws, int nsplit, __nv_
 template <int HD, int G>
 static cudaError_t launch_partial(dim3 grid, cudaStream_t s, const __nv_bfloat16* q, int ldq,
                                   const __nv_bfloat16* kc, const __nv_bfloat16* vc, int n_heads, int n_kv,
-                                  int64_t s_max, const int32_t* pos, float* ws, int nsplit, int chunk, float scale) {
+                                  int64_t s_max, const int32_t* pos, int pos_stride, float* ws, int nsplit, int chunk,
+                                  float scale) {
   return launch_pdl(PDL_ATTN, k_decode_partial<HD, G>, grid, dim3(THREADS), 0, s, q, ldq, kc, vc, n_heads, n_kv, s_max, pos,
-                    ws, nsplit, chunk, scale);
+                    pos_stride, ws, nsplit, chunk, scale);
 }
 
 template <int HD>
 static int attention(int group, int rows, dim3 grid, cudaStream_t s, const __nv_bfloat16* q, int ldq,
                      const __nv_bfloat16* kc, const __nv_bfloat16* vc, int n_heads, int n_kv, int64_t s_max,
-                     const int32_t* pos, float* ws, int nsplit, int chunk, float scale, __nv_bfloat16* out,
-                     int ldo) {
+                     const int32_t* pos, int pos_stride, float* ws, int nsplit, int chunk, float scale,
+                     __nv_bfloat16* out, int ldo) {
   cudaError_t e;
   switch (group) {
     case 1:
-      e = launch_partial<HD, 1>(grid, s, q, ldq, kc, vc, n_heads, n_kv, s_max, pos, ws, nsplit, chunk, scale);
+      e = launch_partial<HD, 1>(grid, s, q, ldq, kc, vc, n_heads, n_kv, s_max, pos, pos_stride, ws, nsplit, chunk,
+                                  scale);
       break;
     case 2:
-      e = launch_partial<HD, 2>(grid, s, q, ldq, kc, vc, n_heads, n_kv, s_max, pos, ws, nsplit, chunk, scale);
+      e = launch_partial<HD, 2>(grid, s, q, ldq, kc, vc, n_heads, n_kv, s_max, pos, pos_stride, ws, nsplit, chunk,
+                                  scale);
       break;
     case 4:
-      e = launch_partial<HD, 4>(grid, s, q, ldq, kc, vc, n_heads, n_kv, s_max, pos, ws, nsplit, chunk, scale);
+      e = launch_partial<HD, 4>(grid, s, q, ldq, kc, vc, n_heads, n_kv, s_max, pos, pos_stride, ws, nsplit, chunk,
+                                  scale);
       break;
     case 8:
-      e = launch_partial<HD, 8>(grid, s, q, ldq, kc, vc, n_heads, n_kv, s_max, pos, ws, nsplit, chunk, scale);
+      e = launch_partial<HD, 8>(grid, s, q, ldq, kc, vc, n_heads, n_kv, s_max, pos, pos_stride, ws, nsplit, chunk,
+                                  scale);
       break;
     default:
       return bz_fail(BZ_EINVAL, "decode_attention: heads per kv head must be 1, 2, 4 or 8");
@@ -338,8 +345,8 @@ extern "C" int bz_decode_workspace_bytes(int rows, int n_heads, int n_kv, int he
   return BZ_OK;
 }
 
-extern "C" int bz_rope_append(void* qkv, int ld, int rows, int n_heads, int n_kv, int head_dim, float theta,
-                              void* k_cache, void* v_cache, int64_t s_max, const int32_t* pos, void* stream) {
+static int rope_append(void* qkv, int ld, int rows, int n_heads, int n_kv, int head_dim, float theta, void* k_cache,
+                       void* v_cache, int64_t s_max, const int32_t* pos, int pos_stride, void* stream) {
   if (!qkv || !k_cache || !v_cache || !pos || rows < 0 || n_heads <= 0 || n_kv <= 0 || head_dim % 2 ||
       n_heads % n_kv || s_max <= 0 || head_dim > 2048)
     return bz_fail(BZ_EINVAL, "rope_append: bad args");
@@ -348,14 +355,24 @@ extern "C" int bz_rope_append(void* qkv, int ld, int rows, int n_heads, int n_kv
   cudaError_t e = launch_pdl(PDL_GLUE, decode::k_rope_append, dim3(rows, n_heads + n_kv), dim3(threads), 0,
                              static_cast<cudaStream_t>(stream), static_cast<__nv_bfloat16*>(qkv), ld, n_heads, n_kv,
                              head_dim, log2f(theta), static_cast<__nv_bfloat16*>(k_cache),
-                             static_cast<__nv_bfloat16*>(v_cache), s_max, pos);
+                             static_cast<__nv_bfloat16*>(v_cache), s_max, pos, pos_stride);
   if (e != cudaSuccess) return bz_fail_cuda(e, "bz_rope_append");
   return bz_check_launch("bz_rope_append");
 }
 
-extern "C" int bz_decode_attention(const void* q, int ldq, const void* k_cache, const void* v_cache, int rows,
-                                   int n_heads, int n_kv, int head_dim, int64_t s_max, const int32_t* pos, void* out,
-                                   int ldo, void* workspace, int64_t ws_bytes, void* stream) {
+extern "C" int bz_rope_append(void* qkv, int ld, int rows, int n_heads, int n_kv, int head_dim, float theta,
+                              void* k_cache, void* v_cache, int64_t s_max, const int32_t* pos, void* stream) {
+  return rope_append(qkv, ld, rows, n_heads, n_kv, head_dim, theta, k_cache, v_cache, s_max, pos, 0, stream);
+}
+
+extern "C" int bz_rope_append_rows(void* qkv, int ld, int rows, int n_heads, int n_kv, int head_dim, float theta,
+                                   void* k_cache, void* v_cache, int64_t s_max, const int32_t* pos, void* stream) {
+  return rope_append(qkv, ld, rows, n_heads, n_kv, head_dim, theta, k_cache, v_cache, s_max, pos, 1, stream);
+}
+
+static int decode_attention(const void* q, int ldq, const void* k_cache, const void* v_cache, int rows, int n_heads,
+                            int n_kv, int head_dim, int64_t s_max, const int32_t* pos, int pos_stride, void* out,
+                            int ldo, void* workspace, int64_t ws_bytes, void* stream) {
   if (!q || !k_cache || !v_cache || !pos || !out || !workspace || rows < 0 || n_heads <= 0 || n_kv <= 0 ||
       n_heads % n_kv || s_max <= 0 || ldq % 8)
     return bz_fail(BZ_EINVAL, "decode_attention: bad args");
@@ -377,10 +394,24 @@ extern "C" int bz_decode_attention(const void* q, int ldq, const void* k_cache, 
   auto* ob = static_cast<__nv_bfloat16*>(out);
   const int group = n_heads / n_kv;
   if (head_dim == 128)
-    return decode::attention<128>(group, rows, grid, s, qb, ldq, kb, vb, n_heads, n_kv, s_max, pos, ws, nsplit,
+    return decode::attention<128>(group, rows, grid, s, qb, ldq, kb, vb, n_heads, n_kv, s_max, pos, pos_stride, ws, nsplit,
                                   chunk, scale, ob, ldo);
-  return decode::attention<64>(group, rows, grid, s, qb, ldq, kb, vb, n_heads, n_kv, s_max, pos, ws, nsplit, chunk,
+  return decode::attention<64>(group, rows, grid, s, qb, ldq, kb, vb, n_heads, n_kv, s_max, pos, pos_stride, ws, nsplit, chunk,
                                scale, ob, ldo);
+}
+
+extern "C" int bz_decode_attention(const void* q, int ldq, const void* k_cache, const void* v_cache, int rows,
+                                   int n_heads, int n_kv, int head_dim, int64_t s_max, const int32_t* pos, void* out,
+                                   int ldo, void* workspace, int64_t ws_bytes, void* stream) {
+  return decode_attention(q, ldq, k_cache, v_cache, rows, n_heads, n_kv, head_dim, s_max, pos, 0, out, ldo, workspace,
+                          ws_bytes, stream);
+}
+
+extern "C" int bz_decode_attention_rows(const void* q, int ldq, const void* k_cache, const void* v_cache, int rows,
+                                        int n_heads, int n_kv, int head_dim, int64_t s_max, const int32_t* pos,
+                                        void* out, int ldo, void* workspace, int64_t ws_bytes, void* stream) {
+  return decode_attention(q, ldq, k_cache, v_cache, rows, n_heads, n_kv, head_dim, s_max, pos, 1, out, ldo, workspace,
+                          ws_bytes, stream);
 }
 
 const void* bz::module_anchor_decode() { return reinterpret_cast<const void*>(decode::k_rope_append); }

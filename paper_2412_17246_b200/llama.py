@@ -239,12 +239,14 @@ class LlamaExecutor:
         self._rmsnorm(x, L["attn_norm"], h)
         self._gemm(h, L["wqkv"], qkv)
         kc, vc = kv.k[k], kv.v[k]
-        self.lib.bz_rope_append(qkv.data_ptr(), qkv.stride(0), B, a.n_heads, a.n_kv_heads, a.head_dim,
-                                a.rope_theta, kc.data_ptr(), vc.data_ptr(), kv.max_seq, kv.pos_dev.data_ptr(), s)
-        self.lib.bz_decode_attention(qkv.data_ptr(), qkv.stride(0), kc.data_ptr(), vc.data_ptr(), B, a.n_heads,
-                                     a.n_kv_heads, a.head_dim, kv.max_seq, kv.pos_dev.data_ptr(),
-                                     attn.data_ptr(), attn.stride(0), kv.workspace.data_ptr(),
-                                     kv.workspace.numel(), s)
+        # one device position for the batch, or one per row (continuous batching)
+        rope = self.lib.bz_rope_append_rows if kv.per_row else self.lib.bz_rope_append
+        attend = self.lib.bz_decode_attention_rows if kv.per_row else self.lib.bz_decode_attention
+        rope(qkv.data_ptr(), qkv.stride(0), B, a.n_heads, a.n_kv_heads, a.head_dim, a.rope_theta, kc.data_ptr(),
+             vc.data_ptr(), kv.max_seq, kv.pos_dev.data_ptr(), s)
+        attend(qkv.data_ptr(), qkv.stride(0), kc.data_ptr(), vc.data_ptr(), B, a.n_heads, a.n_kv_heads, a.head_dim,
+               kv.max_seq, kv.pos_dev.data_ptr(), attn.data_ptr(), attn.stride(0), kv.workspace.data_ptr(),
+               kv.workspace.numel(), s)
         return self._attn_out_mlp(k, x, attn, out, signal)
 
     @torch.no_grad()
@@ -312,7 +314,7 @@ class KVCache:
     """
 
     def __init__(self, arch: LlamaArch, batch: int, max_seq: int, device, first: int = 0,
-                 last: Optional[int] = None):
+                 last: Optional[int] = None, per_row: bool = False):
         from ._native import cuda_lib
         import ctypes
 
@@ -321,11 +323,15 @@ class KVCache:
         self.k = {l: torch.zeros(shape, dtype=torch.bfloat16, device=device) for l in range(first, last)}
         self.v = {l: torch.zeros(shape, dtype=torch.bfloat16, device=device) for l in range(first, last)}
         self.batch, self.max_seq = batch, max_seq
-        self.pos_dev = torch.zeros(1, dtype=torch.int32, device=device)
+        # per_row: every row (sequence slot) has its own device position -- continuous
+        # batching; ``length`` then tracks nothing (slots are managed by the caller)
+        self.per_row = per_row
+        self.pos_dev = torch.zeros(batch if per_row else 1, dtype=torch.int32, device=device)
         nbytes = ctypes.c_int64(0)
         cuda_lib().bz_decode_workspace_bytes(batch, arch.n_heads, arch.n_kv_heads, arch.head_dim, max_seq,
                                              ctypes.byref(nbytes))
         self.workspace = torch.empty(nbytes.value, dtype=torch.uint8, device=device)
+        self._arch_heads = arch.n_heads
         self._length = 0
 
     @property
@@ -341,7 +347,10 @@ class KVCache:
 
     def require_room(self):
         """Raise before a decode step is enqueued if the cache has no free position
-        (the device kernels also refuse to write past a panel)."""
+        (the device kernels also refuse to write past a panel).  Per-row caches are
+        managed slot by slot by their caller; the device guard protects them."""
+        if self.per_row:
+            return
         if self._length >= self.max_seq:
             raise ValueError(f"KV cache full ({self._length} of {self.max_seq} positions)")
 
@@ -350,6 +359,27 @@ class KVCache:
         self.require_room()
         self._length += 1
         self.pos_dev.add_(1)
+
+    def rows_view(self, n: int) -> "KVCache":
+        """The first ``n`` rows (sequence slots) of a per-row cache as a cache of batch n
+        sharing its storage and positions (a decode graph per batch-size bucket)."""
+        if not self.per_row or not 0 < n <= self.batch:
+            raise ValueError("rows_view needs a per-row cache and 0 < n <= batch")
+        v = object.__new__(KVCache)
+        v.k = {l: t[:n] for l, t in self.k.items()}
+        v.v = {l: t[:n] for l, t in self.v.items()}
+        v.batch, v.max_seq, v.per_row = n, self.max_seq, True
+        v.pos_dev = self.pos_dev[:n]
+        import ctypes
+        from ._native import cuda_lib
+        nb = ctypes.c_int64(0)
+        first = next(iter(self.k.values()))
+        cuda_lib().bz_decode_workspace_bytes(n, self._arch_heads, first.shape[1], first.shape[3], self.max_seq,
+                                             ctypes.byref(nb))
+        v.workspace = torch.empty(nb.value, dtype=torch.uint8, device=first.device)
+        v._arch_heads = self._arch_heads
+        v._length = 0
+        return v
 
     def bytes(self) -> int:
         return sum(t.numel() * 2 for t in list(self.k.values()) + list(self.v.values()))
@@ -379,11 +409,15 @@ class DecodeGraph:
         side = torch.cuda.Stream(device=dev)
         side.wait_stream(torch.cuda.current_stream(dev))
         saved = kv.length
+        saved_pos = kv.pos_dev.clone() if kv.per_row else None
         with torch.cuda.stream(side):
             # warm-up outside capture (lazy library init); writes position `saved`,
             # which the first real step overwrites before attending to it
             self._body()
-            kv.length = saved
+            if kv.per_row:
+                kv.pos_dev.copy_(saved_pos)
+            else:
+                kv.length = saved
             side.synchronize()
             self.graph = torch.cuda.CUDAGraph()
             with torch.cuda.graph(self.graph, stream=side):
@@ -402,12 +436,13 @@ class DecodeGraph:
         return x
 
     def __call__(self, tokens: Optional[torch.Tensor] = None, hidden: Optional[torch.Tensor] = None):
-        if self.kv.length >= self.kv.max_seq:
+        if not self.kv.per_row and self.kv.length >= self.kv.max_seq:
             raise ValueError("KV cache full")
         if tokens is not None:
             self.tokens.copy_(tokens)
         if hidden is not None:
             self.hidden.copy_(hidden)
         self.graph.replay()
-        self.kv._length += 1
+        if not self.kv.per_row:
+            self.kv._length += 1
         return self.out

@@ -19,6 +19,15 @@ capacity) and the new instance's weights move for real:
   target layers gated on the readiness counter, fused NVLink hand-off);
 * ``static``   -- no scaling.
 
+With ``decode_slots`` > 0 every instance also decodes what it prefilled
+(continuous batching, per-row device positions: ``bz_rope_append_rows`` /
+``bz_decode_attention_rows``): a prefill's keys/values land in a staging cache
+inside its captured graph and are copied into a free slot of the instance's
+decode cache (``bz_copy_panels``); decode steps replay one captured graph over
+the first 4/8/16/32 slots, alternating with prefills when both are pending; each
+request emits its trace's output tokens and TBT is the host-observed time between
+its tokens.
+
 One process drives every GPU (peer access on); prompts are padded to 256-token
 buckets whose forward passes are captured as CUDA graphs.  With more than one
 target GPU the trigger adds as many instances as the policy asks for at once:
@@ -42,7 +51,7 @@ from . import livescale
 from .autoscaler import LoadMetrics, ScalePolicy, should_scale_up
 from .coop import CooperativePair
 from .dataplane import DeviceSlab, HostCache, PeerSlab
-from .llama import LlamaExecutor, SlabWeights
+from .llama import KVCache, LlamaExecutor, SlabWeights
 from .slab import LlamaArch, SlabLayout
 
 
@@ -53,6 +62,9 @@ class Req:
     n_tok: int
     t_done: Optional[float] = None
     served_by: str = ""
+    n_out: int = 0                      # output tokens (the first comes from the prefill)
+    token_t: list = field(default_factory=list)   # host time of every decode token
+    slot: int = -1
 
 
 @dataclass
@@ -62,7 +74,10 @@ class _Instance:
     ex: LlamaExecutor
     stream: torch.cuda.Stream
     ready: bool
-    busy: Optional[tuple] = None   # (req, event)
+    busy: Optional[tuple] = None   # (kind, payload, event): ("prefill", req) | ("decode", [req...])
+    key: str = ""
+    active: dict = field(default_factory=dict)   # decode slot -> request
+    last: str = ""
 
 
 @dataclass
@@ -80,6 +95,9 @@ class RealClockResult:
     pair_runs: list = field(default_factory=list)   # live-host: (start s, splits, host ms)
     instances_added: int = 0
     all_ready_s: Optional[float] = None             # every added instance serving
+    p50_tbt_ms: Optional[float] = None              # decode_slots > 0: time between a request's tokens
+    p99_tbt_ms: Optional[float] = None
+    decode_steps: int = 0
 
 
 def _pct(xs, q):
@@ -94,9 +112,16 @@ class RealClockServer:
     """Source instance on ``src_dev`` (weights resident); the scale target on
     ``tgt_dev`` starts empty."""
 
+    DECODE_GRAPH_ROWS = (4, 8, 16, 32)
+
     def __init__(self, arch: LlamaArch, src_dev: int = 0, tgt_dev: int = 1, tile_bytes: int = 1 << 20,
-                 push_ctas: int = 48, extra_devs: Sequence[int] = ()):
+                 push_ctas: int = 48, extra_devs: Sequence[int] = (), decode_slots: int = 0,
+                 max_new_tokens: int = 128):
         self.arch = arch
+        if decode_slots and decode_slots not in self.DECODE_GRAPH_ROWS:
+            raise ValueError(f"decode_slots must be one of {self.DECODE_GRAPH_ROWS}")
+        self.decode_slots = decode_slots
+        self.s_max = self.BUCKETS[-1] + max_new_tokens + 1
         self.lib = cuda_lib(src_dev)
         self.tgt_devs = [tgt_dev] + [d for d in extra_devs if d not in (src_dev, tgt_dev)]
         for d in [src_dev] + self.tgt_devs:
@@ -141,9 +166,23 @@ class RealClockServer:
         self.graphs = {}
         plan = [("src", self.ex0, self.s0, self.src_dev)] + [
             (f"t{j}", ex, st, d) for j, (ex, st, d) in enumerate(zip(self.tex, self.ts, self.tgt_devs))]
+        self.staging, self.dcache, self.dgraphs = {}, {}, {}
         for name, ex, st, dev in plan:
             for bucket in self.BUCKETS:
-                self.graphs[(name, bucket)] = self._capture(ex, st, dev, bucket)
+                stage = None
+                if decode_slots:
+                    # the prompt's keys/values land here inside the captured prefill
+                    stage = KVCache(arch, 1, bucket, torch.device("cuda", dev))
+                    self.staging[(name, bucket)] = stage
+                self.graphs[(name, bucket)] = self._capture(ex, st, dev, bucket, stage)
+            if decode_slots:
+                with torch.cuda.device(dev), torch.cuda.stream(st):
+                    kv = KVCache(arch, decode_slots, self.s_max, torch.device("cuda", dev), per_row=True)
+                    self.dcache[name] = kv
+                    for n in self.DECODE_GRAPH_ROWS:
+                        if n <= decode_slots:
+                            self.dgraphs[(name, n)] = ex.decode_graph(kv.rows_view(n))
+                st.synchronize()
         d1 = torch.device("cuda", tgt_dev)
         self.pair = CooperativePair(self.ex0, self.ex1, self.tgt.loaded)
         self.pair_tokens = {b: torch.randint(0, arch.vocab, (1, b), device=d0) for b in self.BUCKETS}
@@ -171,16 +210,43 @@ class RealClockServer:
                 return b
         return RealClockServer.BUCKETS[-1]
 
-    def _capture(self, ex, stream, dev, n):
+    def _capture(self, ex, stream, dev, n, kv=None):
         with torch.cuda.device(dev):
             toks = torch.randint(0, self.arch.vocab, (1, n), device=f"cuda:{dev}")
             with torch.cuda.stream(stream):
-                ex.forward(toks)
+                ex.forward(toks, kv=kv)
             stream.synchronize()
             g = torch.cuda.CUDAGraph()
             with torch.cuda.graph(g, stream=stream):
-                ex.forward(toks)
+                ex.forward(toks, kv=kv)
         return g
+
+    def _admit(self, inst, req, bucket: int):
+        """Enqueue (on the instance's stream, after its prefill) the copy of the prompt's
+        keys/values from the bucket's staging cache into a free decode slot, and set that
+        slot's device position to the prompt length."""
+        kv = self.dcache[inst.key]
+        slot = min(set(range(self.decode_slots)) - set(inst.active))
+        req.slot = slot
+        inst.active[slot] = req
+        stage = self.staging.get((inst.key, bucket))
+        a = self.arch
+        n = min(req.n_tok, bucket) if stage is not None else min(req.n_tok, self.s_max - req.n_out - 1)
+        with torch.cuda.device(inst.device), torch.cuda.stream(inst.stream):
+            s = inst.stream.cuda_stream
+            if stage is not None:
+                for l in kv.k:
+                    for src, dst in ((stage.k[l], kv.k[l][slot]), (stage.v[l], kv.v[l][slot])):
+                        self.lib.bz_copy_panels(src.data_ptr(), dst.data_ptr(), a.n_kv_heads,
+                                                bucket * a.head_dim * 2, self.s_max * a.head_dim * 2,
+                                                n * a.head_dim * 2, 16, s)
+            kv.pos_dev[slot:slot + 1].fill_(n)
+
+    def _decode_step(self, inst):
+        """Replay the smallest captured decode step covering every active slot."""
+        top = max(inst.active) + 1
+        rows = next(r for r in self.DECODE_GRAPH_ROWS if r >= top and r <= self.decode_slots)
+        self.dgraphs[(inst.key, rows)]()
 
     def _warm(self):
         # every kernel / library plan both instances use, on their serving streams
@@ -261,11 +327,17 @@ class RealClockServer:
         """Replay ``arrivals`` (seconds, prompt tokens) on the wall clock.  ``time_l``
         (one layer's load time over one layer's execution, livescale.py:4-14) and
         ``pair_batch`` (requests per cooperative run) apply to ``live-host``."""
-        reqs = [Req(i, t, n) for i, (t, n) in enumerate(arrivals)]
-        insts = [_Instance("gpu%d" % self.src_dev, torch.device("cuda", self.src_dev), self.ex0, self.s0, True)]
-        insts += [_Instance("gpu%d" % d, torch.device("cuda", d), ex, st, False)
-                  for d, ex, st in zip(self.tgt_devs, self.tex, self.ts)]
+        reqs = [Req(i, a[0], a[1], n_out=(a[2] if len(a) > 2 and self.decode_slots else 0))
+                for i, a in enumerate(arrivals)]
         keys = ["src"] + [f"t{j}" for j in range(len(self.tgt_devs))]
+        insts = [_Instance("gpu%d" % self.src_dev, torch.device("cuda", self.src_dev), self.ex0, self.s0, True,
+                           key="src")]
+        insts += [_Instance("gpu%d" % d, torch.device("cuda", d), ex, st, False, key=k)
+                  for d, ex, st, k in zip(self.tgt_devs, self.tex, self.ts, keys[1:])]
+        for inst in insts:
+            inst.active.clear()
+        decode_steps = 0
+        finished = 0
         policy = ScalePolicy(upper_bound=capacity_tok_s, lower_bound=0.1 * capacity_tok_s,
                              strategy={"allcache": "allcache", "live-host": "blitz-live"}.get(strategy, "blitz-stop"))
         queue: collections.deque = collections.deque()
@@ -278,7 +350,7 @@ class RealClockServer:
         ready_all_t = None
         pair_runs: list = []
         t0 = time.perf_counter()
-        while done < len(reqs):
+        while done < len(reqs) or finished < len(reqs):
             now = time.perf_counter() - t0
             while nxt < len(reqs) and reqs[nxt].t_arrive <= now:
                 queue.append(reqs[nxt])
@@ -308,12 +380,23 @@ class RealClockServer:
                         ready_all_t = t_ready
             # completions
             for inst in insts:
-                if inst.busy is not None and inst.busy[1].query():
-                    req = inst.busy[0]
-                    req.t_done = time.perf_counter() - t0
-                    req.served_by = inst.name
+                if inst.busy is not None and inst.busy[2].query():
+                    kind, payload, _ = inst.busy
                     inst.busy = None
-                    done += 1
+                    t_now = time.perf_counter() - t0
+                    if kind == "prefill":
+                        payload.t_done = t_now
+                        payload.served_by = inst.name
+                        done += 1
+                        if payload.n_out <= 1:
+                            finished += 1
+                            inst.active.pop(payload.slot, None)
+                    else:
+                        for req in payload:
+                            req.token_t.append(t_now)
+                            if len(req.token_t) >= req.n_out - 1:
+                                finished += 1
+                                inst.active.pop(req.slot, None)
             # live-host: while the new instance loads, serve queued requests as a ZigZag pair
             if (strategy == "live-host" and 0 in load_ev and not insts[1].ready and queue
                     and insts[0].busy is None):
@@ -329,20 +412,54 @@ class RealClockServer:
                     r.t_done = t_run + f / 1e3
                     r.served_by = "pair"
                     done += 1
+                    if r.n_out > 1 and len(insts[0].active) < self.decode_slots:
+                        # the pair ran the prompt; its tokens are decoded on the source
+                        # (its keys/values are not gathered from the two halves: the
+                        # decode step's cost does not depend on them)
+                        self._admit(insts[0], r, 0)
+                    elif r.n_out > 1:
+                        r.n_out = 1      # no free decode slot: counted as a prefill-only request
+                        finished += 1
+                    else:
+                        finished += 1
                 continue
-            # dispatch FCFS to idle ready instances
+            # dispatch to idle ready instances: prefills FCFS; with decoding, a decode step
+            # of the instance's active slots alternates with prefills when both wait
             for inst in insts:
-                if inst.ready and inst.busy is None and queue:
-                    req = queue.popleft()
-                    key = (keys[insts.index(inst)], self.bucket(req.n_tok))
-                    with torch.cuda.device(inst.device), torch.cuda.stream(inst.stream):
-                        self.graphs[key].replay()
+                if not inst.ready or inst.busy is not None:
+                    continue
+                can_prefill = bool(queue) and (not self.decode_slots or len(inst.active) < self.decode_slots)
+                want_decode = bool(inst.active) and (not can_prefill or inst.last == "prefill")
+                with torch.cuda.device(inst.device), torch.cuda.stream(inst.stream):
+                    if want_decode:
+                        live = [r for r in inst.active.values() if r.t_done is not None]
+                        self._decode_step(inst)
+                        decode_steps += 1
                         ev = torch.cuda.Event()
                         ev.record(inst.stream)
-                    inst.busy = (req, ev)
+                        inst.busy = ("decode", live, ev)
+                        inst.last = "decode"
+                    elif can_prefill:
+                        req = queue.popleft()
+                        bucket = self.bucket(req.n_tok)
+                        self.graphs[(inst.key, bucket)].replay()
+                        if req.n_out > 1:
+                            self._admit(inst, req, bucket)
+                        ev = torch.cuda.Event()
+                        ev.record(inst.stream)
+                        inst.busy = ("prefill", req, ev)
+                        inst.last = "prefill"
+            if done == len(reqs) and finished >= len(reqs):
+                break
             time.sleep(poll_sleep_s)
         wall = time.perf_counter() - t0
         ttft = [(r.t_done - r.t_arrive) * 1e3 for r in reqs]
+        tbt = []
+        for r in reqs:
+            prev = r.t_done
+            for t in r.token_t:
+                tbt.append((t - prev) * 1e3)
+                prev = t
         served = collections.Counter(r.served_by for r in reqs)
         load_ms = (ready_t - trigger_t) * 1e3 if ready_t is not None and trigger_t is not None else None
         for d in [self.src_dev] + self.tgt_devs:
@@ -351,7 +468,9 @@ class RealClockServer:
                                p99_ttft_ms=_pct(ttft, 99), mean_ttft_ms=sum(ttft) / len(ttft),
                                scale_trigger_s=trigger_t, scale_ready_s=ready_t, load_ms=load_ms,
                                served=dict(served), wall_s=wall, pair_runs=pair_runs,
-                               instances_added=started, all_ready_s=ready_all_t)
+                               instances_added=started, all_ready_s=ready_all_t,
+                               p50_tbt_ms=_pct(tbt, 50) if tbt else None, p99_tbt_ms=_pct(tbt, 99) if tbt else None,
+                               decode_steps=decode_steps)
 
     def close(self):
         for p in self.peer_on_src + self.peer_next:

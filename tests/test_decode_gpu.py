@@ -364,3 +364,41 @@ def test_decode_on_full_cache_raises_before_writing():
     torch.cuda.synchronize()
     assert torch.equal(kv.k[0], before[0][0]) and torch.equal(kv.v[0], before[0][1])
     slab.close()
+
+
+def test_per_row_positions_continuous_batch():
+    """Continuous batching: rows of one cache at different lengths decode in one step
+    (bz_rope_append_rows / bz_decode_attention_rows), each row against its own fp32
+    recompute; a graph over the first rows (rows_view) replays the same step."""
+    arch = TINY_GQA
+    lay, slab, w = _slab(arch)
+    ref_w = weights_to_cpu_fp32(w)
+    ex = LlamaExecutor(w, max_tokens=64, device="cuda")
+    lens = [20, 12, 7]
+    prompts = [_prompt(1, n, 30 + n, arch.vocab) for n in lens]
+    kv = KVCache(arch, 4, 40, "cuda", per_row=True)          # 4 slots, slot 3 idle
+    first = []
+    for slot, p in enumerate(prompts):
+        one = KVCache(arch, 1, 40, "cuda")
+        lg = ex.forward(p, kv=one)
+        first.append(lg.argmax(-1))
+        for l in kv.k:
+            kv.k[l][slot, :, :p.shape[1]].copy_(one.k[l][0, :, :p.shape[1]])
+            kv.v[l][slot, :, :p.shape[1]].copy_(one.v[l][0, :, :p.shape[1]])
+    kv.pos_dev.copy_(torch.tensor(lens + [0], dtype=torch.int32))
+    toks = torch.cat(first + [torch.zeros(1, dtype=torch.int64, device="cuda")])
+    logits = ex.decode(toks, kv)
+    torch.cuda.synchronize()
+    assert kv.pos_dev.tolist() == [n + 1 for n in lens] + [1]
+    for slot, p in enumerate(prompts):
+        seq = torch.cat([p.cpu(), first[slot].cpu()[:, None]], 1)
+        _check(logits[slot:slot + 1], forward_fp32(arch, ref_w, seq))
+    # the same step captured over the first 3 rows, replayed from the same positions
+    kv.pos_dev.copy_(torch.tensor(lens + [0], dtype=torch.int32))
+    view = kv.rows_view(3)
+    g = ex.decode_graph(view)
+    out = g(toks[:3])
+    torch.cuda.synchronize()
+    assert torch.equal(out, logits[:3]) or _rel(out.cpu(), logits[:3].cpu()) < 1e-3
+    assert kv.pos_dev.tolist()[:3] == [n + 1 for n in lens]
+    slab.close()

@@ -369,35 +369,50 @@ def c3_realclock(arch, n_gpus: int = 2, rate: float = 30.0, duration: float = 9.
     """The C3 burst (5x for 2 s) served on the wall clock by real prefills: the source
     instance on GPU 0, new instances on GPUs 1..n_gpus-1 added as the reference
     trigger asks; strategies static / allcache (host-cache loads) / live-host /
-    blitz (NVLink chain push)."""
+    blitz (NVLink chain push).  TTFT pass: prefill instances only (the P/D split of
+    the paper).  Decode pass (half the rate, so colocated decoding keeps up): every
+    instance also decodes its requests' output tokens in a 32-slot continuous batch
+    -- p50 / p99 TBT on the wall clock."""
     import paper_2412_17246_b200 as ss
     from paper_2412_17246_b200.realclock import RealClockServer
 
-    burst_at = duration / 3
-    trace = ss.generate_trace("burst", {"rate_per_s": rate, "duration_s": duration,
-                                        "prompt_tokens": [512, 2048], "output_tokens": [16, 128],
-                                        "bursts": [{"start_s": burst_at, "duration_s": 2, "multiplier": 5}]},
-                              seed=1)
-    arrivals = [(r.arrival_ms / 1e3, r.prompt_tokens, r.output_tokens) for r in trace]
-    # every instance also decodes what it prefilled (continuous batching, 32 slots): TBT
+    def burst(r):
+        return ss.generate_trace("burst", {"rate_per_s": r, "duration_s": duration,
+                                           "prompt_tokens": [512, 2048], "output_tokens": [16, 128],
+                                           "bursts": [{"start_s": duration / 3, "duration_s": 2, "multiplier": 5}]},
+                                 seed=1)
+
+    trace = burst(rate)
+    arrivals = [(r.arrival_ms / 1e3, r.prompt_tokens) for r in trace]
     srv = RealClockServer(arch, extra_devs=list(range(2, n_gpus)), decode_slots=32, max_new_tokens=128)
     try:
         mean_tok = sum(a[1] for a in arrivals) / len(arrivals)
         pre_ms = sum(srv.prefill_ms(a[1], iters=2) for a in arrivals[:64]) / min(64, len(arrivals))
         capacity = mean_tok / (pre_ms / 1e3)
-        out = {"trace": f"burst {rate:g} req/s x {duration:g} s, 5x for 2 s at t={burst_at:g} s, seed 1 "
+        keys = ("p50_ttft_ms", "p99_ttft_ms", "mean_ttft_ms", "scale_trigger_s", "scale_ready_s", "load_ms",
+                "served", "instances_added", "all_ready_s")
+        out = {"trace": f"burst {rate:g} req/s x {duration:g} s, 5x for 2 s at t={duration / 3:g} s, seed 1 "
                         f"({len(arrivals)} requests, mean prompt {mean_tok:.0f} tokens)",
                "served_by": "real prefills (one request each, prompts padded to 256-token buckets, CUDA graphs) "
-                            f"on GPUs 0..{n_gpus - 1} (source on GPU 0), each instance then decoding its requests' "
-                            "output tokens in a 32-slot continuous batch (captured steps, alternating with "
-                            "prefills), host wall clock; trigger = reference should_scale_up on a 1 s arrival "
-                            "window vs the measured instance capacity",
+                            f"on GPUs 0..{n_gpus - 1} (source on GPU 0), host wall clock; trigger = reference "
+                            "should_scale_up on a 1 s arrival window vs the measured instance capacity",
                "instance_capacity_tok_s": capacity, "strategies": {}}
         for strat in ("static", "allcache", "live-host", "blitz"):
             r = srv.run(arrivals, strat, capacity)
-            out["strategies"][strat] = {k: getattr(r, k) for k in (
-                "p50_ttft_ms", "p99_ttft_ms", "mean_ttft_ms", "p50_tbt_ms", "p99_tbt_ms", "decode_steps",
-                "scale_trigger_s", "scale_ready_s", "load_ms", "served", "instances_added", "all_ready_s")}
+            out["strategies"][strat] = {k: getattr(r, k) for k in keys}
+        # decode pass: colocated continuous-batching decode of every request's output tokens
+        dtrace = burst(rate / 2)
+        darr = [(r.arrival_ms / 1e3, r.prompt_tokens, r.output_tokens) for r in dtrace]
+        dec = {"trace": f"burst {rate / 2:g} req/s x {duration:g} s, 5x for 2 s, seed 1 ({len(darr)} requests, "
+                        f"16-128 output tokens each)",
+               "served_by": "each instance prefills and then decodes its requests in a 32-slot continuous batch "
+                            "(per-row device positions, captured steps over 4/8/16/32 slots, alternating with "
+                            "prefills); TBT = host-observed time between a request's tokens",
+               "strategies": {}}
+        for strat in ("static", "allcache", "blitz"):
+            r = srv.run(darr, strat, capacity / 2)
+            dec["strategies"][strat] = {k: getattr(r, k) for k in keys + ("p50_tbt_ms", "p99_tbt_ms", "decode_steps")}
+        out["with_decode"] = dec
         return out
     finally:
         srv.close()

@@ -1043,184 +1043,6 @@ static double single_tile_time(int M, int N, int K, int ctas, int* bn_out) {
   return best;
 }
 
-// ===========================================================================
-// Decode-size GEMM (M <= 4 rows: a batch-1..4 decode step, every weight byte used
-// once): a weight-streaming GEMV on the CUDA cores.  One warp per output column n:
-// the lanes stream W[n, :] with 16-byte non-coherent loads (4 in flight per lane),
-// multiply with the M activation rows staged in shared memory, fp32 accumulation,
-// shuffle reduction, + residual, bf16 (or fp32) store.  The first weight loads are
-// issued before griddepcontrol.wait (weights are never written by the predecessor),
-// so they overlap the previous kernel's tail.  The tcgen05 kernel's fixed costs
-// (TMEM allocation, pipeline fill, stream-K fix-up) dominate a 33-180 MB weight
-// stream at M = 1; this path streams it at HBM rate.
-constexpr int GEMV_MAX_M = 4;
-constexpr int GEMV_WARPS = 8;
-
-__device__ __forceinline__ uint4 ldg_nc_v4(const void* p) {
-  uint4 r;
-  asm volatile("ld.global.nc.L1::no_allocate.L2::256B.v4.u32 {%0,%1,%2,%3}, [%4];"
-               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
-               : "l"(p));
-  return r;
-}
-
-__device__ __forceinline__ void dot8(const uint4& w, const uint4& x, float& acc) {
-  const __nv_bfloat162* wp = reinterpret_cast<const __nv_bfloat162*>(&w);
-  const __nv_bfloat162* xp = reinterpret_cast<const __nv_bfloat162*>(&x);
-#pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const float2 a = __bfloat1622float2(wp[i]), b = __bfloat1622float2(xp[i]);
-    acc = fmaf(a.x, b.x, acc);
-    acc = fmaf(a.y, b.y, acc);
-  }
-}
-
-template <int M>
-__global__ void __launch_bounds__(GEMV_WARPS * 32) k_gemv_bf16(const __nv_bfloat16* __restrict__ A, int lda,
-                                                               const __nv_bfloat16* __restrict__ B, int ldb, void* C,
-                                                               int ldc, const __nv_bfloat16* __restrict__ R, int ldr,
-                                                               int N, int K, int c_f32, uint32_t* signal) {
-  extern __shared__ __align__(16) uint8_t gemv_smem[];
-  uint4* xs = reinterpret_cast<uint4*>(gemv_smem);   // [M][K / 8]
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int kv = K / 8;                              // 16-byte vectors per row
-  const int n0 = blockIdx.x * GEMV_WARPS + warp;
-  const int nstride = gridDim.x * GEMV_WARPS;
-  // weights first (static), then wait for the activations of the predecessor
-  constexpr int U = 4;
-  uint4 wpre[U];
-  const bool have = n0 < N;
-  if (have) {
-    const uint4* wr = reinterpret_cast<const uint4*>(B + static_cast<int64_t>(n0) * ldb);
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int k = lane + u * 32;
-      wpre[u] = k < kv ? ldg_nc_v4(wr + k) : make_uint4(0, 0, 0, 0);
-    }
-  }
-  pdl_wait();
-  for (int i = threadIdx.x; i < M * kv; i += blockDim.x) {
-    const int m = i / kv, k = i % kv;
-    xs[i] = *reinterpret_cast<const uint4*>(A + static_cast<int64_t>(m) * lda + k * 8);
-  }
-  __syncthreads();
-  pdl_trigger();
-  bool first = true;
-  for (int n = n0; n < N; n += nstride, first = false) {
-    const uint4* wr = reinterpret_cast<const uint4*>(B + static_cast<int64_t>(n) * ldb);
-    float acc[M];
-#pragma unroll
-    for (int m = 0; m < M; ++m) acc[m] = 0.f;
-    int k0 = 0;
-    if (first) {
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int k = lane + u * 32;
-        if (k < kv)
-#pragma unroll
-          for (int m = 0; m < M; ++m) dot8(wpre[u], xs[m * kv + k], acc[m]);
-      }
-      k0 = U * 32;
-    }
-    for (; k0 < kv; k0 += U * 32) {
-      uint4 w[U];
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int k = k0 + lane + u * 32;
-        w[u] = k < kv ? ldg_nc_v4(wr + k) : make_uint4(0, 0, 0, 0);
-      }
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int k = k0 + lane + u * 32;
-        if (k < kv)
-#pragma unroll
-          for (int m = 0; m < M; ++m) dot8(w[u], xs[m * kv + k], acc[m]);
-      }
-    }
-#pragma unroll
-    for (int m = 0; m < M; ++m)
-#pragma unroll
-      for (int o = 16; o; o >>= 1) acc[m] += __shfl_xor_sync(0xffffffffu, acc[m], o);
-    if (lane < M) {
-      float v = acc[0];
-#pragma unroll
-      for (int m = 1; m < M; ++m)
-        if (lane == m) v = acc[m];
-      if (R) v += __bfloat162float(R[static_cast<int64_t>(lane) * ldr + n]);
-      if (c_f32)
-        reinterpret_cast<float*>(C)[static_cast<int64_t>(lane) * ldc + n] = v;
-      else
-        reinterpret_cast<__nv_bfloat16*>(C)[static_cast<int64_t>(lane) * ldc + n] = __float2bfloat16_rn(v);
-    }
-  }
-  if (signal != nullptr) {
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      __threadfence_system();
-      asm volatile("red.release.sys.global.add.u32 [%0], 1;" ::"l"(signal) : "memory");
-    }
-  }
-}
-
-// BZ_GEMV=0 sends decode-size GEMMs to the tcgen05 kernel (A/B measurements)
-static bool gemv_enabled() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("BZ_GEMV");
-    v = e ? atoi(e) : 1;
-  }
-  return v != 0;
-}
-
-static int gemv_launch(const void* A, const void* B, void* C, const void* residual, int M, int N, int K, int lda,
-                       int ldb, int ldc, int ldr, int c_f32, uint32_t* signal, int* ctas_out, cudaStream_t s) {
-  int dev = 0, sms = 148;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  // one output column per warp, up to 16 resident CTAs of 8 warps per SM
-  const int want = (N + GEMV_WARPS - 1) / GEMV_WARPS;
-  const int grid = want < 16 * sms ? want : 16 * sms;
-  const size_t smem = static_cast<size_t>(M) * K * 2;
-  if (smem > 48 * 1024) {
-    static bool attr[GEMV_MAX_M + 1][64] = {};
-    auto set = [&](auto kern) {
-      if (dev < 64 && !attr[M][dev]) {
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-        attr[M][dev] = true;
-      }
-    };
-    if (M == 1) set(k_gemv_bf16<1>);
-    if (M == 2) set(k_gemv_bf16<2>);
-    if (M == 3) set(k_gemv_bf16<3>);
-    if (M == 4) set(k_gemv_bf16<4>);
-  }
-  const auto* a = static_cast<const __nv_bfloat16*>(A);
-  const auto* b = static_cast<const __nv_bfloat16*>(B);
-  const auto* r = static_cast<const __nv_bfloat16*>(residual);
-  cudaError_t e;
-  switch (M) {
-    case 1:
-      e = launch_pdl(PDL_GEMM, k_gemv_bf16<1>, dim3(grid), dim3(GEMV_WARPS * 32), smem, s, a, lda, b, ldb, C, ldc, r,
-                     ldr, N, K, c_f32, signal);
-      break;
-    case 2:
-      e = launch_pdl(PDL_GEMM, k_gemv_bf16<2>, dim3(grid), dim3(GEMV_WARPS * 32), smem, s, a, lda, b, ldb, C, ldc, r,
-                     ldr, N, K, c_f32, signal);
-      break;
-    case 3:
-      e = launch_pdl(PDL_GEMM, k_gemv_bf16<3>, dim3(grid), dim3(GEMV_WARPS * 32), smem, s, a, lda, b, ldb, C, ldc, r,
-                     ldr, N, K, c_f32, signal);
-      break;
-    default:
-      e = launch_pdl(PDL_GEMM, k_gemv_bf16<4>, dim3(grid), dim3(GEMV_WARPS * 32), smem, s, a, lda, b, ldb, C, ldc, r,
-                     ldr, N, K, c_f32, signal);
-      break;
-  }
-  if (e != cudaSuccess) return bz_fail_cuda(e, "bz_gemm_bf16 (gemv) launch");
-  if (ctas_out) *ctas_out = grid;
-  return bz_check_launch("bz_gemm_bf16 (gemv)");
-}
-
 static int gemm_impl(const void* A, const void* B, void* C, const void* residual, int M, int N, int K, int lda,
                      int ldb, int ldc, int ldr, int max_ctas, unsigned flags, void* workspace, int64_t ws_bytes,
                      uint32_t* signal, int* ctas_out, void* stream) {
@@ -1237,9 +1059,6 @@ static int gemm_impl(const void* A, const void* B, void* C, const void* residual
   const bool c_f32 = (flags & BZ_GEMM_C_F32) != 0;
   if (c_f32 && (reinterpret_cast<uintptr_t>(C) & 15))
     return bz_fail(BZ_EINVAL, "gemm: fp32 C must be 16-byte aligned");
-  if (M <= GEMV_MAX_M && gemv_enabled() && static_cast<int64_t>(M) * K * 2 <= 200 * 1024)
-    return gemv_launch(A, B, C, residual, M, N, K, lda, ldb, ldc, ldr, c_f32 ? 1 : 0, signal, ctas_out,
-                       static_cast<cudaStream_t>(stream));
   const int po = pair_override();
   // fp32 C is a single-CTA epilogue feature (logit heads: M = sequences)
   bool pair = !c_f32 && (po == 1 || (po == -1 && M >= 2 * BM));

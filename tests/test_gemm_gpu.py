@@ -210,25 +210,3 @@ def test_splitk_partials_leave_streamk_counters_zero():
         _check(c1, a1.float() @ b1.float().t())
         _check(c2, a2.float() @ b2.float().t())
         assert int(ws[:1024].view(torch.int32).abs().sum()) == 0
-
-
-@pytest.mark.parametrize("m,n,k", [(1, 4096, 4096), (2, 12288, 4096), (3, 1000, 11008), (4, 4096, 11008),
-                                   (1, 32000, 4096)])
-def test_decode_gemv_matches_fp32(m, n, k):
-    """M <= 4 (a decode step): the weight-streaming GEMV path, + residual and the
-    fused hand-off signal, vs the fp32 product; BZ_GEMV=0 would route it to tcgen05."""
-    from paper_2412_17246_b200._native import BZ_GEMM_B_STATIC
-    import ctypes
-    torch.manual_seed(m * 31 + n + k)
-    a = torch.randn(m, k, device="cuda").to(torch.bfloat16)
-    b = (torch.randn(n, k, device="cuda") * 0.02).to(torch.bfloat16)
-    r = torch.randn(m, n, device="cuda").to(torch.bfloat16)
-    c = torch.empty(m, n, dtype=torch.bfloat16, device="cuda")
-    sig = torch.zeros(1, dtype=torch.int32, device="cuda")
-    ctas = ctypes.c_int()
-    cuda_lib().bz_gemm_bf16_ex(a.data_ptr(), b.data_ptr(), c.data_ptr(), r.data_ptr(), m, n, k, a.stride(0),
-                               b.stride(0), c.stride(0), r.stride(0), 0, BZ_GEMM_B_STATIC, None, 0, sig.data_ptr(),
-                               ctypes.byref(ctas), torch.cuda.current_stream().cuda_stream)
-    torch.cuda.synchronize()
-    _check(c, a.float() @ b.float().t() + r.float())
-    assert int(sig.item()) == ctas.value > 0

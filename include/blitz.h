@@ -125,6 +125,12 @@ int bz_push_tile_list(const void* src, void* const* dst, uint32_t* const* dst_fl
 int bz_push_tiles_ce(const void* src, void* dst, uint32_t* dst_flags, const uint32_t* wait_flags,
                      const int64_t* tile_off_host, int t0, int t1, int tiles_per_copy, uint32_t epoch,
                      void* stream);
+/* The same with the flag releases on `flag_stream` (each behind an event after its
+ * group's copy), so `stream` carries only copies (+ relay gates) and the copy engine
+ * runs back to back; `stream` joins `flag_stream` at the end. */
+int bz_push_tiles_ce2(const void* src, void* dst, uint32_t* dst_flags, const uint32_t* wait_flags,
+                      const int64_t* tile_off_host, int t0, int t1, int tiles_per_copy, uint32_t epoch,
+                      void* stream, void* flag_stream);
 
 /* bz_multicast_tiles: one multimem.st stream into the multicast VA `mc_dst`
  * (bound to every receiver's slab); flags go through `mc_flags` (the

@@ -120,6 +120,7 @@ _SIGNATURES = {
     "bz_push_tile_list": [_P, _PP, _PP, _I, _P, _P, _P, _I, _U32, _I, _P],
     "bz_multicast_tiles": [_P, _P, _P, _P, _P, _I, _I, _U32, _I, _P],
     "bz_push_tiles_ce": [_P, _P, _P, _P, _P, _I, _I, _I, _U32, _P],
+    "bz_push_tiles_ce2": [_P, _P, _P, _P, _P, _I, _I, _I, _U32, _P, _P],
     "bz_stage_tiles_ce": [_P, _P, _P, _P, _I, _I, _I, _U32, _P],
     "bz_stage_tiles_sm": [_P, _P, _P, _P, _I, _I, _U32, _I, _P],
     "bz_track_layers": [_P, _P, _I, _U32, _P, _P, _P],

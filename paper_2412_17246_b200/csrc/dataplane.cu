@@ -17,6 +17,8 @@
 #include <stdint.h>
 #include <stdlib.h>
 
+#include <vector>
+
 #include "../../include/blitz.h"
 #include "common.cuh"
 
@@ -578,24 +580,71 @@ extern "C" int bz_stage_tiles_ce(const void* host_src, void* dst, uint32_t* dst_
 
 // Chain hop on the copy engines: no SM moves bytes (the SMs stay with the
 // cooperating instance's GEMMs).  Per group of tiles: [relay: one-warp gate on
-// the group's upstream flags] -> cudaMemcpyAsync into the peer mapping ->
-// flag kernel (system-scope release into the peer's flag array).
-extern "C" int bz_push_tiles_ce(const void* src, void* dst, uint32_t* dst_flags, const uint32_t* wait_flags,
-                                const int64_t* tile_off_host, int t0, int t1, int tiles_per_copy, uint32_t epoch,
-                                void* stream) {
+// the group's upstream flags] -> cudaMemcpyAsync into the peer mapping -> flag
+// kernel (system-scope release into the peer's flag array).
+//
+// With a `flag_stream` the flag kernels run there, each behind an event recorded
+// after its group's copy: the copy stream then carries only copies (and relay
+// gates), so the copy engine streams back to back instead of idling for a kernel
+// launch between groups.
+static cudaEvent_t pooled_event(int dev, size_t i) {
+  static std::vector<cudaEvent_t> pool[64];
+  auto& v = pool[dev < 64 ? dev : 63];
+  while (v.size() <= i) {
+    cudaEvent_t e;
+    if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) return nullptr;
+    v.push_back(e);
+  }
+  return v[i];
+}
+
+static int push_ce(const void* src, void* dst, uint32_t* dst_flags, const uint32_t* wait_flags,
+                   const int64_t* tile_off_host, int t0, int t1, int tiles_per_copy, uint32_t epoch, void* stream,
+                   void* flag_stream) {
   if (!src || !dst || !dst_flags || !tile_off_host || t0 < 0 || t1 < t0 || tiles_per_copy < 1)
     return bz_fail(BZ_EINVAL, "push_ce: bad arguments");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  for (int t = t0; t < t1; t += tiles_per_copy) {
+  cudaStream_t fs = static_cast<cudaStream_t>(flag_stream);
+  int dev = 0;
+  cudaGetDevice(&dev);
+  size_t group = 0;
+  for (int t = t0; t < t1; t += tiles_per_copy, ++group) {
     const int te = min(t1, t + tiles_per_copy);
     if (wait_flags) k_wait_range<<<1, 32, 0, s>>>(wait_flags, t, te, epoch);
     const int64_t b = tile_off_host[t], e = tile_off_host[te];
     cudaError_t err = cudaMemcpyAsync(static_cast<char*>(dst) + b, static_cast<const char*>(src) + b,
                                       static_cast<size_t>(e - b), cudaMemcpyDeviceToDevice, s);
     if (err != cudaSuccess) return bz_fail_cuda(err, "push_ce memcpy");
-    k_set_flags<<<(te - t + 127) / 128, 128, 0, s>>>(dst_flags, t, te, epoch, wait_flags != nullptr);
+    if (fs) {
+      cudaEvent_t ev = pooled_event(dev, group);
+      if (!ev) return bz_fail(BZ_ECUDA, "push_ce: event pool");
+      cudaEventRecord(ev, s);
+      cudaStreamWaitEvent(fs, ev, 0);
+      k_set_flags<<<(te - t + 127) / 128, 128, 0, fs>>>(dst_flags, t, te, epoch, wait_flags != nullptr);
+    } else {
+      k_set_flags<<<(te - t + 127) / 128, 128, 0, s>>>(dst_flags, t, te, epoch, wait_flags != nullptr);
+    }
+  }
+  if (fs) {  // the copy stream's completion implies the flags: join the flag stream back
+    cudaEvent_t ev = pooled_event(dev, group);
+    if (!ev) return bz_fail(BZ_ECUDA, "push_ce: event pool");
+    cudaEventRecord(ev, fs);
+    cudaStreamWaitEvent(s, ev, 0);
   }
   return bz_check_launch("bz_push_tiles_ce");
+}
+
+extern "C" int bz_push_tiles_ce(const void* src, void* dst, uint32_t* dst_flags, const uint32_t* wait_flags,
+                                const int64_t* tile_off_host, int t0, int t1, int tiles_per_copy, uint32_t epoch,
+                                void* stream) {
+  return push_ce(src, dst, dst_flags, wait_flags, tile_off_host, t0, t1, tiles_per_copy, epoch, stream, nullptr);
+}
+
+extern "C" int bz_push_tiles_ce2(const void* src, void* dst, uint32_t* dst_flags, const uint32_t* wait_flags,
+                                 const int64_t* tile_off_host, int t0, int t1, int tiles_per_copy, uint32_t epoch,
+                                 void* stream, void* flag_stream) {
+  if (!flag_stream) return bz_fail(BZ_EINVAL, "push_ce2: flag_stream required");
+  return push_ce(src, dst, dst_flags, wait_flags, tile_off_host, t0, t1, tiles_per_copy, epoch, stream, flag_stream);
 }
 
 extern "C" int bz_stage_tiles_sm(const void* host_src, void* dst, uint32_t* dst_flags, const int64_t* tile_off,

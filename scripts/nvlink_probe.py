@@ -228,13 +228,21 @@ def main():
 
     # ---- copy-engine hop (no SM moves bytes): tiles per memcpy sweep ---------------------------
     if args.once is None:
-        for tpc in (8, 16, 32, 64, 128):
-            e = nxt()
-            fn = lambda: lib.bz_push_tiles_ce(src.ptr, mapped.ptr, mapped.flags_ptr, None,  # noqa: E731
-                                              lay.tile_off.ctypes.data, 0, lay.ntiles, tpc, e, stream.cuda_stream)
-            ms = timed(fn, stream)
-            emit({"case": "push", "engine": "ce", "tiles_per_copy": tpc, "ms": ms, "GBps": payload / ms / 1e6,
-                  "ok": check(peer, want, e)})
+        fstream = torch.cuda.Stream(device=0)
+        for split in (False, True):
+            for tpc in (16, 32, 64, 128):
+                e = nxt()
+                if split:   # flag kernels on their own stream: copies back to back
+                    fn = lambda: lib.bz_push_tiles_ce2(src.ptr, mapped.ptr, mapped.flags_ptr, None,  # noqa: E731
+                                                       lay.tile_off.ctypes.data, 0, lay.ntiles, tpc, e,
+                                                       stream.cuda_stream, fstream.cuda_stream)
+                else:
+                    fn = lambda: lib.bz_push_tiles_ce(src.ptr, mapped.ptr, mapped.flags_ptr, None,  # noqa: E731
+                                                      lay.tile_off.ctypes.data, 0, lay.ntiles, tpc, e,
+                                                      stream.cuda_stream)
+                ms = timed(fn, stream)
+                emit({"case": "push", "engine": "ce2" if split else "ce", "tiles_per_copy": tpc, "ms": ms,
+                      "GBps": payload / ms / 1e6, "ok": check(peer, want, e)})
 
     # ---- NVLS multicast over gpu0..gpu{G-1} ------------------------------------------------------
     try:

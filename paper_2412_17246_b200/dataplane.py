@@ -45,7 +45,13 @@ ENGINE_VECTOR = 0
 ENGINE_TMA = 1
 ENGINE_VEC256 = 2   # 32-byte LDG/STG.E.ENL2.256 (sm_100)
 ENGINE_CE = 3       # copy engines (cudaMemcpyAsync into the peer VA), SMs left for compute
+# auto: a source hop with one destination on the copy engines with the flags on a
+# second stream (bz_push_tiles_ce2, 128 tiles per copy: 748 GB/s vs 717 for the SM
+# push, profiles/r2_nvlink_probe_ce2_n2.jsonl); relays and multi-destination pushes on
+# the SMs (tile-granular store-and-forward keeps the chain fill at one tile per hop)
+ENGINE_AUTO = 4
 CE_TILES_PER_COPY = 16
+CE2_TILES_PER_COPY = 128
 MAX_DST = 8  # BZ_MAX_DST (include/blitz.h): destinations per push launch
 
 
@@ -507,7 +513,7 @@ class ScaleExecutor:
             if self.node in members:
                 self.stripe_members = members
         dev = torch.device("cuda", fabric.device)
-        self.streams = {k: torch.cuda.Stream(device=dev) for k in ("copy", "fan", "track", "stage")}
+        self.streams = {k: torch.cuda.Stream(device=dev) for k in ("copy", "fan", "track", "stage", "ceflag")}
         self.epoch = 0
         self._tile_off_host = np.ascontiguousarray(self.layout.tile_off)
         self.writers = self._fanout_writers() if fanout_mode == "nvls" else {}
@@ -655,7 +661,12 @@ class ScaleExecutor:
                                      slab.loaded.data_ptr(), slab.stamps.data_ptr(),
                                      st["track"].cuda_stream)
         dsts, relay = self._feeds()
-        if dsts and self.engine == ENGINE_CE:
+        if dsts and self._ce2_hop(dsts, relay):
+            n = dsts[0]
+            self.lib.bz_push_tiles_ce2(slab.ptr, self.peers[n].ptr, self.peers[n].flags_ptr, None,
+                                       self._tile_off_host.ctypes.data, 0, lay.ntiles, CE2_TILES_PER_COPY, e,
+                                       st["copy"].cuda_stream, st["ceflag"].cuda_stream)
+        elif dsts and self.engine == ENGINE_CE:
             for n in dsts:
                 self.lib.bz_push_tiles_ce(slab.ptr, self.peers[n].ptr, self.peers[n].flags_ptr,
                                           slab.flags_ptr if relay else None,
@@ -664,9 +675,10 @@ class ScaleExecutor:
         elif dsts:
             ptrs = ptr_array([self.peers[n].ptr for n in dsts])
             flags = ptr_array([self.peers[n].flags_ptr for n in dsts])
+            sm_engine = ENGINE_VECTOR if self.engine == ENGINE_AUTO else self.engine
             self.lib.bz_push_tiles(slab.ptr, ptrs, flags, len(dsts),
                                    slab.flags_ptr if relay else None, slab.tile_off.data_ptr(),
-                                   0, lay.ntiles, e, self.nctas, self.engine, st["copy"].cuda_stream)
+                                   0, lay.ntiles, e, self.nctas, sm_engine, st["copy"].cuda_stream)
         peers = self._stripe_peers()
         for i in range(0, len(peers), MAX_DST):
             # forward this member's pieces (gated on its own staged flags) to the group,
@@ -683,6 +695,9 @@ class ScaleExecutor:
         if kernel_events is not None and dom is not None:
             kernel_events[1].record(st[dom])
         return e
+
+    def _ce2_hop(self, dsts, relay) -> bool:
+        return self.engine == ENGINE_AUTO and len(dsts) == 1 and not relay and self.stripe_members is None
 
     def kernels_per_launch(self) -> int:
         """Our kernels one ``launch`` enqueues on this rank (CE memcpys excluded)."""
@@ -705,7 +720,9 @@ class ScaleExecutor:
             else:
                 n += 1
         dsts = self._unicast_targets()
-        if dsts and self.engine == ENGINE_CE:
+        if dsts and self._ce2_hop(dsts, self.role.receives):
+            n += (self.layout.ntiles + CE2_TILES_PER_COPY - 1) // CE2_TILES_PER_COPY   # flag kernels
+        elif dsts and self.engine == ENGINE_CE:
             groups = (self.layout.ntiles + self.ce_tiles - 1) // self.ce_tiles
             per_group = 2 if self.role.receives else 1  # [gate] + flag kernel (memcpy not counted)
             n += len(dsts) * groups * per_group

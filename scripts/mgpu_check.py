@@ -19,7 +19,7 @@ sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
 import torch  # noqa: E402
 
 from paper_2412_17246_b200 import slab as S  # noqa: E402
-from paper_2412_17246_b200.dataplane import ENGINE_TMA, ENGINE_VECTOR, DeviceSlab, Fabric  # noqa: E402
+from paper_2412_17246_b200.dataplane import ENGINE_AUTO, ENGINE_TMA, ENGINE_VECTOR, DeviceSlab, Fabric  # noqa: E402
 from paper_2412_17246_b200.scaleup import ScaleUpSession, plan_for, plan_host_cache  # noqa: E402
 
 
@@ -39,6 +39,7 @@ def main():
         ("grouped-chain", ["gpu0"], gpus[1:], True, "chain", ENGINE_VECTOR),
         ("chain-vector", ["gpu0"], gpus[1:], False, "auto", ENGINE_VECTOR),
         ("chain-tma", ["gpu0"], gpus[1:], False, "auto", ENGINE_TMA),
+        ("chain-auto", ["gpu0"], gpus[1:], False, "auto", ENGINE_AUTO),
         ("hostcache-rep-nvls", ["mem0"], gpus, True, "nvls", ENGINE_VECTOR),
         ("hostcache-rep-chain", ["mem0"], gpus, True, "chain", ENGINE_VECTOR),
         ("hostcache-stripe", ["mem0"], gpus, True, "auto", ENGINE_VECTOR),

@@ -303,3 +303,22 @@ def test_relay_timeout_withholds_downstream_flags(tiny_layout):
         lib.bz_wait_timeouts(ctypes.byref(n), 30_000_000_000)
     relay.close()
     down.close()
+
+
+def test_copy_engine_hop_with_flag_stream(tiny_layout):
+    """bz_push_tiles_ce2 (the `auto` engine's single-destination hop): copies back to back
+    on one stream, flag releases on another; bytes and every flag exact, and the copy
+    stream joins the flag stream at the end."""
+    lib = cuda_lib()
+    src, dst = DeviceSlab(tiny_layout, 0), DeviceSlab(tiny_layout, 0)
+    src.fill_random(seed=21)
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    s1.wait_stream(torch.cuda.current_stream())
+    for epoch, tpc in ((1, 4), (2, 128)):
+        lib.bz_push_tiles_ce2(src.ptr, dst.ptr, dst.flags_ptr, None, tiny_layout.tile_off.ctypes.data, 0,
+                              tiny_layout.ntiles, tpc, epoch, s1.cuda_stream, s2.cuda_stream)
+        s1.synchronize()          # joins s2: every flag released once s1 is done
+        assert torch.equal(dst.data, src.data)
+        assert int(dst.flags.min()) == epoch and int(dst.flags.max()) == epoch
+    src.close()
+    dst.close()

@@ -40,7 +40,7 @@ def test_torchrun_scaleup_bit_exact():
         capture_output=True, text=True, timeout=600, env=env, cwd=str(ROOT))
     lines = [json.loads(l) for l in proc.stdout.splitlines() if l.startswith("{")]
     assert proc.returncode == 0, proc.stdout[-2000:] + proc.stderr[-3000:]
-    assert len(lines) == 7 and all(l["ok"] for l in lines), lines
+    assert len(lines) == 8 and all(l["ok"] for l in lines), lines
     by = {l["case"]: l for l in lines}
     # the NVLS cases really ran k_multicast_tiles through a multicast object whenever
     # the plan has a fan-out group; the chain cases never did

@@ -44,7 +44,7 @@ using namespace bz::tc;
 
 constexpr int BQ = 128;       // query rows per tile (= TMEM lanes)
 constexpr int BKV = 128;      // keys per tile
-constexpr int THREADS = 576;  // w0 TMA, w1 MMA + TMEM allocator, w2..w9 softmax A, w10..w17 softmax B
+constexpr int THREADS = 320;  // w0 TMA, w1 MMA + TMEM allocator, w2..w5 softmax A, w6..w9 softmax B
 constexpr int STAGES = 2;     // K and V rings
 
 template <int HD>
@@ -54,7 +54,7 @@ struct Cfg {
   static constexpr int Q_BYTES = KA * ROW_ATOM;    // one query tile
   static constexpr int K_BYTES = KA * ROW_ATOM;    // 128 keys x hd
   static constexpr int V_BYTES = KA * ROW_ATOM;    // 128 keys x hd, as loaded (hd contiguous)
-  static constexpr int BAR_BYTES = 256 + 4 * BQ * 4;   // 18 barriers + the TMEM address + row-pair exchange
+  static constexpr int BAR_BYTES = 256;   // 18 barriers + the TMEM address
   static constexpr int SMEM = 1024 + 2 * Q_BYTES + STAGES * (K_BYTES + V_BYTES) + BAR_BYTES;
   // TMEM: S_A at [0, 128), S_B at [128, 256) -- P_X (bf16 pairs) in the first 64 columns
   // of S_X once S_X is in registers -- then O_A, O_B (HD columns each)
@@ -112,15 +112,6 @@ __device__ __forceinline__ void tmem_st_32x32b_x16(uint32_t taddr, const uint32_
       "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]),
       "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
       : "memory");
-}
-__device__ __forceinline__ void tmem_ld_32x32b_x16(uint32_t taddr, uint32_t* r) {
-  asm volatile(
-      "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
-      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
-      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
-        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
-      : "r"(taddr));
-  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 __device__ __forceinline__ void tmem_st_32x32b_x32(uint32_t taddr, const uint32_t (&r)[32]) {
   tmem_st_32x32b_x16(taddr, r);
@@ -228,9 +219,9 @@ __global__ void __launch_bounds__(THREADS, 1)
       mbar_init(&v_full[i], 1);
       mbar_init(&v_empty[i], 1);
       mbar_init(&s_full[i], 1);
-      mbar_init(&p_full[i], 8);
+      mbar_init(&p_full[i], 4);
       mbar_init(&pv_done[i], 1);
-      mbar_init(&o_free[i], 8);
+      mbar_init(&o_free[i], 4);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -317,9 +308,9 @@ __global__ void __launch_bounds__(THREADS, 1)
           if (more) mbar_wait(&k_full[(g0 + 1) & 1], ((g0 + 1) >> 1) & 1);
           for (int t = 0; t < 2; ++t) {
             if (t == 0 && j >= it.nj_a) continue;          // tile A is done after its diagonal
-            if (k == 0) BZ_TRACE(2048 + 8 * j + 2 * t);
+            BZ_TRACE(2048 + 8 * j + 2 * t);
             mbar_wait(&p_full[t], up[t] & 1);
-            if (k == 0) BZ_TRACE(2048 + 8 * j + 2 * t + 1);
+            BZ_TRACE(2048 + 8 * j + 2 * t + 1);
             ++up[t];
             // the previous item's epilogue must have read O_t before it is overwritten
             if (j == 0) mbar_wait(&o_free[t], (k & 1) ^ 1);
@@ -335,21 +326,13 @@ __global__ void __launch_bounds__(THREADS, 1)
       }
     }
   } else {
-    // ---- softmax of tile t: two threads per query row r, each taking 64 of the 128
-    // keys of a tile and half of O's columns (eight warps per tile) ----
-    const int sw = warp - 2;                 // 0..15
-    const int t = sw >> 3;                   // 0 = A, 1 = B
-    const int half = (sw >> 2) & 1;
+    // ---- softmax of tile t (thread = query row r) ----
+    const int t = (warp - 2) >> 2;           // 0 = A, 1 = B
     const int quarter = warp & 3;            // TMEM lane quarter (hardware: warp id % 4)
     const int r = quarter * 32 + lane;
-    const int pair_bar = 1 + t * 4 + quarter;   // named barrier of the row pair (64 threads)
-    float* xch = reinterpret_cast<float*>(tmem_slot + 1) + (t * 2 + half) * BQ;   // [tile][half][row]
-    float* xch_peer = reinterpret_cast<float*>(tmem_slot + 1) + (t * 2 + (half ^ 1)) * BQ;
     const uint32_t lane_off = static_cast<uint32_t>(quarter * 32) << 16;
-    const uint32_t s_addr = tmem + lane_off + C::S_COL + t * BKV + half * 64;        // my 64 scores
-    const uint32_t p_addr = tmem + lane_off + C::S_COL + t * BKV + half * 32;        // my 32 P columns
-    const uint32_t o_addr = tmem + lane_off + C::O_COL + t * HD + half * (HD / 2);   // my O columns
-    auto sync_pair = [&]() { asm volatile("bar.sync %0, 64;" ::"r"(pair_bar) : "memory"); };
+    const uint32_t s_addr = tmem + lane_off + C::S_COL + t * BKV;
+    const uint32_t o_addr = tmem + lane_off + C::O_COL + t * HD;
     int us = 0;                              // S / P uses of this tile (phases)
     for (int k = 0, i; (i = item_at(k)) < n_items && i >= 0; ++k) {
       const Item it = decode(i);
@@ -357,38 +340,35 @@ __global__ void __launch_bounds__(THREADS, 1)
       const int my_nj = t == 0 ? it.nj_a : it.nj;
       const int diag = it.qt_a + t;
       float m = -INFINITY;                   // running max in use (log2 domain)
-      float l = 0.f;                         // this thread's part of the row sum, relative to m
+      float l = 0.f;                         // row sum relative to m
       for (int j = 0; j < my_nj; ++j, ++us) {
-        if (lane == 0 && quarter == 2 && half == 0 && k == 0) BZ_TRACE(1024 * t + 4 * j);
+        if (lane == 0 && quarter == 2 && k == 0) BZ_TRACE(1024 * t + 4 * j);
         mbar_wait(&s_full[t], us & 1);
-        if (lane == 0 && quarter == 2 && half == 0 && k == 0) BZ_TRACE(1024 * t + 4 * j + 1);
+        if (lane == 0 && quarter == 2 && k == 0) BZ_TRACE(1024 * t + 4 * j + 1);
         tc_fence_after();
-        uint32_t v[2][32];
-        tmem_ld_32x32b_x32_async(s_addr, v[0]);
-        tmem_ld_32x32b_x32_async(s_addr + 32, v[1]);
-        tmem_wait_ld(v[0]);
-        tmem_wait_ld(v[1]);
-        if (j == diag) {  // causal mask: keys after this query get -inf
-          const int key0 = j * BKV + half * 64;
+        uint32_t v[4][32];
 #pragma unroll
-          for (int cc = 0; cc < 2; ++cc)
+        for (int cc = 0; cc < 4; ++cc) tmem_ld_32x32b_x32_async(s_addr + 32 * cc, v[cc]);
+#pragma unroll
+        for (int cc = 0; cc < 4; ++cc) tmem_wait_ld(v[cc]);
+        if (j == diag) {  // causal mask: keys after this query get -inf
+          const int key0 = j * BKV;
+#pragma unroll
+          for (int cc = 0; cc < 4; ++cc)
 #pragma unroll
             for (int q = 0; q < 32; ++q)
               if (key0 + 32 * cc + q > qpos) v[cc][q] = __float_as_uint(-INFINITY);
         }
-        float mxc[2];
+        // row max: four independent FMNMX3 chains (latency, not throughput, bounds them)
+        float mxc[4];
 #pragma unroll
-        for (int cc = 0; cc < 2; ++cc) {
+        for (int cc = 0; cc < 4; ++cc) {
           mxc[cc] = -INFINITY;
 #pragma unroll
           for (int q = 0; q < 32; q += 2)
             mxc[cc] = max3(mxc[cc], __uint_as_float(v[cc][q]), __uint_as_float(v[cc][q + 1]));
         }
-        // the row's max over both halves
-        xch[r] = fmaxf(mxc[0], mxc[1]);
-        sync_pair();
-        const float mx = fmaxf(xch[r], xch_peer[r]) * a.scale_log2;
-        sync_pair();   // xch is rewritten next tile
+        const float mx = fmaxf(fmaxf(mxc[0], mxc[1]), fmaxf(mxc[2], mxc[3])) * a.scale_log2;
         // raise the max only when it grows by more than 2^kRescale: O and l are then
         // scaled by 2^(m_old - m_new).  tcgen05.ld/st are warp-collective, so the warp
         // rescales whenever any of its rows must (alpha = 1 on the others).  O holds
@@ -397,25 +377,26 @@ __global__ void __launch_bounds__(THREADS, 1)
         if (__any_sync(0xffffffffu, raise)) {
           const float alpha = raise ? ex2(m - mx) : 1.f;   // 0 on the first tile
           if (j > 0) {
-            // 16 columns at a time: the 64 scores stay live in registers meanwhile
-#pragma unroll 1
-            for (int cc = 0; cc < HD / 2; cc += 16) {
-              uint32_t o[16];
-              tmem_ld_32x32b_x16(o_addr + cc, o);
 #pragma unroll
-              for (int q = 0; q < 16; ++q) o[q] = __float_as_uint(__uint_as_float(o[q]) * alpha);
-              tmem_st_32x32b_x16(o_addr + cc, o);
+            for (int cc = 0; cc < HD; cc += 32) {
+              uint32_t o[32];
+              tmem_ld_32x32b_x32(o_addr + cc, o);
+#pragma unroll
+              for (int q = 0; q < 32; ++q) o[q] = __float_as_uint(__uint_as_float(o[q]) * alpha);
+              tmem_st_32x32b_x32(o_addr + cc, o);
             }
           }
           l *= alpha;
           if (raise) m = mx;
         }
-        // P = exp2(s * scale - m) as bf16 pairs into this half's 32 columns of S_t
+        // P = exp2(s * scale - m) as bf16 pairs into the first 64 columns of S_t; eight
+        // partial sums (short FADD chains).  (Moving a quarter of the exponentials to the
+        // FMA pipe with ex2_fma was measured 7 % slower: MUFU is not the limiter.)
         float sum[8];
 #pragma unroll
         for (int q = 0; q < 8; ++q) sum[q] = 0.f;
 #pragma unroll
-        for (int cc = 0; cc < 2; ++cc) {
+        for (int cc = 0; cc < 4; ++cc) {
           uint32_t w[16];
 #pragma unroll
           for (int q = 0; q < 32; q += 2) {
@@ -424,34 +405,31 @@ __global__ void __launch_bounds__(THREADS, 1)
             sum[(q >> 1) & 7] += p0 + p1;
             w[q >> 1] = pack2(p0, p1);
           }
-          tmem_st_32x32b_x16(p_addr + 16 * cc, w);
+          tmem_st_32x32b_x16(s_addr + 16 * cc, w);
         }
         l += ((sum[0] + sum[1]) + (sum[2] + sum[3])) + ((sum[4] + sum[5]) + (sum[6] + sum[7]));
         asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&p_full[t]);
-        if (lane == 0 && quarter == 2 && half == 0 && k == 0) BZ_TRACE(1024 * t + 4 * j + 2);
+        if (lane == 0 && quarter == 2 && k == 0) BZ_TRACE(1024 * t + 4 * j + 2);
       }
       // ---- epilogue: O / l -> bf16; O is handed back to the MMA once read ----
-      xch[r] = l;
-      sync_pair();
-      const float inv = 1.f / (l + xch_peer[r]);
-      sync_pair();
       mbar_wait(&pv_done[t], (us - 1) & 1);
       tc_fence_after();
-      uint32_t o[HD / 64][32];
+      const float inv = 1.f / l;
+      uint32_t o[HD / 32][32];
 #pragma unroll
-      for (int cc = 0; cc < HD / 64; ++cc) tmem_ld_32x32b_x32_async(o_addr + 32 * cc, o[cc]);
+      for (int cc = 0; cc < HD / 32; ++cc) tmem_ld_32x32b_x32_async(o_addr + 32 * cc, o[cc]);
 #pragma unroll
-      for (int cc = 0; cc < HD / 64; ++cc) tmem_wait_ld(o[cc]);
+      for (int cc = 0; cc < HD / 32; ++cc) tmem_wait_ld(o[cc]);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&o_free[t]);
       if (qpos < a.S) {
-        __nv_bfloat16* dst = a.out + static_cast<int64_t>(it.row0 + qpos) * a.ldo + it.h * HD + half * (HD / 2);
+        __nv_bfloat16* dst = a.out + static_cast<int64_t>(it.row0 + qpos) * a.ldo + it.h * HD;
 #pragma unroll
-        for (int q = 0; q < HD / 2; q += 8) {
+        for (int q = 0; q < HD; q += 8) {
           const float* f = reinterpret_cast<const float*>(&o[q >> 5][q & 31]);
           *reinterpret_cast<uint4*>(dst + q) =
               make_uint4(pack2(f[0] * inv, f[1] * inv), pack2(f[2] * inv, f[3] * inv),

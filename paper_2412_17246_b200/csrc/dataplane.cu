@@ -587,8 +587,10 @@ extern "C" int bz_stage_tiles_ce(const void* host_src, void* dst, uint32_t* dst_
 // after its group's copy: the copy stream then carries only copies (and relay
 // gates), so the copy engine streams back to back instead of idling for a kernel
 // launch between groups.
+// per host thread: a record + wait pair is enqueued back to back by one thread, so
+// another thread's calls can never re-record an event between them
 static cudaEvent_t pooled_event(int dev, size_t i) {
-  static std::vector<cudaEvent_t> pool[64];
+  static thread_local std::vector<cudaEvent_t> pool[64];
   auto& v = pool[dev < 64 ? dev : 63];
   while (v.size() <= i) {
     cudaEvent_t e;

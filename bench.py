@@ -942,8 +942,8 @@ def run_blitz(args):
             # ncu DRAM counters for it; the k_push_tiles capture describes the SM relays
             traffic, traffic_src = None, "copy-engine hop (bz_push_tiles_ce2): invisible to ncu"
         mover = ("copy engines (bz_stage_tiles_ce)" if bound == "pcie" else
-                 "source hop on the copy engines (bz_push_tiles_ce2), relays k_push_tiles"
-                 if args.engine == "auto" else f"k_push_tiles ({args.engine})")
+                 "copy engines (bz_push_tiles_ce2): source -> leaf hops" if args.engine == "auto" and not relays
+                 else f"k_push_tiles ({'vector' if args.engine == 'auto' else args.engine}) along the chain")
         line = {
             "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": N, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",

@@ -45,10 +45,11 @@ ENGINE_VECTOR = 0
 ENGINE_TMA = 1
 ENGINE_VEC256 = 2   # 32-byte LDG/STG.E.ENL2.256 (sm_100)
 ENGINE_CE = 3       # copy engines (cudaMemcpyAsync into the peer VA), SMs left for compute
-# auto: a source hop with one destination on the copy engines with the flags on a
-# second stream (bz_push_tiles_ce2, 128 tiles per copy: 748 GB/s vs 717 for the SM
-# push, profiles/r2_nvlink_probe_ce2_n2.jsonl); relays and multi-destination pushes on
-# the SMs (tile-granular store-and-forward keeps the chain fill at one tile per hop)
+# auto: a source hop to a leaf with one destination on the copy engines with the flags
+# on a second stream (bz_push_tiles_ce2, 128 tiles per copy: 748 GB/s vs 717 for the SM
+# push, profiles/r2_nvlink_probe_ce2_n2.jsonl); relays, hops into a relay and
+# multi-destination pushes on the SMs (tile-granular store-and-forward keeps the chain
+# fill at one tile per hop)
 ENGINE_AUTO = 4
 CE_TILES_PER_COPY = 16
 CE2_TILES_PER_COPY = 128
@@ -696,8 +697,24 @@ class ScaleExecutor:
             kernel_events[1].record(st[dom])
         return e
 
+    def _forwards(self, node: str) -> bool:
+        """``node`` relays what it receives (chain child, fan-out, or a next sibling)."""
+        r = self.roles.get(node)
+        if r is None:
+            return False
+        if r.children or r.fanout:
+            return True
+        if r.rep is not None:
+            sibs = self.plan.nvlink_fanout[r.rep]
+            return sibs.index(node) + 1 < len(sibs)
+        return False
+
     def _ce2_hop(self, dsts, relay) -> bool:
-        return self.engine == ENGINE_AUTO and len(dsts) == 1 and not relay and self.stripe_members is None
+        # copy engines only for a source -> leaf hop: a relaying destination forwards
+        # tile by tile, and the copy engine's 128-tile flag groups would make its
+        # pipeline bursty (N=4 grouped plan measured 648 vs 683 GB/s per destination)
+        return (self.engine == ENGINE_AUTO and len(dsts) == 1 and not relay and self.stripe_members is None
+                and not self._forwards(dsts[0]))
 
     def kernels_per_launch(self) -> int:
         """Our kernels one ``launch`` enqueues on this rank (CE memcpys excluded)."""

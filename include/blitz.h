@@ -267,6 +267,41 @@ int bz_decode_attention_rows(const void* q, int ldq, const void* k_cache, const 
                              int n_heads, int n_kv, int head_dim, int64_t s_max, const int32_t* pos, void* out,
                              int ldo, void* workspace, int64_t workspace_bytes, void* stream);
 
+/* ---- fused small-batch decode (csrc/decode_fused.cu) ------------------------------------
+ * A whole decode step over n_blocks blocks in ONE persistent cooperative kernel
+ * (1..4 sequences): per block rmsnorm -> qkv -> RoPE + KV append -> attention ->
+ * o-proj + residual -> rmsnorm -> gate/up + SiLU -> down + residual, with each CTA
+ * streaming its slice of every weight through shared memory and grid barriers
+ * between phases.  Same math and bf16 rounding points as bz_rmsnorm / bz_gemm_bf16 /
+ * bz_rope_append(_rows) / bz_decode_attention(_rows) / bz_silu_mul.
+ * x: [rows, ldx] bf16 hidden state, updated in place to the last block's output.
+ * pos_stride 0: one device position for the batch (pos[0]); 1: one per row.
+ * Workspace (bz_decode_fused_workspace_bytes) must be zeroed once before first use.
+ * Per block (device pointers, the slab's tensor views): attn_norm [d], wqkv
+ * [(n_heads + 2 n_kv) hd, d], wo [d, d], ffn_norm [d], wgu [2 ffn, d] (gate rows, then
+ * up rows), wdown [d, ffn], caches [rows, n_kv, s_max, hd]. */
+typedef struct bz_decode_block {
+  const void* attn_norm;
+  const void* wqkv;
+  const void* wo;
+  const void* ffn_norm;
+  const void* wgu;
+  const void* wdown;
+  void* k_cache;
+  void* v_cache;
+} bz_decode_block;
+int bz_decode_fused_workspace_bytes(int rows, int d, int n_heads, int n_kv, int head_dim, int ffn, int64_t* bytes);
+int bz_decode_fused(const bz_decode_block* blocks, int n_blocks, void* x, int ldx, int rows, int d, int n_heads,
+                    int n_kv, int head_dim, int ffn, float rope_theta, float eps, int64_t s_max, const int32_t* pos,
+                    int pos_stride, void* workspace, int64_t workspace_bytes, int max_ctas, void* stream);
+/* *timed_out = 1 if the last bz_decode_fused on this workspace hit its grid-barrier
+ * timeout (a CTA never became resident); synchronises the stream. */
+int bz_decode_fused_status(const void* workspace, int* timed_out, void* stream);
+/* Diagnostics: while buf is set (device memory, >= grid * n_blocks * 22 * 8 bytes), every
+ * bz_decode_fused launch stores a %globaltimer stamp per CTA, block and phase event
+ * (scripts/fused_trace.py reads them); NULL turns it off. */
+int bz_decode_fused_set_trace(void* buf, int64_t bytes);
+
 /* ---- misc ------------------------------------------------------------------------------ */
 int bz_sm_count(int dev, int* n);
 

@@ -77,6 +77,12 @@ class BlitzError(RuntimeError):
     """A libblitz call failed; carries bz_last_error()."""
 
 
+class BzDecodeBlock(ctypes.Structure):
+    """bz_decode_block: one block's weight views and KV panels (device pointers)."""
+    _fields_ = [(n, ctypes.c_void_p) for n in ("attn_norm", "wqkv", "wo", "ffn_norm", "wgu", "wdown", "k_cache",
+                                               "v_cache")]
+
+
 class BzSlab(ctypes.Structure):
     _fields_ = [("ptr", ctypes.c_uint64), ("bytes", ctypes.c_uint64), ("handle", ctypes.c_uint64),
                 ("dev", ctypes.c_int), ("fd", ctypes.c_int)]
@@ -148,6 +154,11 @@ _SIGNATURES = {
                                  _P],
     "bz_prefill_attention_workspace_bytes": [_I, _I, _I, _I, ctypes.POINTER(ctypes.c_int64)],
     "bz_prefill_attention": [_P, _I, _I, _I, _I, _I, _I, _P, ctypes.c_int64, _P, _I, _P],
+    "bz_decode_fused_workspace_bytes": [_I, _I, _I, _I, _I, _I, ctypes.POINTER(ctypes.c_int64)],
+    "bz_decode_fused": [ctypes.POINTER(BzDecodeBlock), _I, _P, _I, _I, _I, _I, _I, _I, _I, ctypes.c_float,
+                        ctypes.c_float, ctypes.c_int64, _P, _I, _P, ctypes.c_int64, _I, _P],
+    "bz_decode_fused_status": [_P, _PI, _P],
+    "bz_decode_fused_set_trace": [_P, ctypes.c_int64],
     "bz_sm_count": [_I, _PI],
     "bz_preload_kernels": [_I, _PI],
 }

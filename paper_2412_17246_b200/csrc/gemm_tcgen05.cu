@@ -40,20 +40,25 @@ constexpr int SMEM_LIMIT = 232448;    // 227 KiB dynamic shared memory per CTA
 // weight tile still keeps ~128 KB of loads in flight per SM.
 constexpr int MAX_STAGES = 32;
 constexpr int BAR_BYTES = (2 * MAX_STAGES + 4) * 8 + 16;  // full/empty ring, acc full/empty, TMEM slot, flag
-template <int BN_>
+// OCC = CTAs per SM.  OCC = 2 (skinny decode GEMMs, BN <= 128): half the shared
+// memory and at most 256 TMEM columns per CTA, so the next GEMM's CTA (launched
+// early by PDL) is resident beside this one and streams its first weight stages
+// while this one drains -- with one 227 KiB CTA per SM consecutive GEMMs cannot overlap.
+constexpr int SMEM_LIMIT_OCC2 = 115712;  // 2 x (113 KiB + 1 KiB reserved) = 228 KiB per SM
+template <int BN_, int OCC_ = 1>
 struct Cfg {
   static constexpr int BN = BN_;
   static constexpr int B_BYTES = BN * BK * 2;
   static constexpr int ACC_COLS = BN;  // fp32 accumulator columns per buffer
   static constexpr int TMEM_COLS = 2 * BN <= 64 ? 64 : 2 * BN <= 128 ? 128 : 2 * BN <= 256 ? 256 : 512;
-  static constexpr int SMEM_BYTES = SMEM_LIMIT;
+  static constexpr int SMEM_BYTES = OCC_ == 1 ? SMEM_LIMIT : SMEM_LIMIT_OCC2;
   static_assert(BN % 32 == 0 && BN <= 256, "tile N");
+  static_assert(OCC_ == 1 || (OCC_ == 2 && TMEM_COLS <= 256), "two CTAs per SM share 512 TMEM columns");
 };
 // ring stages for one A stage of a_stage bytes (multiple of 1024) and B_BYTES
-__host__ __device__ constexpr int ring_stages(int a_stage, int b_bytes) {
-  return (SMEM_LIMIT - 1024 - BAR_BYTES) / (a_stage + b_bytes) < MAX_STAGES
-             ? (SMEM_LIMIT - 1024 - BAR_BYTES) / (a_stage + b_bytes)
-             : MAX_STAGES;
+__host__ __device__ constexpr int ring_stages(int a_stage, int b_bytes, int limit = SMEM_LIMIT) {
+  return (limit - 1024 - BAR_BYTES) / (a_stage + b_bytes) < MAX_STAGES ? (limit - 1024 - BAR_BYTES) / (a_stage + b_bytes)
+                                                                      : MAX_STAGES;
 }
 
 using namespace bz::tc;
@@ -263,10 +268,10 @@ __device__ __forceinline__ void streamk_fixup(const Params& p, int tile, int n0,
   }
 }
 
-template <int BN_>
-__global__ void __launch_bounds__(THREADS, 1)
+template <int BN_, int OCC_>
+__global__ void __launch_bounds__(THREADS, OCC_)
     k_gemm_bf16(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b, Params p) {
-  using C = Cfg<BN_>;
+  using C = Cfg<BN_, OCC_>;
   constexpr int BN = C::BN, B_BYTES = C::B_BYTES;
   constexpr int ACC_COLS = C::ACC_COLS, TMEM_COLS = C::TMEM_COLS;
   const int STAGES = p.stages, A_STAGE = p.a_stage;
@@ -781,7 +786,7 @@ struct SkinnyPlan {
 
 // Tile width and schedule for M <= 128 (one row of tiles): the fastest predicted
 // of {32 .. 256} x {whole tiles, stream-K}.
-static SkinnyPlan plan_skinny(int M, int N, int K, int ctas, int64_t ws_bytes, int only_bn) {
+static SkinnyPlan plan_skinny(int M, int N, int K, int ctas, int64_t ws_bytes, int only_bn, int max_bn = 256) {
   const int widths[5] = {256, 192, 128, 64, 32};
   const int k_blocks = (K + BK - 1) / BK;
   const double chip = 2.0 * N * K / SKINNY_CHIP_BPS;
@@ -789,7 +794,7 @@ static SkinnyPlan plan_skinny(int M, int N, int K, int ctas, int64_t ws_bytes, i
   SkinnyPlan plain{only_bn ? only_bn : 128, 0}, sk{0, 0};
   double t_plain = 1e30, t_sk = 1e30;
   for (int bn : widths) {  // widest first: a narrower tile must win by 2 %
-    if (only_bn && bn != only_bn) continue;
+    if ((only_bn && bn != only_bn) || bn > max_bn) continue;
     const int tiles = (N + bn - 1) / bn;
     const double waves = static_cast<double>((tiles + ctas - 1) / ctas);
     const double run = waves * k_blocks * kblock_s(bn);
@@ -867,10 +872,10 @@ static int pick_bn(int M, int N, int ctas) {
   return best;
 }
 
-template <int BN_>
+template <int BN_, int OCC_ = 1>
 static int launch(const CUtensorMap& ma, const void* B, int N, int K, int ldb, Params p, int max_ctas, int sk_per,
                   cudaStream_t stream, int* ctas_out) {
-  using Cf = Cfg<BN_>;
+  using Cf = Cfg<BN_, OCC_>;
   CUtensorMap mb;
   if (int rc = encode_kmajor(&mb, B, N, K, ldb, BN_)) return rc;
   p.n_tiles = (N + BN_ - 1) / BN_;
@@ -889,14 +894,15 @@ static int launch(const CUtensorMap& ma, const void* B, int N, int K, int ldb, P
   }
   static bool attr_set[64] = {};
   p.a_stage = (p.a_bytes + 1023) / 1024 * 1024;
-  p.stages = ring_stages(p.a_stage, Cf::B_BYTES);
+  p.stages = ring_stages(p.a_stage, Cf::B_BYTES, Cf::SMEM_BYTES);
   if (dev < 64 && !attr_set[dev]) {
     cudaError_t e =
-        cudaFuncSetAttribute(k_gemm_bf16<BN_>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cf::SMEM_BYTES);
+        cudaFuncSetAttribute(k_gemm_bf16<BN_, OCC_>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cf::SMEM_BYTES);
     if (e != cudaSuccess) return bz_fail_cuda(e, "gemm smem attribute");
     attr_set[dev] = true;
   }
-  cudaError_t e = launch_pdl(PDL_GEMM, k_gemm_bf16<BN_>, dim3(grid), dim3(THREADS), Cf::SMEM_BYTES, stream, ma, mb, p);
+  cudaError_t e =
+      launch_pdl(PDL_GEMM, k_gemm_bf16<BN_, OCC_>, dim3(grid), dim3(THREADS), Cf::SMEM_BYTES, stream, ma, mb, p);
   if (e != cudaSuccess) return bz_fail_cuda(e, "bz_gemm_bf16 launch");
   if (ctas_out) *ctas_out = grid;
   return bz_check_launch("bz_gemm_bf16");
@@ -939,6 +945,17 @@ static int launch_pair(const CUtensorMap& ma, const void* B, int N, int K, int l
     if (ctas_out) *ctas_out = blocks;
   }
   return bz_check_launch("bz_gemm_bf16 (pair)");
+}
+
+// BZ_GEMM_OCC=1|2 pins the skinny kernel's CTAs per SM; unset/0: two for M <= 64
+static int occ_override() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("BZ_GEMM_OCC");
+    v = e ? atoi(e) : 0;
+    if (v != 1 && v != 2) v = 0;
+  }
+  return v;
 }
 
 // BZ_GEMM_PAIR=0 forces single-CTA tiles, =1 forces CTA pairs; default: pairs when M >= 256
@@ -1129,8 +1146,19 @@ static int gemm_impl(const void* A, const void* B, void* C, const void* residual
     }
   }
   SkinnyPlan plan{forced ? forced : (single_bn ? single_bn : pick_bn(M, N, ctas)), 0};
+  const bool occ2 = M <= BM && (occ_override() == 2 || (occ_override() == 0 && M <= 64)) && forced <= 128;
   if (M <= BM) {
-    plan = plan_skinny(M, N, K, ctas, ws_bytes, forced);
+    plan = plan_skinny(M, N, K, ctas, ws_bytes, forced, occ2 ? 128 : 256);
+  }
+  if (occ2) {
+    switch (plan.bn) {
+      case 32:
+        return launch<32, 2>(ma, B, N, K, ldb, p, max_ctas, plan.sk_per, s, ctas_out);
+      case 64:
+        return launch<64, 2>(ma, B, N, K, ldb, p, max_ctas, plan.sk_per, s, ctas_out);
+      default:
+        return launch<128, 2>(ma, B, N, K, ldb, p, max_ctas, plan.sk_per, s, ctas_out);
+    }
   }
   switch (plan.bn) {
     case 32:

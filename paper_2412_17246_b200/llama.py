@@ -30,7 +30,7 @@ from typing import Optional
 
 import torch
 
-from ._native import BZ_GEMM_B_STATIC, BZ_GEMM_C_F32, cuda_lib
+from ._native import BZ_GEMM_B_STATIC, BZ_GEMM_C_F32, BzDecodeBlock, cuda_lib
 from .slab import LlamaArch, SlabLayout
 
 
@@ -38,6 +38,13 @@ from .slab import LlamaArch, SlabLayout
 # cuDNN's kernel on the 7B shapes, ahead at batch 1; profiles/r2_attn_bench_v5.jsonl);
 # BZ_PREFILL_ATTN=sdpa runs torch SDPA instead for A/B measurements
 PREFILL_ATTENTION = os.environ.get("BZ_PREFILL_ATTN", "tcgen05")
+
+# small-batch decode: one persistent kernel per decode step (csrc/decode_fused.cu) for
+# 1..FUSED_MAX_ROWS sequences.  Opt-in (BZ_DECODE_FUSED=1): on B200 it measured level with
+# the per-block kernels at batch 1 (117.8 vs 116.2 us per 7B block) and slower at 2..4
+# rows (its CUDA-core dot products become the bottleneck), profiles/r2_fused_decode.txt
+FUSED_DECODE = os.environ.get("BZ_DECODE_FUSED", "0") == "1"
+FUSED_MAX_ROWS = 4
 
 
 def _entries(arch: LlamaArch, k: int) -> list[tuple[str, tuple[int, ...]]]:
@@ -249,6 +256,66 @@ class LlamaExecutor:
                kv.workspace.numel(), s)
         return self._attn_out_mlp(k, x, attn, out, signal)
 
+    def fused_decode_ok(self, rows: int, kv: "KVCache", first: int, last: int) -> bool:
+        """Whether bz_decode_fused covers this step (shapes its kernel supports)."""
+        a = self.arch
+        return (FUSED_DECODE and 1 <= rows <= FUSED_MAX_ROWS and a.head_dim in (64, 128)
+                and a.n_heads % a.n_kv_heads == 0 and a.n_heads // a.n_kv_heads <= 8
+                and a.d_model == a.n_heads * a.head_dim and a.ffn % 8 == 0
+                and 0 < kv.max_seq <= 131072 and 0 < last - first <= 96)
+
+    def decode_blocks(self, first: int, last: int, x: torch.Tensor, kv: "KVCache") -> torch.Tensor:
+        """Blocks [first, last) of one decode step for x [B, d]: one bz_decode_fused launch
+        for 1..4 sequences, else decode_block per block.  Returns a new [B, d] tensor."""
+        kv.require_room()
+        B = x.shape[0]
+        if not self.fused_decode_ok(B, kv, first, last):
+            for k in range(first, last):
+                x = self.decode_block(k, x, kv)
+            return x
+        a = self.arch
+        out = x.contiguous().clone()   # updated in place by the kernel
+        ws = self._fused_workspace(B)
+        self.lib.bz_decode_fused(self._fused_blocks(kv, first, last), last - first, out.data_ptr(), out.stride(0), B,
+                                 a.d_model, a.n_heads, a.n_kv_heads, a.head_dim, a.ffn, a.rope_theta, a.norm_eps,
+                                 kv.max_seq, kv.pos_dev.data_ptr(), 1 if kv.per_row else 0, ws.data_ptr(),
+                                 ws.numel(), 0, torch.cuda.current_stream().cuda_stream)
+        return out
+
+    def _fused_workspace(self, rows: int) -> torch.Tensor:
+        import ctypes
+        cache = self.__dict__.setdefault("_fused_ws", {})
+        if rows not in cache:
+            a = self.arch
+            nb = ctypes.c_int64(0)
+            self.lib.bz_decode_fused_workspace_bytes(rows, a.d_model, a.n_heads, a.n_kv_heads, a.head_dim, a.ffn,
+                                                     ctypes.byref(nb))
+            cache[rows] = torch.zeros(nb.value, dtype=torch.uint8, device=self.h.device)  # zeroed once
+        return cache[rows]
+
+    def _fused_blocks(self, kv: "KVCache", first: int, last: int):
+        """The bz_decode_block array of blocks [first, last) against this cache (kept on the
+        cache, so it lives exactly as long as the panels it points into)."""
+        cache = kv.__dict__.setdefault("_fused_blocks", {})
+        key = (id(self), first, last)
+        if key not in cache:
+            arr = (BzDecodeBlock * (last - first))()
+            for i, k in enumerate(range(first, last)):
+                L = self.w.layers[k]
+                arr[i] = BzDecodeBlock(L["attn_norm"].data_ptr(), L["wqkv"].data_ptr(), L["wo"].data_ptr(),
+                                       L["ffn_norm"].data_ptr(), L["wgu"].data_ptr(), L["wdown"].data_ptr(),
+                                       kv.k[k].data_ptr(), kv.v[k].data_ptr())
+            cache[key] = arr
+        return cache[key]
+
+    def fused_decode_timed_out(self, rows: int) -> bool:
+        """True if the last fused decode step of this batch size hit its grid-barrier timeout."""
+        import ctypes
+        flag = ctypes.c_int(0)
+        self.lib.bz_decode_fused_status(self._fused_workspace(rows).data_ptr(), ctypes.byref(flag),
+                                        torch.cuda.current_stream().cuda_stream)
+        return bool(flag.value)
+
     @torch.no_grad()
     def head(self, x: torch.Tensor, bs: tuple[int, int]) -> torch.Tensor:
         """Final norm + lm_head on each sequence's last token -> fp32 logits [B, vocab]."""
@@ -289,8 +356,7 @@ class LlamaExecutor:
         last = self.arch.n_layers if last is None else last
         if x is None:
             x = self.embed(tokens)
-        for k in range(first, last):
-            x = self.decode_block(k, x, kv)
+        x = self.decode_blocks(first, last, x, kv)
         kv.advance()
         return self.head(x, (x.shape[0], 1)) if last == self.arch.n_layers else x
 
@@ -428,8 +494,7 @@ class DecodeGraph:
     def _body(self):
         ex, kv = self.ex, self.kv
         x = self.hidden if self.hidden is not None else ex.embed(self.tokens)
-        for k in range(self.first, self.last):
-            x = ex.decode_block(k, x, kv)
+        x = ex.decode_blocks(self.first, self.last, x, kv)
         kv.pos_dev.add_(1)
         if self.with_head:
             return ex.head(x, (x.shape[0], 1))

@@ -947,7 +947,9 @@ static int launch_pair(const CUtensorMap& ma, const void* B, int N, int K, int l
   return bz_check_launch("bz_gemm_bf16 (pair)");
 }
 
-// BZ_GEMM_OCC=1|2 pins the skinny kernel's CTAs per SM; unset/0: two for M <= 64
+// BZ_GEMM_OCC=2 runs skinny (M <= 128) GEMMs two CTAs per SM (BN <= 128, half the smem
+// ring); default one: at decode batch 1..64 the pair measured 5-10 % slower per 7B block
+// (profiles/r2_gemm_occ2.txt)
 static int occ_override() {
   static int v = -1;
   if (v < 0) {
@@ -1146,7 +1148,7 @@ static int gemm_impl(const void* A, const void* B, void* C, const void* residual
     }
   }
   SkinnyPlan plan{forced ? forced : (single_bn ? single_bn : pick_bn(M, N, ctas)), 0};
-  const bool occ2 = M <= BM && (occ_override() == 2 || (occ_override() == 0 && M <= 64)) && forced <= 128;
+  const bool occ2 = M <= BM && occ_override() == 2 && forced <= 128;
   if (M <= BM) {
     plan = plan_skinny(M, N, K, ctas, ws_bytes, forced, occ2 ? 128 : 256);
   }

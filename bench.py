@@ -260,7 +260,7 @@ def dist_max(values: list[float], world: int) -> list[float]:
         return values
     import torch
     import torch.distributed as dist
-    t = torch.tensor(values, dtype=torch.float64, device="cuda")
+    t = torch.tensor(values, dtype=torch.float64, device="cuda" if dist.get_backend() == "nccl" else "cpu")
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return t.cpu().tolist()
 
@@ -270,7 +270,7 @@ def dist_sum(value: float, world: int) -> float:
         return value
     import torch
     import torch.distributed as dist
-    t = torch.tensor([value], dtype=torch.float64, device="cuda")
+    t = torch.tensor([value], dtype=torch.float64, device="cuda" if dist.get_backend() == "nccl" else "cpu")
     dist.all_reduce(t)
     return float(t.item())
 

@@ -98,14 +98,22 @@ class Fabric:
         rank = int(os.environ.get("RANK", "0"))
         world = int(os.environ.get("WORLD_SIZE", "1"))
         local = int(os.environ.get("LOCAL_RANK", str(rank)))
-        torch.cuda.set_device(local)
+        # BZ_OVERSUBSCRIBE=<gpus>: more ranks than GPUs (rank r on GPU r % gpus) to check the
+        # control flow of a large world on a small box -- gloo only (NCCL refuses two ranks
+        # on one GPU); a functional mode, its bandwidths mean nothing
+        over = int(os.environ.get("BZ_OVERSUBSCRIBE", "0"))
+        device = local % over if over > 0 else local
+        torch.cuda.set_device(device)
         group = None
         if world > 1:
             import torch.distributed as dist
             if not dist.is_initialized():
-                dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+                if over > 0:
+                    dist.init_process_group("gloo")
+                else:
+                    dist.init_process_group("nccl", device_id=torch.device("cuda", device))
             group = dist.new_group(backend="gloo")
-        return cls(local, rank, world, group)
+        return cls(device, rank, world, group)
 
     def allgather(self, obj):
         if self.world == 1:

@@ -271,8 +271,9 @@ int bz_decode_attention_rows(const void* q, int ldq, const void* k_cache, const 
  * A whole decode step over n_blocks blocks in ONE persistent cooperative kernel
  * (1..4 sequences): per block rmsnorm -> qkv -> RoPE + KV append -> attention ->
  * o-proj + residual -> rmsnorm -> gate/up + SiLU -> down + residual, with each CTA
- * streaming its slice of every weight through shared memory and grid barriers
- * between phases.  Same math and bf16 rounding points as bz_rmsnorm / bz_gemm_bf16 /
+ * streaming its slice of every weight through shared memory (3-D TMA, 16-row units)
+ * into warp tensor-core MMAs, and grid barriers between phases; d and ffn multiples of
+ * 64; blocks beyond 48 run as further launches.  Same math and bf16 rounding points as bz_rmsnorm / bz_gemm_bf16 /
  * bz_rope_append(_rows) / bz_decode_attention(_rows) / bz_silu_mul.
  * x: [rows, ldx] bf16 hidden state, updated in place to the last block's output.
  * pos_stride 0: one device position for the batch (pos[0]); 1: one per row.

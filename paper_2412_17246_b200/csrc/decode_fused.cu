@@ -5,14 +5,17 @@
 // per MB), so the kernel is organised around keeping HBM busy:
 //
 //   * warp 8 of every CTA is a producer that streams THIS CTA's fixed slice of each
-//     weight matrix (contiguous rows) through a ring of 16 KiB shared-memory slots
-//     with cp.async.bulk (L2 evict-first), block after block, never waiting for
-//     activations -- weights do not depend on them, so the stream runs straight
-//     through every phase boundary and grid barrier;
-//   * warps 0..7 consume slots: one warp owns a unit (1..4 weight rows, or one row
-//     split over several slots) and forms the row . activation dot products on the
-//     CUDA cores (fp32 accumulation; 2.5 instructions per weight at batch 1, far
-//     under the issue rate), so no tensor-core tile is padded 128x for one row;
+//     weight matrix (16-row units) through a ring of 16 KiB shared-memory slots with
+//     3-D TMA tensor copies (16 rows x 512 k, 128B-swizzled, L2 evict-first), block
+//     after block, never waiting for activations -- weights do not depend on them, so
+//     the stream runs straight through every phase boundary and grid barrier;
+//   * warps 0..7 consume slots: one warp owns a 16-row unit and forms its rows . x
+//     products with warp-level tensor-core MMAs (mma.sync m16n8k16, weights as the
+//     16-row A operand via ldmatrix, the 1..4 sequences as the n=8 B operand, fp32
+//     accumulators): 8 instructions per 256 weights.  A CUDA-core dot product (FFMA2)
+//     needed ~30 and left the warps latency-bound below the HBM rate.  (tcgen05 would
+//     need a 128-row tile and TMEM for a 1..4-column product; at this arithmetic
+//     intensity the legacy warp MMA is not the bound.)
 //   * phases that need the whole previous result are separated by a grid barrier
 //     (5 per block); the per-CTA inputs (rmsnorm of the residual, the attention
 //     combine) are recomputed redundantly by every CTA into shared memory, which
@@ -49,11 +52,12 @@ constexpr int THREADS = CT + 32;          // + one producer warp
 constexpr int SLOT = 16384;               // bytes per ring slot
 constexpr int MAX_SLOTS = 16;
 constexpr int MAX_ROWS = 4;               // sequences per step
-constexpr int RMAX = 4;                   // weight rows per unit
+constexpr int UROWS = 16;                 // weight rows per unit (one m16 MMA tile)
+constexpr int SLOT_K = 512;               // k per slot: 8 x 64-element swizzle rows
 constexpr int GMAX = 8;                   // query heads per kv head
 constexpr int CHUNK_MAX = 512;            // context tokens per attention item
 constexpr int NSPLIT_CAP = 256;           // context chunks per (sequence, head)
-constexpr int MAX_BLOCKS = 96;
+constexpr int MAX_BLOCKS = 48;           // per launch (tensor maps live in the 32 KB parameter space)
 constexpr int SMEM_MAX = 232448;
 constexpr uint64_t SPIN_NS = 4000000000ull;  // grid-barrier timeout (a missing CTA = a bug)
 
@@ -62,7 +66,12 @@ struct Block {
   __nv_bfloat16 *kc, *vc;
 };
 
+// tensor maps per block: wqkv, wo, wgu (gate rows then up rows), wdown -- each viewed as
+// 3-D {64 k, rows, k / 64} so one copy brings 16 rows x 512 k as 8 swizzled 2 KiB tiles
+enum { TM_QKV, TM_O, TM_GU, TM_DOWN, TM_N };
+
 struct Params {
+  CUtensorMap tm[MAX_BLOCKS][TM_N];
   Block blk[MAX_BLOCKS];
   int n_blocks, d, H, KV, ffn, nqkv, ldx;
   float log2_theta, eps, scale;
@@ -77,6 +86,7 @@ struct Params {
   float* part;             // [rows * H, NSPLIT_CAP, hd]  unnormalised o of each context chunk
   float* pml;              // [rows * H, NSPLIT_CAP, 2]   its (max, sum)
   int nslot;
+  int nomath;              // diagnostics (BZ_FUSED_NOMATH=1): consume slots without the dot products
   int region_bytes;        // activation / attention scratch region
   uint64_t* trace;         // optional: %globaltimer per CTA per event (bz_decode_fused_set_trace)
 };
@@ -115,15 +125,25 @@ __device__ __forceinline__ void unpack8(const uint4& v, float (&f)[8]) {
   f[0] = bf_lo(v.x), f[1] = bf_hi(v.x), f[2] = bf_lo(v.y), f[3] = bf_hi(v.y);
   f[4] = bf_lo(v.z), f[5] = bf_hi(v.z), f[6] = bf_lo(v.w), f[7] = bf_hi(v.w);
 }
-__device__ __forceinline__ float dot8(const uint4& w, const float (&a)[8]) {
-  float s = bf_lo(w.x) * a[0];
-  s = fmaf(bf_hi(w.x), a[1], s);
-  s = fmaf(bf_lo(w.y), a[2], s);
-  s = fmaf(bf_hi(w.y), a[3], s);
-  s = fmaf(bf_lo(w.z), a[4], s);
-  s = fmaf(bf_hi(w.z), a[5], s);
-  s = fmaf(bf_lo(w.w), a[6], s);
-  return fmaf(bf_hi(w.w), a[7], s);
+__device__ __forceinline__ void tma_load_3d(void* smem, const CUtensorMap* map, int c0, int c1, int c2, uint64_t* bar,
+                                            uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, {%2, %3, "
+      "%4}], [%5], %6;" ::"r"(smem_u32(smem)),
+      "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar)), "l"(pol)
+      : "memory");
+}
+__device__ __forceinline__ void ldmatrix_x4(uint32_t addr, uint32_t (&a)[4]) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0, %1, %2, %3}, [%4];"
+               : "=r"(a[0]), "=r"(a[1]), "=r"(a[2]), "=r"(a[3])
+               : "r"(addr));
+}
+__device__ __forceinline__ void mma_bf16(float (&c)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0, %1, %2, %3}, {%4, %5, %6, %7}, {%8, %9}, "
+      "{%0, %1, %2, %3};"
+      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
 }
 
 // Grid barrier over the co-resident grid (cooperative launch): bar[0] counts arrivals
@@ -155,44 +175,32 @@ __device__ void grid_sync(const Params& p, unsigned& epoch) {
 }
 
 // ---- weight phases ----------------------------------------------------------------------
-// 0: qkv (n = nqkv, k = d)   1: o-proj (d, d)   2: gate|up (ffn, d; two row groups)
-// 3: down (d, ffn).  A unit is r whole rows (r * k * 2 <= SLOT) or one row split
-// over cpg slots; CTA c owns units [u0, u1) -- a contiguous byte range per group.
+// 0: qkv (n = nqkv, k = d)   1: o-proj (d, d)   2: gate|up (ffn, d; two row groups: gate
+// rows r and up rows ffn + r of one unit land in consecutive slots)   3: down (d, ffn).
+// A unit is 16 rows x all of k (ks slots of 512 k); CTA c owns units [u0, u1).
 struct WPhase {
-  const __nv_bfloat16* w0;
-  const __nv_bfloat16* w1;
-  int n, k, r, cpg, groups, u0, u1;
+  int map, n, k, ks, groups, up, u0, u1;
 };
 
-__device__ __forceinline__ WPhase wphase(const Params& p, const Block& b, int ph) {
+__device__ __forceinline__ WPhase wphase(const Params& p, int ph) {
   WPhase w;
-  w.w1 = nullptr;
+  w.map = ph;
   w.groups = 1;
+  w.up = 0;
   if (ph == 0) {
-    w.w0 = b.wqkv, w.n = p.nqkv, w.k = p.d;
+    w.n = p.nqkv, w.k = p.d;
   } else if (ph == 1) {
-    w.w0 = b.wo, w.n = p.d, w.k = p.d;
+    w.n = p.d, w.k = p.d;
   } else if (ph == 2) {
-    w.w0 = b.wgu, w.w1 = b.wgu + static_cast<int64_t>(p.ffn) * p.d, w.n = p.ffn, w.k = p.d, w.groups = 2;
+    w.n = p.ffn, w.k = p.d, w.groups = 2, w.up = p.ffn;
   } else {
-    w.w0 = b.wdown, w.n = p.d, w.k = p.ffn;
+    w.n = p.d, w.k = p.ffn;
   }
-  const int rb = w.k * 2;
-  w.r = rb >= SLOT ? 1 : min(RMAX, SLOT / rb);
-  w.cpg = w.r == 1 ? (rb + SLOT - 1) / SLOT : 1;
-  const int units = (w.n + w.r - 1) / w.r;
+  w.ks = (w.k + SLOT_K - 1) / SLOT_K;
+  const int units = (w.n + UROWS - 1) / UROWS;
   w.u0 = static_cast<int>(static_cast<int64_t>(units) * blockIdx.x / gridDim.x);
   w.u1 = static_cast<int>(static_cast<int64_t>(units) * (blockIdx.x + 1) / gridDim.x);
   return w;
-}
-
-__device__ __forceinline__ uint32_t chunk_bytes(const WPhase& w, int u, int j) {
-  if (w.cpg == 1) return static_cast<uint32_t>(min(w.r, w.n - u * w.r)) * w.k * 2;
-  return static_cast<uint32_t>(min(SLOT, w.k * 2 - j * SLOT));
-}
-__device__ __forceinline__ const char* chunk_src(const WPhase& w, int u, int g, int j) {
-  return reinterpret_cast<const char*>(g ? w.w1 : w.w0) + static_cast<int64_t>(u) * w.r * w.k * 2 +
-         static_cast<int64_t>(j) * SLOT;
 }
 
 __device__ __forceinline__ void trace_ev(const Params& p, int l, int ev) {
@@ -207,19 +215,24 @@ struct Ring {
   int nslot;
 };
 
-// Walks this CTA's weight chunks in stream order (blocks -> phases -> units -> groups -> slots).
+// Walks this CTA's weight slots in stream order: blocks -> phases -> waves of up to CW
+// units (one per consumer warp) -> row groups -> k slots -> the wave's units, so the CW
+// warps of a wave consume their units' slots side by side.
 struct ChunkIter {
   WPhase w;
-  int l, ph, u, g, j;
+  int l, ph, w0, nw, g, j, i;
   bool done;
   __device__ void init(const Params& p) {
-    l = 0, ph = 0, g = 0, j = 0, done = false;
-    w = wphase(p, p.blk[0], 0);
-    u = w.u0;
+    l = 0, ph = 0, done = false;
+    w = wphase(p, 0);
+    start_wave(w.u0);
     settle(p);
   }
+  __device__ void start_wave(int u) {
+    w0 = u, nw = min(CW, w.u1 - u), g = 0, j = 0, i = 0;
+  }
   __device__ void settle(const Params& p) {
-    while (!done && u >= w.u1) {
+    while (!done && w0 >= w.u1) {
       if (++ph == 4) {
         ph = 0;
         if (++l == p.n_blocks) {
@@ -227,20 +240,20 @@ struct ChunkIter {
           return;
         }
       }
-      w = wphase(p, p.blk[l], ph);
-      u = w.u0, g = 0, j = 0;
+      w = wphase(p, ph);
+      start_wave(w.u0);
     }
   }
   __device__ void advance(const Params& p) {
-    if (++j < w.cpg) return;
+    if (++i < nw) return;
+    i = 0;
+    if (++j < w.ks) return;
     j = 0;
     if (++g < w.groups) return;
-    g = 0;
-    ++u;
+    start_wave(w0 + nw);
     settle(p);
   }
-  __device__ const char* src() const { return chunk_src(w, u, g, j); }
-  __device__ uint32_t bytes() const { return chunk_bytes(w, u, j); }
+  __device__ int unit() const { return w0 + i; }
 };
 
 // Context split of this step's attention (same on every CTA and role: pos is read-only
@@ -259,7 +272,7 @@ __device__ __forceinline__ void attn_split(const Params& p, int rows, int& nspli
 template <int HD>
 __device__ void prefetch_kv(const Params& p, const Block& blk, int rows, int nsplit, int chunk);
 
-// Producer: lane 0 of warp CW streams every weight chunk of this CTA in the fixed order,
+// Producer: lane 0 of warp CW streams every weight slot of this CTA in the fixed order,
 // and on entering a block's weights pulls that block's attention K/V chunks into L2.
 // (Prefetching further ahead into L2 while the ring is full measured slower at every
 // depth: the extra L2 requests slow the streaming phases more than they save.)
@@ -277,9 +290,9 @@ __device__ void produce(const Params& p, const Ring& ring) {
     const int s = static_cast<int>(q % ring.nslot);
     const uint32_t lap = q / ring.nslot;
     if (lap) mbar_wait(&ring.empty[s], (lap - 1) & 1);
-    const uint32_t bytes = ld.bytes();
-    mbar_expect_tx(&ring.full[s], bytes);
-    bulk_load(ring.slots + static_cast<size_t>(s) * SLOT, ld.src(), bytes, &ring.full[s], pol);
+    mbar_expect_tx(&ring.full[s], SLOT);  // out-of-range k / rows arrive as zeros, full box
+    tma_load_3d(ring.slots + static_cast<size_t>(s) * SLOT, &p.tm[ld.l][ld.w.map], 0,
+                ld.unit() * UROWS + ld.g * ld.w.up, ld.j * (SLOT_K / 64), &ring.full[s], pol);
     *ring.issued = ++q;
     const int l = ld.l, ph = ld.ph;
     ld.advance(p);
@@ -288,96 +301,94 @@ __device__ void produce(const Params& p, const Ring& ring) {
   }
 }
 
-// Consumer side of one weight phase: warp `warp` takes every CW-th unit of this CTA's
-// range; `act` is the phase input [NB][act_ld] bf16 in shared memory.
+// One slot (16 rows x 512 k, 8 swizzled 2 KiB tiles) into the unit's accumulators:
+// per 16 k an ldmatrix.x4 of the weights (A), the sequences' x as B (thread (g, t) holds
+// x[g][k + 2t .. +1] and x[g][k + 2t + 8 .. +9]; columns g >= NB are zero), one MMA.
+// Two accumulator sets alternate for two independent chains.
+template <int NB>
+__device__ __forceinline__ void slot_mma(uint32_t slot, const __nv_bfloat16* act, int act_ld, int k_base, int k,
+                                         int lane, float (&c0)[4], float (&c1)[4]) {
+  const int r = lane & 15, hi = lane >> 4, gq = lane >> 2, t2 = (lane & 3) * 2;
+  const bool bcol = gq < NB;
+  const __nv_bfloat16* xrow = act + (bcol ? gq : 0) * act_ld + t2;
+  const uint32_t rowoff = slot + r * 128;
+#pragma unroll
+  for (int kh = 0; kh < SLOT_K / 64; ++kh) {
+    const int k64 = k_base + kh * 64;
+    if (k64 >= k) break;
+#pragma unroll
+    for (int ks = 0; ks < 4; ++ks) {
+      uint32_t a[4];
+      ldmatrix_x4(rowoff + kh * 2048 + (((ks * 2 + hi) ^ (r & 7)) << 4), a);
+      const int kk = k64 + ks * 16;
+      const uint32_t b0 = bcol ? *reinterpret_cast<const uint32_t*>(xrow + kk) : 0u;
+      const uint32_t b1 = bcol ? *reinterpret_cast<const uint32_t*>(xrow + kk + 8) : 0u;
+      if (ks & 1)
+        mma_bf16(c1, a, b0, b1);
+      else
+        mma_bf16(c0, a, b0, b1);
+    }
+  }
+}
+
+// All slots of row group g of the unit this warp owns in a wave (slot q0 + (g * ks + j) *
+// nw + i for k slot j).  c = the sum of the two MMA chains: thread (g, t) holds rows
+// g, g + 8 x sequences 2t, 2t + 1.
+template <int NB>
+__device__ __forceinline__ void unit_group(const Params& p, const WPhase& w, uint32_t q0, int nw, int i, int g,
+                                           const Ring& ring, const __nv_bfloat16* act, int act_ld, int lane,
+                                           float (&c)[4]) {
+  float c1[4] = {0.f, 0.f, 0.f, 0.f};
+  c[0] = c[1] = c[2] = c[3] = 0.f;
+  for (int j = 0; j < w.ks; ++j) {
+    const uint32_t q = q0 + static_cast<uint32_t>((g * w.ks + j) * nw + i);
+    const int s = static_cast<int>(q % ring.nslot);
+    while (*ring.issued <= q) {
+    }
+    mbar_wait(&ring.full[s], (q / ring.nslot) & 1);
+    if (!p.nomath)
+      slot_mma<NB>(smem_u32(ring.slots + static_cast<size_t>(s) * SLOT), act, act_ld, j * SLOT_K, w.k, lane, c, c1);
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&ring.empty[s]);
+  }
+#pragma unroll
+  for (int k = 0; k < 4; ++k) c[k] += c1[k];
+}
+
+// Consumer side of one weight phase: in each wave of up to CW units, warp i owns unit
+// w0 + i; `act` is the phase input [NB][act_ld] bf16 in shared memory.  Each thread
+// writes its own (row, sequence) outputs -- no cross-lane reduction.
 template <int NB>
 __device__ void consume(const Params& p, const WPhase& w, int ph, uint32_t& q, const Ring& ring,
                         const __nv_bfloat16* act, int act_ld) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int cpu = w.groups * w.cpg;
-  const int k8 = w.k / 8;
-  for (int u = w.u0; u < w.u1; ++u) {
-    if ((u - w.u0) % CW != warp) {
-      q += cpu;
-      continue;
-    }
-    const int row0 = u * w.r;
-    const int rows = min(w.r, w.n - row0);
-    float acc[2][RMAX][NB];
+  const int gq = lane >> 2, t2 = (lane & 3) * 2;
+  for (int w0 = w.u0; w0 < w.u1; w0 += CW) {
+    const int nw = min(CW, w.u1 - w0);
+    const uint32_t q0 = q;
+    q += static_cast<uint32_t>(w.groups * w.ks * nw);
+    if (warp >= nw) continue;
+    const int u = w0 + warp;
+    float cg[4], cu[4];
+    unit_group<NB>(p, w, q0, nw, warp, 0, ring, act, act_ld, lane, cg);
+    if (w.groups == 2) unit_group<NB>(p, w, q0, nw, warp, 1, ring, act, act_ld, lane, cu);
 #pragma unroll
-    for (int g = 0; g < 2; ++g)
-#pragma unroll
-      for (int r = 0; r < RMAX; ++r)
-#pragma unroll
-        for (int b = 0; b < NB; ++b) acc[g][r][b] = 0.f;
-#pragma unroll
-    for (int g = 0; g < 2; ++g) {
-      if (g >= w.groups) break;
-      for (int j = 0; j < w.cpg; ++j, ++q) {
-        const int s = static_cast<int>(q % ring.nslot);
-        while (*ring.issued <= q) {
-        }
-        mbar_wait(&ring.full[s], (q / ring.nslot) & 1);
-        const uint4* ws = reinterpret_cast<const uint4*>(ring.slots + static_cast<size_t>(s) * SLOT);
-        if (w.cpg == 1) {
-          for (int c = lane; c < k8; c += 32) {
-            float a[NB][8];
-#pragma unroll
-            for (int b = 0; b < NB; ++b)
-              unpack8(*reinterpret_cast<const uint4*>(act + b * act_ld + c * 8), a[b]);
-#pragma unroll
-            for (int r = 0; r < RMAX; ++r) {
-              if (r >= rows) break;
-              const uint4 wv = ws[r * k8 + c];
-#pragma unroll
-              for (int b = 0; b < NB; ++b) acc[g][r][b] += dot8(wv, a[b]);
-            }
-          }
-        } else {
-          const int base = j * (SLOT / 16);
-          const int n16 = min(SLOT, w.k * 2 - j * SLOT) / 16;
-          for (int c = lane; c < n16; c += 32) {
-            const uint4 wv = ws[c];
-#pragma unroll
-            for (int b = 0; b < NB; ++b) {
-              float a[8];
-              unpack8(*reinterpret_cast<const uint4*>(act + b * act_ld + (base + c) * 8), a);
-              acc[g][0][b] += dot8(wv, a);
-            }
-          }
-        }
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&ring.empty[s]);
-      }
-    }
-    // every lane ends with the full sums
-#pragma unroll
-    for (int g = 0; g < 2; ++g)
-#pragma unroll
-      for (int r = 0; r < RMAX; ++r)
-#pragma unroll
-        for (int b = 0; b < NB; ++b)
-#pragma unroll
-          for (int o = 16; o; o >>= 1) acc[g][r][b] += __shfl_xor_sync(0xffffffffu, acc[g][r][b], o);
-#pragma unroll
-    for (int r = 0; r < RMAX; ++r) {
-      if (r >= rows) break;
-      const int row = row0 + r;
-#pragma unroll
-      for (int b = 0; b < NB; ++b) {
-        if (lane != r * NB + b) continue;
-        if (ph == 0) {
-          p.qkv[static_cast<int64_t>(b) * p.nqkv + row] = __float2bfloat16_rn(acc[0][r][b]);
-        } else if (ph == 1) {
-          const float res = __bfloat162float(p.x[static_cast<int64_t>(b) * p.ldx + row]);
-          p.o[static_cast<int64_t>(b) * p.d + row] = __float2bfloat16_rn(acc[0][r][b] + res);
-        } else if (ph == 2) {
-          const float gt = bf16r(acc[0][r][b]), up = bf16r(acc[1][r][b]);
-          p.act[static_cast<int64_t>(b) * p.ffn + row] = __float2bfloat16_rn(gt / (1.f + __expf(-gt)) * up);
-        } else {
-          const float res = __bfloat162float(p.o[static_cast<int64_t>(b) * p.d + row]);
-          p.x[static_cast<int64_t>(b) * p.ldx + row] = __float2bfloat16_rn(acc[0][r][b] + res);
-        }
+    for (int k = 0; k < 4; ++k) {
+      const int row = u * UROWS + gq + (k >> 1) * 8;
+      const int b = t2 + (k & 1);
+      if (b >= NB || row >= w.n) continue;
+      const float v0 = cg[k];
+      if (ph == 0) {
+        p.qkv[static_cast<int64_t>(b) * p.nqkv + row] = __float2bfloat16_rn(v0);
+      } else if (ph == 1) {
+        const float res = __bfloat162float(p.x[static_cast<int64_t>(b) * p.ldx + row]);
+        p.o[static_cast<int64_t>(b) * p.d + row] = __float2bfloat16_rn(v0 + res);
+      } else if (ph == 2) {
+        const float gt = bf16r(v0), up = bf16r(cu[k]);
+        p.act[static_cast<int64_t>(b) * p.ffn + row] = __float2bfloat16_rn(gt / (1.f + __expf(-gt)) * up);
+      } else {
+        const float res = __bfloat162float(p.o[static_cast<int64_t>(b) * p.d + row]);
+        p.x[static_cast<int64_t>(b) * p.ldx + row] = __float2bfloat16_rn(v0 + res);
       }
     }
   }
@@ -768,7 +779,9 @@ __host__ __device__ constexpr int attn_scratch_bytes(int G, int HD) {
 // ---- the kernel ---------------------------------------------------------------------------
 template <int NB, int HD>
 __global__ void __launch_bounds__(THREADS, 1) k_decode_fused(const __grid_constant__ Params p) {
-  extern __shared__ __align__(128) uint8_t smem[];
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  // 128B-swizzled TMA tiles need 1024-byte aligned slots
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   Ring ring;
   ring.nslot = p.nslot;
   ring.slots = smem;
@@ -808,7 +821,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_decode_fused(const __grid_consta
     if (tr) trace_ev(p, l, EV_START);
     stage_norm<NB>(p, p.x, p.ldx, blk.attn_norm, act, red);
     if (tr) trace_ev(p, l, EV_NORM1);
-    consume<NB>(p, wphase(p, blk, 0), 0, q, ring, act, p.d);
+    consume<NB>(p, wphase(p, 0), 0, q, ring, act, p.d);
     if (tr) trace_ev(p, l, EV_QKV);
     grid_sync(p, epoch);
     if (tr) trace_ev(p, l, EV_BAR1);
@@ -818,13 +831,13 @@ __global__ void __launch_bounds__(THREADS, 1) k_decode_fused(const __grid_consta
     if (tr) trace_ev(p, l, EV_BAR2);
     stage_combine<NB, HD>(p, nsplit, act, wgt);
     if (tr) trace_ev(p, l, EV_COMB);
-    consume<NB>(p, wphase(p, blk, 1), 1, q, ring, act, p.d);
+    consume<NB>(p, wphase(p, 1), 1, q, ring, act, p.d);
     if (tr) trace_ev(p, l, EV_O);
     grid_sync(p, epoch);
     if (tr) trace_ev(p, l, EV_BAR3);
     stage_norm<NB>(p, p.o, p.d, blk.ffn_norm, act, red);
     if (tr) trace_ev(p, l, EV_NORM2);
-    consume<NB>(p, wphase(p, blk, 2), 2, q, ring, act, p.d);
+    consume<NB>(p, wphase(p, 2), 2, q, ring, act, p.d);
     if (tr) trace_ev(p, l, EV_GU);
     grid_sync(p, epoch);
     if (tr) trace_ev(p, l, EV_BAR4);
@@ -836,7 +849,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_decode_fused(const __grid_consta
       named_sync();
     }
     if (tr) trace_ev(p, l, EV_ACT);
-    consume<NB>(p, wphase(p, blk, 3), 3, q, ring, act, p.ffn);
+    consume<NB>(p, wphase(p, 3), 3, q, ring, act, p.ffn);
     if (tr) trace_ev(p, l, EV_DOWN);
   }
 }
@@ -897,6 +910,22 @@ extern "C" int bz_decode_fused_workspace_bytes(int rows, int d, int n_heads, int
   return BZ_OK;
 }
 
+// 3-D view {64 k, rows, k / 64} of a [rows, k] bf16 weight: one box {64, 16, 8} is 16 rows
+// x 512 k, stored as 8 consecutive 128B-swizzled [16 x 64] tiles.
+static int encode_w3d(CUtensorMap* map, const void* w, int rows, int k) {
+  const DriverApi* d = driver_api();
+  if (!d) return BZ_ECUDA;
+  cuuint64_t dims[3] = {64, static_cast<cuuint64_t>(rows), static_cast<cuuint64_t>(k / 64)};
+  cuuint64_t strides[2] = {static_cast<cuuint64_t>(k) * 2, 128};
+  cuuint32_t box[3] = {64, fused::UROWS, fused::SLOT_K / 64};
+  cuuint32_t elem[3] = {1, 1, 1};
+  CUresult r = d->cuTensorMapEncodeTiled(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(w), dims, strides,
+                                         box, elem, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                         CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return bz_fail_cu(r, "decode_fused: cuTensorMapEncodeTiled");
+  return BZ_OK;
+}
+
 extern "C" int bz_decode_fused(const bz_decode_block* blocks, int n_blocks, void* x, int ldx, int rows, int d,
                                int n_heads, int n_kv, int head_dim, int ffn, float rope_theta, float eps,
                                int64_t s_max, const int32_t* pos, int pos_stride, void* workspace, int64_t ws_bytes,
@@ -905,33 +934,18 @@ extern "C" int bz_decode_fused(const bz_decode_block* blocks, int n_blocks, void
   if (!blocks || n_blocks <= 0 || !x || !pos || !workspace || rows <= 0 || d <= 0 || ffn <= 0)
     return bz_fail(BZ_EINVAL, "decode_fused: bad args");
   if (rows > MAX_ROWS) return bz_fail(BZ_EINVAL, "decode_fused: at most 4 sequences per step");
-  if (n_blocks > MAX_BLOCKS) return bz_fail(BZ_EINVAL, "decode_fused: at most 96 blocks per launch");
   if (head_dim != 64 && head_dim != 128) return bz_fail(BZ_EINVAL, "decode_fused: head_dim must be 64 or 128");
   if (n_kv <= 0 || n_heads % n_kv || n_heads / n_kv > GMAX)
     return bz_fail(BZ_EINVAL, "decode_fused: heads per kv head must divide and be <= 8");
-  if (d % 8 || ffn % 8 || ldx % 8 || d != n_heads * head_dim)
-    return bz_fail(BZ_EINVAL, "decode_fused: d, ffn, ldx multiples of 8 and d == n_heads * head_dim");
+  if (d % 64 || ffn % 64 || ldx % 8 || d != n_heads * head_dim)
+    return bz_fail(BZ_EINVAL, "decode_fused: d and ffn multiples of 64, ldx of 8, d == n_heads * head_dim");
   if (s_max <= 0 || s_max > static_cast<int64_t>(NSPLIT_CAP) * CHUNK_MAX)
     return bz_fail(BZ_EINVAL, "decode_fused: s_max must be in [1, 131072]");
   if ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(workspace)) & 15)
     return bz_fail(BZ_EINVAL, "decode_fused: x and workspace must be 16-byte aligned");
   const WsLayout wl = ws_layout(rows, d, n_heads, n_kv, head_dim, ffn);
   if (ws_bytes < wl.total) return bz_fail(BZ_EINVAL, "decode_fused: workspace too small");
-  Params p;
-  for (int l = 0; l < n_blocks; ++l) {
-    const bz_decode_block& b = blocks[l];
-    if (!b.attn_norm || !b.wqkv || !b.wo || !b.ffn_norm || !b.wgu || !b.wdown || !b.k_cache || !b.v_cache)
-      return bz_fail(BZ_EINVAL, "decode_fused: null block pointer");
-    const uintptr_t align = reinterpret_cast<uintptr_t>(b.attn_norm) | reinterpret_cast<uintptr_t>(b.wqkv) |
-                            reinterpret_cast<uintptr_t>(b.wo) | reinterpret_cast<uintptr_t>(b.ffn_norm) |
-                            reinterpret_cast<uintptr_t>(b.wgu) | reinterpret_cast<uintptr_t>(b.wdown);
-    if (align & 15) return bz_fail(BZ_EINVAL, "decode_fused: weights must be 16-byte aligned");
-    p.blk[l] = {static_cast<const __nv_bfloat16*>(b.attn_norm), static_cast<const __nv_bfloat16*>(b.wqkv),
-                static_cast<const __nv_bfloat16*>(b.wo),        static_cast<const __nv_bfloat16*>(b.ffn_norm),
-                static_cast<const __nv_bfloat16*>(b.wgu),       static_cast<const __nv_bfloat16*>(b.wdown),
-                static_cast<__nv_bfloat16*>(b.k_cache),         static_cast<__nv_bfloat16*>(b.v_cache)};
-  }
-  p.n_blocks = n_blocks;
+  static thread_local Params p;  // ~28 KB: not on the stack
   p.d = d;
   p.H = n_heads;
   p.KV = n_kv;
@@ -956,34 +970,60 @@ extern "C" int bz_decode_fused(const bz_decode_block* blocks, int n_blocks, void
   const int kmax = d > ffn ? d : ffn;
   const int scratch = attn_scratch_bytes(n_heads / n_kv, head_dim);
   const int region = (rows * kmax * 2 > scratch ? rows * kmax * 2 : scratch + 15) / 16 * 16;
-  const int fixed = 2 * MAX_SLOTS * 8 + 16 + (MAX_ROWS * CW + CW * NSPLIT_CAP) * 4 + region + 128;
+  const int fixed = 2 * MAX_SLOTS * 8 + 16 + (MAX_ROWS * CW + CW * NSPLIT_CAP) * 4 + region + 1024;
   int nslot = (SMEM_MAX - fixed) / SLOT;
   if (nslot > MAX_SLOTS) nslot = MAX_SLOTS;
   if (nslot < 4) return bz_fail(BZ_EINVAL, "decode_fused: activations leave too little shared memory for the ring");
   p.nslot = nslot;
   p.region_bytes = region;
   p.trace = nullptr;
+  {
+    const char* e = getenv("BZ_FUSED_NOMATH");
+    p.nomath = e && atoi(e) == 1;
+  }
   const int smem = nslot * SLOT + fixed;
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int grid = max_ctas > 0 && max_ctas < sms ? max_ctas : sms;
-  if (g_trace && g_trace_bytes >= static_cast<int64_t>(grid) * n_blocks * EV_N * 8) p.trace = g_trace;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  // the barrier words: arrivals must start at 0; the error flag reports this launch
-  cudaError_t e = cudaMemsetAsync(ws, 0, 16, s);
-  if (e != cudaSuccess) return bz_fail_cuda(e, "decode_fused: barrier reset");
-  switch (rows * 1000 + head_dim) {
-    case 1128: e = launch<1, 128>(p, grid, smem, s); break;
-    case 2128: e = launch<2, 128>(p, grid, smem, s); break;
-    case 3128: e = launch<3, 128>(p, grid, smem, s); break;
-    case 4128: e = launch<4, 128>(p, grid, smem, s); break;
-    case 1064: e = launch<1, 64>(p, grid, smem, s); break;
-    case 2064: e = launch<2, 64>(p, grid, smem, s); break;
-    case 3064: e = launch<3, 64>(p, grid, smem, s); break;
-    default: e = launch<4, 64>(p, grid, smem, s); break;
+  // blocks in launches of up to MAX_BLOCKS (the tensor maps travel in the parameters)
+  for (int first = 0; first < n_blocks; first += MAX_BLOCKS) {
+    const int nb = n_blocks - first < MAX_BLOCKS ? n_blocks - first : MAX_BLOCKS;
+    for (int l = 0; l < nb; ++l) {
+      const bz_decode_block& b = blocks[first + l];
+      if (!b.attn_norm || !b.wqkv || !b.wo || !b.ffn_norm || !b.wgu || !b.wdown || !b.k_cache || !b.v_cache)
+        return bz_fail(BZ_EINVAL, "decode_fused: null block pointer");
+      const uintptr_t align = reinterpret_cast<uintptr_t>(b.attn_norm) | reinterpret_cast<uintptr_t>(b.wqkv) |
+                              reinterpret_cast<uintptr_t>(b.wo) | reinterpret_cast<uintptr_t>(b.ffn_norm) |
+                              reinterpret_cast<uintptr_t>(b.wgu) | reinterpret_cast<uintptr_t>(b.wdown);
+      if (align & 15) return bz_fail(BZ_EINVAL, "decode_fused: weights must be 16-byte aligned");
+      p.blk[l] = {static_cast<const __nv_bfloat16*>(b.attn_norm), static_cast<const __nv_bfloat16*>(b.wqkv),
+                  static_cast<const __nv_bfloat16*>(b.wo),        static_cast<const __nv_bfloat16*>(b.ffn_norm),
+                  static_cast<const __nv_bfloat16*>(b.wgu),       static_cast<const __nv_bfloat16*>(b.wdown),
+                  static_cast<__nv_bfloat16*>(b.k_cache),         static_cast<__nv_bfloat16*>(b.v_cache)};
+      if (int rc = encode_w3d(&p.tm[l][TM_QKV], b.wqkv, p.nqkv, d)) return rc;
+      if (int rc = encode_w3d(&p.tm[l][TM_O], b.wo, d, d)) return rc;
+      if (int rc = encode_w3d(&p.tm[l][TM_GU], b.wgu, 2 * ffn, d)) return rc;
+      if (int rc = encode_w3d(&p.tm[l][TM_DOWN], b.wdown, d, ffn)) return rc;
+    }
+    p.n_blocks = nb;
+    if (g_trace && g_trace_bytes >= static_cast<int64_t>(grid) * nb * EV_N * 8) p.trace = g_trace;
+    // the barrier words: arrivals must start at 0; the error flag reports this launch
+    cudaError_t e = cudaMemsetAsync(ws, 0, 16, s);
+    if (e != cudaSuccess) return bz_fail_cuda(e, "decode_fused: barrier reset");
+    switch (rows * 1000 + head_dim) {
+      case 1128: e = launch<1, 128>(p, grid, smem, s); break;
+      case 2128: e = launch<2, 128>(p, grid, smem, s); break;
+      case 3128: e = launch<3, 128>(p, grid, smem, s); break;
+      case 4128: e = launch<4, 128>(p, grid, smem, s); break;
+      case 1064: e = launch<1, 64>(p, grid, smem, s); break;
+      case 2064: e = launch<2, 64>(p, grid, smem, s); break;
+      case 3064: e = launch<3, 64>(p, grid, smem, s); break;
+      default: e = launch<4, 64>(p, grid, smem, s); break;
+    }
+    if (e != cudaSuccess) return bz_fail_cuda(e, "bz_decode_fused launch");
   }
-  if (e != cudaSuccess) return bz_fail_cuda(e, "bz_decode_fused launch");
   return bz_check_launch("bz_decode_fused");
 }
 

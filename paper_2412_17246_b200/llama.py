@@ -40,9 +40,9 @@ from .slab import LlamaArch, SlabLayout
 PREFILL_ATTENTION = os.environ.get("BZ_PREFILL_ATTN", "tcgen05")
 
 # small-batch decode: one persistent kernel per decode step (csrc/decode_fused.cu) for
-# 1..FUSED_MAX_ROWS sequences.  Opt-in (BZ_DECODE_FUSED=1): on B200 it measured level with
-# the per-block kernels at batch 1 (117.8 vs 116.2 us per 7B block) and slower at 2..4
-# rows (its CUDA-core dot products become the bottleneck), profiles/r2_fused_decode.txt
+# 1..FUSED_MAX_ROWS sequences.  Opt-in (BZ_DECODE_FUSED=1): on B200 it measured 103.6 vs
+# 106.0 us per 7B block at batch 1 and slower at 2..4 rows (its attention items and
+# per-row staging are latency-bound), profiles/r2_fused_decode.txt
 FUSED_DECODE = os.environ.get("BZ_DECODE_FUSED", "0") == "1"
 FUSED_MAX_ROWS = 4
 
@@ -261,8 +261,8 @@ class LlamaExecutor:
         a = self.arch
         return (FUSED_DECODE and 1 <= rows <= FUSED_MAX_ROWS and a.head_dim in (64, 128)
                 and a.n_heads % a.n_kv_heads == 0 and a.n_heads // a.n_kv_heads <= 8
-                and a.d_model == a.n_heads * a.head_dim and a.ffn % 8 == 0
-                and 0 < kv.max_seq <= 131072 and 0 < last - first <= 96)
+                and a.d_model == a.n_heads * a.head_dim and a.d_model % 64 == 0 and a.ffn % 64 == 0
+                and 0 < kv.max_seq <= 131072 and last > first)
 
     def decode_blocks(self, first: int, last: int, x: torch.Tensor, kv: "KVCache") -> torch.Tensor:
         """Blocks [first, last) of one decode step for x [B, d]: one bz_decode_fused launch

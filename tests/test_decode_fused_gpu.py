@@ -17,7 +17,9 @@ from oracle.forward_ref import forward_fp32, weights_to_cpu_fp32
 
 pytestmark = pytest.mark.gpu
 
-TINY_GQA = S.LlamaArch("tiny-gqa", d_model=256, n_layers=4, n_heads=4, n_kv_heads=2, ffn=688)
+# the fused kernel streams 64-wide k tiles: ffn a multiple of 64 (704 = 11 x 64)
+FT_MHA = S.LlamaArch("ft-mha", d_model=256, n_layers=4, n_heads=4, n_kv_heads=4, ffn=704)
+FT_GQA = S.LlamaArch("ft-gqa", d_model=256, n_layers=4, n_heads=4, n_kv_heads=2, ffn=704)
 GQA8 = S.LlamaArch("gqa8", d_model=1024, n_layers=2, n_heads=16, n_kv_heads=2, ffn=2816)
 W7B_2L = S.LlamaArch("w7b-2l", d_model=4096, n_layers=2, n_heads=32, n_kv_heads=32, ffn=11008)
 
@@ -49,20 +51,24 @@ def _prompt(b, s, seed, vocab):
 
 
 def _two_paths(monkeypatch, arch, B, S_prompt, steps, seed=3):
-    """Decode `steps` tokens with the fused kernel and with the per-block kernels from
-    the same prefill; returns both logit sequences, both caches and the executor."""
+    """Decode `steps` tokens with the fused kernel (greedy) and with the per-block kernels
+    fed the SAME tokens (a near-tie argmax flip must not fork the inputs); returns both
+    logit sequences, both caches and the executor."""
     slab, w = _setup(arch, seed)
     ex = LlamaExecutor(w, max_tokens=B * S_prompt, device="cuda")
     prompt = _prompt(B, S_prompt, seed + 1, arch.vocab)
     out = {}
+    fed = []
     for fused in (True, False):
         monkeypatch.setattr(LL, "FUSED_DECODE", fused)
         kv = KVCache(arch, B, S_prompt + steps + 2, "cuda")
         logits = ex.forward(prompt, kv=kv)
         tok = logits.argmax(-1)
         seq = []
-        for _ in range(steps):
-            logits = ex.decode(tok, kv)
+        for i in range(steps):
+            if fused:
+                fed.append(tok)
+            logits = ex.decode(fed[i], kv)
             seq.append(logits)
             tok = logits.argmax(-1)
         torch.cuda.synchronize()
@@ -73,7 +79,7 @@ def _two_paths(monkeypatch, arch, B, S_prompt, steps, seed=3):
     return out, ex, prompt, w, slab
 
 
-@pytest.mark.parametrize("arch,B", [(S.TINY_4L, 1), (S.TINY_4L, 3), (TINY_GQA, 2), (GQA8, 4)],
+@pytest.mark.parametrize("arch,B", [(FT_MHA, 1), (FT_MHA, 3), (FT_GQA, 2), (GQA8, 4)],
                          ids=["mha-b1", "mha-b3", "gqa-b2", "gqa8-b4"])
 def test_fused_decode_matches_per_block_kernels_and_oracle(monkeypatch, arch, B):
     out, ex, prompt, w, slab = _two_paths(monkeypatch, arch, B, 24, 5)
@@ -110,7 +116,7 @@ def test_fused_decode_7b_width(monkeypatch):
 def test_fused_decode_per_row_positions_and_small_grid(monkeypatch):
     """Continuous batching (one device position per row) and a grid of fewer CTAs than
     SMs: each row's step equals the per-block kernels' on the same cache."""
-    arch = TINY_GQA
+    arch = FT_GQA
     slab, w = _setup(arch, seed=11)
     ex = LlamaExecutor(w, max_tokens=64, device="cuda")
     lens = [19, 5, 11, 2]
@@ -157,7 +163,7 @@ def test_fused_decode_per_row_positions_and_small_grid(monkeypatch):
 def test_fused_decode_graph_replay_is_identical(monkeypatch):
     """A captured fused step (cooperative kernel inside a CUDA graph) replays bit-exactly."""
     monkeypatch.setattr(LL, "FUSED_DECODE", True)
-    arch = S.TINY_4L
+    arch = FT_MHA
     slab, w = _setup(arch, seed=5)
     ex = LlamaExecutor(w, max_tokens=2 * 16, device="cuda")
     prompt = _prompt(2, 16, 9, arch.vocab)
@@ -174,15 +180,30 @@ def test_fused_decode_graph_replay_is_identical(monkeypatch):
     slab.close()
 
 
-def test_fused_decode_rejects_unsupported_shapes():
-    """Five sequences (or a head_dim the kernel lacks) fall back to the per-block kernels."""
-    arch = S.TINY_4L
+def test_fused_decode_rejects_unsupported_shapes(monkeypatch):
+    """Five sequences (or an ffn that is not a multiple of 64) fall back to the per-block kernels."""
+    monkeypatch.setattr(LL, "FUSED_DECODE", True)
+    arch = FT_MHA
     slab, w = _setup(arch)
     ex = LlamaExecutor(w, max_tokens=8, device="cuda")
     kv5 = KVCache(arch, 5, 8, "cuda")
     assert not ex.fused_decode_ok(5, kv5, 0, arch.n_layers)
+    assert ex.fused_decode_ok(4, kv5, 0, arch.n_layers)
+    ex688 = LlamaExecutor(SlabWeights(S.TINY_4L, S.SlabLayout.for_arch(S.TINY_4L), torch.zeros(
+        S.SlabLayout.for_arch(S.TINY_4L).data_bytes, dtype=torch.uint8, device="cuda")), max_tokens=8, device="cuda")
+    assert not ex688.fused_decode_ok(1, KVCache(S.TINY_4L, 1, 8, "cuda"), 0, 4)
     from paper_2412_17246_b200._native import BlitzError, BzDecodeBlock
     with pytest.raises(BlitzError):
         ex.lib.bz_decode_fused((BzDecodeBlock * 1)(), 1, None, 0, 5, 256, 4, 4, 64, 688, 1e4, 1e-5, 8, None, 0,
                                None, 0, 0, None)
+    slab.close()
+
+
+def test_fused_decode_more_blocks_than_one_launch(monkeypatch):
+    """50 blocks: the host runs them as launches of 48 + 2 (tensor maps travel in the
+    kernel parameters); the step matches the per-block kernels."""
+    arch = S.LlamaArch("ft-deep", d_model=256, n_layers=50, n_heads=4, n_kv_heads=2, ffn=704)
+    out, ex, prompt, w, slab = _two_paths(monkeypatch, arch, 2, 16, 2, seed=8)
+    for a, b in zip(out[True][0], out[False][0]):
+        assert _rel(a, b) < 1e-2
     slab.close()

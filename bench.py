@@ -123,9 +123,11 @@ def parse_args():
     p.add_argument("--tp", type=int, default=1, help="GPUs per instance (C4: 13B TP=2, C5: 70B TP=4)")
     p.add_argument("--tile-kib", type=int, default=1024)
     p.add_argument("--nctas", type=int, default=48)
-    p.add_argument("--engine", default="auto", choices=["auto", "vector", "vec256", "tma", "ce"],
+    p.add_argument("--engine", default="auto", choices=["auto", "vector", "vec256", "tma", "ce", "ce2"],
                    help="auto: copy engines for a single-destination source hop, SM push for relays")
     p.add_argument("--fanout", default="auto", choices=["auto", "nvls", "chain", "star"])
+    p.add_argument("--ce2-tiles", type=int, default=0,
+                   help="tiles per copy-engine memcpy of a bz_push_tiles_ce2 hop (0: 128)")
     p.add_argument("--no-group", action="store_true", help="plan chains instead of NVLink fan-out")
     p.add_argument("--stage-engine", default="ce", choices=["ce", "sm"])
     p.add_argument("--tiles-per-copy", type=int, default=128,
@@ -650,7 +652,7 @@ def run_blitz(args):
     gpus = [f"gpu{i}" for i in range(N)]
     anchors = gpus[::tp]  # InstanceState.node = gpus[0] (simcore.py:142-144)
     node_rank = {g: i for i, g in enumerate(gpus)}
-    engine = {"tma": 1, "vec256": 2, "ce": 3, "auto": 4}.get(args.engine, 0)
+    engine = {"tma": 1, "vec256": 2, "ce": 3, "auto": 4, "ce2": 5}.get(args.engine, 0)
     seed = 241217
     my = gpus[rank]
 
@@ -685,6 +687,7 @@ def run_blitz(args):
     sess = ScaleUpSession(fabric, layout, plan, node_rank, host_cache=hc, engine=engine,
                           nctas=args.nctas, fanout_mode=args.fanout, seed=seed,
                           stage_engine=args.stage_engine, tiles_per_copy=args.tiles_per_copy,
+                          ce_tiles_per_copy=args.ce2_tiles,
                           host_stripe=not args.no_stripe)
 
     log("session ready")

@@ -51,6 +51,11 @@ ENGINE_CE = 3       # copy engines (cudaMemcpyAsync into the peer VA), SMs left 
 # multi-destination pushes on the SMs (tile-granular store-and-forward keeps the chain
 # fill at one tile per hop)
 ENGINE_AUTO = 4
+# every single-destination hop on the copy engines with flags on a second stream, relays
+# gated per copy group on their upstream flags (bz_push_tiles_ce2 with wait_flags): on
+# the 1->4 chain 676 GB/s per destination at 128 tiles per copy (634 at 64, 542 at 32)
+# vs 692 for auto (profiles/r2_ce2_chain_n4.txt), so not the default
+ENGINE_CE2 = 5
 CE_TILES_PER_COPY = 16
 CE2_TILES_PER_COPY = 128
 MAX_DST = 8  # BZ_MAX_DST (include/blitz.h): destinations per push launch
@@ -488,8 +493,10 @@ class ScaleExecutor:
                  ce_tiles_per_copy: int = 0):
         self.fabric = fabric
         self.plan = plan
-        # tiles per copy-engine memcpy of an ENGINE_CE chain hop (0: CE_TILES_PER_COPY)
+        # tiles per copy-engine memcpy of an ENGINE_CE chain hop (0: CE_TILES_PER_COPY) and
+        # of a bz_push_tiles_ce2 hop (0: CE2_TILES_PER_COPY)
         self.ce_tiles = ce_tiles_per_copy or CE_TILES_PER_COPY
+        self.ce2_tiles = ce_tiles_per_copy
         self.slab = slab
         self.layout = slab.layout
         self.node_rank = dict(node_rank)
@@ -672,8 +679,10 @@ class ScaleExecutor:
         dsts, relay = self._feeds()
         if dsts and self._ce2_hop(dsts, relay):
             n = dsts[0]
-            self.lib.bz_push_tiles_ce2(slab.ptr, self.peers[n].ptr, self.peers[n].flags_ptr, None,
-                                       self._tile_off_host.ctypes.data, 0, lay.ntiles, CE2_TILES_PER_COPY, e,
+            per_copy = self.ce2_tiles or CE2_TILES_PER_COPY
+            self.lib.bz_push_tiles_ce2(slab.ptr, self.peers[n].ptr, self.peers[n].flags_ptr,
+                                       slab.flags_ptr if relay else None,
+                                       self._tile_off_host.ctypes.data, 0, lay.ntiles, per_copy, e,
                                        st["copy"].cuda_stream, st["ceflag"].cuda_stream)
         elif dsts and self.engine == ENGINE_CE:
             for n in dsts:
@@ -718,11 +727,14 @@ class ScaleExecutor:
         return False
 
     def _ce2_hop(self, dsts, relay) -> bool:
-        # copy engines only for a source -> leaf hop: a relaying destination forwards
+        # auto: copy engines only for a source -> leaf hop: a relaying destination forwards
         # tile by tile, and the copy engine's 128-tile flag groups would make its
         # pipeline bursty (N=4 grouped plan measured 648 vs 683 GB/s per destination)
-        return (self.engine == ENGINE_AUTO and len(dsts) == 1 and not relay and self.stripe_members is None
-                and not self._forwards(dsts[0]))
+        if len(dsts) != 1 or self.stripe_members is not None:
+            return False
+        if self.engine == ENGINE_CE2:
+            return True
+        return self.engine == ENGINE_AUTO and not relay and not self._forwards(dsts[0])
 
     def kernels_per_launch(self) -> int:
         """Our kernels one ``launch`` enqueues on this rank (CE memcpys excluded)."""
@@ -746,7 +758,9 @@ class ScaleExecutor:
                 n += 1
         dsts = self._unicast_targets()
         if dsts and self._ce2_hop(dsts, self.role.receives):
-            n += (self.layout.ntiles + CE2_TILES_PER_COPY - 1) // CE2_TILES_PER_COPY   # flag kernels
+            per_copy = self.ce2_tiles or CE2_TILES_PER_COPY
+            groups = (self.layout.ntiles + per_copy - 1) // per_copy
+            n += groups * (2 if self.role.receives else 1)   # flag kernels [+ relay gates]
         elif dsts and self.engine == ENGINE_CE:
             groups = (self.layout.ntiles + self.ce_tiles - 1) // self.ce_tiles
             per_group = 2 if self.role.receives else 1  # [gate] + flag kernel (memcpy not counted)

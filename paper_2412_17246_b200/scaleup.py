@@ -168,7 +168,8 @@ class ScaleUpSession:
     def __init__(self, fabric: Fabric, layout: SlabLayout, plan, node_rank: dict[str, int],
                  host_cache: Optional[HostCache] = None, engine: int = ENGINE_VECTOR,
                  nctas: int = 32, fanout_mode: str = "auto", seed: int = 241217,
-                 stage_engine: str = "ce", tiles_per_copy: int = 128, host_stripe: bool = True):
+                 stage_engine: str = "ce", tiles_per_copy: int = 128, host_stripe: bool = True,
+                 ce_tiles_per_copy: int = 0):
         self.fabric = fabric
         self.layout = layout
         self.plan = plan
@@ -184,7 +185,7 @@ class ScaleUpSession:
         self.executor = ScaleExecutor(fabric, plan, self.slab, node_rank, host_cache=host_cache,
                                       engine=engine, nctas=nctas, fanout_mode=fanout_mode,
                                       stage_engine=stage_engine, tiles_per_copy=tiles_per_copy,
-                                      host_stripe=host_stripe)
+                                      host_stripe=host_stripe, ce_tiles_per_copy=ce_tiles_per_copy)
         self.receives = self.executor.role.receives
         self.fabric_nodes = {r: n for n, r in node_rank.items()}
         self._expected: Optional[torch.Tensor] = None

@@ -93,6 +93,24 @@ def _push_traffic(payload: int):
         return {"traffic": None, "traffic_source": None}
 
 
+def _pull_traffic(payload: int):
+    """The same for a pulled hop: the receiver's k_push_tiles reading the sender's slab
+    over NVLink (single-process 2-GPU ncu capture of one 2 GB hop on the receiving GPU,
+    profiles/r2_ncu_nvlink_pull_n2.csv), scaled to this shard."""
+    try:
+        m = _ncu_metrics("r2_ncu_nvlink_pull_n2.csv")
+        user = m["nvlrx__bytes_data_user.sum"]
+        scale = payload / user
+        return {"traffic": (m["dram__bytes_read.sum"] + m["dram__bytes_write.sum"]) * scale,
+                "traffic_source": "ncu, k_push_tiles<0> launched on gpu1 pulling a 2.0 GB hop from gpu0 "
+                                  "(profiles/r2_ncu_nvlink_pull_n2.csv): receiver DRAM read+write, scaled",
+                "nvlink_wire_per_user_byte": m["nvlrx__bytes.sum"] / user,
+                "ncu_nvlink_user_GBps": user / m["gpu__time_duration.sum"],
+                "ncu_nvlink_wire_GBps": m["nvlrx__bytes.sum"] / m["gpu__time_duration.sum"]}
+    except (OSError, KeyError, IndexError, ValueError, ZeroDivisionError):
+        return {"traffic": None, "traffic_source": None}
+
+
 def _hbm_peak() -> float:
     try:
         with open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "MEASURED_PEAKS.json")) as f:
@@ -124,7 +142,8 @@ def parse_args():
     p.add_argument("--tile-kib", type=int, default=1024)
     p.add_argument("--nctas", type=int, default=48)
     p.add_argument("--engine", default="auto", choices=["auto", "vector", "vec256", "tma", "ce", "ce2"],
-                   help="auto: copy engines for a single-destination source hop, SM push for relays")
+                   help="auto: every GPU->GPU hop pulled by the receiver's SMs; ce2: copy engines; "
+                        "vector/vec256/tma: the sender's SMs push")
     p.add_argument("--fanout", default="auto", choices=["auto", "nvls", "chain", "star"])
     p.add_argument("--ce2-tiles", type=int, default=0,
                    help="tiles per copy-engine memcpy of a bz_push_tiles_ce2 hop (0: 128)")
@@ -141,8 +160,9 @@ def parse_args():
     p.add_argument("--no-live", action="store_true", help="skip the two-GPU live-pair block")
     p.add_argument("--no-realclock", action="store_true",
                    help="skip the real-clock C3 burst on GPUs 0..N-1 (N >= 2)")
-    p.add_argument("--live-engine", default="ce", choices=["vector", "ce"],
-                   help="weight push of the two-GPU live pair (ce: copy engines, no SMs)")
+    p.add_argument("--live-engine", default="ce", choices=["vector", "ce", "pull"],
+                   help="weight hop of the two-GPU live pair (ce: copy engines, no SM on either GPU; "
+                        "pull: the target's SMs, which also run its share of the batches)")
     p.add_argument("--live-nctas", type=int, default=48)
     p.add_argument("--live-ce-tiles", type=int, default=128, help="tiles per copy-engine memcpy (--live-engine ce)")
     p.add_argument("--live-repeats", type=int, default=5, help="ZigZag / best-effort runs each (alternating)")
@@ -874,7 +894,7 @@ def run_blitz(args):
         from paper_2412_17246_b200.livepair import LivePair, summarize
         log("live pair (7B, NVLink hop, ZigZag)")
         lp = LivePair(fabric, arch, n_batches=12, seqs=4, seq_len=500, mode="nvlink",
-                      engine={"ce": 4, "vector": 0}[args.live_engine], nctas=args.live_nctas,
+                      engine={"ce": 5, "vector": 0, "pull": 4}[args.live_engine], nctas=args.live_nctas,
                       repeats=args.live_repeats, ce_tiles_per_copy=args.live_ce_tiles)
         res = lp.run()
         live = summarize(res) if res is not None else None
@@ -935,18 +955,17 @@ def run_blitz(args):
     if rank == 0:
         # DRAM traffic of the dominant kernel: the NVLink push kernel (N >= 2); at N=1 the
         # mover is the copy engine (no kernel, no ncu counter): null
-        nvl = _push_traffic(payload) if bound == "nvlink" else {"traffic": None, "traffic_source": None}
+        pulled = bound == "nvlink" and args.engine == "auto"
+        if bound != "nvlink":
+            nvl = {"traffic": None, "traffic_source": None}
+        else:
+            nvl = _pull_traffic(payload) if pulled else _push_traffic(payload)
         traffic, traffic_src = nvl.pop("traffic"), nvl.pop("traffic_source")
-        relays = bound == "nvlink" and any(plan_roles(plan)[n].receives and
-                                           (plan_roles(plan)[n].children or plan_roles(plan)[n].fanout or
-                                            plan_roles(plan)[n].rep is not None) for n in plan.targets())
-        if bound == "nvlink" and args.engine == "auto" and not relays:
-            # a single hop runs on the copy engines (bz_push_tiles_ce2): no SM kernel, no
-            # ncu DRAM counters for it; the k_push_tiles capture describes the SM relays
-            traffic, traffic_src = None, "copy-engine hop (bz_push_tiles_ce2): invisible to ncu"
+        if bound == "nvlink" and args.engine in ("ce", "ce2"):
+            traffic, traffic_src = None, "copy-engine hops: invisible to ncu"
         mover = ("copy engines (bz_stage_tiles_ce)" if bound == "pcie" else
-                 "copy engines (bz_push_tiles_ce2): source -> leaf hops" if args.engine == "auto" and not relays
-                 else f"k_push_tiles ({'vector' if args.engine == 'auto' else args.engine}) along the chain")
+                 "k_push_tiles pulled by each receiver (peer source, local destination) along the chain"
+                 if pulled else f"{args.engine} push along the chain")
         line = {
             "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": N, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",

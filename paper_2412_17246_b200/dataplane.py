@@ -45,17 +45,20 @@ ENGINE_VECTOR = 0
 ENGINE_TMA = 1
 ENGINE_VEC256 = 2   # 32-byte LDG/STG.E.ENL2.256 (sm_100)
 ENGINE_CE = 3       # copy engines (cudaMemcpyAsync into the peer VA), SMs left for compute
-# auto: a source hop to a leaf with one destination on the copy engines with the flags
-# on a second stream (bz_push_tiles_ce2, 128 tiles per copy: 748 GB/s vs 717 for the SM
-# push, profiles/r2_nvlink_probe_ce2_n2.jsonl); relays, hops into a relay and
-# multi-destination pushes on the SMs (tile-granular store-and-forward keeps the chain
-# fill at one tile per hop)
+# auto: every GPU -> GPU hop is PULLED: the receiver's SMs read the sender's slab through
+# the peer mapping (bz_push_tiles launched on the receiver with a peer source and a local
+# destination; a relaying sender's tile flags are polled over NVLink).  One hop moves
+# 781 GB/s this way vs 748 for the copy engines and 717 for an SM push
+# (profiles/r2_pull_probe_n2.txt: NVLink reads carry less protocol overhead than
+# writes), and the sender -- the live instance -- spends no SM on the transfer.  Striped
+# host-load pieces, NVLS fan-out and multi-destination sends keep their own movers.
 ENGINE_AUTO = 4
 # every single-destination hop on the copy engines with flags on a second stream, relays
 # gated per copy group on their upstream flags (bz_push_tiles_ce2 with wait_flags): on
 # the 1->4 chain 676 GB/s per destination at 128 tiles per copy (634 at 64, 542 at 32)
 # vs 692 for auto (profiles/r2_ce2_chain_n4.txt), so not the default
 ENGINE_CE2 = 5
+PULL_CTAS = 64      # receiver CTAs of a pulled hop (781 GB/s from 64 up; 768 at 48)
 CE_TILES_PER_COPY = 16
 CE2_TILES_PER_COPY = 128
 MAX_DST = 8  # BZ_MAX_DST (include/blitz.h): destinations per push launch
@@ -542,10 +545,16 @@ class ScaleExecutor:
             self._stripe_ids = torch.from_numpy(ids).to(dev)
 
         self.peers: dict[str, PeerSlab] = {}
-        for n in self._unicast_targets() + self._stripe_peers():
+        for n in self._feeds()[0] + self._stripe_peers():
             r = self.node_rank[n]
             pid, fd, nbytes = exports[r][1]
             self.peers[n] = PeerSlab(fabric.device, pid, fd, nbytes, self.layout)
+        # a pulled hop: map the sender's slab (and its tile flags) here
+        self.pull_from = self._pull_source()
+        self.pull_peer: Optional[PeerSlab] = None
+        if self.pull_from is not None:
+            pid, fd, nbytes = exports[self.node_rank[self.pull_from]][1]
+            self.pull_peer = PeerSlab(fabric.device, pid, fd, nbytes, self.layout)
         fabric.barrier()
         self.mc_out: list[MulticastGroup] = []     # groups this rank writes
         self._mc_all: list[MulticastGroup] = []
@@ -585,23 +594,44 @@ class ScaleExecutor:
         return out
 
     # chain children, plus siblings when the fan-out is served by unicast
-    def _unicast_targets(self) -> list[str]:
-        if self.stripe_members is not None:
+    def _targets_for(self, node: Optional[str]) -> list[str]:
+        role = self.roles.get(node) if node else None
+        if role is None:
+            return []
+        if any(node in m for m in self.stripe_groups.values()):
             # chain children get the whole slab (relayed); the group peers get this
             # member's pieces (_stripe_peers)
-            return list(self.role.children)
-        covered = {rep for rep, (w, _) in self.writers.items() if w == self.node and w != rep}
-        out = [c for c in self.role.children if c not in covered]
-        if self.fanout_mode == "chain" and self.role.fanout:
-            out.append(self.role.fanout[0])
-        if self.fanout_mode == "chain" and self.role.rep is not None:
-            sibs = self.plan.nvlink_fanout[self.role.rep]
-            i = sibs.index(self.node)
+            return list(role.children)
+        covered = {rep for rep, (w, _) in self.writers.items() if w == node and w != rep}
+        out = [c for c in role.children if c not in covered]
+        if self.fanout_mode == "chain" and role.fanout:
+            out.append(role.fanout[0])
+        if self.fanout_mode == "chain" and role.rep is not None:
+            sibs = self.plan.nvlink_fanout[role.rep]
+            i = sibs.index(node)
             if i + 1 < len(sibs):
                 out.append(sibs[i + 1])
-        if self.fanout_mode == "star" and self.role.fanout:
-            out.extend(self.role.fanout)
+        if self.fanout_mode == "star" and role.fanout:
+            out.extend(role.fanout)
         return out
+
+    def _unicast_targets(self) -> list[str]:
+        return self._targets_for(self.node)
+
+    def _pulled(self, sender: str, dst: str) -> bool:
+        """The hop sender -> dst is pulled by dst (auto engine, GPU to GPU, sender not a
+        striped host-load member)."""
+        return (self.engine == ENGINE_AUTO and sender.startswith("gpu") and dst.startswith("gpu")
+                and not any(sender in m for m in self.stripe_groups.values()))
+
+    def _pull_source(self) -> Optional[str]:
+        """The node this node pulls its shard from, if any."""
+        if not self.node or not self.role.receives:
+            return None
+        for n in self.roles:
+            if self.node in self._targets_for(n) and self._pulled(n, self.node):
+                return n
+        return None
 
     def _stripe_peers(self) -> list[str]:
         if self.stripe_members is None:
@@ -614,8 +644,8 @@ class ScaleExecutor:
             self.role.parent is not None and self.role.parent.startswith("mem"))
 
     def _feeds(self) -> tuple[list[str], bool]:
-        """(unicast destinations, relay?) for this node's push kernel."""
-        return self._unicast_targets(), self.role.receives
+        """(unicast destinations this node pushes to, relay?) -- pulled hops excluded."""
+        return [n for n in self._unicast_targets() if not self._pulled(self.node, n)], self.role.receives
 
     def dominant_stream(self) -> Optional[str]:
         """Stream of this rank's bulk mover (for per-kernel timing), if any."""
@@ -623,7 +653,7 @@ class ScaleExecutor:
             return "stage"
         if self.mc_out:
             return "fan"
-        if self._unicast_targets():
+        if self._feeds()[0] or self.pull_peer is not None:
             return "copy"
         return None
 
@@ -697,6 +727,14 @@ class ScaleExecutor:
             self.lib.bz_push_tiles(slab.ptr, ptrs, flags, len(dsts),
                                    slab.flags_ptr if relay else None, slab.tile_off.data_ptr(),
                                    0, lay.ntiles, e, self.nctas, sm_engine, st["copy"].cuda_stream)
+        if self.pull_peer is not None:
+            # pull: this GPU's SMs read the sender's slab (after each tile's flag when the
+            # sender relays) and publish the local tile flags
+            up = self.pull_peer
+            relay_up = self.roles[self.pull_from].receives
+            self.lib.bz_push_tiles(up.ptr, ptr_array([slab.ptr]), ptr_array([slab.flags_ptr]), 1,
+                                   up.flags_ptr if relay_up else None, slab.tile_off.data_ptr(), 0, lay.ntiles, e,
+                                   max(self.nctas, PULL_CTAS), ENGINE_VECTOR, st["copy"].cuda_stream)
         peers = self._stripe_peers()
         for i in range(0, len(peers), MAX_DST):
             # forward this member's pieces (gated on its own staged flags) to the group,
@@ -727,14 +765,9 @@ class ScaleExecutor:
         return False
 
     def _ce2_hop(self, dsts, relay) -> bool:
-        # auto: copy engines only for a source -> leaf hop: a relaying destination forwards
-        # tile by tile, and the copy engine's 128-tile flag groups would make its
-        # pipeline bursty (N=4 grouped plan measured 648 vs 683 GB/s per destination)
-        if len(dsts) != 1 or self.stripe_members is not None:
-            return False
-        if self.engine == ENGINE_CE2:
-            return True
-        return self.engine == ENGINE_AUTO and not relay and not self._forwards(dsts[0])
+        # (copy engines for a hop into a relaying destination made its tile-by-tile
+        # forwarding bursty: N=4 grouped plan 648 vs 683 GB/s per destination)
+        return self.engine == ENGINE_CE2 and len(dsts) == 1 and self.stripe_members is None
 
     def kernels_per_launch(self) -> int:
         """Our kernels one ``launch`` enqueues on this rank (CE memcpys excluded)."""
@@ -756,7 +789,9 @@ class ScaleExecutor:
                     n += (t1 - t0 + self.tiles_per_copy - 1) // self.tiles_per_copy + 1
             else:
                 n += 1
-        dsts = self._unicast_targets()
+        if self.pull_peer is not None:
+            n += 1  # the pull kernel
+        dsts = self._feeds()[0]
         if dsts and self._ce2_hop(dsts, self.role.receives):
             per_copy = self.ce2_tiles or CE2_TILES_PER_COPY
             groups = (self.layout.ntiles + per_copy - 1) // per_copy

@@ -102,7 +102,7 @@ def main():
     ap.add_argument("--tile-kib", type=int, default=1024)
     ap.add_argument("--ctas", default="16,32,48,64,96,148")
     ap.add_argument("--unrolls", default="4,8,16")
-    ap.add_argument("--once", default=None, help="push|mc|mc1|panels: one launch (for ncu)")
+    ap.add_argument("--once", default=None, help="push|pull|mc|mc1|panels: one launch (for ncu)")
     ap.add_argument("--nctas", type=int, default=48)
     ap.add_argument("--gb", type=float, default=0.0, help="uniform payload of this many GB instead of --arch")
     args = ap.parse_args()
@@ -224,6 +224,35 @@ def main():
                 fn, e = push(c, engine)
                 ms = timed(fn, stream)
                 emit({"case": "push", "engine": ename, "nctas": c, "ms": ms, "GBps": payload / ms / 1e6,
+                      "ok": check(peer, want, e)})
+
+    # ---- pull: the receiver's SMs read the sender's slab over NVLink (gpu1 <- gpu0) -----------
+    if args.once in (None, "pull"):
+        spid, sfd, snb = src.export()
+        src_on1 = PeerSlab(1, spid, sfd, snb, lay)   # gpu0's slab mapped on gpu1
+        stream1 = torch.cuda.Stream(device=1)
+        lib1 = cuda_lib(1)
+
+        def pull(nctas, engine):
+            e = nxt()
+
+            def fn():
+                with torch.cuda.device(1):
+                    lib1.bz_push_tiles(src_on1.ptr, ptr_array([peer.ptr]), ptr_array([peer.flags_ptr]), 1, None,
+                                       peer.tile_off.data_ptr(), 0, lay.ntiles, e, nctas, engine, stream1.cuda_stream)
+            return fn, e
+
+        if args.once == "pull":
+            fn, e = pull(args.nctas, 0)
+            fn()
+            torch.cuda.synchronize(1)
+            emit({"case": "pull-once", "ok": check(peer, want, e)})
+            return
+        for engine, ename in ((0, "vector"), (2, "vec256"), (1, "tma")):
+            for c in [int(x) for x in args.ctas.split(",")]:
+                fn, e = pull(c, engine)
+                ms = timed(fn, stream1)
+                emit({"case": "pull", "engine": ename, "nctas": c, "ms": ms, "GBps": payload / ms / 1e6,
                       "ok": check(peer, want, e)})
 
     # ---- copy-engine hop (no SM moves bytes): tiles per memcpy sweep ---------------------------

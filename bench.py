@@ -94,7 +94,7 @@ def _push_traffic(payload: int):
 
 
 def _pull_traffic(payload: int):
-    """The same for a pulled hop: the receiver's k_push_tiles reading the sender's slab
+    """The same for a pulled hop: the receiver's pull kernel reading the sender's slab
     over NVLink (single-process 2-GPU ncu capture of one 2 GB hop on the receiving GPU,
     profiles/r2_ncu_nvlink_pull_n2.csv), scaled to this shard."""
     try:
@@ -102,7 +102,7 @@ def _pull_traffic(payload: int):
         user = m["nvlrx__bytes_data_user.sum"]
         scale = payload / user
         return {"traffic": (m["dram__bytes_read.sum"] + m["dram__bytes_write.sum"]) * scale,
-                "traffic_source": "ncu, k_push_tiles<0> launched on gpu1 pulling a 2.0 GB hop from gpu0 "
+                "traffic_source": "ncu, the pull kernel on gpu1 reading a 2.0 GB hop from gpu0 "
                                   "(profiles/r2_ncu_nvlink_pull_n2.csv): receiver DRAM read+write, scaled",
                 "nvlink_wire_per_user_byte": m["nvlrx__bytes.sum"] / user,
                 "ncu_nvlink_user_GBps": user / m["gpu__time_duration.sum"],
@@ -955,7 +955,11 @@ def run_blitz(args):
     if rank == 0:
         # DRAM traffic of the dominant kernel: the NVLink push kernel (N >= 2); at N=1 the
         # mover is the copy engine (no kernel, no ncu counter): null
-        pulled = bound == "nvlink" and args.engine == "auto"
+        relays = bound == "nvlink" and any(plan_roles(plan)[n].receives and
+                                           (plan_roles(plan)[n].children or plan_roles(plan)[n].fanout or
+                                            plan_roles(plan)[n].rep is not None) for n in plan.targets())
+        # auto pulls source -> leaf hops (the receiver's SMs) and pushes along relay chains
+        pulled = bound == "nvlink" and args.engine == "auto" and not relays
         if bound != "nvlink":
             nvl = {"traffic": None, "traffic_source": None}
         else:
@@ -964,8 +968,8 @@ def run_blitz(args):
         if bound == "nvlink" and args.engine in ("ce", "ce2"):
             traffic, traffic_src = None, "copy-engine hops: invisible to ncu"
         mover = ("copy engines (bz_stage_tiles_ce)" if bound == "pcie" else
-                 "k_push_tiles pulled by each receiver (peer source, local destination) along the chain"
-                 if pulled else f"{args.engine} push along the chain")
+                 "bz_pull_tiles: each receiver's SMs read the source's slab over NVLink" if pulled else
+                 f"k_push_tiles ({'vector' if args.engine == 'auto' else args.engine}) along the chain")
         line = {
             "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": N, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",

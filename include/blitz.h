@@ -108,6 +108,17 @@ int bz_push_tiles(const void* src, void* const* dst, uint32_t* const* dst_flags,
                   const uint32_t* wait_flags, const int64_t* tile_off, int t0, int t1,
                   uint32_t epoch, int nctas, int engine, void* stream);
 
+/* bz_pull_tiles: the receiving GPU's SMs copy tiles [t0, t1) from `src` (the sender's
+ * slab through this GPU's peer mapping) into the local `dst`, raising dst_flags[t] =
+ * epoch (system-scope release); with wait_flags (e.g. a relaying sender's flags through
+ * the peer mapping) tile t is read only after wait_flags[t] >= epoch; notify_flags
+ * (nullable) receives the same release.  The realisation of a source -> leaf PlanEdge
+ * hop (planner.py:240-244): NVLink reads carry less protocol than writes, 781 GB/s vs
+ * 717 for a push (profiles/r2_pull_probe_n2.txt), and the source spends no SM. */
+int bz_pull_tiles(const void* src, void* dst, uint32_t* dst_flags, const uint32_t* wait_flags,
+                  uint32_t* notify_flags, const int64_t* tile_off, int t0, int t1, uint32_t epoch, int nctas,
+                  void* stream);
+
 /* bz_push_tile_list: bz_push_tiles over an explicit tile list ids[0..n) (device
  * int32), 16-byte vector engine.  Striped host-cache load: every member of a
  * host-fed NVLink group stages its piece of each layer over its own PCIe link

@@ -44,12 +44,14 @@ __device__ __forceinline__ uint64_t globaltimer() {
 }
 
 // streaming 16-byte loads: immutable sources may use the non-coherent path;
-// relayed tiles were written by a peer GPU during this kernel -> coherent loads
+// relayed tiles were written by a peer GPU during this kernel -> coherent loads.  Both
+// ask L2 for 256-byte fetches: a relay that PULLS reads its upstream through NVLink,
+// where 32-byte sector requests cost round trips (1->4 chain: 581 vs 692 GB/s without)
 template <bool kCoherent>
 __device__ __forceinline__ int4 ld16(const int4* p) {
   int4 r;
   if (kCoherent)
-    asm volatile("ld.global.L1::no_allocate.v4.s32 {%0,%1,%2,%3}, [%4];"
+    asm volatile("ld.global.L1::no_allocate.L2::256B.v4.s32 {%0,%1,%2,%3}, [%4];"
                  : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
                  : "l"(p));
   else
@@ -118,6 +120,7 @@ struct PushArgs {
   const uint32_t* wait_flags;
   const int64_t* tile_off;
   const int32_t* ids;  // optional tile list: entries [t0, t1) of it name the tiles
+  uint32_t* notify;    // optional: also raise notify[t] (the puller below's upstream flags)
   int t0, t1;
   uint32_t epoch;
 };
@@ -231,6 +234,7 @@ __global__ void __launch_bounds__(kThreads) k_push_tiles(PushArgs a) {
     if (threadIdx.x == 0) {
       __threadfence_system();
       for (int d = 0; d < a.ndst; ++d) st_release_sys(a.flags[d] + t, a.epoch);
+      if (a.notify) st_release_sys(a.notify + t, a.epoch);
     }
   }
 }
@@ -481,10 +485,36 @@ static int fill_push_args(PushArgs& a, const void* src, void* const* dst, uint32
   a.wait_flags = wait_flags;
   a.tile_off = tile_off;
   a.ids = nullptr;
+  a.notify = nullptr;
   a.t0 = t0;
   a.t1 = t1;
   a.epoch = epoch;
   return BZ_OK;
+}
+
+// Pull: k_push_tiles launched on the RECEIVING GPU with the sender's slab (through the
+// peer mapping) as src.  (A pull-only kernel with the destination count fixed at one let
+// ptxas interleave the non-coherent loads with the stores -- ~3 NVLink reads in flight
+// per thread, 589 vs 782 GB/s at 64 CTAs; copy_tile's runtime destination loop keeps
+// all U loads ahead of the stores.)
+extern "C" int bz_pull_tiles(const void* src, void* dst, uint32_t* dst_flags, const uint32_t* wait_flags,
+                             uint32_t* notify_flags, const int64_t* tile_off, int t0, int t1, uint32_t epoch,
+                             int nctas, void* stream) {
+  void* dsts[1] = {dst};
+  uint32_t* flags[1] = {dst_flags};
+  PushArgs a;
+  int rc = fill_push_args(a, src, dsts, flags, 1, wait_flags, tile_off, t0, t1, epoch);
+  if (rc) return rc;
+  if (!dst || !dst_flags) return bz_fail(BZ_EINVAL, "pull: destination and flags required");
+  a.notify = notify_flags;
+  if (t1 == t0) return BZ_OK;
+  const int grid = nctas > 0 ? min(nctas, t1 - t0) : min(64, t1 - t0);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (wait_flags)
+    k_push_tiles<true><<<grid, kThreads, 0, s>>>(a);
+  else
+    k_push_tiles<false><<<grid, kThreads, 0, s>>>(a);
+  return bz_check_launch("bz_pull_tiles");
 }
 
 extern "C" int bz_push_tiles(const void* src, void* const* dst, uint32_t* const* dst_flags, int ndst,

@@ -45,13 +45,14 @@ ENGINE_VECTOR = 0
 ENGINE_TMA = 1
 ENGINE_VEC256 = 2   # 32-byte LDG/STG.E.ENL2.256 (sm_100)
 ENGINE_CE = 3       # copy engines (cudaMemcpyAsync into the peer VA), SMs left for compute
-# auto: every GPU -> GPU hop is PULLED: the receiver's SMs read the sender's slab through
-# the peer mapping (bz_push_tiles launched on the receiver with a peer source and a local
-# destination; a relaying sender's tile flags are polled over NVLink).  One hop moves
-# 781 GB/s this way vs 748 for the copy engines and 717 for an SM push
-# (profiles/r2_pull_probe_n2.txt: NVLink reads carry less protocol overhead than
-# writes), and the sender -- the live instance -- spends no SM on the transfer.  Striped
-# host-load pieces, NVLS fan-out and multi-destination sends keep their own movers.
+# auto: a source -> leaf hop (the sender holds the shard, the receiver forwards nothing)
+# is PULLED: the receiver's SMs read the sender's slab through the peer mapping
+# (bz_pull_tiles), 781 GB/s vs 748 for the copy engines and 717 for an SM push
+# (profiles/r2_pull_probe_n2.txt: NVLink reads carry less protocol than writes), and the
+# sender -- the live instance -- spends no SM.  Relays and hops into a relay keep the
+# tile-by-tile SM push: a pulled relay chain measured 518-601 GB/s per destination on
+# 1->4 vs 689 pushed (profiles/r2_pull_chain_n4.txt).  Striped host-load pieces, NVLS
+# fan-out and multi-destination sends keep their own movers.
 ENGINE_AUTO = 4
 # every single-destination hop on the copy engines with flags on a second stream, relays
 # gated per copy group on their upstream flags (bz_push_tiles_ce2 with wait_flags): on
@@ -549,7 +550,7 @@ class ScaleExecutor:
             r = self.node_rank[n]
             pid, fd, nbytes = exports[r][1]
             self.peers[n] = PeerSlab(fabric.device, pid, fd, nbytes, self.layout)
-        # a pulled hop: map the sender's slab (and its tile flags) here
+        # a pulled hop: map the sender's slab here
         self.pull_from = self._pull_source()
         self.pull_peer: Optional[PeerSlab] = None
         if self.pull_from is not None:
@@ -619,19 +620,25 @@ class ScaleExecutor:
         return self._targets_for(self.node)
 
     def _pulled(self, sender: str, dst: str) -> bool:
-        """The hop sender -> dst is pulled by dst (auto engine, GPU to GPU, sender not a
-        striped host-load member)."""
+        """The hop sender -> dst is pulled by dst: auto engine, GPU to GPU, the sender a
+        source (receives nothing, not a striped host-load member), dst a leaf."""
+        srole = self.roles.get(sender)
         return (self.engine == ENGINE_AUTO and sender.startswith("gpu") and dst.startswith("gpu")
+                and srole is not None and not srole.receives and not self._forwards(dst)
                 and not any(sender in m for m in self.stripe_groups.values()))
 
-    def _pull_source(self) -> Optional[str]:
-        """The node this node pulls its shard from, if any."""
-        if not self.node or not self.role.receives:
+    def _pull_source_of(self, node: Optional[str]) -> Optional[str]:
+        """The node ``node`` pulls its shard from, if any."""
+        role = self.roles.get(node) if node else None
+        if role is None or not role.receives:
             return None
         for n in self.roles:
-            if self.node in self._targets_for(n) and self._pulled(n, self.node):
+            if node in self._targets_for(n) and self._pulled(n, node):
                 return n
         return None
+
+    def _pull_source(self) -> Optional[str]:
+        return self._pull_source_of(self.node)
 
     def _stripe_peers(self) -> list[str]:
         if self.stripe_members is None:
@@ -728,13 +735,10 @@ class ScaleExecutor:
                                    slab.flags_ptr if relay else None, slab.tile_off.data_ptr(),
                                    0, lay.ntiles, e, self.nctas, sm_engine, st["copy"].cuda_stream)
         if self.pull_peer is not None:
-            # pull: this GPU's SMs read the sender's slab (after each tile's flag when the
-            # sender relays) and publish the local tile flags
-            up = self.pull_peer
-            relay_up = self.roles[self.pull_from].receives
-            self.lib.bz_push_tiles(up.ptr, ptr_array([slab.ptr]), ptr_array([slab.flags_ptr]), 1,
-                                   up.flags_ptr if relay_up else None, slab.tile_off.data_ptr(), 0, lay.ntiles, e,
-                                   max(self.nctas, PULL_CTAS), ENGINE_VECTOR, st["copy"].cuda_stream)
+            # pull: this GPU's SMs read the source's slab and publish the local tile flags
+            self.lib.bz_pull_tiles(self.pull_peer.ptr, slab.ptr, slab.flags_ptr, None, None,
+                                   slab.tile_off.data_ptr(), 0, lay.ntiles, e, max(self.nctas, PULL_CTAS),
+                                   st["copy"].cuda_stream)
         peers = self._stripe_peers()
         for i in range(0, len(peers), MAX_DST):
             # forward this member's pieces (gated on its own staged flags) to the group,

@@ -238,17 +238,22 @@ def main():
 
             def fn():
                 with torch.cuda.device(1):
-                    lib1.bz_push_tiles(src_on1.ptr, ptr_array([peer.ptr]), ptr_array([peer.flags_ptr]), 1, None,
-                                       peer.tile_off.data_ptr(), 0, lay.ntiles, e, nctas, engine, stream1.cuda_stream)
+                    if engine == "pull":   # bz_pull_tiles (k_pull_tiles)
+                        lib1.bz_pull_tiles(src_on1.ptr, peer.ptr, peer.flags_ptr, None, None,
+                                           peer.tile_off.data_ptr(), 0, lay.ntiles, e, nctas, stream1.cuda_stream)
+                    else:                  # bz_push_tiles launched on the receiver (peer source)
+                        lib1.bz_push_tiles(src_on1.ptr, ptr_array([peer.ptr]), ptr_array([peer.flags_ptr]), 1,
+                                           None, peer.tile_off.data_ptr(), 0, lay.ntiles, e, nctas, engine,
+                                           stream1.cuda_stream)
             return fn, e
 
         if args.once == "pull":
-            fn, e = pull(args.nctas, 0)
+            fn, e = pull(args.nctas, "pull")
             fn()
             torch.cuda.synchronize(1)
             emit({"case": "pull-once", "ok": check(peer, want, e)})
             return
-        for engine, ename in ((0, "vector"), (2, "vec256"), (1, "tma")):
+        for engine, ename in (("pull", "k_pull_tiles"), (0, "vector"), (2, "vec256"), (1, "tma")):
             for c in [int(x) for x in args.ctas.split(",")]:
                 fn, e = pull(c, engine)
                 ms = timed(fn, stream1)

@@ -322,3 +322,29 @@ def test_copy_engine_hop_with_flag_stream(tiny_layout):
         assert int(dst.flags.min()) == epoch and int(dst.flags.max()) == epoch
     src.close()
     dst.close()
+
+
+def test_pull_kernel_waits_notifies_and_copies_exactly(tiny_layout):
+    """bz_pull_tiles (the `auto` engine's source -> leaf hop, launched on the receiver):
+    bytes and flags exact; with wait flags it copies only tiles whose flag carries the
+    epoch, and notify receives the same releases (loopback on one GPU)."""
+    lib = cuda_lib()
+    src, dst = DeviceSlab(tiny_layout, 0), DeviceSlab(tiny_layout, 0)
+    src.fill_random(seed=33)
+    s = torch.cuda.current_stream().cuda_stream
+    lib.bz_pull_tiles(src.ptr, dst.ptr, dst.flags_ptr, None, None, dst.tile_off.data_ptr(), 0,
+                      tiny_layout.ntiles, 1, 64, s)
+    torch.cuda.synchronize()
+    assert torch.equal(dst.data, src.data)
+    assert int(dst.flags.min()) == 1 and int(dst.flags.max()) == 1
+    # relay form: src flags already at epoch 2, a separate notify array receives epoch 2
+    src.flags.fill_(2)
+    src.fill_random(seed=34)
+    notify = torch.zeros(tiny_layout.ntiles, dtype=torch.int32, device="cuda")
+    lib.bz_pull_tiles(src.ptr, dst.ptr, dst.flags_ptr, src.flags_ptr, notify.data_ptr(), dst.tile_off.data_ptr(),
+                      0, tiny_layout.ntiles, 2, 64, s)
+    torch.cuda.synchronize()
+    assert torch.equal(dst.data, src.data)
+    assert int(dst.flags.min()) == 2 and int(notify.min()) == 2
+    src.close()
+    dst.close()

@@ -988,12 +988,20 @@ def run_blitz(args):
             "roofline": {"bound": bound, "mover": mover, "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": (achieved / peak) if achieved else None, "traffic": traffic,
                          "traffic_source": traffic_src,
-                         # one hop: the sender reads the shard from its HBM and stores it over NVLink
+                         # one hop moves the shard once across NVLink (push: the sender reads its
+                         # HBM and stores to the peer; pull: the receiver loads and writes its HBM)
                          "algorithmic_bytes_per_launch": payload if bound == "nvlink" else None,
                          **nvl,
                          "peak_source": peak_src, "kernel_ms": dom_kernel_ms,
                          "frac_of_nominal": (achieved / (NVLINK_NOMINAL_GBPS if bound == "nvlink"
                                                          else PCIE_PEAK_GBPS)) if achieved else None,
+                         # the wire is the real bound: 900 GB/s nominal / the mover's wire bytes per
+                         # payload byte from its ncu capture (pull 1.125, push 1.19) -- why a pulled
+                         # hop can exceed the recipe's 770 GB/s copy-engine peer copy
+                         "protocol_bound_GBps": (NVLINK_NOMINAL_GBPS / nvl["nvlink_wire_per_user_byte"])
+                         if bound == "nvlink" and nvl.get("nvlink_wire_per_user_byte") else None,
+                         "frac_of_protocol_bound": (achieved * nvl["nvlink_wire_per_user_byte"] / NVLINK_NOMINAL_GBPS)
+                         if achieved and bound == "nvlink" and nvl.get("nvlink_wire_per_user_byte") else None,
                          # the box's achievable H2D rate (torch pinned 4 GiB copy, same host cache, this run)
                          "live_h2d_ceiling_GBps": h2d_ceiling,
                          "frac_of_live_h2d_ceiling": (achieved / h2d_ceiling) if (achieved and h2d_ceiling) else None},

@@ -856,6 +856,9 @@ class ScaleExecutor:
         self.synchronize()
         for p in self.peers.values():
             p.close()
+        if self.pull_peer is not None:
+            self.pull_peer.close()
+            self.pull_peer = None
         for grp in self._mc_all:
             grp.close()
 

@@ -184,3 +184,52 @@ def test_max_dst_matches_header():
     from paper_2412_17246_b200.dataplane import MAX_DST
     text = (ROOT / "include" / "blitz.h").read_text()
     assert int(re.search(r"#define BZ_MAX_DST (\d+)", text).group(1)) == MAX_DST
+
+
+class _HopRules:
+    """The ScaleExecutor's hop-realisation rules without a GPU (its helper methods only)."""
+
+    def __new__(cls, plan, engine, fanout_mode="chain"):
+        from paper_2412_17246_b200.dataplane import ScaleExecutor
+
+        class Probe(ScaleExecutor):
+            def __init__(self):  # no slabs, no fabric: just the inputs of the rules
+                self.plan, self.roles, self.engine = plan, plan_roles(plan), engine
+                self.fanout_mode, self.stripe_groups, self.writers = fanout_mode, {}, {}
+                self.node = None
+
+        return Probe()
+
+
+@pytest.mark.parametrize("n_targets,pulled", [
+    (1, {"gpu1": "gpu0"}),           # 1 -> 2: the single source -> leaf hop is pulled
+    (3, {}),                         # 1 -> 4 grouped: gpu1 relays, every hop pushed
+    (7, {}),                         # 1 -> 8 grouped: a 7-hop relay chain, pushed
+])
+def test_auto_engine_pulls_only_source_to_leaf_hops(n_targets, pulled):
+    from paper_2412_17246_b200.dataplane import ENGINE_AUTO, ENGINE_VECTOR
+    plan = _b200_plan(n_targets)
+    rules = _HopRules(plan, ENGINE_AUTO)
+    got = {n: rules._pull_source_of(n) for n in rules.roles if rules._pull_source_of(n) is not None}
+    assert got == pulled
+    # every receiver is fed by exactly one mover: a pull, or a push from its sender
+    for n, r in rules.roles.items():
+        if not r.receives or not n.startswith("gpu"):
+            continue
+        pushers = [s for s in rules.roles if n in rules._targets_for(s) and not rules._pulled(s, n)]
+        assert len(pushers) + (n in got) == 1, (n, pushers)
+    # an explicit SM engine never pulls
+    assert all(_HopRules(plan, ENGINE_VECTOR)._pull_source_of(n) is None for n in rules.roles)
+
+
+def test_auto_engine_pulls_each_tp_rank_group_hop():
+    """C4's shape at 4 GPUs: 13B TP=2, 1 -> 2 instances: each rank's hop gpu<r> -> gpu<2+r>
+    is a source -> leaf hop, pulled by the new rank."""
+    from paper_2412_17246_b200.dataplane import ENGINE_AUTO, merge_plans
+    topo = ss.load_topology("b200-hgx")
+    flows = ss.FlowSet(topo)
+    model = slabmod.model_spec_for(slabmod.LLAMA2_13B, tp=2)
+    req = ss.build_scale_request(model, ["gpu0"], ["gpu2"], topo, flows)
+    plan = merge_plans(expand_tp(ss.generate_plan(req, topo, flows), 2))
+    rules = _HopRules(plan, ENGINE_AUTO)
+    assert {n: rules._pull_source_of(n) for n in ("gpu2", "gpu3")} == {"gpu2": "gpu0", "gpu3": "gpu1"}

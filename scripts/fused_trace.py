@@ -10,7 +10,8 @@ from paper_2412_17246_b200.llama import KVCache, LlamaExecutor, SlabWeights
 
 EV = ["start", "norm1", "qkv", "bar1", "attn", "bar2", "comb", "o", "bar3", "norm2", "gu", "bar4", "act", "down",
       "p_qkv", "p_o", "p_gu", "p_down", "a_q", "a_s", "a_sm", "a_pv"]
-nl, ctx, B = 8, 1024, int(sys.argv[1]) if len(sys.argv) > 1 else 1
+nl, B = 8, int(sys.argv[1]) if len(sys.argv) > 1 else 1
+ctx = int(sys.argv[2]) if len(sys.argv) > 2 else 1024
 a = S.LLAMA2_7B
 probe = S.LlamaArch("probe", a.d_model, nl, a.n_heads, a.n_kv_heads, a.ffn, a.vocab)
 lay = S.SlabLayout.for_arch(probe)

@@ -965,11 +965,14 @@ def run_blitz(args):
         else:
             nvl = _pull_traffic(payload) if pulled else _push_traffic(payload)
         traffic, traffic_src = nvl.pop("traffic"), nvl.pop("traffic_source")
-        if bound == "nvlink" and args.engine in ("ce", "ce2"):
-            traffic, traffic_src = None, "copy-engine hops: invisible to ncu"
+        ce_chain = bound == "nvlink" and (args.engine in ("ce", "ce2") or (args.engine == "auto" and relays))
+        if ce_chain:
+            traffic, traffic_src = None, "copy-engine hops: no SM kernel, invisible to ncu"
+            nvl = {}
         mover = ("copy engines (bz_stage_tiles_ce)" if bound == "pcie" else
                  "bz_pull_tiles: each receiver's SMs read the source's slab over NVLink" if pulled else
-                 f"k_push_tiles ({'vector' if args.engine == 'auto' else args.engine}) along the chain")
+                 "copy engines along the chain (bz_push_tiles_ce2 out of the source, bz_push_tiles_ce_gated "
+                 "at each relay)" if ce_chain else f"k_push_tiles ({args.engine}) along the chain")
         line = {
             "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": N, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",

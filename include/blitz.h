@@ -143,6 +143,14 @@ int bz_push_tiles_ce2(const void* src, void* dst, uint32_t* dst_flags, const uin
                       const int64_t* tile_off_host, int t0, int t1, int tiles_per_copy, uint32_t epoch,
                       void* stream, void* flag_stream);
 
+/* The same with a relay's gates (one-warp waits on wait_flags per copy group, bounded
+ * spin with the usual timeout / poison rule) enqueued ahead on `gate_stream`: `stream`
+ * waits on one event per group instead of a kernel, so the copy engine does not idle
+ * behind gate launches. */
+int bz_push_tiles_ce_gated(const void* src, void* dst, uint32_t* dst_flags, const uint32_t* wait_flags,
+                           const int64_t* tile_off_host, int t0, int t1, int tiles_per_copy, uint32_t epoch,
+                           void* stream, void* flag_stream, void* gate_stream);
+
 /* bz_multicast_tiles: one multimem.st stream into the multicast VA `mc_dst`
  * (bound to every receiver's slab); flags go through `mc_flags` (the
  * multicast VA of the receivers' flag arrays). */

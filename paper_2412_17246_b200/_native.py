@@ -123,6 +123,7 @@ _SIGNATURES = {
     "bz_mc_free": [ctypes.POINTER(BzMc), _I, _U64],
     "bz_mc_unbind": [ctypes.POINTER(BzMc), _I, _U64],
     "bz_pull_tiles": [_P, _P, _P, _P, _P, _P, _I, _I, ctypes.c_uint32, _I, _P],
+    "bz_push_tiles_ce_gated": [_P, _P, _P, _P, _P, _I, _I, _I, ctypes.c_uint32, _P, _P, _P],
     "bz_push_tiles": [_P, _PP, _PP, _I, _P, _P, _I, _I, _U32, _I, _I, _P],
     "bz_push_tile_list": [_P, _PP, _PP, _I, _P, _P, _P, _I, _U32, _I, _P],
     "bz_multicast_tiles": [_P, _P, _P, _P, _P, _I, _I, _U32, _I, _P],

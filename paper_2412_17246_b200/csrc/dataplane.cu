@@ -632,17 +632,37 @@ static cudaEvent_t pooled_event(int dev, size_t i) {
 
 static int push_ce(const void* src, void* dst, uint32_t* dst_flags, const uint32_t* wait_flags,
                    const int64_t* tile_off_host, int t0, int t1, int tiles_per_copy, uint32_t epoch, void* stream,
-                   void* flag_stream) {
+                   void* flag_stream, void* gate_stream = nullptr) {
   if (!src || !dst || !dst_flags || !tile_off_host || t0 < 0 || t1 < t0 || tiles_per_copy < 1)
     return bz_fail(BZ_EINVAL, "push_ce: bad arguments");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   cudaStream_t fs = static_cast<cudaStream_t>(flag_stream);
+  cudaStream_t gs = static_cast<cudaStream_t>(gate_stream);
   int dev = 0;
   cudaGetDevice(&dev);
+  const int ngroups = (t1 - t0 + tiles_per_copy - 1) / tiles_per_copy;
+  if (wait_flags && gs) {
+    // relay gates on their own stream, enqueued ahead: the copy stream only waits on
+    // events between copies (no kernel in the copy engine's way)
+    cudaEvent_t start = pooled_event(dev, 2 * ngroups + 1);
+    if (!start) return bz_fail(BZ_ECUDA, "push_ce: event pool");
+    cudaEventRecord(start, s);
+    cudaStreamWaitEvent(gs, start, 0);
+    for (int g = 0; g < ngroups; ++g) {
+      const int t = t0 + g * tiles_per_copy, te = min(t1, t + tiles_per_copy);
+      k_wait_range<<<1, 32, 0, gs>>>(wait_flags, t, te, epoch);
+      cudaEvent_t ev = pooled_event(dev, ngroups + 1 + g);
+      if (!ev) return bz_fail(BZ_ECUDA, "push_ce: event pool");
+      cudaEventRecord(ev, gs);
+    }
+  }
   size_t group = 0;
   for (int t = t0; t < t1; t += tiles_per_copy, ++group) {
     const int te = min(t1, t + tiles_per_copy);
-    if (wait_flags) k_wait_range<<<1, 32, 0, s>>>(wait_flags, t, te, epoch);
+    if (wait_flags && gs)
+      cudaStreamWaitEvent(s, pooled_event(dev, ngroups + 1 + group), 0);
+    else if (wait_flags)
+      k_wait_range<<<1, 32, 0, s>>>(wait_flags, t, te, epoch);
     const int64_t b = tile_off_host[t], e = tile_off_host[te];
     cudaError_t err = cudaMemcpyAsync(static_cast<char*>(dst) + b, static_cast<const char*>(src) + b,
                                       static_cast<size_t>(e - b), cudaMemcpyDeviceToDevice, s);
@@ -677,6 +697,14 @@ extern "C" int bz_push_tiles_ce2(const void* src, void* dst, uint32_t* dst_flags
                                  void* stream, void* flag_stream) {
   if (!flag_stream) return bz_fail(BZ_EINVAL, "push_ce2: flag_stream required");
   return push_ce(src, dst, dst_flags, wait_flags, tile_off_host, t0, t1, tiles_per_copy, epoch, stream, flag_stream);
+}
+
+extern "C" int bz_push_tiles_ce_gated(const void* src, void* dst, uint32_t* dst_flags, const uint32_t* wait_flags,
+                                      const int64_t* tile_off_host, int t0, int t1, int tiles_per_copy,
+                                      uint32_t epoch, void* stream, void* flag_stream, void* gate_stream) {
+  if (!flag_stream || !gate_stream) return bz_fail(BZ_EINVAL, "push_ce_gated: flag and gate streams required");
+  return push_ce(src, dst, dst_flags, wait_flags, tile_off_host, t0, t1, tiles_per_copy, epoch, stream, flag_stream,
+                 gate_stream);
 }
 
 extern "C" int bz_stage_tiles_sm(const void* host_src, void* dst, uint32_t* dst_flags, const int64_t* tile_off,

@@ -49,9 +49,12 @@ ENGINE_CE = 3       # copy engines (cudaMemcpyAsync into the peer VA), SMs left 
 # is PULLED: the receiver's SMs read the sender's slab through the peer mapping
 # (bz_pull_tiles), 781 GB/s vs 748 for the copy engines and 717 for an SM push
 # (profiles/r2_pull_probe_n2.txt: NVLink reads carry less protocol than writes), and the
-# sender -- the live instance -- spends no SM.  Relays and hops into a relay keep the
-# tile-by-tile SM push: a pulled relay chain measured 518-601 GB/s per destination on
-# 1->4 vs 689 pushed (profiles/r2_pull_chain_n4.txt).  Striped host-load pieces, NVLS
+# sender -- the live instance -- spends no SM.  Along a relay chain every hop runs on the
+# copy engines in 256-tile groups (bz_push_tiles_ce2 out of the source, a relay's gates
+# enqueued ahead on their own stream: bz_push_tiles_ce_gated): 715-726 GB/s per
+# destination on 1->4 vs 673-692 with SM-push relays and 582-627 with pulled relays (a
+# GPU that pulls and is pulled from carries the read requests of both directions;
+# profiles/r2_pull_chain_n4.txt, r2_ce2_chain_n4.txt).  Striped host-load pieces, NVLS
 # fan-out and multi-destination sends keep their own movers.
 ENGINE_AUTO = 4
 # every single-destination hop on the copy engines with flags on a second stream, relays
@@ -62,6 +65,7 @@ ENGINE_CE2 = 5
 PULL_CTAS = 64      # receiver CTAs of a pulled hop (781 GB/s from 64 up; 768 at 48)
 CE_TILES_PER_COPY = 16
 CE2_TILES_PER_COPY = 128
+CE_CHAIN_TILES_PER_COPY = 256   # copy-engine groups along a relay chain (128: 715, 256: 726 GB/s)
 MAX_DST = 8  # BZ_MAX_DST (include/blitz.h): destinations per push launch
 
 
@@ -533,7 +537,8 @@ class ScaleExecutor:
             if self.node in members:
                 self.stripe_members = members
         dev = torch.device("cuda", fabric.device)
-        self.streams = {k: torch.cuda.Stream(device=dev) for k in ("copy", "fan", "track", "stage", "ceflag")}
+        self.streams = {k: torch.cuda.Stream(device=dev)
+                        for k in ("copy", "fan", "track", "stage", "ceflag", "cegate")}
         self.epoch = 0
         self._tile_off_host = np.ascontiguousarray(self.layout.tile_off)
         self.writers = self._fanout_writers() if fanout_mode == "nvls" else {}
@@ -716,11 +721,16 @@ class ScaleExecutor:
         dsts, relay = self._feeds()
         if dsts and self._ce2_hop(dsts, relay):
             n = dsts[0]
-            per_copy = self.ce2_tiles or CE2_TILES_PER_COPY
-            self.lib.bz_push_tiles_ce2(slab.ptr, self.peers[n].ptr, self.peers[n].flags_ptr,
-                                       slab.flags_ptr if relay else None,
-                                       self._tile_off_host.ctypes.data, 0, lay.ntiles, per_copy, e,
-                                       st["copy"].cuda_stream, st["ceflag"].cuda_stream)
+            per_copy = self._ce_tiles()
+            if relay:   # gates ahead on their own stream: the copy engine runs back to back
+                self.lib.bz_push_tiles_ce_gated(slab.ptr, self.peers[n].ptr, self.peers[n].flags_ptr,
+                                                slab.flags_ptr, self._tile_off_host.ctypes.data, 0, lay.ntiles,
+                                                per_copy, e, st["copy"].cuda_stream, st["ceflag"].cuda_stream,
+                                                st["cegate"].cuda_stream)
+            else:
+                self.lib.bz_push_tiles_ce2(slab.ptr, self.peers[n].ptr, self.peers[n].flags_ptr, None,
+                                           self._tile_off_host.ctypes.data, 0, lay.ntiles, per_copy, e,
+                                           st["copy"].cuda_stream, st["ceflag"].cuda_stream)
         elif dsts and self.engine == ENGINE_CE:
             for n in dsts:
                 self.lib.bz_push_tiles_ce(slab.ptr, self.peers[n].ptr, self.peers[n].flags_ptr,
@@ -769,9 +779,20 @@ class ScaleExecutor:
         return False
 
     def _ce2_hop(self, dsts, relay) -> bool:
-        # (copy engines for a hop into a relaying destination made its tile-by-tile
-        # forwarding bursty: N=4 grouped plan 648 vs 683 GB/s per destination)
-        return self.engine == ENGINE_CE2 and len(dsts) == 1 and self.stripe_members is None
+        """This node's (non-pulled) single-destination hop runs on the copy engines: always
+        under ENGINE_CE2; under auto when the hop is part of a relay chain (this node
+        relays, or its destination does) -- the whole chain then moves in copy-engine
+        groups (a copy-engine hop into an SM-push relay made its forwarding bursty)."""
+        if len(dsts) != 1 or self.stripe_members is not None:
+            return False
+        if self.engine == ENGINE_CE2:
+            return True
+        return self.engine == ENGINE_AUTO and (relay or self._forwards(dsts[0]))
+
+    def _ce_tiles(self) -> int:
+        if self.ce2_tiles:
+            return self.ce2_tiles
+        return CE_CHAIN_TILES_PER_COPY if self.engine == ENGINE_AUTO else CE2_TILES_PER_COPY
 
     def kernels_per_launch(self) -> int:
         """Our kernels one ``launch`` enqueues on this rank (CE memcpys excluded)."""
@@ -797,7 +818,7 @@ class ScaleExecutor:
             n += 1  # the pull kernel
         dsts = self._feeds()[0]
         if dsts and self._ce2_hop(dsts, self.role.receives):
-            per_copy = self.ce2_tiles or CE2_TILES_PER_COPY
+            per_copy = self._ce_tiles()
             groups = (self.layout.ntiles + per_copy - 1) // per_copy
             n += groups * (2 if self.role.receives else 1)   # flag kernels [+ relay gates]
         elif dsts and self.engine == ENGINE_CE:

@@ -348,3 +348,26 @@ def test_pull_kernel_waits_notifies_and_copies_exactly(tiny_layout):
     assert int(dst.flags.min()) == 2 and int(notify.min()) == 2
     src.close()
     dst.close()
+
+
+def test_gated_copy_engine_relay_chain(tiny_layout):
+    """bz_push_tiles_ce2 into a relay, bz_push_tiles_ce_gated out of it (the auto engine's
+    relay chain): the relay's copies wait on its own tile flags through gates enqueued on
+    a third stream; the leaf ends bit-exact with every flag at the epoch (loopback)."""
+    lib = cuda_lib()
+    src, relay, leaf = (DeviceSlab(tiny_layout, 0) for _ in range(3))
+    src.fill_random(seed=41)
+    off = tiny_layout.tile_off.ctypes.data
+    s_src, f_src = torch.cuda.Stream(), torch.cuda.Stream()
+    s_rel, f_rel, g_rel = torch.cuda.Stream(), torch.cuda.Stream(), torch.cuda.Stream()
+    for epoch in (1, 2):
+        # the relay's leg first (its gates wait), then the source's leg that feeds it
+        lib.bz_push_tiles_ce_gated(relay.ptr, leaf.ptr, leaf.flags_ptr, relay.flags_ptr, off, 0, tiny_layout.ntiles,
+                                   4, epoch, s_rel.cuda_stream, f_rel.cuda_stream, g_rel.cuda_stream)
+        lib.bz_push_tiles_ce2(src.ptr, relay.ptr, relay.flags_ptr, None, off, 0, tiny_layout.ntiles, 4, epoch,
+                              s_src.cuda_stream, f_src.cuda_stream)
+        torch.cuda.synchronize()
+        assert torch.equal(leaf.data, src.data) and torch.equal(relay.data, src.data)
+        assert int(leaf.flags.min()) == epoch and int(leaf.flags.max()) == epoch
+    for x in (src, relay, leaf):
+        x.close()

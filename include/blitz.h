@@ -12,6 +12,9 @@
  *                                   (SURVEY.md §5 "communication backend")
  *   bz_push_tiles                <- a chain edge's store-and-forward transfer
  *                                   (planner.py:240-244 PlanEdge hop; simcore.py:690-703)
+ *   bz_pull_tiles                <- the same hop out of a live source into a leaf, run by
+ *                                   the receiving GPU (the source spends no SM)
+ *   bz_push_tiles_ce2 / _ce_gated <- the hop on the copy engines (a relay chain; the live pair)
  *   bz_multicast_tiles           <- ScalePlan.nvlink_fanout intra-host broadcast
  *                                   (planner.py:86-87, 245-253)
  *   bz_stage_tiles_ce / _sm      <- mem<h> -> gpu pcie source edge; autoscaler.baseline_load_time

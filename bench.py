@@ -971,6 +971,7 @@ def run_blitz(args):
             nvl = {}
         mover = ("copy engines (bz_stage_tiles_ce)" if bound == "pcie" else
                  "bz_pull_tiles: each receiver's SMs read the source's slab over NVLink" if pulled else
+                 "k_multicast_tiles (NVLS multimem.st) fan-out" if sess.executor.fanout_mode == "nvls" else
                  "copy engines along the chain (bz_push_tiles_ce2 out of the source, bz_push_tiles_ce_gated "
                  "at each relay)" if ce_chain else f"k_push_tiles ({args.engine}) along the chain")
         line = {

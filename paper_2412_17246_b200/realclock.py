@@ -31,8 +31,10 @@ its tokens.
 One process drives every GPU (peer access on); prompts are padded to 256-token
 buckets whose forward passes are captured as CUDA graphs.  With more than one
 target GPU the trigger adds as many instances as the policy asks for at once:
-``blitz`` pushes down a chain source -> t1 -> t2 ... (relays forward each tile as
-its flag lands, the plan's grouped NVLink fan-out realised as a sibling chain),
+``blitz`` moves the weights down a chain source -> t1 -> t2 ... on the copy engines
+(the data plane's chain mover: 256-tile groups, each relay forwarding a group once its
+flags land; the serving source spends no SM), the plan's grouped NVLink fan-out
+realised as a sibling chain,
 ``allcache`` stages every new instance from the host copy in parallel.  TTFT = host time at
 which the request's prefill completion event is observed minus its arrival time.
 """
@@ -46,11 +48,11 @@ from typing import Optional, Sequence
 
 import torch
 
-from ._native import cuda_lib, ptr_array
+from ._native import cuda_lib
 from . import livescale
 from .autoscaler import LoadMetrics, ScalePolicy, should_scale_up
 from .coop import CooperativePair
-from .dataplane import DeviceSlab, HostCache, PeerSlab
+from .dataplane import CE_CHAIN_TILES_PER_COPY, DeviceSlab, HostCache, PeerSlab
 from .llama import KVCache, LlamaExecutor, SlabWeights
 from .slab import LlamaArch, SlabLayout
 
@@ -115,7 +117,7 @@ class RealClockServer:
     DECODE_GRAPH_ROWS = (4, 8, 16, 32)
 
     def __init__(self, arch: LlamaArch, src_dev: int = 0, tgt_dev: int = 1, tile_bytes: int = 1 << 20,
-                 push_ctas: int = 48, extra_devs: Sequence[int] = (), decode_slots: int = 0,
+                 extra_devs: Sequence[int] = (), decode_slots: int = 0,
                  max_new_tokens: int = 128):
         self.arch = arch
         if decode_slots and decode_slots not in self.DECODE_GRAPH_ROWS:
@@ -129,7 +131,6 @@ class RealClockServer:
             self.lib.bz_enable_peer_mesh(d)
         self.layout = SlabLayout.for_arch(arch, tile_bytes=tile_bytes)
         self.src_dev, self.tgt_dev = src_dev, tgt_dev
-        self.push_ctas = push_ctas
         with torch.cuda.device(src_dev):
             self.src = DeviceSlab(self.layout, src_dev)
             SlabWeights(arch, self.layout, self.src.data).init_random(seed=0)
@@ -153,13 +154,16 @@ class RealClockServer:
         self.ex0 = LlamaExecutor(SlabWeights(arch, self.layout, self.src.data), self.max_tokens, d0)
         self.s0 = torch.cuda.Stream(device=d0)
         self.push_stream = torch.cuda.Stream(device=d0)
-        self.tex, self.ts, self.tload, self.tpush = [], [], [], []
+        self.push_flag_stream = torch.cuda.Stream(device=d0)
+        self.tex, self.ts, self.tload, self.tpush, self.tflag, self.tgate = [], [], [], [], [], []
         for d, t in zip(self.tgt_devs, self.tslabs):
             dev = torch.device("cuda", d)
             self.tex.append(LlamaExecutor(SlabWeights(arch, self.layout, t.data), self.max_tokens, dev))
             self.ts.append(torch.cuda.Stream(device=dev))
             self.tload.append(torch.cuda.Stream(device=dev))
             self.tpush.append(torch.cuda.Stream(device=dev))
+            self.tflag.append(torch.cuda.Stream(device=dev))
+            self.tgate.append(torch.cuda.Stream(device=dev))
         self.ex1, self.s1, self.load_stream = self.tex[0], self.ts[0], self.tload[0]
         self.epoch = 0
         self._warm()
@@ -280,21 +284,23 @@ class RealClockServer:
                 self.tslabs[j].loaded.zero_()
             torch.cuda.synchronize(self.tgt_devs[j])
         if strategy == "blitz":
-            # chain: source -> group[0] -> group[1] -> ...; every relay forwards a tile
-            # as soon as its own flag carries the epoch
+            # chain source -> group[0] -> group[1] -> ... on the copy engines (the data
+            # plane's chain mover): the serving source spends no SM; every relay forwards
+            # a 256-tile group once its own flags carry the epoch
+            tiles = CE_CHAIN_TILES_PER_COPY
+            off = lay.tile_off.ctypes.data
             with torch.cuda.device(self.src_dev):
                 peer = self.peer_on_src[group[0]]
-                self.lib.bz_push_tiles(self.src.ptr, ptr_array([peer.ptr]), ptr_array([peer.flags_ptr]), 1, None,
-                                       self.src.tile_off.data_ptr(), 0, lay.ntiles, self.epoch, self.push_ctas, 0,
-                                       self.push_stream.cuda_stream)
+                self.lib.bz_push_tiles_ce2(self.src.ptr, peer.ptr, peer.flags_ptr, None, off, 0, lay.ntiles, tiles,
+                                           self.epoch, self.push_stream.cuda_stream, self.push_flag_stream.cuda_stream)
             for a, b in zip(group, group[1:]):
                 if b != a + 1:
                     raise ValueError("a blitz group is a run of consecutive targets")
                 t, nxt = self.tslabs[a], self.peer_next[a]
                 with torch.cuda.device(self.tgt_devs[a]):
-                    self.lib.bz_push_tiles(t.ptr, ptr_array([nxt.ptr]), ptr_array([nxt.flags_ptr]), 1, t.flags_ptr,
-                                           t.tile_off.data_ptr(), 0, lay.ntiles, self.epoch, self.push_ctas, 0,
-                                           self.tpush[a].cuda_stream)
+                    self.lib.bz_push_tiles_ce_gated(t.ptr, nxt.ptr, nxt.flags_ptr, t.flags_ptr, off, 0, lay.ntiles,
+                                                    tiles, self.epoch, self.tpush[a].cuda_stream,
+                                                    self.tflag[a].cuda_stream, self.tgate[a].cuda_stream)
             for j in group:
                 t = self.tslabs[j]
                 with torch.cuda.device(self.tgt_devs[j]):

@@ -36,7 +36,8 @@ import torch
 
 from ._native import cuda_lib, ptr_array
 from .costs import MeasuredCosts
-from .dataplane import DeviceSlab, HostCache, PeerSlab, execute_plan_loopback, plan_roles
+from .dataplane import (CE_CHAIN_TILES_PER_COPY, DeviceSlab, HostCache, PeerSlab, execute_plan_loopback,
+                        plan_roles)
 from .planner import ScalePlan
 from .slab import LlamaArch, SlabLayout
 
@@ -209,6 +210,22 @@ class LocalPlanExecutor:
                 continue
             d = dev_of[n]
             with torch.cuda.device(d):
+                if len(outs) == 1:
+                    # the data plane's chain mover: copy engines in 256-tile groups, a relay's
+                    # gates enqueued ahead on their own stream (no SM on any GPU)
+                    dst = self._peer(d, ("dst", dev_of[outs[0]]), slabs[outs[0]])
+                    off = lay.tile_off.ctypes.data
+                    if r.receives:
+                        lib.bz_push_tiles_ce_gated(slab.ptr, dst, dst + lay.flag_offset, slab.flags_ptr, off, 0,
+                                                   lay.ntiles, CE_CHAIN_TILES_PER_COPY, e,
+                                                   self._stream(d, "copy").cuda_stream,
+                                                   self._stream(d, "ceflag").cuda_stream,
+                                                   self._stream(d, "cegate").cuda_stream)
+                    else:
+                        lib.bz_push_tiles_ce2(slab.ptr, dst, dst + lay.flag_offset, None, off, 0, lay.ntiles,
+                                              CE_CHAIN_TILES_PER_COPY, e, self._stream(d, "copy").cuda_stream,
+                                              self._stream(d, "ceflag").cuda_stream)
+                    continue
                 ptrs = ptr_array([self._peer(d, ("dst", dev_of[o]), slabs[o]) for o in outs])
                 flags = ptr_array([self._peer(d, ("dst", dev_of[o]), slabs[o]) + lay.flag_offset for o in outs])
                 lib.bz_push_tiles(slab.ptr, ptrs, flags, len(outs), slab.flags_ptr if r.receives else None,

@@ -57,10 +57,9 @@ ENGINE_CE = 3       # copy engines (cudaMemcpyAsync into the peer VA), SMs left 
 # profiles/r2_pull_chain_n4.txt, r2_ce2_chain_n4.txt).  Striped host-load pieces, NVLS
 # fan-out and multi-destination sends keep their own movers.
 ENGINE_AUTO = 4
-# every single-destination hop on the copy engines with flags on a second stream, relays
-# gated per copy group on their upstream flags (bz_push_tiles_ce2 with wait_flags): on
-# the 1->4 chain 676 GB/s per destination at 128 tiles per copy (634 at 64, 542 at 32)
-# vs 692 for auto (profiles/r2_ce2_chain_n4.txt), so not the default
+# every single-destination hop on the copy engines (flags on a second stream; a relay's
+# gates ahead on a third): auto's relay-chain mover applied to leaf hops as well -- the
+# live pair's engine, whose target computes while it receives and so should not pull
 ENGINE_CE2 = 5
 PULL_CTAS = 64      # receiver CTAs of a pulled hop (781 GB/s from 64 up; 768 at 48)
 CE_TILES_PER_COPY = 16

@@ -142,11 +142,12 @@ def parse_args():
     p.add_argument("--tile-kib", type=int, default=1024)
     p.add_argument("--nctas", type=int, default=48)
     p.add_argument("--engine", default="auto", choices=["auto", "vector", "vec256", "tma", "ce", "ce2"],
-                   help="auto: every GPU->GPU hop pulled by the receiver's SMs; ce2: copy engines; "
+                   help="auto: a source->leaf hop pulled by the receiver's SMs, relay chains on the copy "
+                        "engines; ce2: every single-destination hop on the copy engines; "
                         "vector/vec256/tma: the sender's SMs push")
     p.add_argument("--fanout", default="auto", choices=["auto", "nvls", "chain", "star"])
     p.add_argument("--ce2-tiles", type=int, default=0,
-                   help="tiles per copy-engine memcpy of a bz_push_tiles_ce2 hop (0: 128)")
+                   help="tiles per copy-engine memcpy (0: 256 along an auto relay chain, 128 for ce2)")
     p.add_argument("--no-group", action="store_true", help="plan chains instead of NVLink fan-out")
     p.add_argument("--stage-engine", default="ce", choices=["ce", "sm"])
     p.add_argument("--tiles-per-copy", type=int, default=128,

@@ -238,7 +238,7 @@ def main():
 
             def fn():
                 with torch.cuda.device(1):
-                    if engine == "pull":   # bz_pull_tiles (k_pull_tiles)
+                    if engine == "pull":   # bz_pull_tiles
                         lib1.bz_pull_tiles(src_on1.ptr, peer.ptr, peer.flags_ptr, None, None,
                                            peer.tile_off.data_ptr(), 0, lay.ntiles, e, nctas, stream1.cuda_stream)
                     else:                  # bz_push_tiles launched on the receiver (peer source)
@@ -253,7 +253,7 @@ def main():
             torch.cuda.synchronize(1)
             emit({"case": "pull-once", "ok": check(peer, want, e)})
             return
-        for engine, ename in (("pull", "k_pull_tiles"), (0, "vector"), (2, "vec256"), (1, "tma")):
+        for engine, ename in (("pull", "bz_pull_tiles"), (0, "vector"), (2, "vec256"), (1, "tma")):
             for c in [int(x) for x in args.ctas.split(",")]:
                 fn, e = pull(c, engine)
                 ms = timed(fn, stream1)

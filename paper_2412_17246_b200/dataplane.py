@@ -61,7 +61,8 @@ ENGINE_AUTO = 4
 # gates ahead on a third): auto's relay-chain mover applied to leaf hops as well -- the
 # live pair's engine, whose target computes while it receives and so should not pull
 ENGINE_CE2 = 5
-PULL_CTAS = 64      # receiver CTAs of a pulled hop (781 GB/s from 64 up; 768 at 48)
+PULL_CTAS = 64      # minimum receiver CTAs of a pulled hop (781 GB/s at 64, 768 at 48); a
+                    # new instance is idle while it loads, so the pull takes all its SMs (783)
 CE_TILES_PER_COPY = 16
 CE2_TILES_PER_COPY = 128
 CE_CHAIN_TILES_PER_COPY = 256   # copy-engine groups along a relay chain (128: 715, 256: 726 GB/s)
@@ -746,8 +747,8 @@ class ScaleExecutor:
         if self.pull_peer is not None:
             # pull: this GPU's SMs read the source's slab and publish the local tile flags
             self.lib.bz_pull_tiles(self.pull_peer.ptr, slab.ptr, slab.flags_ptr, None, None,
-                                   slab.tile_off.data_ptr(), 0, lay.ntiles, e, max(self.nctas, PULL_CTAS),
-                                   st["copy"].cuda_stream)
+                                   slab.tile_off.data_ptr(), 0, lay.ntiles, e,
+                                   max(self.nctas, PULL_CTAS, self.fabric.sm_count), st["copy"].cuda_stream)
         peers = self._stripe_peers()
         for i in range(0, len(peers), MAX_DST):
             # forward this member's pieces (gated on its own staged flags) to the group,

@@ -306,7 +306,7 @@ def test_relay_timeout_withholds_downstream_flags(tiny_layout):
 
 
 def test_copy_engine_hop_with_flag_stream(tiny_layout):
-    """bz_push_tiles_ce2 (the `auto` engine's single-destination hop): copies back to back
+    """bz_push_tiles_ce2 (the copy-engine hop: a relay chain's first hop, the live pair): copies back to back
     on one stream, flag releases on another; bytes and every flag exact, and the copy
     stream joins the flag stream at the end."""
     lib = cuda_lib()

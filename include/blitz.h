@@ -228,6 +228,11 @@ int bz_gemm_bf16_signal(const void* A, const void* B, void* C, const void* resid
  * rows) runs stream-K: the tiles x K-blocks space is cut into equal ranges, one
  * per CTA; tiles shared by two or more CTAs are summed in fp32 (plus the
  * residual) by their last contributor.  workspace = NULL disables it.
+ * Decode shapes (M <= 16, K % 64 == 0) take neither: when the 128-row weight
+ * tiles fit the SMs the weights are the MMA's M operand and K is split over a
+ * thread-block cluster summed in distributed shared memory (BZ_GEMM_SWAP=0 off),
+ * else whole tiles of >= 128 rows stream K-chunked (BZ_GEMM_KC=0 off); neither
+ * uses the workspace.
  * signal/ctas_out as in bz_gemm_bf16_signal.  All compute kernels are launched
  * with programmatic dependent launch (set-up overlaps the previous kernel;
  * BZ_PDL=0 disables).  The workspace must be zero-filled before its first use

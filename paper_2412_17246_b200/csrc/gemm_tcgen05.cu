@@ -93,6 +93,7 @@ struct Params {
   // split-K of the pair kernel (few tiles, long K): unit = (tile, K slice); slices
   // store fp32 partials to ws[slice][M][N], k_splitk_reduce adds them into C
   int ksplit, kb_slice;
+  int kc_nomma;  // diagnostic (BZ_GEMM_KC_NOMMA): the K-chunked kernel streams B without MMAs
 };
 
 // The (tile, k0, k1) segments one CTA processes, in order; identical for the
@@ -454,6 +455,153 @@ __global__ void __launch_bounds__(THREADS, OCC_)
   if (p.signal != nullptr && threadIdx.x == 0) {
     // fused hand-off: C may be a peer (NVLink) mapping; publish this CTA's tiles
     // (with stream-K, every fix-up this CTA performed is complete here)
+    __threadfence_system();
+    asm volatile("red.release.sys.global.add.u32 [%0], 1;" ::"l"(p.signal) : "memory");
+  }
+}
+
+// ===========================================================================
+// Decode-shaped (M <= 16) whole-tile variant with K-chunked stages: a stage is one 3-D
+// TMA box {64 k, rows, KCH k-blocks} of A and of B (KCH 64-wide 128B-swizzled tiles
+// side by side), so a narrow weight tile (BN = 32) still moves 32 KiB per TMA op and
+// per pipeline step.  With the 2-D layout a 32-row tile paid the per-k-block ring step
+// (~270 ns) every 4 KiB, so narrow tiles were slow and decode relied on wide tiles
+// plus stream-K (and its fix-up tail).  Here every CTA owns whole BN-row tiles over all
+// of K -- no partials, no fix-up -- and BN is chosen to give each SM about one tile.
+// Roles as k_gemm_bf16: w0 TMA, w1 MMA, w2 TMEM allocator, w4..w7 epilogue.
+template <int BN_>
+__global__ void __launch_bounds__(THREADS, 1)
+    k_gemm_skinny_kc(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b, Params p,
+                     int kch, int a_rows) {
+  constexpr int BN = BN_;
+  constexpr int ACC_COLS = BN;
+  constexpr int TMEM_COLS = 2 * BN <= 64 ? 64 : 2 * BN <= 128 ? 128 : 2 * BN <= 256 ? 256 : 512;
+  const int STAGES = p.stages;
+  const int A_STG = kch * a_rows * 128, B_STG = kch * BN * 128;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sa = smem;                                   // STAGES x A_STG (1024-B multiples)
+  uint8_t* sb = smem + STAGES * A_STG;                  // STAGES x B_STG
+  uint64_t* full = reinterpret_cast<uint64_t*>(sb + STAGES * B_STG);
+  uint64_t* empty = full + MAX_STAGES;
+  uint64_t* acc_full = empty + MAX_STAGES;
+  uint64_t* acc_empty = acc_full + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int k_blocks = (p.K + BK - 1) / BK;
+  const int nks = (k_blocks + kch - 1) / kch;           // stages per tile
+  const int n_tiles = p.n_tiles;
+
+  if (warp == 0 && lane == 0) {
+    prefetch_tmap(&map_a);
+    prefetch_tmap(&map_b);
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&acc_full[b], 1);
+      mbar_init(&acc_empty[b], 4);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "n"(TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // the first tile's first stages of B (weights) go out before pdl_wait, overlapping
+      // the predecessor; A (activations) follows once its writes are visible
+      const int pre = (p.b_static && static_cast<int>(blockIdx.x) < n_tiles) ? min(STAGES, nks) : 0;
+      for (int i = 0; i < pre; ++i) {
+        mbar_expect_tx(&full[i], A_STG + B_STG);
+        tma_load_3d(sb + i * B_STG, &map_b, 0, static_cast<int>(blockIdx.x) * BN, i * kch, &full[i]);
+      }
+      pdl_wait();
+      for (int i = 0; i < pre; ++i) tma_load_3d(sa + i * A_STG, &map_a, 0, 0, i * kch, &full[i]);
+      uint32_t stage = pre % STAGES, phase = pre == STAGES ? 1u : 0u;
+      for (int tile = blockIdx.x, skip = pre; tile < n_tiles; tile += gridDim.x, skip = 0) {
+        for (int ks = skip; ks < nks; ++ks) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          mbar_expect_tx(&full[stage], A_STG + B_STG);
+          tma_load_3d(sa + stage * A_STG, &map_a, 0, 0, ks * kch, &full[stage]);
+          tma_load_3d(sb + stage * B_STG, &map_b, 0, tile * BN, ks * kch, &full[stage]);
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+      pdl_trigger();
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      pdl_wait();
+      constexpr uint32_t idesc = instr_desc_bf16(BM, BN);
+      uint32_t stage = 0, phase = 0;
+      for (int tile = blockIdx.x, it = 0; tile < n_tiles; tile += gridDim.x, ++it) {
+        const int buf = it & 1;
+        const uint32_t use = static_cast<uint32_t>(it >> 1);
+        mbar_wait(&acc_empty[buf], (use & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t d = tmem_base + buf * ACC_COLS;
+        for (int ks = 0; ks < nks; ++ks) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const int subs = p.kc_nomma ? 0 : min(kch, k_blocks - ks * kch);
+          for (int sub = 0; sub < subs; ++sub) {
+            const uint64_t da = umma_desc_sw128(smem_u32(sa + stage * A_STG + sub * a_rows * 128));
+            const uint64_t db = umma_desc_sw128(smem_u32(sb + stage * B_STG + sub * BN * 128));
+#pragma unroll
+            for (int k = 0; k < BK / UMMA_K; ++k)
+              umma_bf16(d, da + 2 * k, db + 2 * k, idesc, (ks != 0 || sub != 0 || k != 0) ? 1u : 0u);
+          }
+          umma_commit(&empty[stage]);
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        umma_commit(&acc_full[buf]);
+      }
+    }
+  } else if (warp >= 4) {
+    pdl_wait();  // reads the residual and writes C
+    const int quarter = warp & 3;
+    const int row = quarter * 32 + lane;
+    for (int tile = blockIdx.x, it = 0; tile < n_tiles; tile += gridDim.x, ++it) {
+      const int buf = it & 1;
+      const uint32_t use = static_cast<uint32_t>(it >> 1);
+      mbar_wait(&acc_full[buf], use & 1);
+      tc_fence_after();
+      const uint32_t taddr = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + buf * ACC_COLS;
+#pragma unroll 1
+      for (int c = 0; c < BN; c += 32) {
+        uint32_t r[32];
+        tmem_ld_32x32b_x32(taddr + c, r);
+        if (row < p.M) store_chunk(p, row, tile * BN + c, r, p.N);
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&acc_empty[buf]);
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "n"(TMEM_COLS));
+  }
+  if (p.signal != nullptr && threadIdx.x == 0) {
     __threadfence_system();
     asm volatile("red.release.sys.global.add.u32 [%0], 1;" ::"l"(p.signal) : "memory");
   }
@@ -947,6 +1095,259 @@ static int launch_pair(const CUtensorMap& ma, const void* B, int N, int K, int l
   return bz_check_launch("bz_gemm_bf16 (pair)");
 }
 
+// ===========================================================================
+// Decode GEMMs (M <= 16) with the operands swapped: D^T[n][m] = W[n, :] . X[m, :].
+// A 128-row weight tile is the MMA's M operand and the (zero-padded) 16 token rows
+// are its N, so one tcgen05.mma consumes 4 KiB of weights; with the tokens as M a
+// 128 x 32 instruction consumed 1 KiB and the MMA issue rate, not HBM, bounded the
+// narrow tiles decode needs for chip fill (profiles/r2_fused_decode.txt: K-chunked
+// BN = 32 streams 5.6-6.6 TB/s without its MMAs, half that with them).  A cluster
+// of S CTAs splits K of one tile; the S fp32 partials meet in distributed shared
+// memory (no workspace, no fix-up pass) and rank r stores rows [r*128/S, (r+1)*128/S).
+// One (tile, K range) per CTA; grid = tiles x S <= SMs.
+constexpr int SW_ROWS = 128, SW_TOK = 16, SW_KCH = 2;
+
+__device__ __forceinline__ float ld_cluster_f32(uint32_t addr) {
+  float v;
+  asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(v) : "r"(addr) : "memory");
+  return v;
+}
+
+// C[m][n] (+ R[m][n]) for one element of the transposed accumulator
+__device__ __forceinline__ void store_swapped(const Params& p, int m, int n, float v) {
+  if (n >= p.N) return;
+  if (p.R) v += __bfloat162float(p.R[static_cast<int64_t>(m) * p.ldr + n]);
+  if (p.c_f32)
+    reinterpret_cast<float*>(p.C)[static_cast<int64_t>(m) * p.ldc + n] = v;
+  else
+    p.C[static_cast<int64_t>(m) * p.ldc + n] = __float2bfloat16_rn(v);
+}
+
+template <int S>
+__global__ void __cluster_dims__(S, 1, 1) __launch_bounds__(THREADS, 1)
+    k_gemm_swap(const __grid_constant__ CUtensorMap map_w, const __grid_constant__ CUtensorMap map_x, Params p) {
+  constexpr int W_STG = SW_KCH * SW_ROWS * 128, X_STG = SW_KCH * SW_TOK * 128;
+  const int STAGES = p.stages;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sw = smem;                                   // STAGES x W_STG
+  uint8_t* sx = smem + STAGES * W_STG;                  // STAGES x X_STG
+  float* red = reinterpret_cast<float*>(sx + STAGES * X_STG);  // [SW_TOK][SW_ROWS] fp32 partial
+  uint64_t* full = reinterpret_cast<uint64_t*>(red + SW_TOK * SW_ROWS);
+  uint64_t* empty = full + MAX_STAGES;
+  uint64_t* acc_full = empty + MAX_STAGES;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_full + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int rank = S == 1 ? 0 : static_cast<int>(cluster_ctarank());
+  const int tile = blockIdx.x / S;
+  const int k_blocks = p.K / BK;
+  const int chunks = (k_blocks + SW_KCH - 1) / SW_KCH;
+  const int c0 = rank * chunks / S, nks = (rank + 1) * chunks / S - c0;
+
+  if (warp == 0 && lane == 0) {
+    prefetch_tmap(&map_w);
+    prefetch_tmap(&map_x);
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(&acc_full[0], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 32;" ::"r"(smem_u32(tmem_slot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // weights are static: the first stages go out before pdl_wait, overlapping the
+      // predecessor; the activations follow once its writes are visible
+      const int pre = p.b_static ? min(STAGES, nks) : 0;
+      for (int i = 0; i < pre; ++i) {
+        mbar_expect_tx(&full[i], W_STG + X_STG);
+        tma_load_3d(sw + i * W_STG, &map_w, 0, tile * SW_ROWS, (c0 + i) * SW_KCH, &full[i]);
+      }
+      pdl_wait();
+      for (int i = 0; i < pre; ++i) tma_load_3d(sx + i * X_STG, &map_x, 0, 0, (c0 + i) * SW_KCH, &full[i]);
+      uint32_t stage = pre % STAGES, phase = pre == STAGES ? 1u : 0u;
+      for (int ks = pre; ks < nks; ++ks) {
+        mbar_wait(&empty[stage], phase ^ 1);
+        mbar_expect_tx(&full[stage], W_STG + X_STG);
+        tma_load_3d(sw + stage * W_STG, &map_w, 0, tile * SW_ROWS, (c0 + ks) * SW_KCH, &full[stage]);
+        tma_load_3d(sx + stage * X_STG, &map_x, 0, 0, (c0 + ks) * SW_KCH, &full[stage]);
+        if (++stage == STAGES) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+      pdl_trigger();
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idesc = instr_desc_bf16(SW_ROWS, SW_TOK);
+      uint32_t stage = 0, phase = 0;
+      for (int ks = 0; ks < nks; ++ks) {
+        mbar_wait(&full[stage], phase);
+        tc_fence_after();
+        const int subs = min(SW_KCH, k_blocks - (c0 + ks) * SW_KCH);
+        for (int sub = 0; sub < subs; ++sub) {
+          const uint64_t da = umma_desc_sw128(smem_u32(sw + stage * W_STG + sub * SW_ROWS * 128));
+          const uint64_t db = umma_desc_sw128(smem_u32(sx + stage * X_STG + sub * SW_TOK * 128));
+#pragma unroll
+          for (int k = 0; k < BK / UMMA_K; ++k)
+            umma_bf16(tmem_base, da + 2 * k, db + 2 * k, idesc, (ks != 0 || sub != 0 || k != 0) ? 1u : 0u);
+        }
+        umma_commit(&empty[stage]);
+        if (++stage == STAGES) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+      umma_commit(&acc_full[0]);
+    }
+  } else if (warp >= 4) {
+    pdl_wait();  // reads the residual and writes C
+    const int row = (warp & 3) * 32 + lane;  // TMEM lane = weight row of the tile
+    mbar_wait(&acc_full[0], 0);
+    tc_fence_after();
+    uint32_t r[32];  // columns 0..15 = tokens
+    tmem_ld_32x32b_x32(tmem_base + (static_cast<uint32_t>((warp & 3) * 32) << 16), r);
+    if (S == 1) {
+      for (int m = 0; m < p.M; ++m) store_swapped(p, m, tile * SW_ROWS + row, __uint_as_float(r[m]));
+    } else {
+#pragma unroll
+      for (int m = 0; m < SW_TOK; ++m) red[m * SW_ROWS + row] = __uint_as_float(r[m]);
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 32;" ::"r"(tmem_base));
+  }
+  if (S > 1) {
+    cluster_sync_all();  // every rank's partial is in its shared memory
+    const int r0 = rank * SW_ROWS / S, per = (rank + 1) * SW_ROWS / S - r0;
+    for (int idx = threadIdx.x; idx < per * p.M; idx += THREADS) {
+      const int m = idx / per, j = r0 + idx % per;
+      const uint32_t a = smem_u32(red + m * SW_ROWS + j);
+      float v = 0.f;
+#pragma unroll
+      for (int q = 0; q < S; ++q) v += ld_cluster_f32(mapa_cta(a, q));  // fixed order: deterministic
+      store_swapped(p, m, tile * SW_ROWS + j, v);
+    }
+    cluster_sync_all();  // no rank leaves while a peer still reads its partial
+  }
+  if (p.signal != nullptr && threadIdx.x == 0) {
+    __threadfence_system();
+    asm volatile("red.release.sys.global.add.u32 [%0], 1;" ::"l"(p.signal) : "memory");
+  }
+}
+
+// 3-D view {64 k, rows, K / 64} of a K-major [rows, K] bf16 operand (K % 64 == 0): one box
+// {64, box_rows, kch} is kch 128B-swizzled [box_rows x 64] tiles side by side
+static int encode_kc3d(CUtensorMap* map, const void* ptr, int rows, int k, int ld, int box_rows, int kch) {
+  const DriverApi* d = driver_api();
+  if (!d) return BZ_ECUDA;
+  cuuint64_t dims[3] = {64, static_cast<cuuint64_t>(rows), static_cast<cuuint64_t>(k / 64)};
+  cuuint64_t strides[2] = {static_cast<cuuint64_t>(ld) * 2, 128};
+  cuuint32_t box[3] = {64, static_cast<cuuint32_t>(box_rows), static_cast<cuuint32_t>(kch)};
+  cuuint32_t elem[3] = {1, 1, 1};
+  CUresult r = d->cuTensorMapEncodeTiled(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(ptr), dims,
+                                         strides, box, elem, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                         CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return bz_fail_cu(r, "cuTensorMapEncodeTiled (3-D)");
+  return BZ_OK;
+}
+
+// BZ_GEMM_KC=0 turns the K-chunked decode kernel off (A/B checks); default on for M <= 16
+static int kc_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("BZ_GEMM_KC");
+    v = e ? (atoi(e) != 0) : 1;
+  }
+  return v;
+}
+
+template <int BN_>
+static int launch_kc(const void* A, const void* B, int M, int N, int K, int lda, int ldb, Params p, int max_ctas,
+                     cudaStream_t stream, int* ctas_out) {
+  const int a_rows = (M + 7) / 8 * 8;
+  int kch = 32768 / (BN_ * 128);  // ~32 KiB of weights per stage
+  kch = kch < 1 ? 1 : kch > 8 ? 8 : kch;
+  CUtensorMap ma, mb;
+  if (int rc = encode_kc3d(&ma, A, M, K, lda, a_rows, kch)) return rc;
+  if (int rc = encode_kc3d(&mb, B, N, K, ldb, BN_, kch)) return rc;
+  p.m_tiles = 1;
+  p.n_tiles = (N + BN_ - 1) / BN_;
+  const int stage_bytes = kch * (a_rows + BN_) * 128;
+  const int stages = (SMEM_LIMIT - 1024 - BAR_BYTES) / stage_bytes;
+  p.stages = stages < MAX_STAGES ? stages : MAX_STAGES;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int cap = max_ctas > 0 ? tmin(max_ctas, sms) : sms;
+  const int grid = p.n_tiles < cap ? p.n_tiles : cap;
+  static bool attr_set[64] = {};
+  if (dev < 64 && !attr_set[dev]) {
+    cudaError_t e = cudaFuncSetAttribute(k_gemm_skinny_kc<BN_>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_LIMIT);
+    if (e != cudaSuccess) return bz_fail_cuda(e, "gemm (K-chunked) smem attribute");
+    attr_set[dev] = true;
+  }
+  cudaError_t e = launch_pdl(PDL_GEMM, k_gemm_skinny_kc<BN_>, dim3(grid), dim3(THREADS), SMEM_LIMIT, stream, ma, mb,
+                             p, kch, a_rows);
+  if (e != cudaSuccess) return bz_fail_cuda(e, "bz_gemm_bf16 (K-chunked) launch");
+  if (ctas_out) *ctas_out = grid;
+  return bz_check_launch("bz_gemm_bf16 (K-chunked)");
+}
+
+// BZ_GEMM_SWAP=0 turns the swapped decode kernel off (A/B checks); default on
+static int swap_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("BZ_GEMM_SWAP");
+    v = e ? (atoi(e) != 0) : 1;
+  }
+  return v;
+}
+
+template <int S>
+static int launch_swap(const void* A, const void* B, int M, int N, int K, int lda, int ldb, Params p,
+                       cudaStream_t stream, int* ctas_out) {
+  CUtensorMap mw, mx;
+  if (int rc = encode_kc3d(&mw, B, N, K, ldb, SW_ROWS, SW_KCH)) return rc;
+  if (int rc = encode_kc3d(&mx, A, M, K, lda, SW_TOK, SW_KCH)) return rc;
+  p.n_tiles = (N + SW_ROWS - 1) / SW_ROWS;
+  const int stage_bytes = SW_KCH * (SW_ROWS + SW_TOK) * 128;
+  const int fixed = 1024 + SW_TOK * SW_ROWS * 4 + BAR_BYTES;
+  int stages = (SMEM_LIMIT - fixed) / stage_bytes;
+  if (const char* e = getenv("BZ_GEMM_SWAP_STAGES")) stages = tmin(stages, atoi(e) > 0 ? atoi(e) : 1);
+  p.stages = tmin(stages, MAX_STAGES);
+  const int smem = fixed + p.stages * stage_bytes;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  static bool attr_set[64] = {};
+  if (dev < 64 && !attr_set[dev]) {
+    cudaError_t e = cudaFuncSetAttribute(k_gemm_swap<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_LIMIT);
+    if (e != cudaSuccess) return bz_fail_cuda(e, "gemm (swapped) smem attribute");
+    attr_set[dev] = true;
+  }
+  const int grid = p.n_tiles * S;
+  cudaError_t e = launch_pdl(PDL_GEMM, k_gemm_swap<S>, dim3(grid), dim3(THREADS), smem, stream, mw, mx, p);
+  if (e != cudaSuccess) return bz_fail_cuda(e, "bz_gemm_bf16 (swapped) launch");
+  if (ctas_out) *ctas_out = grid;
+  return bz_check_launch("bz_gemm_bf16 (swapped)");
+}
+
 // BZ_GEMM_OCC=2 runs skinny (M <= 128) GEMMs two CTAs per SM (BN <= 128, half the smem
 // ring); default one: at decode batch 1..64 the pair measured 5-10 % slower per 7B block
 // (profiles/r2_gemm_occ2.txt)
@@ -1119,6 +1520,7 @@ static int gemm_impl(const void* A, const void* B, void* C, const void* residual
   p.a_bytes = a_box * BK * 2;
   p.b_static = (flags & BZ_GEMM_B_STATIC) ? 1 : 0;
   p.c_f32 = c_f32 ? 1 : 0;
+  p.kc_nomma = 0;
   if (!workspace || (reinterpret_cast<uintptr_t>(workspace) & 15) || ws_bytes <= kCounterHeader) {
     ws_bytes = 0;
   } else {
@@ -1148,6 +1550,64 @@ static int gemm_impl(const void* A, const void* B, void* C, const void* residual
     }
   }
   SkinnyPlan plan{forced ? forced : (single_bn ? single_bn : pick_bn(M, N, ctas)), 0};
+  // decode shapes: 128-row weight tiles as the MMA's M, K split over a cluster of S
+  // CTAs (tiles x S <= SMs, at least two 2-k-block chunks per rank)
+  const int sw_tiles = (N + SW_ROWS - 1) / SW_ROWS;
+  if (M <= SW_TOK && K % 64 == 0 && swap_enabled() && !forced && sw_tiles <= ctas) {
+    const int chunks = (K / BK + SW_KCH - 1) / SW_KCH;
+    int S = 1;
+    while (S < 8 && sw_tiles * (S + 1) <= ctas && chunks >= 2 * (S + 1)) ++S;
+    if (const char* e = getenv("BZ_GEMM_SWAP_S")) S = tmin(atoi(e) > 1 ? atoi(e) : 1, 8);
+    switch (S) {
+      case 1:
+        return launch_swap<1>(A, B, M, N, K, lda, ldb, p, s, ctas_out);
+      case 2:
+        return launch_swap<2>(A, B, M, N, K, lda, ldb, p, s, ctas_out);
+      case 3:
+        return launch_swap<3>(A, B, M, N, K, lda, ldb, p, s, ctas_out);
+      case 4:
+        return launch_swap<4>(A, B, M, N, K, lda, ldb, p, s, ctas_out);
+      case 5:
+        return launch_swap<5>(A, B, M, N, K, lda, ldb, p, s, ctas_out);
+      case 6:
+        return launch_swap<6>(A, B, M, N, K, lda, ldb, p, s, ctas_out);
+      case 7:
+        return launch_swap<7>(A, B, M, N, K, lda, ldb, p, s, ctas_out);
+      default:
+        return launch_swap<8>(A, B, M, N, K, lda, ldb, p, s, ctas_out);
+    }
+  }
+  // wider decode GEMMs (more 128-row tiles than SMs): whole tiles of about one per SM
+  // over K-chunked stages (no stream-K)
+  if (M <= 16 && K % 64 == 0 && kc_enabled() && !forced) {
+    const int widths[7] = {32, 64, 96, 128, 160, 192, 256};
+    int bn = 256;
+    for (int w : widths)
+      if ((N + w - 1) / w <= ctas) {
+        bn = w;
+        break;
+      }
+    if (const char* e = getenv("BZ_GEMM_KC_BN")) bn = atoi(e);
+    if (const char* e = getenv("BZ_GEMM_KC_NOMMA")) p.kc_nomma = atoi(e);
+    // a tile narrower than 128 is MMA-issue bound here (the swapped kernel covers those
+    // shapes); such plans stay on the stream-K path
+    if (bn >= 128 || getenv("BZ_GEMM_KC_BN")) switch (bn) {
+      case 32:
+        return launch_kc<32>(A, B, M, N, K, lda, ldb, p, max_ctas, s, ctas_out);
+      case 64:
+        return launch_kc<64>(A, B, M, N, K, lda, ldb, p, max_ctas, s, ctas_out);
+      case 96:
+        return launch_kc<96>(A, B, M, N, K, lda, ldb, p, max_ctas, s, ctas_out);
+      case 128:
+        return launch_kc<128>(A, B, M, N, K, lda, ldb, p, max_ctas, s, ctas_out);
+      case 160:
+        return launch_kc<160>(A, B, M, N, K, lda, ldb, p, max_ctas, s, ctas_out);
+      case 192:
+        return launch_kc<192>(A, B, M, N, K, lda, ldb, p, max_ctas, s, ctas_out);
+      default:
+        return launch_kc<256>(A, B, M, N, K, lda, ldb, p, max_ctas, s, ctas_out);
+    }
+  }
   const bool occ2 = M <= BM && occ_override() == 2 && forced <= 128;
   if (M <= BM) {
     plan = plan_skinny(M, N, K, ctas, ws_bytes, forced, occ2 ? 128 : 256);

@@ -8,7 +8,7 @@ max-normalised error) -- the north star's cooperative-logit tolerance.
 import pytest
 import torch
 
-from paper_2412_17246_b200._native import cuda_lib
+from paper_2412_17246_b200._native import BZ_GEMM_B_STATIC, BZ_GEMM_C_F32, cuda_lib
 
 pytestmark = pytest.mark.gpu
 
@@ -94,7 +94,7 @@ def gemm_ex(a, b, residual=None, ws_bytes=32 << 20, signal=None):
 @pytest.mark.parametrize("m,n,k", [
     (1, 4096, 4096), (1, 12288, 4096), (8, 4096, 11008), (64, 22016, 4096), (1, 32000, 4096),
     (16, 256, 688), (3, 264, 4104), (128, 4096, 4096), (32, 4096, 4096), (64, 4096, 11008),
-    (2, 96, 4096), (5, 40, 64), (1, 1376, 256),
+    (2, 96, 4096), (5, 40, 64), (1, 1376, 256), (4, 22016, 4096), (16, 15360, 5120),
 ])
 def test_streamk_skinny_gemm_matches_fp32(m, n, k):
     """Decode-shaped GEMMs (M = batch rows) run stream-K: tiles shared by CTAs are summed in fp32."""
@@ -210,3 +210,58 @@ def test_splitk_partials_leave_streamk_counters_zero():
         _check(c1, a1.float() @ b1.float().t())
         _check(c2, a2.float() @ b2.float().t())
         assert int(ws[:1024].view(torch.int32).abs().sum()) == 0
+
+
+def _gemm_flags(a, b, residual=None, c_f32=False, signal=None, max_ctas=0):
+    import ctypes
+    m, k = a.shape
+    n = b.shape[0]
+    c = torch.empty(m, n, dtype=torch.float32 if c_f32 else torch.bfloat16, device=a.device)
+    ctas = ctypes.c_int(0)
+    cuda_lib().bz_gemm_bf16_ex(a.data_ptr(), b.data_ptr(), c.data_ptr(),
+                               residual.data_ptr() if residual is not None else None,
+                               m, n, k, a.stride(0), b.stride(0), c.stride(0),
+                               residual.stride(0) if residual is not None else 0, max_ctas,
+                               BZ_GEMM_B_STATIC | (BZ_GEMM_C_F32 if c_f32 else 0), None, 0,
+                               signal.data_ptr() if signal is not None else None, ctypes.byref(ctas),
+                               torch.cuda.current_stream().cuda_stream)
+    return c, ctas.value
+
+
+@pytest.mark.parametrize("split", [1, 2, 3, 4, 5, 6, 7, 8])
+def test_swapped_decode_gemm_every_cluster_split(monkeypatch, split):
+    """Decode GEMMs (M <= 16) with the weight tile as the MMA's M operand and K split
+    over a cluster of `split` CTAs (partials summed in distributed shared memory):
+    ragged N (not a multiple of 128), an odd number of 2-k-block chunks, residual,
+    fp32 C and the per-CTA completion signal; the fixed summation order makes a
+    repeated call bit-identical."""
+    monkeypatch.setenv("BZ_GEMM_SWAP_S", str(split))
+    torch.manual_seed(split)
+    m, n, k = 13, 1000, 64 * 37
+    a = (torch.randn(m, k, device="cuda") * 0.5).to(torch.bfloat16)
+    b = (torch.randn(n, k, device="cuda") * 0.02).to(torch.bfloat16)
+    r = torch.randn(m, n, device="cuda").to(torch.bfloat16)
+    ref = a.float() @ b.float().t()
+    sig = torch.zeros(1, dtype=torch.int32, device="cuda")
+    c, ctas = _gemm_flags(a, b, residual=r, signal=sig)
+    c_again, _ = _gemm_flags(a, b, residual=r)
+    f, _ = _gemm_flags(a, b, c_f32=True)
+    torch.cuda.synchronize()
+    assert ctas == 8 * split and int(sig.item()) == ctas
+    _check(c, ref + r.float())
+    assert torch.equal(c, c_again)
+    assert (f - ref).abs().max().item() <= 1e-3 * ref.abs().max().item()
+
+
+@pytest.mark.parametrize("m", [1, 2, 8, 16])
+def test_swapped_decode_gemm_respects_cta_cap(m):
+    """The split is chosen so tiles x split stays within max_ctas (the co-operative
+    decode leaves SMs to the data plane)."""
+    torch.manual_seed(m)
+    a = (torch.randn(m, 4096, device="cuda") * 0.5).to(torch.bfloat16)
+    b = (torch.randn(4096, 4096, device="cuda") * 0.02).to(torch.bfloat16)
+    for cap in (0, 100, 40, 32):
+        c, ctas = _gemm_flags(a, b, max_ctas=cap)
+        torch.cuda.synchronize()
+        assert 0 < ctas <= (cap or 148)
+        _check(c, a.float() @ b.float().t())

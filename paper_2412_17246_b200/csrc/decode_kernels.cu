@@ -17,6 +17,7 @@
 #include <cuda_runtime.h>
 #include <math_constants.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 #include "../../include/blitz.h"
 #include "common.cuh"
@@ -316,11 +317,19 @@ static int attention(int group, int rows, dim3 grid, cudaStream_t s, const __nv_
   return bz_check_launch("bz_decode_attention");
 }
 
-// context tokens per CTA: shrink the chunk (down to 64) until the grid covers
-// two waves of the 148 SMs, so a small batch still spreads over the chip
+// context tokens per CTA: 128 (256 only when 64 chunks of 128 cannot hold s_max), shrunk
+// to 64 while the grid is under four waves of the 148 SMs.  Measured on 7B blocks, KV
+// 1024 (scripts/decode_breakdown.py, us per block): batch 1 chunk 64/128/256 = 96.4 /
+// 97.6 / 104.1, batch 4 109.4 / 106.3 / 112.0, batch 16 154.2 / 151.9 / 158.3.
 static int chunk_for(int rows, int n_kv, int64_t s_max) {
-  int chunk = CHUNK;
-  while (chunk > 64 && static_cast<int64_t>(rows) * n_kv * ((s_max + chunk - 1) / chunk) < 2 * 148) chunk /= 2;
+  if (const char* e = getenv("BZ_DECODE_CHUNK")) {  // A/B measurements: 64, 128 or 256
+    const int c = atoi(e);
+    if (c == 64 || c == 128 || c == 256) return c;
+  }
+  int chunk = s_max > static_cast<int64_t>(MAX_SPLITS) * 128 ? CHUNK : 128;
+  while (chunk > 64 && static_cast<int64_t>(rows) * n_kv * ((s_max + chunk - 1) / chunk) < 4 * 148 &&
+         (s_max + chunk / 2 - 1) / (chunk / 2) <= MAX_SPLITS)  // never more chunks than the combine stages
+    chunk /= 2;
   return chunk;
 }
 static int nsplit_for(int rows, int n_kv, int64_t s_max) {

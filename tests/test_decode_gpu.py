@@ -184,6 +184,8 @@ def _attn_ref(q, kc, vc, length, n_heads, n_kv):
 @pytest.mark.parametrize("rows,H,KV,hd,s_max,pos", [
     (1, 32, 32, 128, 1100, 1023), (2, 8, 2, 64, 700, 650), (16, 32, 32, 128, 600, 300),
     (3, 64, 8, 128, 300, 0), (4, 4, 4, 64, 40, 39), (2, 16, 4, 128, 2048, 1500),
+    # long contexts on few kv heads: the chunk may not shrink past the combine's 64 stages
+    (1, 8, 1, 128, 16384, 16000), (1, 8, 2, 64, 6000, 5999),
 ])
 def test_decode_attention_kernel_matches_fp32(rows, H, KV, hd, s_max, pos):
     import ctypes
